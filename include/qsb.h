@@ -1,0 +1,179 @@
+/* qsb.h -- C ABI of the B200 state-vector backend (libqsb.so).
+ *
+ * This is the drop-in boundary for the reference's simulation hot path.  The
+ * reference (qforge, header-only C++20 under /root/reference/proj/include)
+ * has no plugin or FFI layer: its seam is the StateVector member API that
+ * every executor calls.  Each entry point below replaces one member of that
+ * seam; the file:line in brackets is the reference interface it replaces
+ * (paths relative to /root/reference/proj/include/qforge/).  The C++ facade
+ * under paper_2212_14201_b200/include/qforge/ re-exposes the reference's own
+ * types (Program, Gate, StateVector, run, expectation, ...) on top of this
+ * ABI, and INTEGRATION.md shows the bindings a maintainer would add.
+ *
+ * Conventions (identical to the reference):
+ *   - amplitude index i has bit q = qubit q (qubit 0 is the least significant
+ *     bit); amplitudes are complex128, interleaved (re, im)  [statevector.hpp:134-156]
+ *   - operand lists are most-significant-first; for a gate, the full operand
+ *     list is controls ++ targets and CNOT/CZ/TOFFOLI carry their defining
+ *     control(s) inside targets                           [circuit.hpp:108-114]
+ *   - matrices are row-major, interleaved (re, im), 2^k x 2^k, with local bit
+ *     b of the row/column index living at targets[k-1-b]   [statevector.hpp:385-390]
+ *
+ * Errors: every function returns QS_OK (0) or a negative status; no C++
+ * exception crosses the ABI.  qs_last_error() returns the message of the last
+ * failure on the calling thread.  QS_ERR_VALIDATION maps to
+ * qforge::ValidationError, QS_ERR_RUNTIME to qforge::Error   [error.hpp:10-20].
+ *
+ * Threading: a state handle is owned by one thread at a time;
+ * each handle has one CUDA stream on its device.  Host buffers belong to the
+ * caller and every call is synchronous with respect to them on return.
+ */
+#ifndef QSB_H_
+#define QSB_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define QSB_ABI_VERSION 1
+
+/* status codes */
+#define QS_OK 0
+#define QS_ERR_VALIDATION -1 /* bad operands, sizes, non-unitary matrix   */
+#define QS_ERR_RUNTIME -2    /* e.g. collapse onto a zero-probability outcome */
+#define QS_ERR_CUDA -3       /* CUDA / NCCL failure                         */
+#define QS_ERR_MEMORY -4     /* allocation failure                          */
+#define QS_ERR_UNSUPPORTED -5
+
+/* Gate kinds, numbered exactly as qforge::GateKind          [circuit.hpp:22-27] */
+enum qs_gate_kind {
+  QS_I = 0, QS_X, QS_Y, QS_Z, QS_H, QS_S, QS_T,
+  QS_RX, QS_RY, QS_RZ, QS_U3,
+  QS_CNOT, QS_CZ, QS_SWAP, QS_TOFFOLI,
+  QS_CUSTOM
+};
+
+#define QS_MAX_TARGETS 8
+#define QS_MAX_CONTROLS 40
+
+/* One gate application, the flat equivalent of qforge::Gate [circuit.hpp:115-139]. */
+typedef struct qs_gate {
+  int32_t kind;          /* enum qs_gate_kind                                  */
+  int32_t dagger;        /* Gate::dagger                                       */
+  uint32_t num_targets;  /* Gate::targets.size()                               */
+  uint32_t num_controls; /* Gate::controls.size() (extra controls only)        */
+  uint32_t targets[QS_MAX_TARGETS];   /* most significant first              */
+  uint32_t controls[QS_MAX_CONTROLS];
+  double params[3];      /* RX/RY/RZ: params[0]; U3: theta, phi, lambda        */
+  const double* matrix;  /* Custom only: 2^nt x 2^nt row-major interleaved    */
+} qs_gate;
+
+typedef struct qs_state* qs_state_t;
+
+/* --- library -------------------------------------------------------------- */
+const char* qs_last_error(void);
+int qs_abi_version(void);
+/* Number of this library's own kernel launches since load (bench evidence). */
+uint64_t qs_kernel_launches(void);
+
+/* --- lifecycle ------------------------------------------------------------- */
+/* StateVector(n): |0...0> on `device`.  max_qubits bounds n (the reference caps
+ * at 30 [statevector.hpp:137-138]; pass 0 for that default).                   */
+int qs_create(uint32_t num_qubits, int device, uint32_t max_qubits, qs_state_t* out);
+int qs_destroy(qs_state_t s);
+/* StateVector copy constructor (device-to-device)     [statevector.hpp:134] */
+int qs_clone(qs_state_t src, qs_state_t* out);
+uint32_t qs_num_qubits(qs_state_t s);
+int qs_device(qs_state_t s);
+/* Raw device pointer of the amplitudes (for zero-copy interop, e.g. torch).  */
+void* qs_device_ptr(qs_state_t s);
+/* Resets to |0...0>. */
+int qs_reset(qs_state_t s);
+/* Resets to the basis state |index>. */
+int qs_set_basis_state(qs_state_t s, uint64_t index);
+int qs_sync(qs_state_t s);
+
+/* --- amplitude I/O (logical index order) -----------------------------------
+ * from_amplitudes / amplitudes()           [statevector.hpp:143-156]         */
+int qs_set_amplitudes(qs_state_t s, const double* interleaved, uint64_t offset, uint64_t count);
+int qs_get_amplitudes(qs_state_t s, double* interleaved, uint64_t offset, uint64_t count);
+
+/* --- single gates: one HBM pass each (the reference's per-gate kernels) ----- */
+/* StateVector::apply_gate: validation, dagger, named-matrix dispatch  [statevector.hpp:469-538] */
+int qs_apply_gate(qs_state_t s, const qs_gate* g);
+/* apply_1q: 2x2 matrix m (row-major interleaved) on target    [statevector.hpp:268-290] */
+int qs_apply_1q(qs_state_t s, uint32_t target, const double m[8], const uint32_t* controls, uint32_t nc);
+/* apply_diag_1q: diag(d0, d1)                                  [statevector.hpp:292-319] */
+int qs_apply_diag(qs_state_t s, uint32_t target, const double d[4], const uint32_t* controls, uint32_t nc);
+/* apply_flip: X / CNOT / TOFFOLI                               [statevector.hpp:321-339] */
+int qs_apply_flip(qs_state_t s, uint32_t target, const uint32_t* controls, uint32_t nc);
+/* apply_swap2                                                  [statevector.hpp:341-361] */
+int qs_apply_swap(qs_state_t s, uint32_t a, uint32_t b, const uint32_t* controls, uint32_t nc);
+/* apply_matrix: dense 2^k x 2^k on targets (msb first), need not be unitary
+ *                                                              [statevector.hpp:363-467] */
+int qs_apply_matrix(qs_state_t s, const uint32_t* targets, uint32_t k, const double* m,
+                    const uint32_t* controls, uint32_t nc);
+
+/* --- batched circuits: the fused hot path ------------------------------------
+ * Applies gates[0..n) in order.  The planner groups them into shared-memory
+ * tile passes (many gates per HBM pass); results equal sequential apply_gate
+ * within rounding.  Replaces the run() gate loop + fuse_circuit
+ *                               [simulator.hpp:147-159, fusion.hpp:108-133]  */
+#define QS_PLAN_DEFAULT 0u
+#define QS_PLAN_UNFUSED 1u    /* one kernel per gate (reference execution order) */
+#define QS_PLAN_DENSE_FUSION 2u /* reference fuse_circuit blocks, dense k<=5 kernels */
+#define QS_PLAN_TILED 3u      /* shared-memory tile passes (default)            */
+int qs_apply_circuit(qs_state_t s, const qs_gate* gates, uint64_t n, uint32_t plan,
+                     uint32_t max_fused_qubits);
+
+/* Compiled circuit handle: plan once, run many times (bench / parameter sweeps). */
+typedef struct qs_plan* qs_plan_t;
+int qs_plan_create(uint32_t num_qubits, const qs_gate* gates, uint64_t n, uint32_t plan,
+                   uint32_t max_fused_qubits, qs_plan_t* out);
+int qs_plan_destroy(qs_plan_t p);
+int qs_plan_execute(qs_state_t s, qs_plan_t p);
+/* Planner statistics: passes (HBM sweeps) and kernel launches per execute.   */
+int qs_plan_stats(qs_plan_t p, uint64_t* passes, uint64_t* launches, uint64_t* gates);
+
+/* --- reductions (fixed-order trees; run-to-run deterministic) -------------- */
+int qs_norm2(qs_state_t s, double* out);                              /* [statevector.hpp:158-162] */
+int qs_prob_one(qs_state_t s, uint32_t q, double* out);               /* [statevector.hpp:181-186] */
+/* marginal over qubits[0..m): result bit b <-> qubits[b]           [statevector.hpp:190-208] */
+int qs_probs(qs_state_t s, const uint32_t* qubits, uint32_t m, double* out);
+/* |a_i|^2 for i in [offset, offset+count)                           [statevector.hpp:210-215] */
+int qs_probs_full(qs_state_t s, double* out, uint64_t offset, uint64_t count);
+/* sum_i |a_i|^2 (i+1), the bench digest                                  [bench.hpp:141-148] */
+int qs_checksum(qs_state_t s, double* out);
+
+/* --- measurement ------------------------------------------------------------ */
+/* collapse onto outcome with known probability                 [statevector.hpp:228-247] */
+int qs_collapse(qs_state_t s, uint32_t q, int outcome, double prob);
+/* measure_collapse: outcome = (u < P(0)) ? 0 : 1                [statevector.hpp:219-225] */
+int qs_measure_collapse(qs_state_t s, uint32_t q, double u, int* outcome);
+int qs_scale(qs_state_t s, double re, double im);                     /* [statevector.hpp:164-166] */
+
+/* BasisSampler: cumulative |a|^2 in index order, upper-bound search of u*total
+ * [statevector.hpp:542-570].  With exact != 0 the cumulative array reproduces
+ * the reference's serial left-to-right double accumulation bit for bit (so
+ * counts equal the reference's for the same amplitudes and draws); otherwise a
+ * parallel scan is used.  out_index[i] is the basis state drawn for u[i].   */
+int qs_sample(qs_state_t s, const double* uniforms, uint64_t shots, int exact, uint64_t* out_index);
+/* Draws `shots` uniforms from the reference stream Rng(seed) (mt19937_64,
+ * (next()>>11)*2^-53 [rng.hpp:33-35]) and samples them; out_index as above. */
+int qs_sample_seeded(qs_state_t s, uint64_t seed, uint64_t shots, int exact, uint64_t* out_index);
+
+/* --- expectation values -------------------------------------------------------
+ * <psi| P_t |psi> for Pauli strings, one read pass per batch of terms
+ * (replaces the per-term state copy + serial dot of       [variational.hpp:33-47]).
+ * Term t has letters[t*n .. t*n+n) in {'I','X','Y','Z'} indexed by qubit.
+ * out[2t], out[2t+1] = real and imaginary part of <psi|P_t|psi>.            */
+int qs_expect_pauli(qs_state_t s, const char* letters, uint32_t nterms, double* out);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* QSB_H_ */

@@ -1,0 +1,139 @@
+"""Pins the C oracle (oracle/qsim_oracle.c) against golden vectors emitted by
+the unmodified reference (oracle/_ref/ref_driver; tests/golden/README.md).
+
+CPU only.  The oracle is trusted as the GPU checker only after these pass.
+"""
+import numpy as np
+import pytest
+
+import golden_io as gio
+import oracle_lib as ol
+
+
+def test_rng_stream_bit_exact():
+    # rng.hpp:9-46 -- mt19937_64, uniform=(next()>>11)*2^-53, derive, below
+    c = gio.case("rng")
+    for s in c["streams"]:
+        r = ol.Rng(s["seed"])
+        assert [str(r.next()) for _ in range(8)] == s["next"]
+        u = ol.Rng(s["seed"])
+        assert [u.uniform() for _ in range(8)] == s["uniform"]
+        assert str(ol.Rng(s["seed"], derive_index=3).next()) == s["derive3"]
+        assert str(ol.lib().qo_splitmix64(s["seed"])) == s["splitmix"]
+        assert str(ol.Rng(s["seed"]).below(10)) == s["below10"]
+
+
+def _same_gates(a, b):
+    assert len(a) == len(b)
+    for x, y in zip(a, b):
+        assert (x.kind, x.targets, x.controls, x.dagger) == (y.kind, y.targets, y.controls, y.dagger)
+        assert x.params == y.params  # bit-exact angles
+
+
+@pytest.mark.parametrize("name", [c["name"] for c in gio.cases("state") if c["name"].startswith("random_")
+                                  and not c["name"].endswith("fused")])
+def test_random_circuit_generator_bit_exact(name):
+    # bench.hpp:72-94
+    _, n, d, seed = name.split("_")
+    circ = gio.read_circuit(name + ".circ")
+    _same_gates(ol.gen("random_circuit", int(n), int(d), int(seed)), circ.gates)
+
+
+def test_synthetic_generators_match_reference_side():
+    _same_gates(ol.gen("ghz", 6), gio.read_circuit("ghz_6.circ").gates)
+    _same_gates(ol.gen("qft", 6, 13), gio.read_circuit("qft_6_13.circ").gates)
+    _same_gates(ol.gen("qft", 10, 717), gio.read_circuit("qft_10_717.circ").gates)
+    _same_gates(ol.gen("hea", 8, 3, 5), gio.read_circuit("hea_8_3_5.circ").gates)
+    _same_gates(ol.gen("ghz", 20), gio.read_circuit("ghz_20.circ").gates)
+    _same_gates(ol.gen("qft", 20, 0x5A5A5), gio.read_circuit("qft_20.circ").gates)
+
+
+STATE_CASES = [c for c in gio.cases("state")]
+
+
+@pytest.mark.parametrize("c", STATE_CASES, ids=[c["name"] for c in STATE_CASES])
+def test_oracle_final_state_and_reductions(c):
+    circ = gio.read_circuit(c["name"] + ".circ")
+    n = circ.qubits
+    want = gio.read_amps(c["name"] + ".amps")
+    got = ol.run_gates(n, circ.gates)
+    # fused reference runs differ from unfused ones only by rounding
+    tol = 1e-12 if not c["fusion"] else 1e-11
+    assert np.max(np.abs(got - want)) <= tol
+    # reductions on the reference's own amplitudes must agree bit for bit
+    # where the reduction order is the reference's (chunked_sum, serial loops)
+    assert ol.checksum(want, n) == c["checksum"]
+    assert ol.norm2(want, n) == c["norm2"]
+    assert [ol.prob_one(want, n, q) for q in range(n)] == c["prob_one"]
+    assert ol.probs(want, n, c["marginal_qubits"]).tolist() == c["marginal"]
+    # and on the oracle's own evolution within |dprob| <= 1e-12
+    assert abs(ol.checksum(got, n) - c["checksum"]) <= 1e-12 * (1 << n)
+    assert np.max(np.abs(np.array([ol.prob_one(got, n, q) for q in range(n)]) - c["prob_one"])) <= 1e-12
+
+
+def test_oracle_ulp_level_agreement():
+    # The restatement follows the reference's expression structure; it is bit
+    # for bit on the RX/RY/RZ/CNOT layers of gen_random_circuit and within a
+    # few ulps elsewhere (complex products contract to FMA differently).
+    for c in STATE_CASES:
+        if c["fusion"] or c["name"].startswith("custom_"):
+            continue
+        circ = gio.read_circuit(c["name"] + ".circ")
+        got = ol.run_gates(circ.qubits, circ.gates)
+        want = gio.read_amps(c["name"] + ".amps")
+        if c["name"].startswith("random_"):
+            assert np.array_equal(got.view(np.uint64), want.view(np.uint64)), c["name"]
+        else:
+            assert np.max(np.abs(got - want)) <= 4e-16, c["name"]
+
+
+@pytest.mark.parametrize("c", gio.cases("sample"), ids=[c["name"] for c in gio.cases("sample")])
+def test_oracle_counts_identical(c):
+    # simulator.hpp:164-178 + BasisSampler statevector.hpp:542-570
+    circ = gio.read_circuit(c["name"] + ".circ")
+    a = ol.run_gates(circ.qubits, circ.gates)
+    idx = ol.sample_seeded(a, circ.qubits, c["seed"], c["shots"])
+    assert gio.counts_from_indices(idx, circ.measures, circ.cbits) == c["counts"]
+
+
+def test_oracle_collapse_sequence():
+    c = gio.case("collapse")
+    circ = gio.read_circuit(c["circuit"])
+    a = ol.run_gates(circ.qubits, circ.gates)
+    for i, step in enumerate(c["steps"]):
+        assert ol.measure_collapse(a, circ.qubits, step["q"], step["u"]) == step["outcome"]
+        assert abs(ol.norm2(a, circ.qubits) - step["norm2"]) <= 1e-14
+        if i == 2:
+            assert np.max(np.abs(a - gio.read_amps("collapse_mid.amps"))) <= 1e-14
+
+
+@pytest.mark.parametrize("c", gio.cases("expectation"), ids=[c["name"] for c in gio.cases("expectation")])
+def test_oracle_expectation(c):
+    circ = gio.read_circuit(c["name"] + ".circ")
+    a = ol.run_gates(circ.qubits, circ.gates)
+    terms = ol.parse_hamiltonian(c["hamiltonian"], circ.qubits)
+    re, im = ol.expectation(a, circ.qubits, terms)
+    assert abs(re - c["value"]) <= 1e-12
+    assert abs(im) <= 1e-10
+
+
+@pytest.mark.parametrize("name", ["ghz_20", "qft_20"])
+def test_oracle_config1_digest(name):
+    c = gio.case(name)
+    circ = gio.read_circuit(name + ".circ")
+    a = ol.run_gates(20, circ.gates)
+    assert abs(ol.checksum(a, 20) - c["checksum"]) <= 1e-9
+    idx = np.array(c["idx"])
+    assert np.max(np.abs(a[idx].real - c["re"])) <= 1e-12
+    assert np.max(np.abs(a[idx].imag - c["im"])) <= 1e-12
+    assert np.max(np.abs(ol.probs_full(a, 20)[:256] - c["probs_head"])) <= 1e-12
+    assert np.max(np.abs(ol.probs(a, 20, c["marginal_qubits"]) - c["marginal"])) <= 1e-12
+
+
+def test_qft_closed_form_small():
+    # QFT generator convention pinned against the DFT closed form
+    for n, x in ((6, 13), (10, 717)):
+        a = ol.run_gates(n, ol.gen("qft", n, x))
+        k = np.arange(1 << n)
+        want = np.exp(2j * np.pi * x * k / (1 << n)) / np.sqrt(1 << n)
+        assert np.max(np.abs(a - want)) <= 1e-12
