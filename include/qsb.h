@@ -95,6 +95,8 @@ int qs_reset(qs_state_t s);
 /* Resets to the basis state |index>. */
 int qs_set_basis_state(qs_state_t s, uint64_t index);
 int qs_sync(qs_state_t s);
+/* The state's CUDA stream (cudaStream_t) for event timing / interop.         */
+void* qs_stream(qs_state_t s);
 
 /* --- amplitude I/O (logical index order) -----------------------------------
  * from_amplitudes / amplitudes()           [statevector.hpp:143-156]         */
@@ -135,8 +137,24 @@ int qs_plan_create(uint32_t num_qubits, const qs_gate* gates, uint64_t n, uint32
                    uint32_t max_fused_qubits, qs_plan_t* out);
 int qs_plan_destroy(qs_plan_t p);
 int qs_plan_execute(qs_state_t s, qs_plan_t p);
+/* Enqueue without waiting (the state's stream is returned by qs_stream).    */
+int qs_plan_enqueue(qs_state_t s, qs_plan_t p);
+/* Execute with a CUDA event around every step; step_ms[i] receives the device
+ * time of step i (qs_plan_stats' launch count entries).                       */
+int qs_plan_execute_timed(qs_state_t s, qs_plan_t p, float* step_ms);
 /* Planner statistics: passes (HBM sweeps) and kernel launches per execute.   */
 int qs_plan_stats(qs_plan_t p, uint64_t* passes, uint64_t* launches, uint64_t* gates);
+
+/* --- reference-mode gate fusion ----------------------------------------------
+ * fuse_gate_run / fuse_circuit (fusion.hpp:20-133) on one run of gates: greedy
+ * dependency-graph fusion into Custom blocks of <= max_fused_qubits qubits.
+ * The result owns its matrices; qs_fused_get fills a qs_gate whose matrix
+ * pointer stays valid until qs_fused_free.                                     */
+typedef struct qs_fused* qs_fused_t;
+int qs_fuse(const qs_gate* gates, uint64_t n, uint32_t num_qubits, uint32_t max_fused_qubits, qs_fused_t* out);
+uint64_t qs_fused_count(qs_fused_t f);
+int qs_fused_get(qs_fused_t f, uint64_t i, qs_gate* out);
+int qs_fused_free(qs_fused_t f);
 
 /* --- reductions (fixed-order trees; run-to-run deterministic) -------------- */
 int qs_norm2(qs_state_t s, double* out);                              /* [statevector.hpp:158-162] */
@@ -171,6 +189,10 @@ int qs_sample_seeded(qs_state_t s, uint64_t seed, uint64_t shots, int exact, uin
  * Term t has letters[t*n .. t*n+n) in {'I','X','Y','Z'} indexed by qubit.
  * out[2t], out[2t+1] = real and imaginary part of <psi|P_t|psi>.            */
 int qs_expect_pauli(qs_state_t s, const char* letters, uint32_t nterms, double* out);
+
+/* --- test hooks ------------------------------------------------------------ */
+/* The sampler's cumulative array (exact or parallel scan) and its total.      */
+int qs_debug_cumulative(qs_state_t s, int exact, double* cum_out, double* total_out);
 
 #ifdef __cplusplus
 }

@@ -1,0 +1,875 @@
+// Per-gate kernels, reductions, measurement and sampling for complex128 state
+// vectors on sm_100a.  Every kernel here is one streaming pass over HBM (or
+// less); the multi-gate shared-memory passes live in tile.cu.
+//
+// Reference correspondences (proj/include/qforge/):
+//   k_mat1 / k_diag / k_flip / k_swap   statevector.hpp:268-361
+//   k_dense<K>                          statevector.hpp:69-106, 363-467
+//   reductions                          statevector.hpp:110-130, 158-215; bench.hpp:141-148
+//   k_collapse                          statevector.hpp:228-247
+//   sampler (serial-equivalent scan)    statevector.hpp:542-570
+//   k_pauli                             variational.hpp:33-47
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <atomic>
+#include <cmath>
+#include <cstring>
+
+#include "kernels.hpp"
+
+namespace qsb {
+
+namespace {
+
+constexpr int kThreads = 256;
+constexpr int kMaxSlots = QS_MAX_TARGETS + QS_MAX_CONTROLS;
+
+// Reserved bit positions (targets and controls) sorted ascending, and the
+// forced-one control mask: the GroupIndexer of statevector.hpp:42-64.
+struct Slots {
+  uint32_t count;
+  uint32_t pos[kMaxSlots];
+  unsigned long long force;
+};
+
+Slots make_slots(const std::vector<uint32_t>& targets, const std::vector<uint32_t>& controls) {
+  Slots s{};
+  std::vector<uint32_t> all(targets);
+  all.insert(all.end(), controls.begin(), controls.end());
+  std::sort(all.begin(), all.end());
+  s.count = static_cast<uint32_t>(all.size());
+  for (size_t i = 0; i < all.size(); ++i) s.pos[i] = all[i];
+  s.force = 0;
+  for (auto c : controls) s.force |= 1ull << c;
+  return s;
+}
+
+__device__ __forceinline__ uint64_t deposit(uint64_t g, const Slots& s) {
+  for (uint32_t k = 0; k < s.count; ++k) {
+    const uint32_t p = s.pos[k];
+    const uint64_t low = g & ((1ull << p) - 1);
+    g = ((g >> p) << (p + 1)) | low;
+  }
+  return g | s.force;
+}
+
+__device__ __forceinline__ double2 cmul(double2 a, double2 b) {
+  return make_double2(fma(a.x, b.x, -a.y * b.y), fma(a.x, b.y, a.y * b.x));
+}
+// m0*a + m1*b
+__device__ __forceinline__ double2 cmv2(double2 m0, double2 a, double2 m1, double2 b) {
+  double re = m0.x * a.x;
+  re = fma(-m0.y, a.y, re);
+  re = fma(m1.x, b.x, re);
+  re = fma(-m1.y, b.y, re);
+  double im = m0.x * a.y;
+  im = fma(m0.y, a.x, im);
+  im = fma(m1.x, b.y, im);
+  im = fma(m1.y, b.x, im);
+  return make_double2(re, im);
+}
+// |a|^2 exactly as g++ contracts std::norm: fma(re, re, im*im).
+__device__ __forceinline__ double norm_ref(double2 a) { return __fma_rn(a.x, a.x, __dmul_rn(a.y, a.y)); }
+
+uint32_t grid_for(uint64_t work, int device, int per_sm = 8) {
+  const uint64_t blocks = (work + kThreads - 1) / kThreads;
+  const uint64_t cap = static_cast<uint64_t>(num_sms(device)) * per_sm;
+  return static_cast<uint32_t>(std::max<uint64_t>(1, std::min(blocks, cap)));
+}
+
+// ------------------------------------------------------------------ gates
+
+__global__ void __launch_bounds__(kThreads) k_mat1(double2* __restrict__ a, uint64_t groups, Slots sl,
+                                                   uint64_t bit, double2 m0, double2 m1, double2 m2,
+                                                   double2 m3) {
+  for (uint64_t g = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; g < groups;
+       g += (uint64_t)gridDim.x * blockDim.x) {
+    const uint64_t i0 = deposit(g, sl), i1 = i0 | bit;
+    const double2 x = a[i0], y = a[i1];
+    a[i0] = cmv2(m0, x, m1, y);
+    a[i1] = cmv2(m2, x, m3, y);
+  }
+}
+
+// skip_zero: only the bit-set half is multiplied by d1 (the target is then a
+// forced-one slot); otherwise pairs get (d0, d1).
+__global__ void __launch_bounds__(kThreads) k_diag(double2* __restrict__ a, uint64_t groups, Slots sl,
+                                                   uint64_t bit, double2 d0, double2 d1, int skip_zero) {
+  for (uint64_t g = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; g < groups;
+       g += (uint64_t)gridDim.x * blockDim.x) {
+    const uint64_t i0 = deposit(g, sl);
+    if (skip_zero) {
+      a[i0] = cmul(a[i0], d1);
+    } else {
+      a[i0] = cmul(a[i0], d0);
+      a[i0 | bit] = cmul(a[i0 | bit], d1);
+    }
+  }
+}
+
+__global__ void __launch_bounds__(kThreads) k_flip(double2* __restrict__ a, uint64_t groups, Slots sl,
+                                                   uint64_t bit) {
+  for (uint64_t g = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; g < groups;
+       g += (uint64_t)gridDim.x * blockDim.x) {
+    const uint64_t i0 = deposit(g, sl);
+    const double2 x = a[i0], y = a[i0 | bit];
+    a[i0] = y;
+    a[i0 | bit] = x;
+  }
+}
+
+__global__ void __launch_bounds__(kThreads) k_swap(double2* __restrict__ a, uint64_t groups, Slots sl,
+                                                   uint64_t ba, uint64_t bb) {
+  for (uint64_t g = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; g < groups;
+       g += (uint64_t)gridDim.x * blockDim.x) {
+    const uint64_t base = deposit(g, sl);
+    const double2 x = a[base | ba], y = a[base | bb];
+    a[base | ba] = y;
+    a[base | bb] = x;
+  }
+}
+
+// Dense 2^K x 2^K block (K <= 5): a group of 2^K consecutive lanes handles one
+// amplitude group; lane r owns output row r with its matrix row in registers;
+// inputs are exchanged through shared memory (broadcast reads).
+struct TargetMasks {
+  unsigned long long m[QS_MAX_TARGETS];  // m[b] = 1 << targets[K-1-b]
+};
+
+template <int K>
+__global__ void __launch_bounds__(kThreads) k_dense(double2* __restrict__ a, uint64_t groups, Slots sl,
+                                                    TargetMasks tm, const double2* __restrict__ M) {
+  constexpr int G = 1 << K;
+  constexpr int GPB = kThreads / G;  // groups per block iteration
+  __shared__ double2 v[kThreads];
+  const int tid = threadIdx.x, r = tid & (G - 1), gl = tid >> K;
+  double2 row[G];
+#pragma unroll
+  for (int c = 0; c < G; ++c) row[c] = M[r * G + c];
+  uint64_t offr = 0;
+#pragma unroll
+  for (int b = 0; b < K; ++b)
+    if ((r >> b) & 1) offr |= tm.m[b];
+  for (uint64_t gb = (uint64_t)blockIdx.x * GPB; gb < groups; gb += (uint64_t)gridDim.x * GPB) {
+    const uint64_t g = gb + gl;
+    const bool valid = g < groups;
+    const uint64_t idx = valid ? (deposit(g, sl) | offr) : 0;
+    v[tid] = valid ? a[idx] : make_double2(0, 0);
+    __syncwarp();
+    double re = 0, im = 0;
+#pragma unroll
+    for (int c = 0; c < G; ++c) {
+      const double2 x = v[(gl << K) + c];
+      re = fma(row[c].x, x.x, re);
+      re = fma(-row[c].y, x.y, re);
+      im = fma(row[c].x, x.y, im);
+      im = fma(row[c].y, x.x, im);
+    }
+    __syncwarp();
+    if (valid) a[idx] = make_double2(re, im);
+  }
+}
+
+// Dense block with K > 5: one group per 2^K threads spread over the block,
+// matrix rows read through the cache.  Rare (custom gates wider than the
+// fusion cap); correctness path.
+__global__ void __launch_bounds__(kThreads) k_dense_wide(double2* __restrict__ a, uint64_t groups, Slots sl,
+                                                         TargetMasks tm, int K, const double2* __restrict__ M) {
+  extern __shared__ double2 vbuf[];
+  const int G = 1 << K;
+  for (uint64_t g = blockIdx.x; g < groups; g += gridDim.x) {
+    const uint64_t base = deposit(g, sl);
+    for (int r = threadIdx.x; r < G; r += blockDim.x) {
+      uint64_t off = 0;
+      for (int b = 0; b < K; ++b)
+        if ((r >> b) & 1) off |= tm.m[b];
+      vbuf[r] = a[base | off];
+    }
+    __syncthreads();
+    for (int r = threadIdx.x; r < G; r += blockDim.x) {
+      uint64_t off = 0;
+      for (int b = 0; b < K; ++b)
+        if ((r >> b) & 1) off |= tm.m[b];
+      double re = 0, im = 0;
+      for (int c = 0; c < G; ++c) {
+        const double2 mm = M[(uint64_t)r * G + c], x = vbuf[c];
+        re = fma(mm.x, x.x, re);
+        re = fma(-mm.y, x.y, re);
+        im = fma(mm.x, x.y, im);
+        im = fma(mm.y, x.x, im);
+      }
+      a[base | off] = make_double2(re, im);
+    }
+    __syncthreads();
+  }
+}
+
+// ------------------------------------------------------------- reductions
+// Fixed grid and fixed per-block ranges: run-to-run deterministic (no atomics).
+constexpr uint32_t kRedBlocks = 1184;
+
+__device__ __forceinline__ double block_sum(double v, double* sh) {
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_down_sync(0xffffffffu, v, o);
+  const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+  if (l == 0) sh[w] = v;
+  __syncthreads();
+  double t = 0;
+  if (threadIdx.x == 0)
+    for (int i = 0; i < (int)(blockDim.x >> 5); ++i) t += sh[i];
+  __syncthreads();
+  return t;  // valid in thread 0
+}
+
+// mode 0: sum |a|^2 ; 1: sum over i with bit q set ; 2: sum |a_i|^2 (i+1)
+__global__ void __launch_bounds__(kThreads) k_reduce(const double2* __restrict__ a, uint64_t n_items, int mode,
+                                                     uint64_t bit, double* __restrict__ partial) {
+  __shared__ double sh[kThreads / 32];
+  const uint64_t chunk = (n_items + gridDim.x - 1) / gridDim.x;
+  const uint64_t lo = blockIdx.x * chunk, hi = min(n_items, lo + chunk);
+  double s = 0;
+  for (uint64_t g = lo + threadIdx.x; g < hi; g += blockDim.x) {
+    if (mode == 1) {
+      const uint64_t low = g & (bit - 1);
+      const uint64_t i = ((g & ~(bit - 1)) << 1) | bit | low;
+      s += norm_ref(a[i]);
+    } else if (mode == 2) {
+      s += norm_ref(a[g]) * (double)(g + 1);
+    } else {
+      s += norm_ref(a[g]);
+    }
+  }
+  const double t = block_sum(s, sh);
+  if (threadIdx.x == 0) partial[blockIdx.x] = t;
+}
+
+__global__ void k_finalize(const double* __restrict__ partial, int count, double* __restrict__ out) {
+  __shared__ double sh[kThreads / 32];
+  double s = 0;
+  for (int i = threadIdx.x; i < count; i += blockDim.x) s += partial[i];
+  const double t = block_sum(s, sh);
+  if (threadIdx.x == 0) *out = t;
+}
+
+// Marginal over m <= 12 qubits: block (x, b) reduces a fixed range of group
+// indices of bin b.
+__global__ void __launch_bounds__(kThreads) k_marginal(const double2* __restrict__ a, uint64_t per_bin, Slots sl,
+                                                       const uint32_t* __restrict__ qubits, uint32_t m,
+                                                       double* __restrict__ partial) {
+  __shared__ double sh[kThreads / 32];
+  const uint32_t bin = blockIdx.y;
+  uint64_t fixed = 0;
+  for (uint32_t b = 0; b < m; ++b)
+    if ((bin >> b) & 1) fixed |= 1ull << qubits[b];
+  const uint64_t chunk = (per_bin + gridDim.x - 1) / gridDim.x;
+  const uint64_t lo = blockIdx.x * chunk, hi = min(per_bin, lo + chunk);
+  double s = 0;
+  for (uint64_t g = lo + threadIdx.x; g < hi; g += blockDim.x) s += norm_ref(a[deposit(g, sl) | fixed]);
+  const double t = block_sum(s, sh);
+  if (threadIdx.x == 0) partial[(uint64_t)bin * gridDim.x + blockIdx.x] = t;
+}
+
+__global__ void k_marginal_finalize(const double* __restrict__ partial, uint32_t per, uint32_t bins,
+                                    double* __restrict__ out) {
+  const uint32_t b = blockIdx.x * blockDim.x + threadIdx.x;
+  if (b >= bins) return;
+  double s = 0;
+  for (uint32_t i = 0; i < per; ++i) s += partial[(uint64_t)b * per + i];
+  out[b] = s;
+}
+
+// Marginal over many qubits: one thread per bin, serial over its members.
+__global__ void k_marginal_wide(const double2* __restrict__ a, uint64_t per_bin, Slots sl,
+                                const uint32_t* __restrict__ qubits, uint32_t m, double* __restrict__ out) {
+  const uint64_t bins = 1ull << m;
+  for (uint64_t bin = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; bin < bins;
+       bin += (uint64_t)gridDim.x * blockDim.x) {
+    uint64_t fixed = 0;
+    for (uint32_t b = 0; b < m; ++b)
+      if ((bin >> b) & 1) fixed |= 1ull << qubits[b];
+    double s = 0;
+    for (uint64_t g = 0; g < per_bin; ++g) s += norm_ref(a[deposit(g, sl) | fixed]);
+    out[bin] = s;
+  }
+}
+
+__global__ void __launch_bounds__(kThreads) k_probs(const double2* __restrict__ a, uint64_t off, uint64_t count,
+                                                    double* __restrict__ p) {
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < count; i += (uint64_t)gridDim.x * blockDim.x)
+    p[i] = norm_ref(a[off + i]);
+}
+
+__global__ void __launch_bounds__(kThreads) k_collapse(double2* __restrict__ a, uint64_t size, uint64_t bit,
+                                                       int outcome, double inv) {
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < size; i += (uint64_t)gridDim.x * blockDim.x) {
+    const bool one = (i & bit) != 0;
+    if (one == (outcome == 1)) {
+      const double2 x = a[i];
+      a[i] = make_double2(x.x * inv, x.y * inv);
+    } else {
+      a[i] = make_double2(0, 0);
+    }
+  }
+}
+
+__global__ void __launch_bounds__(kThreads) k_scale(double2* __restrict__ a, uint64_t size, double2 f) {
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < size; i += (uint64_t)gridDim.x * blockDim.x)
+    a[i] = cmul(a[i], f);
+}
+
+__global__ void __launch_bounds__(kThreads) k_basis(double2* __restrict__ a, uint64_t size, uint64_t index) {
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < size; i += (uint64_t)gridDim.x * blockDim.x)
+    a[i] = make_double2(i == index ? 1.0 : 0.0, 0.0);
+}
+
+// ------------------------------------------------- serial-equivalent scan
+// The reference's BasisSampler accumulates acc += |a_i|^2 left to right in
+// double (statevector.hpp:544-552); counts depend on those exact roundings.
+// For non-negative addends the running sum is monotone, and while it stays in
+// one binade [2^e, 2^(e+1)) every partial sum is a multiple of u = 2^(e-52),
+// so fl(acc + p) = acc + u * rint(p / u) exactly unless p/u is a tie (then the
+// result depends on acc's parity) or the sum leaves the binade.  We therefore
+//   B) per chunk, guess the starting binade from a plain parallel estimate and
+//      sum the integers rint(p/u) (flagging ties / oversize addends);
+//   C) walk the chunks in order on one warp: a chunk whose guess matches the
+//      exact running value and which cannot leave the binade advances by an
+//      exact integer add; any other chunk is replayed 32 elements at a time
+//      (same integer trick per 32, true serial double adds when it fails);
+//   D) expand the clean chunks in parallel: cum_j = (A_c/u + prefix k) * u.
+// Every cum_j equals the serial double accumulation bit for bit.
+
+__global__ void __launch_bounds__(kThreads) k_chunk_sum(const double* __restrict__ p, uint64_t n, uint64_t C,
+                                                        double* __restrict__ S) {
+  __shared__ double sh[kThreads / 32];
+  const uint64_t lo = blockIdx.x * C, hi = min(n, lo + C);
+  double s = 0;
+  for (uint64_t j = lo + threadIdx.x; j < hi; j += blockDim.x) s += p[j];
+  const double t = block_sum(s, sh);
+  if (threadIdx.x == 0) S[blockIdx.x] = t;
+}
+
+// exclusive scan of chunk sums (estimates only), single block
+__global__ void k_scan_estimate(const double* __restrict__ S, uint32_t nc, double* __restrict__ E) {
+  if (threadIdx.x == 0) {
+    double acc = 0;
+    for (uint32_t c = 0; c < nc; ++c) {
+      E[c] = acc;
+      acc += S[c];
+    }
+  }
+}
+
+struct ChunkInfo {
+  long long K;  // sum of rint(p/u) over the chunk
+  int e;        // assumed binade exponent at chunk start
+  int clean;    // no ties, no oversize addend, normal range
+};
+
+__device__ __forceinline__ bool int_step(double p, double u, long long& k) {
+  // returns false for a tie or an addend too large for the one-binade model
+  const double x = p / u;  // exact: u is a power of two
+  if (!(x < 4503599627370496.0)) return false;  // 2^52
+  const double f = floor(x);
+  const double frac = x - f;
+  if (frac == 0.5) return false;
+  k = (long long)(frac > 0.5 ? f + 1.0 : f);
+  return true;
+}
+
+__global__ void __launch_bounds__(kThreads) k_chunk_ints(const double* __restrict__ p, uint64_t n, uint64_t C,
+                                                         const double* __restrict__ E, ChunkInfo* __restrict__ info) {
+  __shared__ long long shk[kThreads / 32];
+  __shared__ int shb[kThreads / 32];
+  const uint64_t lo = blockIdx.x * C, hi = min(n, lo + C);
+  const double est = E[blockIdx.x];
+  const bool usable = est >= 2.2250738585072014e-308 * 4503599627370496.0;  // u stays normal
+  const int e = usable ? ilogb(est) : 0;
+  const double u = usable ? ldexp(1.0, e - 52) : 1.0;
+  long long K = 0;
+  int bad = usable ? 0 : 1;
+  if (usable)
+    for (uint64_t j = lo + threadIdx.x; j < hi; j += blockDim.x) {
+      long long k;
+      if (int_step(p[j], u, k)) K += k;
+      else bad = 1;
+    }
+  for (int o = 16; o > 0; o >>= 1) {
+    K += __shfl_down_sync(0xffffffffu, K, o);
+    bad |= __shfl_down_sync(0xffffffffu, bad, o);
+  }
+  const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+  if (l == 0) {
+    shk[w] = K;
+    shb[w] = bad;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    long long t = 0;
+    int b = 0;
+    for (int i = 0; i < (int)(blockDim.x >> 5); ++i) {
+      t += shk[i];
+      b |= shb[i];
+    }
+    info[blockIdx.x] = ChunkInfo{t, e, !b};
+  }
+}
+
+__device__ __forceinline__ long long warp_incl_scan_ll(long long v) {
+  const int l = threadIdx.x & 31;
+  for (int o = 1; o < 32; o <<= 1) {
+    const long long t = __shfl_up_sync(0xffffffffu, v, o);
+    if (l >= o) v += t;
+  }
+  return v;
+}
+
+// Phase C: one warp walks the chunks in order.
+__global__ void k_sequential(const double* __restrict__ p, uint64_t n, uint64_t C, uint32_t nc,
+                             const ChunkInfo* __restrict__ info, double* __restrict__ start,
+                             unsigned char* __restrict__ fast, double* __restrict__ cum, double* __restrict__ total) {
+  const int lane = threadIdx.x & 31;
+  double A = 0.0;
+  const double kMinNormalScaled = 2.2250738585072014e-308 * 4503599627370496.0;
+  for (uint32_t c = 0; c < nc; ++c) {
+    const ChunkInfo ci = info[c];
+    const uint64_t lo = (uint64_t)c * C, hi = min(n, lo + C);
+    if (ci.clean && A >= kMinNormalScaled && ilogb(A) == ci.e) {
+      const double u = ldexp(1.0, ci.e - 52);
+      const long long a = (long long)(A / u);
+      if (a + ci.K < 9007199254740991LL) {  // stays below 2^53: no binade exit
+        if (lane == 0) {
+          start[c] = A;
+          fast[c] = 1;
+        }
+        A = (double)(a + ci.K) * u;
+        continue;
+      }
+    }
+    if (lane == 0) fast[c] = 0;
+    for (uint64_t j0 = lo; j0 < hi; j0 += 32) {
+      const uint64_t j = j0 + lane;
+      const double pj = j < hi ? p[j] : 0.0;
+      bool done = false;
+      if (A >= kMinNormalScaled) {
+        const double u = ldexp(1.0, ilogb(A) - 52);
+        long long k = 0;
+        const bool ok = int_step(pj, u, k);
+        if (__all_sync(0xffffffffu, ok)) {
+          const long long incl = warp_incl_scan_ll(k);
+          const long long Ksum = __shfl_sync(0xffffffffu, incl, 31);
+          const long long a = (long long)(A / u);
+          if (a + Ksum < 9007199254740991LL) {
+            if (j < hi) cum[j] = (double)(a + incl) * u;
+            A = (double)(a + Ksum) * u;
+            done = true;
+          }
+        }
+      }
+      if (!done) {
+        double acc = A;
+        for (int t = 0; t < 32; ++t) {
+          const double pt = __shfl_sync(0xffffffffu, pj, t);
+          if (j0 + t < hi) {
+            acc = __dadd_rn(acc, pt);
+            if (lane == t) cum[j] = acc;
+          }
+        }
+        A = acc;
+      }
+    }
+  }
+  if (lane == 0) *total = A;
+}
+
+// Phase D: expand clean chunks in parallel (block per chunk).
+__global__ void __launch_bounds__(kThreads) k_expand(const double* __restrict__ p, uint64_t n, uint64_t C,
+                                                     const ChunkInfo* __restrict__ info,
+                                                     const double* __restrict__ start,
+                                                     const unsigned char* __restrict__ fast, double* __restrict__ cum) {
+  if (!fast[blockIdx.x]) return;
+  __shared__ long long warp_tot[kThreads / 32];
+  const ChunkInfo ci = info[blockIdx.x];
+  const double u = ldexp(1.0, ci.e - 52);
+  long long carry = (long long)(start[blockIdx.x] / u);
+  const uint64_t lo = blockIdx.x * C, hi = min(n, lo + C);
+  const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+  for (uint64_t base = lo; base < hi; base += blockDim.x) {
+    const uint64_t j = base + threadIdx.x;
+    long long k = 0;
+    if (j < hi) int_step(p[j], u, k);
+    const long long incl = warp_incl_scan_ll(k);
+    if (l == 31) warp_tot[w] = incl;
+    __syncthreads();
+    long long before = 0, all = 0;
+    for (int i = 0; i < (int)(blockDim.x >> 5); ++i) {
+      if (i < w) before += warp_tot[i];
+      all += warp_tot[i];
+    }
+    if (j < hi) cum[j] = (double)(carry + before + incl) * u;
+    carry += all;
+    __syncthreads();
+  }
+}
+
+// Plain parallel scan for the fast (non-exact) mode: per-chunk serial sums in
+// a block + the estimated chunk offsets.
+__global__ void __launch_bounds__(kThreads) k_expand_approx(const double* __restrict__ p, uint64_t n, uint64_t C,
+                                                            const double* __restrict__ E, double* __restrict__ cum) {
+  __shared__ double warp_tot[kThreads / 32];
+  double carry = E[blockIdx.x];
+  const uint64_t lo = blockIdx.x * C, hi = min(n, lo + C);
+  const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+  for (uint64_t base = lo; base < hi; base += blockDim.x) {
+    const uint64_t j = base + threadIdx.x;
+    double v = j < hi ? p[j] : 0.0;
+    for (int o = 1; o < 32; o <<= 1) {
+      const double t = __shfl_up_sync(0xffffffffu, v, o);
+      if (l >= o) v += t;
+    }
+    if (l == 31) warp_tot[w] = v;
+    __syncthreads();
+    double before = 0, all = 0;
+    for (int i = 0; i < (int)(blockDim.x >> 5); ++i) {
+      if (i < w) before += warp_tot[i];
+      all += warp_tot[i];
+    }
+    if (j < hi) cum[j] = carry + before + v;
+    carry += all;
+    __syncthreads();
+  }
+}
+
+// upper-bound binary search of u * total (statevector.hpp:554-565)
+__global__ void __launch_bounds__(kThreads) k_search(const double* __restrict__ cum, uint64_t size,
+                                                     const double* __restrict__ total_p, const double* __restrict__ u,
+                                                     uint64_t shots, unsigned long long* __restrict__ out) {
+  const double total = *total_p;
+  for (uint64_t s = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; s < shots; s += (uint64_t)gridDim.x * blockDim.x) {
+    const double target = u[s] * total;
+    uint64_t lo = 0, hi = size - 1;
+    while (lo < hi) {
+      const uint64_t mid = (lo + hi) / 2;
+      if (cum[mid] > target) hi = mid;
+      else lo = mid + 1;
+    }
+    out[s] = lo;
+  }
+}
+
+// ---------------------------------------------------------- expectation
+__global__ void __launch_bounds__(kThreads) k_pauli(const double2* __restrict__ a, uint64_t size, uint64_t xmask,
+                                                    uint64_t smask, double2* __restrict__ partial) {
+  __shared__ double sh[kThreads / 32];
+  const uint64_t chunk = (size + gridDim.x - 1) / gridDim.x;
+  const uint64_t lo = blockIdx.x * chunk, hi = min(size, lo + chunk);
+  double re = 0, im = 0;
+  for (uint64_t j = lo + threadIdx.x; j < hi; j += blockDim.x) {
+    const double2 x = a[j];
+    const double2 y = xmask ? a[j ^ xmask] : x;
+    // conj(y) * x * sign(j)
+    double pr = fma(y.x, x.x, y.y * x.y);
+    double pi = fma(y.x, x.y, -y.y * x.x);
+    if (__popcll(j & smask) & 1) {
+      pr = -pr;
+      pi = -pi;
+    }
+    re += pr;
+    im += pi;
+  }
+  const double tr = block_sum(re, sh);
+  const double ti = block_sum(im, sh);
+  if (threadIdx.x == 0) partial[blockIdx.x] = make_double2(tr, ti);
+}
+
+__global__ void k_finalize2(const double2* __restrict__ partial, int count, double2* __restrict__ out) {
+  __shared__ double sh[kThreads / 32];
+  double re = 0, im = 0;
+  for (int i = threadIdx.x; i < count; i += blockDim.x) {
+    re += partial[i].x;
+    im += partial[i].y;
+  }
+  const double tr = block_sum(re, sh);
+  const double ti = block_sum(im, sh);
+  if (threadIdx.x == 0) *out = make_double2(tr, ti);
+}
+
+inline double2 d2(cd c) { return make_double2(c.real(), c.imag()); }
+
+}  // namespace
+
+// ------------------------------------------------------------ launchers
+
+void launch_op(State& s, const Op& op) {
+  DeviceGuard dg(s.device);
+  const uint32_t n = s.n;
+  switch (op.kind) {
+    case OpKind::Identity: return;
+    case OpKind::Mat1: {
+      const Slots sl = make_slots(op.targets, op.controls);
+      const uint64_t groups = 1ull << (n - sl.count);
+      k_mat1<<<grid_for(groups, s.device), kThreads, 0, s.stream>>>(
+          s.amps, groups, sl, 1ull << op.targets[0], d2(op.m[0]), d2(op.m[1]), d2(op.m[2]), d2(op.m[3]));
+      QSB_LAUNCHED();
+      return;
+    }
+    case OpKind::Diag: {
+      const bool skip_zero = op.m[0] == cd(1.0);  // statevector.hpp:296
+      std::vector<uint32_t> ctrls = op.controls;
+      std::vector<uint32_t> targs;
+      if (skip_zero) ctrls.push_back(op.targets[0]);
+      else targs.push_back(op.targets[0]);
+      const Slots sl = make_slots(targs, ctrls);
+      const uint64_t groups = 1ull << (n - sl.count);
+      k_diag<<<grid_for(groups, s.device), kThreads, 0, s.stream>>>(s.amps, groups, sl, 1ull << op.targets[0],
+                                                                      d2(op.m[0]), d2(op.m[1]), skip_zero ? 1 : 0);
+      QSB_LAUNCHED();
+      return;
+    }
+    case OpKind::Flip: {
+      const Slots sl = make_slots(op.targets, op.controls);
+      const uint64_t groups = 1ull << (n - sl.count);
+      k_flip<<<grid_for(groups, s.device), kThreads, 0, s.stream>>>(s.amps, groups, sl, 1ull << op.targets[0]);
+      QSB_LAUNCHED();
+      return;
+    }
+    case OpKind::Swap: {
+      const Slots sl = make_slots(op.targets, op.controls);
+      const uint64_t groups = 1ull << (n - sl.count);
+      k_swap<<<grid_for(groups, s.device), kThreads, 0, s.stream>>>(s.amps, groups, sl, 1ull << op.targets[0],
+                                                                      1ull << op.targets[1]);
+      QSB_LAUNCHED();
+      return;
+    }
+    case OpKind::Dense: {
+      const int K = static_cast<int>(op.targets.size());
+      const Slots sl = make_slots(op.targets, op.controls);
+      const uint64_t groups = 1ull << (n - sl.count);
+      TargetMasks tm{};
+      for (int b = 0; b < K; ++b) tm.m[b] = 1ull << op.targets[K - 1 - b];
+      const size_t dim = size_t(1) << K;
+      double2* dM = static_cast<double2*>(s.get_scratch(dim * dim * sizeof(double2)));
+      std::vector<double2> hm(dim * dim);
+      for (size_t i = 0; i < dim * dim; ++i) hm[i] = d2(op.m[i]);
+      QSB_CUDA(cudaMemcpyAsync(dM, hm.data(), dim * dim * sizeof(double2), cudaMemcpyHostToDevice, s.stream));
+      const uint64_t work = groups << K;
+      switch (K) {
+        case 2: k_dense<2><<<grid_for(work, s.device), kThreads, 0, s.stream>>>(s.amps, groups, sl, tm, dM); break;
+        case 3: k_dense<3><<<grid_for(work, s.device), kThreads, 0, s.stream>>>(s.amps, groups, sl, tm, dM); break;
+        case 4: k_dense<4><<<grid_for(work, s.device), kThreads, 0, s.stream>>>(s.amps, groups, sl, tm, dM); break;
+        case 5: k_dense<5><<<grid_for(work, s.device, 4), kThreads, 0, s.stream>>>(s.amps, groups, sl, tm, dM); break;
+        default: {
+          const uint32_t blocks = static_cast<uint32_t>(std::min<uint64_t>(groups, num_sms(s.device) * 8ull));
+          k_dense_wide<<<blocks, kThreads, dim * sizeof(double2), s.stream>>>(s.amps, groups, sl, tm, K, dM);
+        }
+      }
+      QSB_LAUNCHED();
+      // the host staging vector must outlive the async copy
+      QSB_CUDA(cudaStreamSynchronize(s.stream));
+      return;
+    }
+  }
+}
+
+void fill_basis(State& s, uint64_t index) {
+  DeviceGuard dg(s.device);
+  k_basis<<<grid_for(s.size, s.device), kThreads, 0, s.stream>>>(s.amps, s.size, index);
+  QSB_LAUNCHED();
+}
+
+namespace {
+double reduce_mode(State& s, int mode, uint32_t q) {
+  DeviceGuard dg(s.device);
+  double* part = static_cast<double*>(s.get_scratch((kRedBlocks + 1) * sizeof(double)));
+  const uint64_t items = mode == 1 ? s.size / 2 : s.size;
+  k_reduce<<<kRedBlocks, kThreads, 0, s.stream>>>(s.amps, items, mode, 1ull << q, part);
+  QSB_LAUNCHED();
+  k_finalize<<<1, kThreads, 0, s.stream>>>(part, kRedBlocks, part + kRedBlocks);
+  QSB_LAUNCHED();
+  double* h = static_cast<double*>(s.get_pinned(sizeof(double)));
+  QSB_CUDA(cudaMemcpyAsync(h, part + kRedBlocks, sizeof(double), cudaMemcpyDeviceToHost, s.stream));
+  QSB_CUDA(cudaStreamSynchronize(s.stream));
+  return *h;
+}
+}  // namespace
+
+double reduce_norm2(State& s) { return reduce_mode(s, 0, 0); }
+double reduce_prob_one(State& s, uint32_t q) { return reduce_mode(s, 1, q); }
+double reduce_checksum(State& s) { return reduce_mode(s, 2, 0); }
+
+void marginal_probs(State& s, const uint32_t* qubits, uint32_t m, double* host_out) {
+  DeviceGuard dg(s.device);
+  std::vector<uint32_t> qs(qubits, qubits + m);
+  const Slots sl = make_slots(qs, {});
+  const uint64_t per_bin = 1ull << (s.n - m);
+  const uint64_t bins = 1ull << m;
+  const size_t out_bytes = bins * sizeof(double);
+  if (m <= 12) {
+    const uint32_t per = static_cast<uint32_t>(std::max<uint64_t>(1, std::min<uint64_t>(kRedBlocks / bins + 1, per_bin)));
+    char* scr = static_cast<char*>(s.get_scratch(256 + m * 4 + bins * per * sizeof(double) + out_bytes));
+    uint32_t* dq = reinterpret_cast<uint32_t*>(scr);
+    double* part = reinterpret_cast<double*>(scr + 256);
+    double* dout = part + bins * per;
+    QSB_CUDA(cudaMemcpyAsync(dq, qubits, m * 4, cudaMemcpyHostToDevice, s.stream));
+    k_marginal<<<dim3(per, static_cast<uint32_t>(bins)), kThreads, 0, s.stream>>>(s.amps, per_bin, sl, dq, m, part);
+    QSB_LAUNCHED();
+    k_marginal_finalize<<<static_cast<uint32_t>((bins + 255) / 256), 256, 0, s.stream>>>(part, per,
+                                                                                         static_cast<uint32_t>(bins), dout);
+    QSB_LAUNCHED();
+    QSB_CUDA(cudaMemcpyAsync(host_out, dout, out_bytes, cudaMemcpyDeviceToHost, s.stream));
+  } else {
+    char* scr = static_cast<char*>(s.get_scratch(256 + out_bytes));
+    uint32_t* dq = reinterpret_cast<uint32_t*>(scr);
+    double* dout = reinterpret_cast<double*>(scr + 256);
+    QSB_CUDA(cudaMemcpyAsync(dq, qubits, m * 4, cudaMemcpyHostToDevice, s.stream));
+    k_marginal_wide<<<grid_for(bins, s.device), kThreads, 0, s.stream>>>(s.amps, per_bin, sl, dq, m, dout);
+    QSB_LAUNCHED();
+    QSB_CUDA(cudaMemcpyAsync(host_out, dout, out_bytes, cudaMemcpyDeviceToHost, s.stream));
+  }
+  QSB_CUDA(cudaStreamSynchronize(s.stream));
+}
+
+void full_probs(State& s, double* host_out, uint64_t offset, uint64_t count) {
+  DeviceGuard dg(s.device);
+  const uint64_t step = 1ull << 26;  // bounded scratch
+  for (uint64_t done = 0; done < count; done += step) {
+    const uint64_t c = std::min(step, count - done);
+    double* dp = static_cast<double*>(s.get_scratch(c * sizeof(double)));
+    k_probs<<<grid_for(c, s.device), kThreads, 0, s.stream>>>(s.amps, offset + done, c, dp);
+    QSB_LAUNCHED();
+    QSB_CUDA(cudaMemcpyAsync(host_out + done, dp, c * sizeof(double), cudaMemcpyDeviceToHost, s.stream));
+    QSB_CUDA(cudaStreamSynchronize(s.stream));
+  }
+}
+
+void collapse(State& s, uint32_t q, int outcome, double inv) {
+  DeviceGuard dg(s.device);
+  k_collapse<<<grid_for(s.size, s.device), kThreads, 0, s.stream>>>(s.amps, s.size, 1ull << q, outcome, inv);
+  QSB_LAUNCHED();
+}
+
+void scale(State& s, double re, double im) {
+  DeviceGuard dg(s.device);
+  k_scale<<<grid_for(s.size, s.device), kThreads, 0, s.stream>>>(s.amps, s.size, make_double2(re, im));
+  QSB_LAUNCHED();
+}
+
+namespace {
+struct SamplerBuffers {
+  double* p;
+  double* cum;
+  double* S;
+  double* E;
+  ChunkInfo* info;
+  double* start;
+  unsigned char* fast;
+  double* total;
+  uint64_t C;
+  uint32_t nc;
+};
+
+SamplerBuffers sampler_buffers(State& s, uint64_t extra_bytes, char** extra) {
+  SamplerBuffers b{};
+  const uint64_t N = s.size;
+  b.C = std::max<uint64_t>(1024, N / 16384);
+  b.nc = static_cast<uint32_t>((N + b.C - 1) / b.C);
+  auto al = [](uint64_t x) { return (x + 255) & ~uint64_t(255); };
+  const uint64_t bytes = al(N * 8) * 2 + al(b.nc * 8) * 3 + al(b.nc * sizeof(ChunkInfo)) + al(b.nc) + 256 + al(extra_bytes);
+  char* base = static_cast<char*>(s.get_scratch(bytes));
+  char* q = base;
+  auto take = [&](uint64_t sz) {
+    char* r = q;
+    q += al(sz);
+    return r;
+  };
+  b.p = reinterpret_cast<double*>(take(N * 8));
+  b.cum = reinterpret_cast<double*>(take(N * 8));
+  b.S = reinterpret_cast<double*>(take(b.nc * 8));
+  b.E = reinterpret_cast<double*>(take(b.nc * 8));
+  b.start = reinterpret_cast<double*>(take(b.nc * 8));
+  b.info = reinterpret_cast<ChunkInfo*>(take(b.nc * sizeof(ChunkInfo)));
+  b.fast = reinterpret_cast<unsigned char*>(take(b.nc));
+  b.total = reinterpret_cast<double*>(take(256));
+  *extra = take(extra_bytes);
+  return b;
+}
+
+void build_cumulative(State& s, SamplerBuffers& b, bool exact) {
+  const uint64_t N = s.size;
+  k_probs<<<grid_for(N, s.device), kThreads, 0, s.stream>>>(s.amps, 0, N, b.p);
+  QSB_LAUNCHED();
+  k_chunk_sum<<<b.nc, kThreads, 0, s.stream>>>(b.p, N, b.C, b.S);
+  QSB_LAUNCHED();
+  k_scan_estimate<<<1, 32, 0, s.stream>>>(b.S, b.nc, b.E);
+  QSB_LAUNCHED();
+  if (exact) {
+    k_chunk_ints<<<b.nc, kThreads, 0, s.stream>>>(b.p, N, b.C, b.E, b.info);
+    QSB_LAUNCHED();
+    k_sequential<<<1, 32, 0, s.stream>>>(b.p, N, b.C, b.nc, b.info, b.start, b.fast, b.cum, b.total);
+    QSB_LAUNCHED();
+    k_expand<<<b.nc, kThreads, 0, s.stream>>>(b.p, N, b.C, b.info, b.start, b.fast, b.cum);
+    QSB_LAUNCHED();
+  } else {
+    k_expand_approx<<<b.nc, kThreads, 0, s.stream>>>(b.p, N, b.C, b.E, b.cum);
+    QSB_LAUNCHED();
+    QSB_CUDA(cudaMemcpyAsync(b.total, b.cum + (N - 1), sizeof(double), cudaMemcpyDeviceToDevice, s.stream));
+  }
+}
+}  // namespace
+
+double exact_cumulative(State& s, double* d_probs, double* d_cum) {
+  DeviceGuard dg(s.device);
+  char* extra;
+  SamplerBuffers b = sampler_buffers(s, 0, &extra);
+  build_cumulative(s, b, true);
+  QSB_CUDA(cudaMemcpyAsync(d_cum, b.cum, s.size * 8, cudaMemcpyDeviceToDevice, s.stream));
+  if (d_probs) QSB_CUDA(cudaMemcpyAsync(d_probs, b.p, s.size * 8, cudaMemcpyDeviceToDevice, s.stream));
+  double* h = static_cast<double*>(s.get_pinned(8));
+  QSB_CUDA(cudaMemcpyAsync(h, b.total, 8, cudaMemcpyDeviceToHost, s.stream));
+  QSB_CUDA(cudaStreamSynchronize(s.stream));
+  return *h;
+}
+
+void sample(State& s, const double* uniforms_host, uint64_t shots, bool exact, uint64_t* out_host) {
+  DeviceGuard dg(s.device);
+  if (shots == 0) return;
+  char* extra;
+  SamplerBuffers b = sampler_buffers(s, shots * 16, &extra);
+  double* du = reinterpret_cast<double*>(extra);
+  unsigned long long* dout = reinterpret_cast<unsigned long long*>(extra + shots * 8);
+  build_cumulative(s, b, exact);
+  QSB_CUDA(cudaMemcpyAsync(du, uniforms_host, shots * 8, cudaMemcpyHostToDevice, s.stream));
+  k_search<<<grid_for(shots, s.device), kThreads, 0, s.stream>>>(b.cum, s.size, b.total, du, shots, dout);
+  QSB_LAUNCHED();
+  QSB_CUDA(cudaMemcpyAsync(out_host, dout, shots * 8, cudaMemcpyDeviceToHost, s.stream));
+  QSB_CUDA(cudaStreamSynchronize(s.stream));
+}
+
+void expect_pauli(State& s, const std::vector<uint64_t>& xmask, const std::vector<uint64_t>& smask,
+                  const std::vector<int>& ny, double* out) {
+  DeviceGuard dg(s.device);
+  const size_t T = xmask.size();
+  double2* part = static_cast<double2*>(s.get_scratch((kRedBlocks + T) * sizeof(double2)));
+  double2* res = part + kRedBlocks;
+  for (size_t t = 0; t < T; ++t) {
+    k_pauli<<<kRedBlocks, kThreads, 0, s.stream>>>(s.amps, s.size, xmask[t], smask[t], part);
+    QSB_LAUNCHED();
+    k_finalize2<<<1, kThreads, 0, s.stream>>>(part, kRedBlocks, res + t);
+    QSB_LAUNCHED();
+  }
+  std::vector<double2> h(T);
+  QSB_CUDA(cudaMemcpyAsync(h.data(), res, T * sizeof(double2), cudaMemcpyDeviceToHost, s.stream));
+  QSB_CUDA(cudaStreamSynchronize(s.stream));
+  for (size_t t = 0; t < T; ++t) {
+    // multiply by i^ny
+    double re = h[t].x, im = h[t].y;
+    for (int k = 0; k < (ny[t] & 3); ++k) {
+      const double r2 = -im, i2 = re;
+      re = r2;
+      im = i2;
+    }
+    out[2 * t] = re;
+    out[2 * t + 1] = im;
+  }
+}
+
+}  // namespace qsb

@@ -1,0 +1,37 @@
+// Launchers for the per-gate kernels, reductions, measurement and sampling
+// (kernels.cu).  All run on the state's stream; host-visible results are
+// synchronous on return.
+#pragma once
+
+#include <cstdint>
+#include <vector>
+
+#include "common.hpp"
+#include "gates.hpp"
+
+namespace qsb {
+
+// One HBM pass per op (the reference's per-gate kernels, statevector.hpp:268-467).
+void launch_op(State& s, const Op& op);
+
+void fill_basis(State& s, uint64_t index);                      // |index>
+double reduce_norm2(State& s);                                   // statevector.hpp:158-162
+double reduce_prob_one(State& s, uint32_t q);                    // :181-186
+double reduce_checksum(State& s);                                // bench.hpp:141-148
+void marginal_probs(State& s, const uint32_t* q, uint32_t m, double* host_out);  // :190-208
+void full_probs(State& s, double* host_out, uint64_t offset, uint64_t count);    // :210-215
+void collapse(State& s, uint32_t q, int outcome, double inv_sqrt_p);             // :228-247
+void scale(State& s, double re, double im);                                      // :164-166
+
+// BasisSampler (statevector.hpp:542-570) + draws.  exact: reproduce the serial
+// cumulative sum bit for bit (see kernels.cu, "serial-equivalent scan").
+void sample(State& s, const double* uniforms_host, uint64_t shots, bool exact, uint64_t* out_host);
+
+// <psi|P|psi> for Pauli strings given as (xmask, zmask, #Y) per term.
+void expect_pauli(State& s, const std::vector<uint64_t>& xmask, const std::vector<uint64_t>& zmask,
+                  const std::vector<int>& ny, double* out);
+
+// Exposed for tests of the exact scan (cum must hold s.size doubles on device).
+double exact_cumulative(State& s, double* d_probs, double* d_cum);
+
+}  // namespace qsb

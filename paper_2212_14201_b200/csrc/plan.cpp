@@ -1,0 +1,74 @@
+#include "plan.hpp"
+
+#include "fusion.hpp"
+#include "kernels.hpp"
+#include "tile.hpp"
+
+namespace qsb {
+
+uint64_t Plan::passes() const {
+  uint64_t p = 0;
+  for (const auto& s : steps)
+    if (s.kind == Step::TileStep || s.op.kind != OpKind::Identity) ++p;
+  return p;
+}
+
+uint64_t Plan::launches() const {
+  uint64_t l = 0;
+  for (const auto& s : steps) {
+    if (s.kind == Step::TileStep) l += 1;
+    else if (s.op.kind != OpKind::Identity) l += 1;
+  }
+  return l;
+}
+
+std::unique_ptr<Plan> make_plan(uint32_t n, const qs_gate* gates, uint64_t count, uint32_t mode,
+                                uint32_t max_fused_qubits) {
+  auto plan = std::make_unique<Plan>();
+  plan->n = n;
+  plan->mode = mode == QS_PLAN_DEFAULT ? QS_PLAN_TILED : mode;
+  plan->gates = count;
+  // validation first (validate_or_throw, circuit.hpp:523), in program order
+  for (uint64_t i = 0; i < count; ++i) validate_gate(gates[i], n);
+
+  std::vector<Op> ops;
+  ops.reserve(count);
+  if (plan->mode == QS_PLAN_DENSE_FUSION) {
+    if (max_fused_qubits < 1 || max_fused_qubits > 5) throw ValidationError("max_fused_qubits must be in [1, 5]");
+    std::vector<GateRec> fused = fuse_gate_run(gates, count, n, max_fused_qubits);
+    for (auto& r : fused) {
+      r.bind();
+      ops.push_back(lower_gate(r.g, n, /*validate=*/false));
+    }
+  } else {
+    for (uint64_t i = 0; i < count; ++i) {
+      Op op = lower_gate(gates[i], n, /*validate=*/false);
+      op.gate_index = i;
+      ops.push_back(std::move(op));
+    }
+  }
+  if (plan->mode == QS_PLAN_TILED) {
+    plan_tiles(n, ops, plan->steps);
+  } else {
+    for (auto& op : ops) {
+      if (op.kind == OpKind::Identity) continue;
+      Step s;
+      s.kind = Step::OpStep;
+      s.op = std::move(op);
+      plan->steps.push_back(std::move(s));
+    }
+  }
+  return plan;
+}
+
+void execute_plan(State& s, const Plan& p) {
+  if (p.n != s.n) throw ValidationError("plan was compiled for a different qubit count");
+  for (const auto& st : p.steps) execute_step(s, st);
+}
+
+void execute_step(State& s, const Step& st) {
+  if (st.kind == Step::OpStep) launch_op(s, st.op);
+  else launch_tile(s, *st.tile);
+}
+
+}  // namespace qsb

@@ -1,0 +1,38 @@
+// Execution plans: a circuit compiled once into a sequence of device steps.
+//   - OpStep: one per-gate kernel (one HBM pass), kernels.cu
+//   - TileStep: one shared-memory tile pass applying many gates, tile.cu
+#pragma once
+
+#include <cstdint>
+#include <memory>
+#include <vector>
+
+#include "common.hpp"
+#include "gates.hpp"
+
+namespace qsb {
+
+struct TileProgram;  // tile.hpp
+
+struct Step {
+  enum Kind { OpStep, TileStep } kind = OpStep;
+  Op op;                               // OpStep
+  std::shared_ptr<TileProgram> tile;   // TileStep
+};
+
+struct Plan {
+  uint32_t n = 0;
+  uint32_t mode = QS_PLAN_DEFAULT;
+  uint64_t gates = 0;     // submitted gate count
+  std::vector<Step> steps;
+  uint64_t passes() const;
+  uint64_t launches() const;
+};
+
+// Lowers and plans `count` gates for an n-qubit state.
+std::unique_ptr<Plan> make_plan(uint32_t n, const qs_gate* gates, uint64_t count, uint32_t mode,
+                                uint32_t max_fused_qubits);
+void execute_plan(State& s, const Plan& p);
+void execute_step(State& s, const Step& st);
+
+}  // namespace qsb

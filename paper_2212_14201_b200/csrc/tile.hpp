@@ -1,0 +1,103 @@
+// Shared-memory tile passes: many gates per HBM sweep.
+//
+// A pass picks a set S of m qubits (always containing the lowest L qubits, so
+// global loads stay coalesced).  The state splits into 2^(n-m) tiles, each the
+// 2^m amplitudes that share the values of the qubits outside S.  One CTA loads
+// a tile into registers (16 amplitudes per thread), applies every gate of the
+// pass whose non-diagonal targets lie in S, and writes the tile back: one HBM
+// read + write for the whole gate run.
+//
+// Inside the CTA, 4 "register qubits" are held in registers; gates act on
+// them with no data movement.  A TRANSPOSE micro-op permutes which tile qubits
+// are register qubits through shared memory (XOR-swizzled, bank-conflict
+// free).  Diagonal gates (RZ, Z, S, T, CZ, controlled phases) never need their
+// qubits in S or in registers: their phase is known per register slot, per
+// thread and per tile; runs of them merge into one PHASE micro-op.  Controls
+// are predicates on the same three index levels.  Uncontrolled SWAPs are
+// free relabels of the tile layout.
+//
+// Gate semantics follow StateVector::apply_gate (statevector.hpp:469-538);
+// the reference has no multi-gate kernel -- this replaces its one-pass-per-
+// gate loop (simulator.hpp:157-159) and its dense fusion (fusion.hpp:20-133).
+#pragma once
+
+#include <cstdint>
+#include <memory>
+#include <vector>
+
+#include "common.hpp"
+#include "gates.hpp"
+#include "plan.hpp"
+
+namespace qsb {
+
+constexpr int kTileR = 4;       // register bits: 16 amplitudes per thread
+constexpr int kTileMaxM = 13;   // tile qubits (2^13 x 16 B = 128 KiB of smem)
+constexpr int kTileMaxT = kTileMaxM - kTileR;
+
+enum TOpType : uint8_t {
+  TO_MAT1 = 1,     // general 2x2 on register bit k
+  TO_MAT1_REAL,    // real 2x2 (RY, H)
+  TO_MAT1_RX,      // real diagonal, imaginary off-diagonal (RX)
+  TO_FLIP,         // X / CNOT / TOFFOLI target on register bit k
+  TO_PHASE,        // diagonal: c * prod_q w_q^{b_q} under a predicate
+  TO_DENSE2,       // dense 4x4 on register bits 0..1
+  TO_DENSE3,       // dense 8x8 on register bits 0..2
+  TO_TRANSPOSE,    // register <-> thread qubit exchange through smem
+};
+
+struct TOp {
+  uint8_t type;
+  uint8_t k;        // register bit (MAT1 / FLIP)
+  uint16_t nlist;   // PHASE: number of non-register (qubit, w) factors
+  uint16_t rmask;   // predicate on the register index p: (p & rmask) == rval
+  uint16_t rval;
+  unsigned long long gmask;  // predicate on the thread's global index bits
+  unsigned long long gval;
+  uint32_t coef;    // offset into the coefficient table (double2 units)
+  uint32_t meta;    // offset into the metadata table (uint32 units)
+};
+
+// Per-config data for global addressing: thread bit k holds qubit tq[k];
+// register bit k holds qubit with stride rs[k].
+struct TileConfigAddr {
+  uint32_t tq[kTileMaxT];
+  unsigned long long rs[kTileR];
+};
+
+struct TileHeader {
+  uint32_t n, m, t, nops;
+  uint32_t S[kTileMaxM];  // tile qubits, ascending
+  TileConfigAddr load, store;
+  uint32_t ops_off, meta_off, coef_off, bytes;
+  unsigned long long ntiles;
+};
+
+struct TileProgram {
+  TileHeader h{};
+  std::vector<TOp> ops;
+  std::vector<uint32_t> meta;
+  std::vector<double2> coef;
+  uint64_t gates = 0;       // source ops covered
+  uint32_t transposes = 0;
+  std::vector<uint64_t> source;  // gate indices, for diagnostics
+  // device copy (per device)
+  mutable void* dev = nullptr;
+  mutable int dev_id = -1;
+  ~TileProgram();
+  void upload(int device) const;
+};
+
+struct TileOptions {
+  uint32_t m = 12;  // tile qubits
+  uint32_t low = 3; // qubits 0..low-1 always in the tile (coalescing)
+};
+TileOptions tile_options_from_env();
+
+void plan_tiles(uint32_t n, std::vector<Op>& ops, std::vector<Step>& steps, const TileOptions& opt);
+inline void plan_tiles(uint32_t n, std::vector<Op>& ops, std::vector<Step>& steps) {
+  plan_tiles(n, ops, steps, tile_options_from_env());
+}
+void launch_tile(State& s, const TileProgram& tp);
+
+}  // namespace qsb

@@ -1,0 +1,687 @@
+// Tile-pass planner (host): partitions a gate list into shared-memory tile
+// passes and compiles each pass into a micro-program for tile.cu.
+#include <algorithm>
+#include <cmath>
+#include <cstdlib>
+#include <cstring>
+#include <map>
+#include <random>
+
+#include "tile.hpp"
+
+namespace qsb {
+
+namespace {
+
+inline uint64_t bit(uint32_t q) { return 1ull << q; }
+
+enum class PK { Mat1, Flip, Diag, SwapRel, Dense, Opaque };
+
+// A kernel-level op with its planning attributes.
+struct POp {
+  PK k;
+  Op op;
+  uint64_t qmask = 0;     // every operand
+  uint64_t needmask = 0;  // qubits that must be tile qubits (non-diagonal targets)
+};
+
+std::vector<POp> preprocess(std::vector<Op>& ops) {
+  std::vector<POp> out;
+  out.reserve(ops.size());
+  auto push = [&](PK k, Op op) {
+    POp p;
+    p.k = k;
+    for (auto q : op.controls) p.qmask |= bit(q);
+    for (auto q : op.targets) p.qmask |= bit(q);
+    switch (k) {
+      case PK::Mat1:
+      case PK::Flip:
+      case PK::SwapRel:
+      case PK::Dense:
+        for (auto q : op.targets) p.needmask |= bit(q);
+        break;
+      default: break;
+    }
+    p.op = std::move(op);
+    out.push_back(std::move(p));
+  };
+  for (auto& op : ops) {
+    switch (op.kind) {
+      case OpKind::Identity: break;
+      case OpKind::Mat1:
+        if (op.m[1] == cd(0) && op.m[2] == cd(0)) {  // diagonal 2x2 (e.g. U3(0,0,l))
+          Op d = op;
+          d.kind = OpKind::Diag;
+          d.m = {op.m[0], op.m[3]};
+          push(PK::Diag, std::move(d));
+        } else {
+          push(PK::Mat1, std::move(op));
+        }
+        break;
+      case OpKind::Flip: push(PK::Flip, std::move(op)); break;
+      case OpKind::Diag: push(PK::Diag, std::move(op)); break;
+      case OpKind::Swap:
+        if (op.controls.empty()) {
+          push(PK::SwapRel, std::move(op));
+        } else {
+          // Fredkin: CNOT(b->a) . CCNOT(C + a -> b) . CNOT(b->a)
+          const uint32_t a = op.targets[0], b = op.targets[1];
+          Op f1;
+          f1.kind = OpKind::Flip;
+          f1.targets = {a};
+          f1.controls = {b};
+          f1.gate_index = op.gate_index;
+          Op f2 = f1;
+          f2.targets = {b};
+          f2.controls = op.controls;
+          f2.controls.push_back(a);
+          push(PK::Flip, f1);
+          push(PK::Flip, f2);
+          push(PK::Flip, f1);
+        }
+        break;
+      case OpKind::Dense:
+        if (op.targets.size() <= 3) push(PK::Dense, std::move(op));
+        else push(PK::Opaque, std::move(op));
+        break;
+    }
+  }
+  return out;
+}
+
+// Ops of `rem` executable in one pass with tile set S, in program order; an op
+// not executable blocks its qubits for every later op.
+size_t scan(const std::vector<POp>& pops, const std::vector<uint32_t>& rem, uint64_t S, std::vector<char>* taken) {
+  uint64_t blocked = 0;
+  size_t cnt = 0;
+  for (size_t i = 0; i < rem.size(); ++i) {
+    const POp& p = pops[rem[i]];
+    if ((p.qmask & blocked) || p.k == PK::Opaque || (p.needmask & ~S)) {
+      blocked |= p.qmask;
+      continue;
+    }
+    ++cnt;
+    if (taken) (*taken)[i] = 1;
+  }
+  return cnt;
+}
+
+struct Cfg {
+  int reg[kTileR];
+  int thr[kTileMaxT];
+};
+
+// Abstract micro-op before finalisation.
+struct AOp {
+  uint8_t type = 0;
+  int cfg = 0;              // config index at this op
+  uint32_t target = 0;      // MAT1 / FLIP qubit
+  std::vector<uint32_t> dense_targets;
+  uint64_t pred = 0;        // control qubits (all must be 1)
+  cd m[4];
+  std::vector<cd> dense;    // row-major
+  // PHASE
+  cd c = 1.0;
+  std::map<uint32_t, cd> w;
+  // TRANSPOSE
+  int from = 0, to = 0;
+};
+
+struct Compiler {
+  uint32_t n, m, t, L;
+  std::vector<uint32_t> S;
+  int tb[64];
+  std::vector<Cfg> cfgs;
+  std::vector<AOp> aops;
+
+  bool has_reg(const Cfg& c, int x, int* pos = nullptr) const {
+    for (int k = 0; k < kTileR; ++k)
+      if (c.reg[k] == x) {
+        if (pos) *pos = k;
+        return true;
+      }
+    return false;
+  }
+
+  // Fill thread bits: lanes 0..L-1 take tile bits 0..L-1 when those are not
+  // register bits; the rest ascending.
+  void fill_threads(Cfg& c) const {
+    std::vector<char> used(m, 0);
+    for (int k = 0; k < kTileR; ++k) used[c.reg[k]] = 1;
+    for (uint32_t k = 0; k < t; ++k) c.thr[k] = -1;
+    for (uint32_t k = 0; k < L; ++k)
+      if (!used[k]) {
+        c.thr[k] = static_cast<int>(k);
+        used[k] = 1;
+      }
+    uint32_t next = 0;
+    for (uint32_t k = 0; k < t; ++k) {
+      if (c.thr[k] >= 0) continue;
+      while (used[next]) ++next;
+      c.thr[k] = static_cast<int>(next);
+      used[next] = 1;
+    }
+  }
+
+  bool store_ok(const Cfg& c) const {
+    for (uint32_t k = 0; k < L; ++k)
+      if (c.thr[k] != static_cast<int>(k)) return false;
+    return true;
+  }
+
+  // Register requirement of op i: exact positions for DENSE, else one tile bit.
+  static bool needs_reg(const POp& p) { return p.k == PK::Mat1 || p.k == PK::Flip || p.k == PK::Dense; }
+
+  // Belady choice of the register set at op index `at` of the pass list.
+  Cfg choose(const Cfg* cur, const std::vector<const POp*>& list, size_t at, bool exclude_low) {
+    Cfg c;
+    for (int k = 0; k < kTileR; ++k) c.reg[k] = -1;
+    std::vector<char> placed(m, 0);
+    const POp& p = *list[at];
+    if (p.k == PK::Dense) {
+      const size_t kd = p.op.targets.size();
+      for (size_t b = 0; b < kd; ++b) {
+        const int x = tb[p.op.targets[kd - 1 - b]];
+        c.reg[b] = x;
+        placed[x] = 1;
+      }
+    } else {
+      const int x = tb[p.op.targets[0]];
+      int pos;
+      if (cur && has_reg(*cur, x, &pos)) c.reg[pos] = x;
+      else
+        for (int k = 0; k < kTileR; ++k)
+          if (c.reg[k] < 0) {
+            c.reg[k] = x;
+            break;
+          }
+      placed[x] = 1;
+    }
+    // next use of every tile bit from `at`
+    std::vector<size_t> next(m, SIZE_MAX);
+    for (size_t j = at; j < list.size(); ++j) {
+      const POp& q = *list[j];
+      if (!needs_reg(q)) continue;
+      for (auto tq : q.op.targets) {
+        const int x = tb[tq];
+        if (next[x] == SIZE_MAX) next[x] = j;
+      }
+    }
+    for (int k = 0; k < kTileR; ++k) {
+      if (c.reg[k] >= 0) continue;
+      // keep the current occupant when it is still useful
+      int best = -1;
+      if (cur) {
+        const int y = cur->reg[k];
+        if (y >= 0 && !placed[y] && next[y] != SIZE_MAX && !(exclude_low && y < static_cast<int>(L))) best = y;
+      }
+      if (best < 0) {
+        size_t bn = SIZE_MAX;
+        for (uint32_t y = 0; y < m; ++y) {
+          if (placed[y] || (exclude_low && y < L)) continue;
+          const size_t ny = next[y];
+          const bool better = best < 0 || ny < bn || (ny == bn && y >= L && best < static_cast<int>(L));
+          if (better) {
+            best = static_cast<int>(y);
+            bn = ny;
+          }
+        }
+      }
+      if (best < 0)  // everything placed (tiny tiles): any free bit
+        for (uint32_t y = 0; y < m; ++y)
+          if (!placed[y]) {
+            best = static_cast<int>(y);
+            break;
+          }
+      c.reg[k] = best;
+      placed[best] = 1;
+    }
+    fill_threads(c);
+    return c;
+  }
+
+  void transpose_to(int& cur, const Cfg& next) {
+    cfgs.push_back(next);
+    AOp a;
+    a.type = TO_TRANSPOSE;
+    a.from = cur;
+    a.to = static_cast<int>(cfgs.size() - 1);
+    a.cfg = a.to;
+    aops.push_back(a);
+    cur = a.to;
+  }
+
+  bool satisfied(const Cfg& c, const POp& p) const {
+    if (p.k == PK::Dense) {
+      const size_t kd = p.op.targets.size();
+      for (size_t b = 0; b < kd; ++b)
+        if (c.reg[b] != tb[p.op.targets[kd - 1 - b]]) return false;
+      return true;
+    }
+    return has_reg(c, tb[p.op.targets[0]]);
+  }
+
+  void compile(const std::vector<const POp*>& list) {
+    // initial (load) config: coalesced, registers from the first needs
+    size_t first = list.size();
+    for (size_t i = 0; i < list.size(); ++i)
+      if (needs_reg(*list[i])) {
+        first = i;
+        break;
+      }
+    Cfg c0;
+    if (first < list.size() && list[first]->k != PK::Dense) {
+      c0 = choose(nullptr, list, first, /*exclude_low=*/true);
+      // choose() may have placed a low bit as the required target: that op
+      // then simply transposes first.
+      bool bad = false;
+      for (int k = 0; k < kTileR; ++k)
+        if (c0.reg[k] < static_cast<int>(L)) bad = true;
+      if (bad) c0 = default_cfg();
+    } else {
+      c0 = default_cfg();
+    }
+    cfgs.push_back(c0);
+    int cur = 0;
+
+    int open = -1;           // open PHASE aop
+    uint64_t x_open = 0;     // non-diagonal targets since it opened
+    for (size_t i = 0; i < list.size(); ++i) {
+      const POp& p = *list[i];
+      uint64_t ctrl = 0;
+      for (auto q : p.op.controls) ctrl |= bit(q);
+      switch (p.k) {
+        case PK::Diag: {
+          const uint32_t tq = p.op.targets[0];
+          const cd d0 = p.op.m[0], d1 = p.op.m[1];
+          const uint64_t qm = ctrl | bit(tq);
+          struct Rep {
+            uint64_t pred;
+            cd c;
+            uint32_t q;
+            cd w;
+          };
+          std::vector<Rep> reps;
+          if (d0 == cd(1.0)) {
+            reps.push_back({ctrl, 1.0, tq, d1});
+            for (auto cq : p.op.controls) reps.push_back({(ctrl & ~bit(cq)) | bit(tq), 1.0, cq, d1});
+          } else {
+            reps.push_back({ctrl, d0, tq, d1 / d0});
+          }
+          bool merged = false;
+          if (open >= 0 && !(qm & x_open)) {
+            for (auto& r : reps)
+              if (r.pred == aops[open].pred) {
+                aops[open].c *= r.c;
+                auto it = aops[open].w.find(r.q);
+                if (it == aops[open].w.end()) aops[open].w[r.q] = r.w;
+                else it->second *= r.w;
+                merged = true;
+                break;
+              }
+          }
+          if (!merged) {
+            const Rep& r = reps.back();  // prefer the predicate holding the target
+            AOp a;
+            a.type = TO_PHASE;
+            a.cfg = cur;
+            a.pred = r.pred;
+            a.c = r.c;
+            a.w[r.q] = r.w;
+            aops.push_back(a);
+            open = static_cast<int>(aops.size() - 1);
+            x_open = 0;
+          }
+          break;
+        }
+        case PK::SwapRel: {
+          const int a = tb[p.op.targets[0]], b = tb[p.op.targets[1]];
+          Cfg c = cfgs[cur];
+          for (int k = 0; k < kTileR; ++k) c.reg[k] = c.reg[k] == a ? b : (c.reg[k] == b ? a : c.reg[k]);
+          for (uint32_t k = 0; k < t; ++k) c.thr[k] = c.thr[k] == a ? b : (c.thr[k] == b ? a : c.thr[k]);
+          cfgs.push_back(c);
+          cur = static_cast<int>(cfgs.size() - 1);
+          x_open |= p.needmask;
+          break;
+        }
+        case PK::Mat1:
+        case PK::Flip:
+        case PK::Dense: {
+          if (!satisfied(cfgs[cur], p)) transpose_to(cur, choose(&cfgs[cur], list, i, false));
+          AOp a;
+          a.cfg = cur;
+          a.pred = ctrl;
+          if (p.k == PK::Flip) {
+            a.type = TO_FLIP;
+            a.target = p.op.targets[0];
+          } else if (p.k == PK::Mat1) {
+            a.type = TO_MAT1;
+            a.target = p.op.targets[0];
+            for (int k = 0; k < 4; ++k) a.m[k] = p.op.m[k];
+          } else {
+            a.type = p.op.targets.size() == 2 ? TO_DENSE2 : TO_DENSE3;
+            a.dense_targets = p.op.targets;
+            a.dense = p.op.m;
+          }
+          aops.push_back(a);
+          x_open |= p.needmask;
+          break;
+        }
+        case PK::Opaque: throw RuntimeError("tile compiler: opaque op inside a pass");
+      }
+    }
+    if (!store_ok(cfgs[cur])) {
+      Cfg c = cfgs[cur];
+      bool low_in_reg = false;
+      for (int k = 0; k < kTileR; ++k)
+        if (c.reg[k] < static_cast<int>(L)) low_in_reg = true;
+      if (low_in_reg) c = default_cfg();
+      else fill_threads(c);
+      transpose_to(cur, c);
+    }
+    final_cfg = cur;
+  }
+  int final_cfg = 0;
+
+  Cfg default_cfg() const {
+    Cfg c;
+    // registers: the highest tile bits not reserved for lanes
+    int k = 0;
+    for (int y = static_cast<int>(m) - 1; y >= 0 && k < kTileR; --y)
+      if (y >= static_cast<int>(L) || m - L < kTileR) c.reg[k++] = y;
+    fill_threads(c);
+    return c;
+  }
+};
+
+// 3 x (m-3) GF(2) swizzle: phys(j) = j ^ (parities of j & a[i]) in the low 3 bits.
+struct Swizzle {
+  uint32_t a[3] = {0, 0, 0};
+  uint32_t phys(uint32_t j) const {
+    uint32_t low = 0;
+    for (int i = 0; i < 3; ++i) low |= static_cast<uint32_t>(__builtin_popcount(j & a[i]) & 1) << i;
+    return j ^ low;
+  }
+};
+
+bool conflict_free(const Swizzle& s, const Cfg& c, uint32_t t) {
+  if (t < 3) return true;
+  uint32_t v[3];
+  for (int i = 0; i < 3; ++i) v[i] = s.phys(1u << c.thr[i]) & 7u;
+  // rank 3 over GF(2)
+  const uint32_t x = v[0], y = v[1], z = v[2];
+  return x && y && z && (x ^ y) && (x ^ z) && (y ^ z) && (x ^ y ^ z);
+}
+
+Swizzle pick_swizzle(const Cfg& a, const Cfg& b, uint32_t m, uint32_t t) {
+  Swizzle s;
+  if (conflict_free(s, a, t) && conflict_free(s, b, t)) return s;
+  std::mt19937 rng(12345u + static_cast<uint32_t>(a.thr[0] * 131 + b.thr[0]));
+  const uint32_t himask = m > 3 ? ((1u << m) - 1) & ~7u : 0;
+  for (int iter = 0; iter < 20000 && himask; ++iter) {
+    for (int i = 0; i < 3; ++i) s.a[i] = rng() & himask;
+    if (conflict_free(s, a, t) && conflict_free(s, b, t)) return s;
+  }
+  return Swizzle{};  // correct, possibly conflicted
+}
+
+std::shared_ptr<TileProgram> finalize(Compiler& C, uint64_t gates, const std::vector<uint64_t>& srcs) {
+  auto tp = std::make_shared<TileProgram>();
+  TileHeader& h = tp->h;
+  h.n = C.n;
+  h.m = C.m;
+  h.t = C.t;
+  for (uint32_t b = 0; b < C.m; ++b) h.S[b] = C.S[b];
+  h.ntiles = 1ull << (C.n - C.m);
+  auto addr_of = [&](const Cfg& c, TileConfigAddr& a) {
+    for (uint32_t k = 0; k < C.t; ++k) a.tq[k] = C.S[c.thr[k]];
+    for (int k = 0; k < kTileR; ++k) a.rs[k] = 1ull << C.S[c.reg[k]];
+  };
+  addr_of(C.cfgs[0], h.load);
+  addr_of(C.cfgs[C.final_cfg], h.store);
+
+  auto split_pred = [&](const Cfg& c, uint64_t pred, TOp& o) {
+    o.rmask = 0;
+    o.rval = 0;
+    o.gmask = 0;
+    o.gval = 0;
+    for (uint32_t q = 0; q < 64; ++q) {
+      if (!((pred >> q) & 1)) continue;
+      int pos;
+      if (C.tb[q] >= 0 && C.has_reg(c, C.tb[q], &pos)) o.rmask |= static_cast<uint16_t>(1u << pos);
+      else o.gmask |= bit(q);
+    }
+    o.rval = o.rmask;
+    o.gval = o.gmask;
+  };
+
+  for (const AOp& a : C.aops) {
+    TOp o{};
+    o.type = a.type;
+    const Cfg& c = C.cfgs[a.cfg];
+    switch (a.type) {
+      case TO_MAT1: {
+        int pos = 0;
+        C.has_reg(c, C.tb[a.target], &pos);
+        o.k = static_cast<uint8_t>(pos);
+        split_pred(c, a.pred, o);
+        bool real = true, rx = true;
+        for (int k = 0; k < 4; ++k)
+          if (a.m[k].imag() != 0) real = false;
+        if (a.m[0].imag() != 0 || a.m[3].imag() != 0 || a.m[1].real() != 0 || a.m[2].real() != 0) rx = false;
+        o.type = real ? TO_MAT1_REAL : (rx ? TO_MAT1_RX : TO_MAT1);
+        o.coef = static_cast<uint32_t>(tp->coef.size());
+        for (int k = 0; k < 4; ++k) tp->coef.push_back(make_double2(a.m[k].real(), a.m[k].imag()));
+        break;
+      }
+      case TO_FLIP: {
+        int pos = 0;
+        C.has_reg(c, C.tb[a.target], &pos);
+        o.k = static_cast<uint8_t>(pos);
+        split_pred(c, a.pred, o);
+        break;
+      }
+      case TO_DENSE2:
+      case TO_DENSE3: {
+        split_pred(c, a.pred, o);
+        o.coef = static_cast<uint32_t>(tp->coef.size());
+        for (const auto& e : a.dense) tp->coef.push_back(make_double2(e.real(), e.imag()));
+        break;
+      }
+      case TO_PHASE: {
+        split_pred(c, a.pred, o);
+        cd G[16];
+        for (int p = 0; p < 16; ++p) G[p] = 1.0;
+        std::vector<std::pair<uint32_t, cd>> list;
+        for (const auto& [q, w] : a.w) {
+          if (w == cd(1.0)) continue;
+          int pos;
+          if (C.tb[q] >= 0 && C.has_reg(c, C.tb[q], &pos)) {
+            for (int p = 0; p < 16; ++p)
+              if ((p >> pos) & 1) G[p] *= w;
+          } else {
+            list.push_back({q, w});
+          }
+        }
+        o.coef = static_cast<uint32_t>(tp->coef.size());
+        o.meta = static_cast<uint32_t>(tp->meta.size());
+        o.nlist = static_cast<uint16_t>(list.size());
+        for (int p = 0; p < 16; ++p) tp->coef.push_back(make_double2(G[p].real(), G[p].imag()));
+        tp->coef.push_back(make_double2(a.c.real(), a.c.imag()));
+        for (auto& [q, w] : list) {
+          tp->coef.push_back(make_double2(w.real(), w.imag()));
+          tp->meta.push_back(q);
+        }
+        break;
+      }
+      case TO_TRANSPOSE: {
+        const Cfg& fa = C.cfgs[a.from];
+        const Cfg& fb = C.cfgs[a.to];
+        const Swizzle sw = pick_swizzle(fa, fb, C.m, C.t);
+        o.meta = static_cast<uint32_t>(tp->meta.size());
+        for (uint32_t k = 0; k < C.t; ++k) tp->meta.push_back(sw.phys(1u << fa.thr[k]));
+        for (int k = 0; k < kTileR; ++k) tp->meta.push_back(sw.phys(1u << fa.reg[k]));
+        for (uint32_t k = 0; k < C.t; ++k) tp->meta.push_back(sw.phys(1u << fb.thr[k]));
+        for (int k = 0; k < kTileR; ++k) tp->meta.push_back(sw.phys(1u << fb.reg[k]));
+        for (uint32_t k = 0; k < C.t; ++k) tp->meta.push_back(C.S[fb.thr[k]]);
+        ++tp->transposes;
+        break;
+      }
+    }
+    tp->ops.push_back(o);
+  }
+  h.nops = static_cast<uint32_t>(tp->ops.size());
+  auto al = [](size_t x) { return static_cast<uint32_t>((x + 15) & ~size_t(15)); };
+  h.ops_off = al(sizeof(TileHeader));
+  h.meta_off = al(h.ops_off + tp->ops.size() * sizeof(TOp));
+  h.coef_off = al(h.meta_off + tp->meta.size() * sizeof(uint32_t));
+  h.bytes = al(h.coef_off + tp->coef.size() * sizeof(double2));
+  tp->gates = gates;
+  tp->source = srcs;
+  return tp;
+}
+
+}  // namespace
+
+TileOptions tile_options_from_env() {
+  TileOptions o;
+  if (const char* e = std::getenv("QSB_TILE_M")) o.m = static_cast<uint32_t>(std::atoi(e));
+  if (const char* e = std::getenv("QSB_TILE_LOW")) o.low = static_cast<uint32_t>(std::atoi(e));
+  o.m = std::max<uint32_t>(8, std::min<uint32_t>(kTileMaxM, o.m));
+  o.low = std::min<uint32_t>(5, o.low);
+  return o;
+}
+
+void plan_tiles(uint32_t n, std::vector<Op>& ops, std::vector<Step>& steps, const TileOptions& opt) {
+  std::vector<POp> pops = preprocess(ops);
+  // Tiny registers cannot host a 16-amplitude-per-thread tile: per-gate kernels.
+  if (n < 6) {
+    for (auto& p : pops) {
+      Step s;
+      s.kind = Step::OpStep;
+      s.op = p.op;
+      steps.push_back(std::move(s));
+    }
+    return;
+  }
+  const uint32_t m = std::min<uint32_t>(n, opt.m);
+  const uint32_t L = std::min<uint32_t>(opt.low, m - kTileR);
+  const uint64_t lowmask = (1ull << L) - 1;
+  const uint64_t allmask = n >= 64 ? ~0ull : (1ull << n) - 1;
+
+  std::vector<uint32_t> rem(pops.size());
+  for (size_t i = 0; i < pops.size(); ++i) rem[i] = static_cast<uint32_t>(i);
+
+  auto emit_ready_opaque = [&]() {
+    uint64_t blocked = 0;
+    std::vector<uint32_t> keep;
+    keep.reserve(rem.size());
+    for (auto idx : rem) {
+      const POp& p = pops[idx];
+      if (p.k == PK::Opaque && !(p.qmask & blocked)) {
+        Step s;
+        s.kind = Step::OpStep;
+        s.op = p.op;
+        steps.push_back(std::move(s));
+        continue;
+      }
+      blocked |= p.qmask;
+      keep.push_back(idx);
+    }
+    rem.swap(keep);
+  };
+
+  emit_ready_opaque();
+  while (!rem.empty()) {
+    uint64_t S = n <= m ? allmask : lowmask;
+    size_t cur = scan(pops, rem, S, nullptr);
+    while (static_cast<uint32_t>(__builtin_popcountll(S)) < m) {
+      // candidates: need-qubits of not-yet-executable ops, in first-seen order
+      std::vector<uint32_t> cand;
+      uint64_t seen = S;
+      {
+        std::vector<char> tk(rem.size(), 0);
+        scan(pops, rem, S, &tk);
+        size_t looked = 0;
+        for (size_t i = 0; i < rem.size() && looked < 256; ++i) {
+          if (tk[i]) continue;
+          ++looked;
+          uint64_t nm = pops[rem[i]].needmask & ~seen;
+          while (nm) {
+            const uint32_t q = static_cast<uint32_t>(__builtin_ctzll(nm));
+            nm &= nm - 1;
+            cand.push_back(q);
+            seen |= bit(q);
+          }
+        }
+      }
+      if (cand.empty()) break;
+      size_t best_cnt = cur;
+      int best = -1;
+      for (auto q : cand) {
+        const size_t c = scan(pops, rem, S | bit(q), nullptr);
+        if (c > best_cnt) {
+          best_cnt = c;
+          best = static_cast<int>(q);
+        }
+      }
+      if (best < 0) {
+        // no single qubit helps: add the need set of the first blocked op
+        std::vector<char> tk(rem.size(), 0);
+        scan(pops, rem, S, &tk);
+        bool added = false;
+        for (size_t i = 0; i < rem.size(); ++i) {
+          if (tk[i] || pops[rem[i]].k == PK::Opaque) continue;
+          const uint64_t ns = S | pops[rem[i]].needmask;
+          if (static_cast<uint32_t>(__builtin_popcountll(ns)) <= m && scan(pops, rem, ns, nullptr) > cur) {
+            S = ns;
+            cur = scan(pops, rem, S, nullptr);
+            added = true;
+          }
+          break;
+        }
+        if (!added) break;
+        continue;
+      }
+      S |= bit(static_cast<uint32_t>(best));
+      cur = best_cnt;
+    }
+    // pad S to exactly m qubits (lowest unused) so tiles have a fixed shape
+    for (uint32_t q = 0; q < n && static_cast<uint32_t>(__builtin_popcountll(S)) < m; ++q) S |= bit(q);
+
+    std::vector<char> tk(rem.size(), 0);
+    const size_t cnt = scan(pops, rem, S, &tk);
+    if (cnt == 0) throw RuntimeError("tile planner made no progress");
+    std::vector<const POp*> list;
+    std::vector<uint32_t> keep;
+    std::vector<uint64_t> srcs;
+    for (size_t i = 0; i < rem.size(); ++i) {
+      if (tk[i]) {
+        list.push_back(&pops[rem[i]]);
+        srcs.push_back(pops[rem[i]].op.gate_index);
+      } else {
+        keep.push_back(rem[i]);
+      }
+    }
+    Compiler C;
+    C.n = n;
+    C.m = m;
+    C.t = m - kTileR;
+    C.L = L;
+    for (int q = 0; q < 64; ++q) C.tb[q] = -1;
+    for (uint32_t q = 0; q < n; ++q)
+      if ((S >> q) & 1) {
+        C.tb[q] = static_cast<int>(C.S.size());
+        C.S.push_back(q);
+      }
+    C.compile(list);
+    Step s;
+    s.kind = Step::TileStep;
+    s.tile = finalize(C, list.size(), srcs);
+    steps.push_back(std::move(s));
+    rem.swap(keep);
+    emit_ready_opaque();
+  }
+}
+
+}  // namespace qsb

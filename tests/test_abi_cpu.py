@@ -1,0 +1,117 @@
+"""CPU-side checks of the product: the C ABI library loads and exports every
+symbol include/qsb.h declares; host-only parts (planner, reference-mode
+fusion, RNG, generators, validation) match the reference.  No GPU needed.
+"""
+import os
+import re
+
+import numpy as np
+import pytest
+
+import golden_io as gio
+from paper_2212_14201_b200 import _native as N
+from paper_2212_14201_b200 import qforge as Q
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def header_functions():
+    src = open(os.path.join(ROOT, "include", "qsb.h")).read()
+    src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
+    return sorted(set(re.findall(r"\b(qs_[a-z0-9_]+)\s*\(", src)))
+
+
+def test_library_exports_every_declared_symbol():
+    L = N.lib()
+    declared = header_functions()
+    assert len(declared) >= 40
+    missing = [f for f in declared if not hasattr(L, f)]
+    assert not missing, missing
+    assert set(declared) == set(N.EXPORTED)
+    assert L.qs_abi_version() == 1
+
+
+def test_rng_mirror_matches_reference_stream():
+    c = gio.case("rng")
+    for s in c["streams"]:
+        r = Q.Rng(s["seed"])
+        assert [str(r.next()) for _ in range(8)] == s["next"]
+        u = Q.Rng(s["seed"])
+        assert [u.uniform() for _ in range(8)] == s["uniform"]
+        assert str(Q.Rng.derive(s["seed"], 3).next()) == s["derive3"]
+        assert str(Q.splitmix64(s["seed"])) == s["splitmix"]
+
+
+def _same(prog, circ):
+    gates = prog.gates()
+    assert len(gates) == len(circ.gates)
+    for a, b in zip(gates, circ.gates):
+        assert (int(a.kind), list(a.targets), list(a.controls), bool(a.dagger)) == \
+               (b.kind, b.targets, b.controls, b.dagger)
+        assert list(a.params) == b.params
+
+
+def test_generators_match_reference_side():
+    _same(Q.gen_random_circuit(8, 6, 42), gio.read_circuit("random_8_6_42.circ"))
+    _same(Q.gen_random_circuit(14, 3, 424242), gio.read_circuit("random_14_3_424242.circ"))
+    _same(Q.gen_ghz(20), gio.read_circuit("ghz_20.circ"))
+    _same(Q.gen_qft(20, 0x5A5A5), gio.read_circuit("qft_20.circ"))
+    _same(Q.gen_qft(10, 717), gio.read_circuit("qft_10_717.circ"))
+    _same(Q.gen_hea(8, 3, 5), gio.read_circuit("hea_8_3_5.circ"))
+    _same(Q.gen_hea(24, 10, 2024), gio.read_circuit("hea_24_10_2024.circ"))
+
+
+FUSE = gio.cases("fuse")
+
+
+@pytest.mark.parametrize("c", FUSE, ids=[c["name"] for c in FUSE])
+def test_reference_mode_fusion_reproduces_fuse_circuit(c):
+    # fusion.hpp:20-133 restated in csrc/fusion.cpp: same blocks, same order,
+    # matrices equal up to matmul rounding.
+    src = gio.read_circuit(c["name"] + ".in.circ")
+    want = gio.read_circuit(c["name"] + ".circ")
+    p = Q.Program(src.qubits, 0)
+    for g in src.gates:
+        p.add(Q.Gate(Q.GateKind(g.kind), g.targets, g.params, g.controls, g.dagger, g.matrix))
+    got = Q.fuse_circuit(p, c["k"]).gates()
+    assert len(got) == c["blocks"] == len(want.gates)
+    for a, b in zip(got, want.gates):
+        assert int(a.kind) == b.kind and list(a.targets) == b.targets and list(a.controls) == b.controls
+        if b.matrix is not None:
+            assert np.max(np.abs(a.matrix - b.matrix)) <= 1e-13
+        else:
+            assert list(a.params) == b.params
+
+
+def test_planner_runs_host_side_and_fuses_passes():
+    # Planning is pure host C++: passes << gates for the bench workloads.
+    p = Q.gen_random_circuit(30, 20, 424242)
+    cc = Q.CompiledCircuit(30, p.gates())
+    st = cc.stats()
+    assert st["gates"] == 1200
+    assert st["passes"] < 120, st
+    unf = Q.CompiledCircuit(30, p.gates(), plan=N.QS_PLAN_UNFUSED).stats()
+    assert unf["passes"] == 1200
+    qft = Q.CompiledCircuit(30, Q.gen_qft(30, 12345).gates()).stats()
+    assert qft["passes"] <= 8, qft
+    dense = Q.CompiledCircuit(28, Q.gen_random_circuit(28, 20, 424242).gates(),
+                              plan=N.QS_PLAN_DENSE_FUSION, max_fused_qubits=3).stats()
+    assert dense["passes"] < 1120
+
+
+def test_validation_errors_without_gpu():
+    bad = [Q.make_gate(Q.GateKind.H, [7])]
+    with pytest.raises(Q.ValidationError):
+        Q.CompiledCircuit(4, bad)
+    dup = [Q.make_gate(Q.GateKind.CNOT, [1, 1])]
+    with pytest.raises(Q.ValidationError):
+        Q.CompiledCircuit(4, dup)
+    nonu = [Q.make_custom_gate([0, 1], np.ones((4, 4)))]
+    with pytest.raises(Q.ValidationError):
+        Q.CompiledCircuit(4, nonu)
+    with pytest.raises(Q.ValidationError):
+        Q.SimOptions(max_fused_qubits=9).validate()
+    p = Q.Program(2, 0)
+    p.add(Q.make_gate(Q.GateKind.RX, [0]))  # missing parameter
+    with pytest.raises(Q.ValidationError):
+        Q.validate_or_throw(p)

@@ -1,0 +1,240 @@
+"""Parity of the CUDA path (libqsb.so, called through the C ABI) against the
+reference's golden vectors and the C oracle.
+
+Tolerances (BASELINE.json north_star): max |d amplitude| <= 1e-10,
+|d prob| <= 1e-12, measurement counts identical for the same seed.
+"""
+import numpy as np
+import pytest
+
+import golden_io as gio
+import oracle_lib as ol
+from paper_2212_14201_b200 import _native as N
+from paper_2212_14201_b200 import qforge as Q
+
+pytestmark = pytest.mark.gpu
+
+AMP_TOL = 1e-10
+PROB_TOL = 1e-12
+PLANS = [N.QS_PLAN_UNFUSED, N.QS_PLAN_DENSE_FUSION, N.QS_PLAN_TILED]
+PLAN_IDS = ["unfused", "dense_fusion", "tiled"]
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _gpu_present():
+    import torch
+    assert torch.cuda.is_available(), "the -m gpu suite needs a CUDA device"
+    N.lib()  # fails loudly when libqsb.so is missing
+
+
+def run_state(circ, plan, k=3):
+    sv = Q.StateVector(circ.qubits)
+    if circ.gates:
+        sv.apply_circuit(circ.gates, plan, k)
+    return sv
+
+
+STATE = gio.cases("state")
+
+
+@pytest.mark.parametrize("plan", PLANS, ids=PLAN_IDS)
+@pytest.mark.parametrize("c", STATE, ids=[c["name"] for c in STATE])
+def test_final_state_and_reductions(c, plan):
+    circ = gio.read_circuit(c["name"] + ".circ")
+    n = circ.qubits
+    sv = run_state(circ, plan)
+    got = sv.amplitudes()
+    want = gio.read_amps(c["name"] + ".amps")
+    assert np.max(np.abs(got - want)) <= AMP_TOL
+    assert abs(sv.checksum() - c["checksum"]) <= PROB_TOL * (1 << n) * (1 << n)
+    assert abs(sv.norm_squared() - c["norm2"]) <= PROB_TOL
+    p1 = np.array([sv.probability_of_one(q) for q in range(n)])
+    assert np.max(np.abs(p1 - c["prob_one"])) <= PROB_TOL
+    marg = sv.probabilities(c["marginal_qubits"])
+    assert np.max(np.abs(marg - c["marginal"])) <= PROB_TOL
+    full = sv.probabilities()
+    assert np.max(np.abs(full - np.abs(want) ** 2)) <= PROB_TOL
+
+
+@pytest.mark.parametrize("c", [c for c in STATE if c["name"].startswith(("mixed_", "custom_", "equiv_"))],
+                         ids=lambda c: c["name"])
+def test_per_gate_api_matches(c):
+    # StateVector::apply_gate one call at a time (statevector.hpp:469-538)
+    circ = gio.read_circuit(c["name"] + ".circ")
+    sv = Q.StateVector(circ.qubits)
+    for g in circ.gates:
+        arr, keep = N.gate_array([g])
+        N.check(N.lib().qs_apply_gate(sv.handle(), arr))
+    assert np.max(np.abs(sv.amplitudes() - gio.read_amps(c["name"] + ".amps"))) <= AMP_TOL
+
+
+SAMPLE = gio.cases("sample")
+
+
+@pytest.mark.parametrize("plan", [N.QS_PLAN_UNFUSED, N.QS_PLAN_TILED], ids=["unfused", "tiled"])
+@pytest.mark.parametrize("c", SAMPLE, ids=[c["name"] for c in SAMPLE])
+def test_counts_identical(c, plan):
+    circ = gio.read_circuit(c["name"] + ".circ")
+    sv = run_state(circ, plan)
+    idx = sv.sample_seeded(c["seed"], c["shots"], exact=True)
+    assert gio.counts_from_indices(idx, circ.measures, circ.cbits) == c["counts"]
+
+
+def test_run_api_counts_and_keys():
+    c = gio.case("sample_partial")
+    circ = gio.read_circuit("sample_partial.circ")
+    p = Q.Program(circ.qubits, circ.cbits)
+    for g in circ.gates:
+        p.add(Q.Gate(Q.GateKind(g.kind), g.targets, g.params, g.controls, g.dagger, g.matrix))
+    for q, cb in circ.measures:
+        p.measure(q, cb)
+    r = Q.run(p, Q.SimOptions(seed=c["seed"]), c["shots"])
+    assert r.counts == c["counts"]
+    key = Q.Program(2, 2)
+    key.add(Q.make_gate(Q.GateKind.X, [0]))
+    key.measure(0, 0)
+    key.measure(1, 1)
+    assert Q.run(key, Q.SimOptions(), 10).counts == {"01": 10}
+
+
+def _oracle_serial_cum(a):
+    n = int(np.log2(a.size))
+    cum = np.zeros(a.size)
+    import ctypes as C
+    ol.lib().qo_sampler_build.restype = C.c_double
+    ol.lib().qo_sampler_build.argtypes = [C.POINTER(C.c_double), C.c_uint32, C.POINTER(C.c_double)]
+    tot = ol.lib().qo_sampler_build(ol._dptr(a.view(np.float64)), n, ol._dptr(cum))
+    return cum, tot
+
+
+@pytest.mark.parametrize("n,seed", [(10, 1), (14, 2), (18, 3), (20, 4), (22, 5)])
+def test_exact_cumulative_is_bitwise_serial(n, seed):
+    # BasisSampler's serial accumulation (statevector.hpp:544-552), bit for bit
+    rng = np.random.default_rng(seed)
+    a = rng.normal(size=1 << n) + 1j * rng.normal(size=1 << n)
+    if seed % 2:
+        a[rng.random(a.size) < 0.3] = 0  # zeros and a skewed distribution
+        a *= np.exp(-np.arange(a.size) / a.size * 8)
+    a /= np.linalg.norm(a)
+    sv = Q.StateVector.from_amplitudes(n, a)
+    cum = np.empty(a.size)
+    tot = N.C.c_double()
+    N.check(N.lib().qs_debug_cumulative(sv.handle(), 1, N.dptr(cum), N.C.byref(tot)))
+    want, wtot = _oracle_serial_cum(a)
+    assert tot.value == wtot
+    assert np.array_equal(cum.view(np.uint64), want.view(np.uint64))
+
+
+def test_collapse_sequence():
+    c = gio.case("collapse")
+    circ = gio.read_circuit(c["circuit"])
+    sv = run_state(circ, N.QS_PLAN_TILED)
+    for i, step in enumerate(c["steps"]):
+        assert sv.measure_collapse(step["q"], step["u"]) == step["outcome"]
+        assert abs(sv.norm_squared() - step["norm2"]) <= 1e-14
+        if i == 2:
+            assert np.max(np.abs(sv.amplitudes() - gio.read_amps("collapse_mid.amps"))) <= 1e-14
+
+
+@pytest.mark.parametrize("c", gio.cases("expectation"), ids=lambda c: c["name"])
+def test_expectation(c):
+    circ = gio.read_circuit(c["name"] + ".circ")
+    sv = run_state(circ, N.QS_PLAN_TILED)
+    terms = ol.parse_hamiltonian(c["hamiltonian"], circ.qubits)
+    vals = sv.expect_pauli([w for w, _ in terms])
+    e = sum(coef * v for (_, coef), v in zip(terms, vals))
+    assert abs(e.real - c["value"]) <= 1e-12
+    assert abs(e.imag) <= 1e-12
+
+
+@pytest.mark.parametrize("name", ["ghz_20", "qft_20"])
+@pytest.mark.parametrize("plan", PLANS, ids=PLAN_IDS)
+def test_config1_digest(name, plan):
+    c = gio.case(name)
+    circ = gio.read_circuit(name + ".circ")
+    sv = run_state(circ, plan)
+    a = sv.amplitudes()
+    idx = np.array(c["idx"])
+    assert np.max(np.abs(a[idx].real - c["re"])) <= AMP_TOL
+    assert np.max(np.abs(a[idx].imag - c["im"])) <= AMP_TOL
+    assert abs(sv.checksum() - c["checksum"]) <= 1e-9
+    assert np.max(np.abs(sv.probabilities()[:256] - c["probs_head"])) <= PROB_TOL
+    assert np.max(np.abs(sv.probabilities(c["marginal_qubits"]) - c["marginal"])) <= PROB_TOL
+
+
+def test_config5_sweep_24q():
+    # HEA(24, 10 layers): expectation + 10 x 10^6-shot sweep, digest-identical
+    c = gio.case("hea_24", big=True)
+    circ = gio.read_circuit("hea_24_10_2024.circ")
+    sv = run_state(circ, N.QS_PLAN_TILED)
+    assert abs(sv.checksum() - c["checksum"]) <= 1e-6
+    terms = []
+    for i in range(23):
+        w = ["I"] * 24
+        w[i] = w[i + 1] = "Z"
+        terms.append(("".join(w), 1.0))
+    for i in range(24):
+        w = ["I"] * 24
+        w[i] = "X"
+        terms.append(("".join(w), 0.5))
+    vals = sv.expect_pauli([w for w, _ in terms])
+    e = sum(coef * v for (_, coef), v in zip(terms, vals))
+    assert abs(e.real - c["expectation"]) <= 1e-10
+    for s in c["seeds"]:
+        idx = sv.sample_seeded(s["seed"], c["shots"], exact=True)
+        hist = np.bincount((idx >> np.uint64(16)).astype(np.int64), minlength=256)
+        assert hist.tolist() == s["hist_top8"], s["seed"]
+        assert str(gio.fnv_indices(idx)) == s["fnv"], s["seed"]
+
+
+def test_error_behaviour():
+    with pytest.raises(Q.ValidationError):
+        Q.StateVector(31)
+    sv = Q.StateVector(3)
+    with pytest.raises(Q.ValidationError):
+        sv.apply_gate(Q.make_gate(Q.GateKind.H, [5]))
+    with pytest.raises(Q.ValidationError):
+        sv.apply_gate(Q.make_custom_gate([0, 1], np.ones((4, 4))))
+    with pytest.raises(Q.ValidationError):
+        sv.probabilities([])
+    with pytest.raises(Q.QforgeError):
+        sv.collapse(0, 1, 0.0)
+    with pytest.raises(Q.ValidationError):
+        Q.StateVector.from_amplitudes(2, [1.0])
+
+
+def _random_unitary(k, rng):
+    m = rng.normal(size=(1 << k, 1 << k)) + 1j * rng.normal(size=(1 << k, 1 << k))
+    q, r = np.linalg.qr(m)
+    return q * (np.diag(r) / np.abs(np.diag(r)))
+
+
+@pytest.mark.parametrize("n", [6, 9, 13, 16])
+def test_tile_path_random_mixed_vs_oracle(n):
+    # Every micro-op kind (MAT1 variants, FLIP, PHASE merges, DENSE2/3,
+    # relabel swaps, controlled swaps, transposes) against the oracle.
+    rng = np.random.default_rng(n)
+    gates = []
+    for i in range(400):
+        kind = rng.integers(0, 16)
+        perm = rng.permutation(n).tolist()
+        if kind in (11, 12, 13):
+            g = Q.make_gate(Q.GateKind(kind), perm[:2])
+        elif kind == 14:
+            g = Q.make_gate(Q.GateKind.TOFFOLI, perm[:3])
+        elif kind == 15:
+            k = int(rng.integers(1, 4))
+            g = Q.make_custom_gate(perm[:k], _random_unitary(k, rng))
+        else:
+            g = Q.make_gate(Q.GateKind(kind), perm[:1], rng.uniform(0, 6.3, size={7: 1, 8: 1, 9: 1, 10: 3}.get(kind, 0)))
+        if rng.random() < 0.25:
+            used = len(g.targets)
+            g.controls = perm[used:used + int(rng.integers(1, 3))]
+        if rng.random() < 0.2:
+            g.dagger = True
+        gates.append(g)
+    want = ol.run_gates(n, gates)
+    for plan in PLANS:
+        sv = Q.StateVector(n)
+        sv.apply_circuit(gates, plan, 3)
+        assert np.max(np.abs(sv.amplitudes() - want)) <= AMP_TOL, plan
