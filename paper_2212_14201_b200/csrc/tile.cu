@@ -2,8 +2,9 @@
 //
 // One CTA of 2^(M-4) threads owns one tile of 2^M amplitudes at a time
 // (persistent loop over tiles); each thread holds 16 amplitudes in registers.
-// The micro-program (TOp list + coefficient / metadata tables) is uniform
-// across the grid and read through the read-only cache.
+// The micro-program (header, TOp list, coefficient and metadata tables) is a
+// __grid_constant__ kernel parameter: it lives in the constant bank, so every
+// warp-uniform read is a constant-cache broadcast instead of an L1 load.
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -15,6 +16,10 @@
 namespace qsb {
 
 namespace {
+
+struct __align__(16) TileBlob {
+  unsigned char b[kTileBlobBytes];
+};
 
 __device__ __forceinline__ double2 cmul(double2 a, double2 b) {
   return make_double2(fma(a.x, b.x, -a.y * b.y), fma(a.x, b.y, a.y * b.x));
@@ -31,35 +36,36 @@ __device__ __forceinline__ double2 cmv2(double2 m0, double2 a, double2 m1, doubl
   return make_double2(re, im);
 }
 
-template <int K, int VAR>
-__device__ __forceinline__ void mat1(double2 (&v)[16], const double2* __restrict__ c, int rmask, int rval) {
-  const double2 m0 = __ldg(c), m1 = __ldg(c + 1), m2 = __ldg(c + 2), m3 = __ldg(c + 3);
+// 2x2 on register bit K.  CHECK: honour the register-index predicate.
+template <int K, int VAR, bool CHECK>
+__device__ __forceinline__ void mat1(double2 (&v)[16], const double2* c, int rmask, int rval) {
+  const double2 m0 = c[0], m1 = c[1], m2 = c[2], m3 = c[3];
 #pragma unroll
   for (int p = 0; p < 16; ++p) {
     if (p & (1 << K)) continue;
     const int p1 = p | (1 << K);
-    if ((p & rmask) != rval) continue;
+    if (CHECK && (p & rmask) != rval) continue;
     const double2 a = v[p], b = v[p1];
     if (VAR == 0) {  // general complex
       v[p] = cmv2(m0, a, m1, b);
       v[p1] = cmv2(m2, a, m3, b);
-    } else if (VAR == 1) {  // real matrix
+    } else if (VAR == 1) {  // real matrix (RY, H)
       v[p] = make_double2(fma(m0.x, a.x, m1.x * b.x), fma(m0.x, a.y, m1.x * b.y));
       v[p1] = make_double2(fma(m2.x, a.x, m3.x * b.x), fma(m2.x, a.y, m3.x * b.y));
-    } else {  // real diagonal, imaginary off-diagonal
+    } else {  // real diagonal, imaginary off-diagonal (RX)
       v[p] = make_double2(fma(m0.x, a.x, -m1.y * b.y), fma(m0.x, a.y, m1.y * b.x));
       v[p1] = make_double2(fma(m3.x, b.x, -m2.y * a.y), fma(m3.x, b.y, m2.y * a.x));
     }
   }
 }
 
-template <int K>
+template <int K, bool CHECK>
 __device__ __forceinline__ void flip(double2 (&v)[16], int rmask, int rval) {
 #pragma unroll
   for (int p = 0; p < 16; ++p) {
     if (p & (1 << K)) continue;
     const int p1 = p | (1 << K);
-    if ((p & rmask) != rval) continue;
+    if (CHECK && (p & rmask) != rval) continue;
     const double2 a = v[p];
     v[p] = v[p1];
     v[p1] = a;
@@ -67,7 +73,7 @@ __device__ __forceinline__ void flip(double2 (&v)[16], int rmask, int rval) {
 }
 
 template <int KD>
-__device__ __forceinline__ void dense(double2 (&v)[16], const double2* __restrict__ M, int rmask, int rval) {
+__device__ __forceinline__ void dense(double2 (&v)[16], const double2* M, int rmask, int rval) {
   constexpr int G = 1 << KD;
 #pragma unroll
   for (int hi = 0; hi < (16 >> KD); ++hi) {
@@ -81,7 +87,7 @@ __device__ __forceinline__ void dense(double2 (&v)[16], const double2* __restric
       double re = 0, im = 0;
 #pragma unroll
       for (int c = 0; c < G; ++c) {
-        const double2 m = __ldg(M + r * G + c);
+        const double2 m = M[r * G + c];
         re = fma(m.x, in[c].x, re);
         re = fma(-m.y, in[c].y, re);
         im = fma(m.x, in[c].y, im);
@@ -94,11 +100,38 @@ __device__ __forceinline__ void dense(double2 (&v)[16], const double2* __restric
 
 template <int VAR>
 __device__ __forceinline__ void mat1_any(double2 (&v)[16], int k, const double2* c, int rmask, int rval) {
-  switch (k) {
-    case 0: mat1<0, VAR>(v, c, rmask, rval); break;
-    case 1: mat1<1, VAR>(v, c, rmask, rval); break;
-    case 2: mat1<2, VAR>(v, c, rmask, rval); break;
-    default: mat1<3, VAR>(v, c, rmask, rval); break;
+  if (rmask == 0) {
+    switch (k) {
+      case 0: mat1<0, VAR, false>(v, c, 0, 0); break;
+      case 1: mat1<1, VAR, false>(v, c, 0, 0); break;
+      case 2: mat1<2, VAR, false>(v, c, 0, 0); break;
+      default: mat1<3, VAR, false>(v, c, 0, 0); break;
+    }
+  } else {
+    switch (k) {
+      case 0: mat1<0, VAR, true>(v, c, rmask, rval); break;
+      case 1: mat1<1, VAR, true>(v, c, rmask, rval); break;
+      case 2: mat1<2, VAR, true>(v, c, rmask, rval); break;
+      default: mat1<3, VAR, true>(v, c, rmask, rval); break;
+    }
+  }
+}
+
+__device__ __forceinline__ void flip_any(double2 (&v)[16], int k, int rmask, int rval) {
+  if (rmask == 0) {
+    switch (k) {
+      case 0: flip<0, false>(v, 0, 0); break;
+      case 1: flip<1, false>(v, 0, 0); break;
+      case 2: flip<2, false>(v, 0, 0); break;
+      default: flip<3, false>(v, 0, 0); break;
+    }
+  } else {
+    switch (k) {
+      case 0: flip<0, true>(v, rmask, rval); break;
+      case 1: flip<1, true>(v, rmask, rval); break;
+      case 2: flip<2, true>(v, rmask, rval); break;
+      default: flip<3, true>(v, rmask, rval); break;
+    }
   }
 }
 
@@ -112,14 +145,13 @@ __device__ __forceinline__ uint64_t reg_offset(int p, const unsigned long long (
 
 template <int M>
 __global__ void __launch_bounds__(1 << (M - 4), (M >= 13 ? 1 : 2))
-    k_tile(double2* __restrict__ amps, const unsigned char* __restrict__ blob) {
-  constexpr int T = 1 << (M - 4);
+    k_tile(double2* __restrict__ amps, const __grid_constant__ TileBlob blob) {
   constexpr int TB = M - 4;
   extern __shared__ double2 sm[];
-  const TileHeader* H = reinterpret_cast<const TileHeader*>(blob);
-  const TOp* ops = reinterpret_cast<const TOp*>(blob + H->ops_off);
-  const uint32_t* meta = reinterpret_cast<const uint32_t*>(blob + H->meta_off);
-  const double2* coef = reinterpret_cast<const double2*>(blob + H->coef_off);
+  const TileHeader* H = reinterpret_cast<const TileHeader*>(blob.b);
+  const TOp* ops = reinterpret_cast<const TOp*>(blob.b + H->ops_off);
+  const uint32_t* meta = reinterpret_cast<const uint32_t*>(blob.b + H->meta_off);
+  const double2* coef = reinterpret_cast<const double2*>(blob.b + H->coef_off);
   const int tid = threadIdx.x;
   const uint32_t nops = H->nops;
   const unsigned long long ntiles = H->ntiles;
@@ -141,10 +173,11 @@ __global__ void __launch_bounds__(1 << (M - 4), (M >= 13 ? 1 : 2))
     for (int k = 0; k < 4; ++k) rs[k] = H->load.rs[k];
     double2 v[16];
 #pragma unroll
-    for (int p = 0; p < 16; ++p) v[p] = amps[G | reg_offset(p, rs)];
+    for (int p = 0; p < 16; ++p) v[p] = __ldcs(amps + (G | reg_offset(p, rs)));
 
+#pragma unroll 1
     for (uint32_t i = 0; i < nops; ++i) {
-      const TOp o = ops[i];
+      const TOp& o = ops[i];
       const bool tp = (G & o.gmask) == o.gval;
       switch (o.type) {
         case TO_MAT1:
@@ -157,27 +190,23 @@ __global__ void __launch_bounds__(1 << (M - 4), (M >= 13 ? 1 : 2))
           if (tp) mat1_any<2>(v, o.k, coef + o.coef, o.rmask, o.rval);
           break;
         case TO_FLIP:
-          if (tp) {
-            switch (o.k) {
-              case 0: flip<0>(v, o.rmask, o.rval); break;
-              case 1: flip<1>(v, o.rmask, o.rval); break;
-              case 2: flip<2>(v, o.rmask, o.rval); break;
-              default: flip<3>(v, o.rmask, o.rval); break;
-            }
-          }
+          if (tp) flip_any(v, o.k, o.rmask, o.rval);
           break;
         case TO_PHASE:
           if (tp) {
             const double2* c = coef + o.coef;
-            double2 F = __ldg(c + 16);
-            for (uint32_t j = 0; j < o.nlist; ++j) {
-              const uint32_t q = meta[o.meta + j];
-              if ((G >> q) & 1) F = cmul(F, __ldg(c + 17 + j));
-            }
+            double2 F = c[16];
+            const uint32_t nl = o.nlist;
+            for (uint32_t j = 0; j < nl; ++j)
+              if ((G >> meta[o.meta + j]) & 1) F = cmul(F, c[17 + j]);
+            const int rm = o.rmask, rv = o.rval;
+            if (rm == 0) {
 #pragma unroll
-            for (int p = 0; p < 16; ++p) {
-              if ((p & o.rmask) != o.rval) continue;
-              v[p] = cmul(v[p], cmul(F, __ldg(c + p)));
+              for (int p = 0; p < 16; ++p) v[p] = cmul(v[p], cmul(F, c[p]));
+            } else {
+#pragma unroll
+              for (int p = 0; p < 16; ++p)
+                if ((p & rm) == rv) v[p] = cmul(v[p], cmul(F, c[p]));
             }
           }
           break;
@@ -226,15 +255,22 @@ __global__ void __launch_bounds__(1 << (M - 4), (M >= 13 ? 1 : 2))
             if ((tid >> k) & 1) G |= 1ull << mt[2 * TB + 8 + k];
           break;
         }
+        case TO_RELABEL: {
+          const uint32_t* mt = meta + o.meta;
+          G = base;
+#pragma unroll
+          for (int k = 0; k < TB; ++k)
+            if ((tid >> k) & 1) G |= 1ull << mt[k];
+          break;
+        }
         default: break;
       }
     }
 #pragma unroll
     for (int k = 0; k < 4; ++k) rs[k] = H->store.rs[k];
 #pragma unroll
-    for (int p = 0; p < 16; ++p) amps[G | reg_offset(p, rs)] = v[p];
+    for (int p = 0; p < 16; ++p) __stcs(amps + (G | reg_offset(p, rs)), v[p]);
   }
-  (void)T;
 }
 
 template <int M>
@@ -252,45 +288,25 @@ void launch_m(State& s, const TileProgram& tp) {
   const unsigned long long ntiles = tp.h.ntiles;
   const unsigned long long cap = static_cast<unsigned long long>(per_sm) * num_sms(s.device);
   const unsigned grid = static_cast<unsigned>(std::min(ntiles, cap));
-  k_tile<M><<<grid, T, smem, s.stream>>>(s.amps, static_cast<const unsigned char*>(tp.dev));
+  if (tp.h.bytes > kTileBlobBytes) throw RuntimeError("tile program exceeds the parameter blob");
+  static thread_local TileBlob blob;
+  std::memcpy(blob.b, tp.blob.data(), tp.h.bytes);
+  k_tile<M><<<grid, T, smem, s.stream>>>(s.amps, blob);
   QSB_LAUNCHED();
 }
 
 }  // namespace
 
-TileProgram::~TileProgram() {
-  if (dev) {
-    int prev = -1;
-    cudaGetDevice(&prev);
-    cudaSetDevice(dev_id);
-    cudaFree(dev);
-    if (prev >= 0) cudaSetDevice(prev);
-  }
-}
-
-void TileProgram::upload(int device) const {
-  if (dev && dev_id == device) return;
-  if (dev) {
-    cudaSetDevice(dev_id);
-    cudaFree(dev);
-    dev = nullptr;
-  }
-  DeviceGuard dg(device);
-  std::vector<unsigned char> blob(h.bytes, 0);
+void TileProgram::pack() {
+  blob.assign(h.bytes, 0);
   std::memcpy(blob.data(), &h, sizeof(TileHeader));
   if (!ops.empty()) std::memcpy(blob.data() + h.ops_off, ops.data(), ops.size() * sizeof(TOp));
   if (!meta.empty()) std::memcpy(blob.data() + h.meta_off, meta.data(), meta.size() * sizeof(uint32_t));
   if (!coef.empty()) std::memcpy(blob.data() + h.coef_off, coef.data(), coef.size() * sizeof(double2));
-  void* d = nullptr;
-  QSB_CUDA(cudaMalloc(&d, blob.size()));
-  QSB_CUDA(cudaMemcpy(d, blob.data(), blob.size(), cudaMemcpyHostToDevice));
-  dev = d;
-  dev_id = device;
 }
 
 void launch_tile(State& s, const TileProgram& tp) {
   DeviceGuard dg(s.device);
-  tp.upload(s.device);
   switch (tp.h.m) {
     case 6: launch_m<6>(s, tp); break;
     case 7: launch_m<7>(s, tp); break;

@@ -44,6 +44,7 @@ enum TOpType : uint8_t {
   TO_DENSE2,       // dense 4x4 on register bits 0..1
   TO_DENSE3,       // dense 8x8 on register bits 0..2
   TO_TRANSPOSE,    // register <-> thread qubit exchange through smem
+  TO_RELABEL,      // SWAP as a relabel: thread-bit -> qubit map changes, no data moves
 };
 
 struct TOp {
@@ -81,12 +82,13 @@ struct TileProgram {
   uint64_t gates = 0;       // source ops covered
   uint32_t transposes = 0;
   std::vector<uint64_t> source;  // gate indices, for diagnostics
-  // device copy (per device)
-  mutable void* dev = nullptr;
-  mutable int dev_id = -1;
-  ~TileProgram();
-  void upload(int device) const;
+  std::vector<unsigned char> blob;  // packed header + tables (the kernel parameter)
+  void pack();
 };
+
+// The packed program travels as a __grid_constant__ kernel parameter (constant
+// bank); the planner keeps every pass below this size.
+constexpr uint32_t kTileBlobBytes = 30 * 1024;
 
 struct TileOptions {
   uint32_t m = 12;  // tile qubits

@@ -342,6 +342,16 @@ struct Compiler {
           cfgs.push_back(c);
           cur = static_cast<int>(cfgs.size() - 1);
           x_open |= p.needmask;
+          // thread bits now name different qubits: refresh the per-thread index
+          bool thread_moved = false;
+          for (uint32_t k = 0; k < t; ++k)
+            if (c.thr[k] == a || c.thr[k] == b) thread_moved = true;
+          if (thread_moved) {
+            AOp r;
+            r.type = TO_RELABEL;
+            r.cfg = cur;
+            aops.push_back(r);
+          }
           break;
         }
         case PK::Mat1:
@@ -527,6 +537,11 @@ std::shared_ptr<TileProgram> finalize(Compiler& C, uint64_t gates, const std::ve
         ++tp->transposes;
         break;
       }
+      case TO_RELABEL: {
+        o.meta = static_cast<uint32_t>(tp->meta.size());
+        for (uint32_t k = 0; k < C.t; ++k) tp->meta.push_back(C.S[c.thr[k]]);
+        break;
+      }
     }
     tp->ops.push_back(o);
   }
@@ -538,6 +553,7 @@ std::shared_ptr<TileProgram> finalize(Compiler& C, uint64_t gates, const std::ve
   h.bytes = al(h.coef_off + tp->coef.size() * sizeof(double2));
   tp->gates = gates;
   tp->source = srcs;
+  tp->pack();
   return tp;
 }
 
@@ -652,32 +668,45 @@ void plan_tiles(uint32_t n, std::vector<Op>& ops, std::vector<Step>& steps, cons
     std::vector<char> tk(rem.size(), 0);
     const size_t cnt = scan(pops, rem, S, &tk);
     if (cnt == 0) throw RuntimeError("tile planner made no progress");
-    std::vector<const POp*> list;
-    std::vector<uint32_t> keep;
-    std::vector<uint64_t> srcs;
-    for (size_t i = 0; i < rem.size(); ++i) {
-      if (tk[i]) {
-        list.push_back(&pops[rem[i]]);
-        srcs.push_back(pops[rem[i]].op.gate_index);
-      } else {
-        keep.push_back(rem[i]);
+    std::vector<size_t> taken_pos;  // positions in rem, program order
+    for (size_t i = 0; i < rem.size(); ++i)
+      if (tk[i]) taken_pos.push_back(i);
+    // Any program-order prefix of the taken ops is dependency-closed, so a
+    // program too large for the parameter blob is cut to a fitting prefix.
+    size_t take = taken_pos.size();
+    std::shared_ptr<TileProgram> prog;
+    while (true) {
+      std::vector<const POp*> list;
+      std::vector<uint64_t> srcs;
+      for (size_t j = 0; j < take; ++j) {
+        list.push_back(&pops[rem[taken_pos[j]]]);
+        srcs.push_back(pops[rem[taken_pos[j]]].op.gate_index);
       }
+      Compiler C;
+      C.n = n;
+      C.m = m;
+      C.t = m - kTileR;
+      C.L = L;
+      for (int q = 0; q < 64; ++q) C.tb[q] = -1;
+      for (uint32_t q = 0; q < n; ++q)
+        if ((S >> q) & 1) {
+          C.tb[q] = static_cast<int>(C.S.size());
+          C.S.push_back(q);
+        }
+      C.compile(list);
+      prog = finalize(C, list.size(), srcs);
+      if (prog->h.bytes <= kTileBlobBytes || take == 1) break;
+      take = std::max<size_t>(1, take * 3 / 4);
     }
-    Compiler C;
-    C.n = n;
-    C.m = m;
-    C.t = m - kTileR;
-    C.L = L;
-    for (int q = 0; q < 64; ++q) C.tb[q] = -1;
-    for (uint32_t q = 0; q < n; ++q)
-      if ((S >> q) & 1) {
-        C.tb[q] = static_cast<int>(C.S.size());
-        C.S.push_back(q);
-      }
-    C.compile(list);
+    if (prog->h.bytes > kTileBlobBytes) throw RuntimeError("tile program for one op exceeds the parameter blob");
+    std::vector<char> used(rem.size(), 0);
+    for (size_t j = 0; j < take; ++j) used[taken_pos[j]] = 1;
+    std::vector<uint32_t> keep;
+    for (size_t i = 0; i < rem.size(); ++i)
+      if (!used[i]) keep.push_back(rem[i]);
     Step s;
     s.kind = Step::TileStep;
-    s.tile = finalize(C, list.size(), srcs);
+    s.tile = prog;
     steps.push_back(std::move(s));
     rem.swap(keep);
     emit_ready_opaque();
