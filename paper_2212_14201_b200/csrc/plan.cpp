@@ -1,6 +1,7 @@
 #include "plan.hpp"
 
 #include "fusion.hpp"
+#include "jit.hpp"
 #include "kernels.hpp"
 #include "tile.hpp"
 
@@ -49,6 +50,7 @@ std::unique_ptr<Plan> make_plan(uint32_t n, const qs_gate* gates, uint64_t count
   }
   if (plan->mode == QS_PLAN_TILED) {
     plan_tiles(n, ops, plan->steps);
+    compile_tile_steps(plan->steps);
   } else {
     for (auto& op : ops) {
       if (op.kind == OpKind::Identity) continue;

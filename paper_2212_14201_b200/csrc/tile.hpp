@@ -82,12 +82,11 @@ struct TileProgram {
   uint64_t gates = 0;       // source ops covered
   uint32_t transposes = 0;
   std::vector<uint64_t> source;  // gate indices, for diagnostics
-  std::vector<unsigned char> blob;  // packed header + tables (the kernel parameter)
-  void pack();
+  std::shared_ptr<struct JitModule> jit;  // specialised kernel (jit.hpp)
 };
 
-// The packed program travels as a __grid_constant__ kernel parameter (constant
-// bank); the planner keeps every pass below this size.
+// The coefficient table travels as a __grid_constant__ kernel parameter
+// (constant bank); the planner keeps every pass's tables below this size.
 constexpr uint32_t kTileBlobBytes = 30 * 1024;
 
 struct TileOptions {

@@ -553,7 +553,6 @@ std::shared_ptr<TileProgram> finalize(Compiler& C, uint64_t gates, const std::ve
   h.bytes = al(h.coef_off + tp->coef.size() * sizeof(double2));
   tp->gates = gates;
   tp->source = srcs;
-  tp->pack();
   return tp;
 }
 

@@ -258,8 +258,3 @@ int te_run(uint32_t n, const qs_gate* gates, uint64_t count, uint32_t mode, uint
 
 }  // extern "C"
 
-// TileProgram::pack lives in tile.cu (device TU); the emulator reads the
-// unpacked tables, so packing is a no-op here.
-namespace qsb {
-void TileProgram::pack() {}
-}  // namespace qsb
