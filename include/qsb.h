@@ -142,6 +142,8 @@ int qs_plan_enqueue(qs_state_t s, qs_plan_t p);
 /* Execute with a CUDA event around every step; step_ms[i] receives the device
  * time of step i (qs_plan_stats' launch count entries).                       */
 int qs_plan_execute_timed(qs_state_t s, qs_plan_t p, float* step_ms);
+/* Executes steps [first, first+count) only (diagnostics, per-pass profiling). */
+int qs_plan_execute_range(qs_state_t s, qs_plan_t p, uint64_t first, uint64_t count);
 /* Planner statistics: passes (HBM sweeps) and kernel launches per execute.   */
 int qs_plan_stats(qs_plan_t p, uint64_t* passes, uint64_t* launches, uint64_t* gates);
 

@@ -89,6 +89,7 @@ _SIGS = {
     "qs_plan_execute": (C.c_int, [_P, _P]),
     "qs_plan_stats": (C.c_int, [_P, _U64P, _U64P, _U64P]),
     "qs_plan_enqueue": (C.c_int, [_P, _P]),
+    "qs_plan_execute_range": (C.c_int, [_P, _P, C.c_uint64, C.c_uint64]),
     "qs_plan_execute_timed": (C.c_int, [_P, _P, C.POINTER(C.c_float)]),
     "qs_stream": (C.c_void_p, [_P]),
     "qs_fuse": (C.c_int, [_GP, C.c_uint64, C.c_uint32, C.c_uint32, C.POINTER(_P)]),

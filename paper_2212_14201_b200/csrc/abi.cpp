@@ -340,6 +340,18 @@ int qs_plan_enqueue(qs_state_t h, qs_plan_t p) {
   });
 }
 
+int qs_plan_execute_range(qs_state_t h, qs_plan_t p, uint64_t first, uint64_t count) {
+  return guarded([&] {
+    if (!p) throw ValidationError("null plan");
+    State& s = st(h);
+    const auto& steps = p->p->steps;
+    if (first > steps.size()) throw ValidationError("step range out of bounds");
+    const uint64_t last = std::min<uint64_t>(steps.size(), first + count);
+    for (uint64_t i = first; i < last; ++i) execute_step(s, steps[i]);
+    s.sync();
+  });
+}
+
 int qs_plan_execute_timed(qs_state_t h, qs_plan_t p, float* step_ms) {
   return guarded([&] {
     if (!p) throw ValidationError("null plan");

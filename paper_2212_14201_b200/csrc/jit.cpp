@@ -266,6 +266,9 @@ struct Gen {
         default: throw RuntimeError("jit: unknown micro-op");
       }
     }
+    // Relabels (free SWAPs) make threads store where other threads loaded; with
+    // no transpose barrier in the pass, every load must retire before any store.
+    if (ti == 0 && std::memcmp(&h.load, &h.store, sizeof(TileConfigAddr)) != 0) s << "    __syncthreads();\n";
     for (int p = 0; p < 16; ++p) {
       unsigned long long off = 0;
       for (int k = 0; k < 4; ++k)
@@ -382,7 +385,8 @@ void compile_tile_steps(std::vector<Step>& steps) {
       continue;
     }
     if (const char* dir = std::getenv("QSB_JIT_DUMP")) {  // diagnostics: keep the generated source
-      if (FILE* f = std::fopen((std::string(dir) + "/" + name + ".cu").c_str(), "w")) {
+      const std::string fn = std::string(dir) + "/step" + std::to_string(&st - steps.data()) + "_" + name + ".cu";
+      if (FILE* f = std::fopen(fn.c_str(), "w")) {
         std::fputs(src.c_str(), f);
         std::fclose(f);
       }

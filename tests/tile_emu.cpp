@@ -242,7 +242,10 @@ int te_run(uint32_t n, const qs_gate* gates, uint64_t count, uint32_t mode, uint
     }
     std::vector<cd> a(size_t(1) << n);
     std::memcpy(a.data(), amps, a.size() * sizeof(cd));
-    for (const auto& s : steps) {
+    const char* lim = std::getenv("TE_MAX_STEPS");
+    const size_t max_steps = lim ? static_cast<size_t>(std::atoll(lim)) : steps.size();
+    for (size_t i = 0; i < steps.size() && i < max_steps; ++i) {
+      const auto& s = steps[i];
       if (s.kind == qsb::Step::OpStep) emu_op(a, n, s.op);
       else emu_tile(a, *s.tile);
     }
