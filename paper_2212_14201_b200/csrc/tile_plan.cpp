@@ -1,6 +1,7 @@
 // Tile-pass planner (host): partitions a gate list into shared-memory tile
 // passes and compiles each pass into a micro-program for tile.cu.
 #include <algorithm>
+#include <cstdio>
 #include <cmath>
 #include <cstdlib>
 #include <cstring>
@@ -261,33 +262,114 @@ struct Compiler {
     return has_reg(c, tb[p.op.targets[0]]);
   }
 
-  void compile(const std::vector<const POp*>& list) {
-    // initial (load) config: coalesced, registers from the first needs
-    size_t first = list.size();
-    for (size_t i = 0; i < list.size(); ++i)
-      if (needs_reg(*list[i])) {
-        first = i;
-        break;
+  // --- intra-pass scheduling ------------------------------------------------
+  // The pass's ops form a DAG (shared qubits; diagonal ops commute with each
+  // other).  We run every op whose targets are register qubits, and when none
+  // is left choose the next register set greedily: fill the 4 slots one by one
+  // with the tile bit that lets the most pending ops run (a topological sweep
+  // in program order), so transposes are amortised over as many gates as
+  // possible.
+  std::vector<std::vector<int>> succ;
+  std::vector<int> indeg;
+
+  void build_dag(const std::vector<const POp*>& list) {
+    const size_t N = list.size();
+    succ.assign(N, {});
+    indeg.assign(N, 0);
+    for (size_t j = 0; j < N; ++j)
+      for (size_t i = 0; i < j; ++i) {
+        if (!(list[i]->qmask & list[j]->qmask)) continue;
+        if (list[i]->k == PK::Diag && list[j]->k == PK::Diag) continue;
+        succ[i].push_back(static_cast<int>(j));
+        ++indeg[j];
       }
-    Cfg c0;
-    if (first < list.size() && list[first]->k != PK::Dense) {
-      c0 = choose(nullptr, list, first, /*exclude_low=*/true);
-      // choose() may have placed a low bit as the required target: that op
-      // then simply transposes first.
-      bool bad = false;
-      for (int k = 0; k < kTileR; ++k)
-        if (c0.reg[k] < static_cast<int>(L)) bad = true;
-      if (bad) c0 = default_cfg();
-    } else {
-      c0 = default_cfg();
+  }
+
+  bool sat_partial(const Cfg& c, const POp& p) const {
+    if (!needs_reg(p)) return true;
+    if (p.k == PK::Dense) {
+      const size_t kd = p.op.targets.size();
+      for (size_t b = 0; b < kd; ++b)
+        if (c.reg[b] != tb[p.op.targets[kd - 1 - b]]) return false;
+      return true;
     }
-    cfgs.push_back(c0);
+    return has_reg(c, tb[p.op.targets[0]]);
+  }
+
+  // (ops runnable with register set c without a transpose, -first index of a
+  // runnable register op) from the current done/indeg state.
+  std::pair<int, int> simulate(const Cfg& c, const std::vector<const POp*>& list, const std::vector<char>& done,
+                               std::vector<int>& scratch) const {
+    const size_t N = list.size();
+    scratch = indeg;
+    int cnt = 0, first = -1;
+    for (size_t j = 0; j < N; ++j) {
+      if (done[j] || scratch[j] != 0) continue;
+      if (!sat_partial(c, *list[j])) continue;
+      ++cnt;
+      if (first < 0 && needs_reg(*list[j])) first = static_cast<int>(j);
+      for (int s2 : succ[j]) --scratch[s2];
+    }
+    return {cnt, first < 0 ? -1000000 : -first};
+  }
+
+  Cfg choose_greedy(const Cfg* cur, const std::vector<const POp*>& list, const std::vector<char>& done,
+                    bool exclude_low) {
+    Cfg c;
+    for (int k = 0; k < kTileR; ++k) c.reg[k] = -1;
+    std::vector<char> placed(m, 0);
+    // a blocked dense op at the front dictates exact slots
+    for (size_t j = 0; j < list.size(); ++j) {
+      if (done[j] || indeg[j] != 0 || !needs_reg(*list[j])) continue;
+      if (cur && sat_partial(*cur, *list[j])) continue;
+      if (list[j]->k == PK::Dense) {
+        const size_t kd = list[j]->op.targets.size();
+        for (size_t b = 0; b < kd; ++b) {
+          const int x = tb[list[j]->op.targets[kd - 1 - b]];
+          c.reg[b] = x;
+          placed[x] = 1;
+        }
+      }
+      break;
+    }
+    std::vector<int> scratch;
+    for (int k = 0; k < kTileR; ++k) {
+      if (c.reg[k] >= 0) continue;
+      int best = -1;
+      std::pair<int, int> bs{-1, -2000000};
+      for (uint32_t y = 0; y < m; ++y) {
+        if (placed[y] || (exclude_low && y < L)) continue;
+        c.reg[k] = static_cast<int>(y);
+        std::pair<int, int> sc = simulate(c, list, done, scratch);
+        // prefer non-lane bits on ties (keeps the store layout coalesced)
+        const bool better = sc > bs || (sc == bs && y >= L && best >= 0 && best < static_cast<int>(L));
+        if (better) {
+          bs = sc;
+          best = static_cast<int>(y);
+        }
+      }
+      if (best < 0)
+        for (uint32_t y = 0; y < m; ++y)
+          if (!placed[y]) {
+            best = static_cast<int>(y);
+            break;
+          }
+      c.reg[k] = best;
+      placed[best] = 1;
+    }
+    fill_threads(c);
+    return c;
+  }
+
+  void compile(const std::vector<const POp*>& list) {
+    build_dag(list);
+    std::vector<char> done(list.size(), 0);
+    cfgs.push_back(choose_greedy(nullptr, list, done, /*exclude_low=*/true));
     int cur = 0;
 
     int open = -1;           // open PHASE aop
     uint64_t x_open = 0;     // non-diagonal targets since it opened
-    for (size_t i = 0; i < list.size(); ++i) {
-      const POp& p = *list[i];
+    auto emit = [&](const POp& p) {
       uint64_t ctrl = 0;
       for (auto q : p.op.controls) ctrl |= bit(q);
       switch (p.k) {
@@ -357,7 +439,6 @@ struct Compiler {
         case PK::Mat1:
         case PK::Flip:
         case PK::Dense: {
-          if (!satisfied(cfgs[cur], p)) transpose_to(cur, choose(&cfgs[cur], list, i, false));
           AOp a;
           a.cfg = cur;
           a.pred = ctrl;
@@ -379,6 +460,19 @@ struct Compiler {
         }
         case PK::Opaque: throw RuntimeError("tile compiler: opaque op inside a pass");
       }
+    };
+    size_t remaining = list.size();
+    while (remaining) {
+      for (size_t j = 0; j < list.size(); ++j) {  // one sweep = closure (index order is topological)
+        if (done[j] || indeg[j] != 0) continue;
+        if (!sat_partial(cfgs[cur], *list[j])) continue;
+        emit(*list[j]);
+        done[j] = 1;
+        --remaining;
+        for (int s2 : succ[j]) --indeg[s2];
+      }
+      if (!remaining) break;
+      transpose_to(cur, choose_greedy(&cfgs[cur], list, done, /*exclude_low=*/false));
     }
     if (!store_ok(cfgs[cur])) {
       Cfg c = cfgs[cur];
@@ -556,6 +650,13 @@ std::shared_ptr<TileProgram> finalize(Compiler& C, uint64_t gates, const std::ve
   return tp;
 }
 
+std::vector<uint32_t> C_S_debug(uint64_t S, uint32_t n) {
+  std::vector<uint32_t> v;
+  for (uint32_t q = 0; q < n; ++q)
+    if ((S >> q) & 1) v.push_back(q);
+  return v;
+}
+
 }  // namespace
 
 TileOptions tile_options_from_env() {
@@ -706,6 +807,16 @@ void plan_tiles(uint32_t n, std::vector<Op>& ops, std::vector<Step>& steps, cons
     Step s;
     s.kind = Step::TileStep;
     s.tile = prog;
+    if (std::getenv("QSB_PLAN_DEBUG")) {
+      int counts[16] = {0};
+      for (const auto& o : prog->ops) counts[o.type & 15]++;
+      std::fprintf(stderr, "pass %zu: ops=%zu gates=%zu transposes=%u mat1=%d flip=%d phase=%d dense=%d relabel=%d S=",
+                   steps.size(), prog->ops.size(), static_cast<size_t>(take), prog->transposes,
+                   counts[TO_MAT1] + counts[TO_MAT1_REAL] + counts[TO_MAT1_RX], counts[TO_FLIP], counts[TO_PHASE],
+                   counts[TO_DENSE2] + counts[TO_DENSE3], counts[TO_RELABEL]);
+      for (auto q : C_S_debug(S, n)) std::fprintf(stderr, "%u,", q);
+      std::fprintf(stderr, "\n");
+    }
     steps.push_back(std::move(s));
     rem.swap(keep);
     emit_ready_opaque();
