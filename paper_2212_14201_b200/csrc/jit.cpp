@@ -230,26 +230,61 @@ struct Gen {
     emit_G(mt + 2 * TB + 8, false);
   }
 
+  bool prefetch = true;
+
   std::string run(const std::string& kname, uint32_t threads, uint32_t minb) {
     const TileHeader& h = tp.h;
     s << "struct __align__(16) QsbCoef { double2 c[" << std::max<size_t>(1, tp.coef.size()) << "]; };\n";
     s << "extern \"C\" __global__ void __launch_bounds__(" << threads << ", " << minb << ") " << kname
       << "(double2* __restrict__ amps, const __grid_constant__ QsbCoef P) {\n";
+    const uint32_t T = 1u << h.t;
     s << "  extern __shared__ double2 sm[];\n";
     s << "  const unsigned tid = threadIdx.x;\n";
-    s << "  for (unsigned long long tile = blockIdx.x; tile < " << h.ntiles << "ull; tile += gridDim.x) {\n";
-    s << "    unsigned long long base = tile;\n";
+    // thread contribution to the global index under the load layout
+    s << "  const unsigned long long TL = 0ull";
+    for (uint32_t k = 0; k < h.t; ++k) s << " | ((unsigned long long)((tid >> " << k << ") & 1u) << " << h.load.tq[k] << ")";
+    s << ";\n";
+    s << "  auto base_of = [&](unsigned long long b) {\n";
     for (uint32_t b = 0; b < h.m && h.ntiles > 1; ++b) {
       const uint32_t q = h.S[b];
-      s << "    base = ((base >> " << q << ") << " << (q + 1) << ") | (base & " << hexll((1ull << q) - 1) << ");\n";
+      s << "    b = ((b >> " << q << ") << " << (q + 1) << ") | (b & " << hexll((1ull << q) - 1) << ");\n";
     }
-    emit_G(h.load.tq, true);
+    s << "    return b;\n  };\n";
+    unsigned long long loff[16];
     for (int p = 0; p < 16; ++p) {
-      unsigned long long off = 0;
+      loff[p] = 0;
       for (int k = 0; k < 4; ++k)
-        if ((p >> k) & 1) off |= h.load.rs[k];
-      name[p] = fresh();
-      s << "    const double2 " << name[p] << " = __ldcs(amps + (G | " << hexll(off) << "));\n";
+        if ((p >> k) & 1) loff[p] |= h.load.rs[k];
+    }
+    if (prefetch) {
+      // Each thread stages its own 16 amplitudes of the next tile in its own
+      // shared-memory slots (slot p*T + tid: conflict-free) with cp.async, so
+      // HBM reads of tile i+1 overlap the arithmetic of tile i.
+      s << "  double2* const PB = sm + " << (tp.transposes ? (1u << h.m) : 0u) << ";\n";
+      s << "  auto prefetch = [&](unsigned long long t) {\n";
+      s << "    const unsigned long long g = base_of(t) | TL;\n";
+      for (int p = 0; p < 16; ++p)
+        s << "    cp_async16(PB + " << p * T << " + tid, amps + (g | " << hexll(loff[p]) << "));\n";
+      s << "    cp_async_commit();\n  };\n";
+      s << "  unsigned long long tile = blockIdx.x;\n";
+      s << "  if (tile < " << h.ntiles << "ull) prefetch(tile);\n";
+      s << "  for (; tile < " << h.ntiles << "ull; tile += gridDim.x) {\n";
+      s << "    const unsigned long long base = base_of(tile);\n";
+      s << "    unsigned long long G = base | TL;\n";
+      s << "    cp_async_wait_all();\n";
+      for (int p = 0; p < 16; ++p) {
+        name[p] = fresh();
+        s << "    const double2 " << name[p] << " = PB[" << p * T << " + tid];\n";
+      }
+      s << "    { const unsigned long long nt = tile + gridDim.x; if (nt < " << h.ntiles << "ull) prefetch(nt); }\n";
+    } else {
+      s << "  for (unsigned long long tile = blockIdx.x; tile < " << h.ntiles << "ull; tile += gridDim.x) {\n";
+      s << "    const unsigned long long base = base_of(tile);\n";
+      s << "    unsigned long long G = base | TL;\n";
+      for (int p = 0; p < 16; ++p) {
+        name[p] = fresh();
+        s << "    const double2 " << name[p] << " = __ldcs(amps + (G | " << hexll(loff[p]) << "));\n";
+      }
     }
     int ti = 0;
     for (const TOp& o : tp.ops) {
@@ -282,6 +317,12 @@ struct Gen {
 
 const char* kPreamble = R"(
 // Generated by libqsb (csrc/jit.cpp) for one shared-memory tile pass.
+__device__ __forceinline__ void cp_async16(double2* smem, const double2* gmem) {
+  const unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(smem));
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(s), "l"(gmem) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_group 0;\n" ::: "memory"); }
 __device__ __forceinline__ double2 cmul(double2 a, double2 b) {
   return make_double2(fma(a.x, b.x, -a.y * b.y), fma(a.x, b.y, a.y * b.x));
 }
@@ -360,11 +401,26 @@ uint64_t fnv(const std::string& s) {
 uint64_t jit_compiles() { return g_compiles.load(); }
 uint64_t jit_cache_hits() { return g_hits.load(); }
 
+namespace {
+bool prefetch_enabled() {
+  const char* e = std::getenv("QSB_TILE_PREFETCH");
+  return !e || std::atoi(e) != 0;
+}
+uint32_t min_blocks_for(const TileProgram& tp) {
+  if (const char* e = std::getenv("QSB_TILE_MINB")) return static_cast<uint32_t>(std::max(1, std::atoi(e)));
+  return prefetch_enabled() ? 1 : (tp.h.m >= 13 ? 1 : 2);
+}
+size_t smem_for(const TileProgram& tp) {
+  const size_t tile_bytes = (size_t(1) << tp.h.m) * sizeof(double2);
+  return (tp.transposes ? tile_bytes : 0) + (prefetch_enabled() ? tile_bytes : 0);
+}
+}  // namespace
+
 std::string tile_source(const TileProgram& tp, const std::string& name) {
   Gen g(tp);
+  g.prefetch = prefetch_enabled();
   const uint32_t threads = 1u << tp.h.t;
-  const uint32_t minb = tp.h.m >= 13 ? 1 : 2;
-  return std::string(kPreamble) + g.run(name, threads, minb);
+  return std::string(kPreamble) + g.run(name, threads, min_blocks_for(tp));
 }
 
 void compile_tile_steps(std::vector<Step>& steps) {
@@ -395,7 +451,8 @@ void compile_tile_steps(std::vector<Step>& steps) {
     jm->name = name;
     jm->source = std::move(src);
     jm->threads = 1u << tp.h.t;
-    jm->min_blocks = tp.h.m >= 13 ? 1 : 2;
+    jm->min_blocks = min_blocks_for(tp);
+    jm->smem = smem_for(tp);
     cache()[jm->source] = jm;
     tp.jit = jm;
     fresh.push_back(jm);
@@ -430,7 +487,7 @@ void launch_tile(State& s, const TileProgram& tp) {
   JitModule& jm = *tp.jit;
   const Driver& d = driver();
   const int dev = s.device & 63;
-  const size_t smem = tp.transposes ? (size_t(1) << tp.h.m) * sizeof(double2) : 0;
+  const size_t smem = jm.smem;
   CUfunction fn;
   int per_sm;
   {
@@ -441,7 +498,7 @@ void launch_tile(State& s, const TileProgram& tp) {
       CUfunction f;
       cu_check(d.moduleGetFunction(&f, mod, jm.name.c_str()), "cuModuleGetFunction");
       cu_check(d.funcSetAttribute(f, CU_FUNC_ATTRIBUTE_MAX_DYNAMIC_SHARED_SIZE_BYTES,
-                                  static_cast<int>((size_t(1) << tp.h.m) * sizeof(double2))),
+                                  static_cast<int>(std::max<size_t>(smem, 1))),
                "cuFuncSetAttribute");
       int occ = 0;
       cu_check(d.occupancy(&occ, f, static_cast<int>(jm.threads), smem), "cuOccupancyMaxActiveBlocksPerMultiprocessor");

@@ -28,6 +28,7 @@ struct JitModule {
   std::vector<char> cubin;
   uint32_t threads = 0;
   uint32_t min_blocks = 1;
+  size_t smem = 0;      // dynamic shared memory per CTA
   std::mutex mu;
   void* mod[64] = {};   // CUmodule per device
   void* fn[64] = {};    // CUfunction per device
