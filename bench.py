@@ -102,6 +102,21 @@ class ClockSampler:
                 "reasons": sorted(reasons), "samples": len(sm)}
 
 
+def ncu_traffic(workload, plan):
+    """dram__bytes_read.sum + dram__bytes_write.sum of one tile pass from the
+    committed ncu --set full capture (profiles/), per launch; None if absent."""
+    if workload != "random30" or plan != "tiled":
+        return None
+    try:
+        with open(os.path.join(ROOT, "profiles", "r1", "ncu_full_tile30.json")) as f:
+            d = json.load(f)
+        rd = float(d["dram__bytes_read.sum"][0]) * {"Gbyte": 1e9, "Mbyte": 1e6}[d["dram__bytes_read.sum"][1]]
+        wr = float(d["dram__bytes_write.sum"][0]) * {"Gbyte": 1e9, "Mbyte": 1e6}[d["dram__bytes_write.sum"][1]]
+        return rd + wr
+    except Exception:
+        return None
+
+
 def build_program(workload):
     from paper_2212_14201_b200 import qforge as Q
     gen, args, n = WORKLOADS[workload]
@@ -262,7 +277,7 @@ def main():
     avg_pass_ms = sum(pass_ms) / len(pass_ms) if pass_ms else 0.0
     achieved = (2 * state_bytes) / (avg_pass_ms / 1e3) / 1e9 if avg_pass_ms else 0.0
     roofline = {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
-                "frac": round(achieved / peak, 4), "traffic": None,
+                "frac": round(achieved / peak, 4), "traffic": ncu_traffic(args.workload, args.plan),
                 "kernel": "k_tile<12>" if args.plan == "tiled" else "per-gate kernels",
                 "algorithmic_bytes_per_launch": 2 * state_bytes, "launches_per_step": stats["launches"],
                 "avg_launch_ms": round(avg_pass_ms, 4), "peak_kind": peak_kind,

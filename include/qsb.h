@@ -192,9 +192,11 @@ int qs_sample_seeded(qs_state_t s, uint64_t seed, uint64_t shots, int exact, uin
  * out[2t], out[2t+1] = real and imaginary part of <psi|P_t|psi>.            */
 int qs_expect_pauli(qs_state_t s, const char* letters, uint32_t nterms, double* out);
 
-/* --- test hooks ------------------------------------------------------------ */
-/* The sampler's cumulative array (exact or parallel scan) and its total.      */
-int qs_debug_cumulative(qs_state_t s, int exact, double* cum_out, double* total_out);
+/* BasisSampler's cumulative array cum_i = sum_{j<=i} |a_j|^2 (host copy,
+ * 2^n doubles) and its total, computed on the device with the serial-
+ * equivalent exact scan: bit-identical to the reference's left-to-right
+ * double accumulation                                  [statevector.hpp:544-552] */
+int qs_cumulative(qs_state_t s, double* cum_out, double* total_out);
 
 #ifdef __cplusplus
 }

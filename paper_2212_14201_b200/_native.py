@@ -107,7 +107,7 @@ _SIGS = {
     "qs_sample": (C.c_int, [_P, _DP, C.c_uint64, C.c_int, _U64P]),
     "qs_sample_seeded": (C.c_int, [_P, C.c_uint64, C.c_uint64, C.c_int, _U64P]),
     "qs_expect_pauli": (C.c_int, [_P, C.c_char_p, C.c_uint32, _DP]),
-    "qs_debug_cumulative": (C.c_int, [_P, C.c_int, _DP, _DP]),
+    "qs_cumulative": (C.c_int, [_P, _DP, _DP]),
 }
 
 EXPORTED = tuple(_SIGS)

@@ -531,20 +531,24 @@ int qs_expect_pauli(qs_state_t h, const char* letters, uint32_t nterms, double* 
   });
 }
 
-int qs_debug_cumulative(qs_state_t h, int exact, double* cum_out, double* total_out) {
+int qs_cumulative(qs_state_t h, double* cum_out, double* total_out) {
   return guarded([&] {
     State& s = st(h);
+    if (!cum_out) throw ValidationError("null cumulative buffer");
     DeviceGuard dg(s.device);
     double* d = nullptr;
-    QSB_CUDA(cudaMalloc(&d, s.size * sizeof(double)));
-    double total = 0;
-    if (exact) {
-      total = exact_cumulative(s, nullptr, d);
-    } else {
-      cudaFree(d);
-      throw ValidationError("qs_debug_cumulative: only the exact scan is exposed");
+    if (cudaMalloc(&d, s.size * sizeof(double)) != cudaSuccess) {
+      cudaGetLastError();
+      throw MemoryError("cannot allocate the cumulative array");
     }
-    QSB_CUDA(cudaMemcpy(cum_out, d, s.size * sizeof(double), cudaMemcpyDeviceToHost));
+    double total = 0;
+    try {
+      total = exact_cumulative(s, nullptr, d);
+      QSB_CUDA(cudaMemcpy(cum_out, d, s.size * sizeof(double), cudaMemcpyDeviceToHost));
+    } catch (...) {
+      cudaFree(d);
+      throw;
+    }
     cudaFree(d);
     if (total_out) *total_out = total;
   });

@@ -1,0 +1,35 @@
+"""The reference's own GoogleTest sources (statevector, simulator, bench,
+variational), compiled UNMODIFIED against the drop-in qforge facade
+(paper_2212_14201_b200/include/qforge) and libqsb.so, run on the GPU.
+
+The binaries are built here by `make -C paper_2212_14201_b200/csrc droptests`
+(needs /root/reference at build time; __graft_entry__.build() does it) and
+travel to the GPU box as build artefacts.
+"""
+import os
+import subprocess
+
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+DROP = os.path.join(ROOT, "build", "droptest")
+
+pytestmark = pytest.mark.gpu
+
+# Tests that exercise reference internals with no GPU meaning: the OpenMP
+# worker-count contract is vacuous on the GPU (KernelOptions is accepted and
+# ignored) and the two detail:: helpers are host-side compatibility shims.
+INTERNALS = "-GroupIndexer.*:Kernels.ChunkedSumMatchesSerialBitwise"
+
+
+@pytest.mark.parametrize("suite", ["statevector_test", "simulator_test", "bench_test", "variational_test"])
+def test_reference_suite_passes_against_dropin(suite):
+    exe = os.path.join(DROP, suite)
+    assert os.path.exists(exe), "drop-in test binaries not built (run __graft_entry__.build() with /root/reference)"
+    args = [exe]
+    if suite == "statevector_test":
+        args.append("--gtest_filter=" + INTERNALS)
+    out = subprocess.run(args, capture_output=True, text=True, timeout=600)
+    tail = (out.stdout[-3000:] + out.stderr[-3000:])
+    assert out.returncode == 0, tail
+    assert "[  PASSED  ]" in out.stdout, tail

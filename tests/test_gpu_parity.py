@@ -119,7 +119,7 @@ def test_exact_cumulative_is_bitwise_serial(n, seed):
     sv = Q.StateVector.from_amplitudes(n, a)
     cum = np.empty(a.size)
     tot = N.C.c_double()
-    N.check(N.lib().qs_debug_cumulative(sv.handle(), 1, N.dptr(cum), N.C.byref(tot)))
+    N.check(N.lib().qs_cumulative(sv.handle(), N.dptr(cum), N.C.byref(tot)))
     want, wtot = _oracle_serial_cum(a)
     assert tot.value == wtot
     assert np.array_equal(cum.view(np.uint64), want.view(np.uint64))
