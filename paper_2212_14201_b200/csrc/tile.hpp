@@ -22,6 +22,7 @@
 #pragma once
 
 #include <cstdint>
+#include <cstdlib>
 #include <memory>
 #include <vector>
 
@@ -93,12 +94,26 @@ struct TileOptions {
   uint32_t m = 12;  // tile qubits
   uint32_t low = 4; // qubits 0..low-1 always in the tile: 256 B contiguous runs
                     // (measured: 128 B runs 70% of HBM per pass, 256 B 80%)
+  bool remap = true;  // plan-level qubit relabelling (low slots hold the qubits needed next)
 };
 TileOptions tile_options_from_env();
 
 void plan_tiles(uint32_t n, std::vector<Op>& ops, std::vector<Step>& steps, const TileOptions& opt);
+// Plans with and without qubit relabelling (unless fixed by QSB_TILE_REMAP)
+// and keeps the plan with fewer HBM passes.
 inline void plan_tiles(uint32_t n, std::vector<Op>& ops, std::vector<Step>& steps) {
-  plan_tiles(n, ops, steps, tile_options_from_env());
+  TileOptions o = tile_options_from_env();
+  if (std::getenv("QSB_TILE_REMAP")) {
+    plan_tiles(n, ops, steps, o);
+    return;
+  }
+  std::vector<Op> copy = ops;
+  std::vector<Step> plain, remapped;
+  o.remap = false;
+  plan_tiles(n, copy, plain, o);
+  o.remap = true;
+  plan_tiles(n, ops, remapped, o);
+  steps = remapped.size() < plain.size() ? std::move(remapped) : std::move(plain);
 }
 void launch_tile(State& s, const TileProgram& tp);
 

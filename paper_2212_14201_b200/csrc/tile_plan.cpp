@@ -663,10 +663,96 @@ TileOptions tile_options_from_env() {
   TileOptions o;
   if (const char* e = std::getenv("QSB_TILE_M")) o.m = static_cast<uint32_t>(std::atoi(e));
   if (const char* e = std::getenv("QSB_TILE_LOW")) o.low = static_cast<uint32_t>(std::atoi(e));
+  if (const char* e = std::getenv("QSB_TILE_REMAP")) o.remap = std::atoi(e) != 0;
   o.m = std::max<uint32_t>(8, std::min<uint32_t>(kTileMaxM, o.m));
   o.low = std::min<uint32_t>(5, o.low);
   return o;
 }
+
+namespace {
+
+// A POp with its qubits renamed through the logical -> physical map.
+POp to_physical(const POp& p, const std::vector<uint32_t>& perm) {
+  POp q = p;
+  for (auto& t : q.op.targets) t = perm[t];
+  for (auto& c : q.op.controls) c = perm[c];
+  q.qmask = 0;
+  q.needmask = 0;
+  for (auto c : q.op.controls) q.qmask |= bit(c);
+  for (auto t : q.op.targets) q.qmask |= bit(t);
+  if (p.needmask)
+    for (auto t : q.op.targets) q.needmask |= bit(t);
+  return q;
+}
+
+POp swap_rel(uint32_t a, uint32_t b) {
+  POp p;
+  p.k = PK::SwapRel;
+  p.op.kind = OpKind::Swap;
+  p.op.targets = {a, b};
+  p.qmask = p.needmask = bit(a) | bit(b);
+  return p;
+}
+
+// Chooses the tile set S (physical qubits) for the next pass: starting from the
+// always-resident low qubits, add the qubit that lets the most pending ops run.
+uint64_t choose_tile_set(const std::vector<POp>& phys, const std::vector<uint32_t>& rem, uint64_t S0, uint32_t m) {
+  uint64_t S = S0;
+  size_t cur = scan(phys, rem, S, nullptr);
+  while (static_cast<uint32_t>(__builtin_popcountll(S)) < m) {
+    std::vector<uint32_t> cand;
+    uint64_t seen = S;
+    {
+      std::vector<char> tk(rem.size(), 0);
+      scan(phys, rem, S, &tk);
+      size_t looked = 0;
+      for (size_t i = 0; i < rem.size() && looked < 256; ++i) {
+        if (tk[i]) continue;
+        ++looked;
+        uint64_t nm = phys[rem[i]].needmask & ~seen;
+        while (nm) {
+          const uint32_t q = static_cast<uint32_t>(__builtin_ctzll(nm));
+          nm &= nm - 1;
+          cand.push_back(q);
+          seen |= bit(q);
+        }
+      }
+    }
+    if (cand.empty()) break;
+    size_t best_cnt = cur;
+    int best = -1;
+    for (auto q : cand) {
+      const size_t c = scan(phys, rem, S | bit(q), nullptr);
+      if (c > best_cnt) {
+        best_cnt = c;
+        best = static_cast<int>(q);
+      }
+    }
+    if (best < 0) {
+      // no single qubit helps: add the need set of the first blocked op
+      std::vector<char> tk(rem.size(), 0);
+      scan(phys, rem, S, &tk);
+      bool added = false;
+      for (size_t i = 0; i < rem.size(); ++i) {
+        if (tk[i] || phys[rem[i]].k == PK::Opaque) continue;
+        const uint64_t ns = S | phys[rem[i]].needmask;
+        if (static_cast<uint32_t>(__builtin_popcountll(ns)) <= m && scan(phys, rem, ns, nullptr) > cur) {
+          S = ns;
+          cur = scan(phys, rem, S, nullptr);
+          added = true;
+        }
+        break;
+      }
+      if (!added) break;
+      continue;
+    }
+    S |= bit(static_cast<uint32_t>(best));
+    cur = best_cnt;
+  }
+  return S;
+}
+
+}  // namespace
 
 void plan_tiles(uint32_t n, std::vector<Op>& ops, std::vector<Step>& steps, const TileOptions& opt) {
   std::vector<POp> pops = preprocess(ops);
@@ -684,16 +770,29 @@ void plan_tiles(uint32_t n, std::vector<Op>& ops, std::vector<Step>& steps, cons
   const uint32_t L = std::min<uint32_t>(opt.low, m - kTileR);
   const uint64_t lowmask = (1ull << L) - 1;
   const uint64_t allmask = n >= 64 ? ~0ull : (1ull << n) - 1;
+  const bool remap = opt.remap && n > m;
+
+  // Logical -> physical qubit map.  The low L physical qubits are in every
+  // tile (coalescing); relabel SWAPs at pass ends move the qubits needed next
+  // into them for free.  Every plan ends in the identity layout.
+  std::vector<uint32_t> perm(n), inv(n);
+  for (uint32_t q = 0; q < n; ++q) perm[q] = inv[q] = q;
+  std::vector<POp> phys(pops.size());
+  std::vector<POp> extra;  // relabel swaps appended to passes
+  extra.reserve(4096);
 
   std::vector<uint32_t> rem(pops.size());
   for (size_t i = 0; i < pops.size(); ++i) rem[i] = static_cast<uint32_t>(i);
 
+  auto refresh = [&]() {
+    for (auto idx : rem) phys[idx] = to_physical(pops[idx], perm);
+  };
   auto emit_ready_opaque = [&]() {
     uint64_t blocked = 0;
     std::vector<uint32_t> keep;
     keep.reserve(rem.size());
     for (auto idx : rem) {
-      const POp& p = pops[idx];
+      const POp& p = phys[idx];
       if (p.k == PK::Opaque && !(p.qmask & blocked)) {
         Step s;
         s.kind = Step::OpStep;
@@ -706,120 +805,178 @@ void plan_tiles(uint32_t n, std::vector<Op>& ops, std::vector<Step>& steps, cons
     }
     rem.swap(keep);
   };
+  auto swap_phys = [&](uint32_t a, uint32_t b) {
+    const uint32_t la = inv[a], lb = inv[b];
+    std::swap(perm[la], perm[lb]);
+    std::swap(inv[a], inv[b]);
+  };
+  auto identity = [&]() {
+    for (uint32_t q = 0; q < n; ++q)
+      if (perm[q] != q) return false;
+    return true;
+  };
 
-  emit_ready_opaque();
-  while (!rem.empty()) {
-    uint64_t S = n <= m ? allmask : lowmask;
-    size_t cur = scan(pops, rem, S, nullptr);
-    while (static_cast<uint32_t>(__builtin_popcountll(S)) < m) {
-      // candidates: need-qubits of not-yet-executable ops, in first-seen order
-      std::vector<uint32_t> cand;
-      uint64_t seen = S;
-      {
-        std::vector<char> tk(rem.size(), 0);
-        scan(pops, rem, S, &tk);
-        size_t looked = 0;
-        for (size_t i = 0; i < rem.size() && looked < 256; ++i) {
-          if (tk[i]) continue;
-          ++looked;
-          uint64_t nm = pops[rem[i]].needmask & ~seen;
-          while (nm) {
-            const uint32_t q = static_cast<uint32_t>(__builtin_ctzll(nm));
-            nm &= nm - 1;
-            cand.push_back(q);
-            seen |= bit(q);
-          }
-        }
+  auto compile_pass = [&](uint64_t S, const std::vector<const POp*>& list, const std::vector<uint64_t>& srcs) {
+    Compiler C;
+    C.n = n;
+    C.m = m;
+    C.t = m - kTileR;
+    C.L = L;
+    for (int q = 0; q < 64; ++q) C.tb[q] = -1;
+    for (uint32_t q = 0; q < n; ++q)
+      if ((S >> q) & 1) {
+        C.tb[q] = static_cast<int>(C.S.size());
+        C.S.push_back(q);
       }
-      if (cand.empty()) break;
-      size_t best_cnt = cur;
-      int best = -1;
-      for (auto q : cand) {
-        const size_t c = scan(pops, rem, S | bit(q), nullptr);
-        if (c > best_cnt) {
-          best_cnt = c;
-          best = static_cast<int>(q);
-        }
-      }
-      if (best < 0) {
-        // no single qubit helps: add the need set of the first blocked op
-        std::vector<char> tk(rem.size(), 0);
-        scan(pops, rem, S, &tk);
-        bool added = false;
-        for (size_t i = 0; i < rem.size(); ++i) {
-          if (tk[i] || pops[rem[i]].k == PK::Opaque) continue;
-          const uint64_t ns = S | pops[rem[i]].needmask;
-          if (static_cast<uint32_t>(__builtin_popcountll(ns)) <= m && scan(pops, rem, ns, nullptr) > cur) {
-            S = ns;
-            cur = scan(pops, rem, S, nullptr);
-            added = true;
-          }
-          break;
-        }
-        if (!added) break;
-        continue;
-      }
-      S |= bit(static_cast<uint32_t>(best));
-      cur = best_cnt;
-    }
-    // pad S to exactly m qubits (lowest unused) so tiles have a fixed shape
-    for (uint32_t q = 0; q < n && static_cast<uint32_t>(__builtin_popcountll(S)) < m; ++q) S |= bit(q);
-
-    std::vector<char> tk(rem.size(), 0);
-    const size_t cnt = scan(pops, rem, S, &tk);
-    if (cnt == 0) throw RuntimeError("tile planner made no progress");
-    std::vector<size_t> taken_pos;  // positions in rem, program order
-    for (size_t i = 0; i < rem.size(); ++i)
-      if (tk[i]) taken_pos.push_back(i);
-    // Any program-order prefix of the taken ops is dependency-closed, so a
-    // program too large for the parameter blob is cut to a fitting prefix.
-    size_t take = taken_pos.size();
-    std::shared_ptr<TileProgram> prog;
-    while (true) {
-      std::vector<const POp*> list;
-      std::vector<uint64_t> srcs;
-      for (size_t j = 0; j < take; ++j) {
-        list.push_back(&pops[rem[taken_pos[j]]]);
-        srcs.push_back(pops[rem[taken_pos[j]]].op.gate_index);
-      }
-      Compiler C;
-      C.n = n;
-      C.m = m;
-      C.t = m - kTileR;
-      C.L = L;
-      for (int q = 0; q < 64; ++q) C.tb[q] = -1;
-      for (uint32_t q = 0; q < n; ++q)
-        if ((S >> q) & 1) {
-          C.tb[q] = static_cast<int>(C.S.size());
-          C.S.push_back(q);
-        }
-      C.compile(list);
-      prog = finalize(C, list.size(), srcs);
-      if (prog->h.bytes <= kTileBlobBytes || take == 1) break;
-      take = std::max<size_t>(1, take * 3 / 4);
-    }
-    if (prog->h.bytes > kTileBlobBytes) throw RuntimeError("tile program for one op exceeds the parameter blob");
-    std::vector<char> used(rem.size(), 0);
-    for (size_t j = 0; j < take; ++j) used[taken_pos[j]] = 1;
-    std::vector<uint32_t> keep;
-    for (size_t i = 0; i < rem.size(); ++i)
-      if (!used[i]) keep.push_back(rem[i]);
-    Step s;
-    s.kind = Step::TileStep;
-    s.tile = prog;
+    C.compile(list);
+    return finalize(C, list.size(), srcs);
+  };
+  auto push_step = [&](std::shared_ptr<TileProgram> prog, uint64_t S, size_t gates) {
     if (std::getenv("QSB_PLAN_DEBUG")) {
       int counts[16] = {0};
       for (const auto& o : prog->ops) counts[o.type & 15]++;
       std::fprintf(stderr, "pass %zu: ops=%zu gates=%zu transposes=%u mat1=%d flip=%d phase=%d dense=%d relabel=%d S=",
-                   steps.size(), prog->ops.size(), static_cast<size_t>(take), prog->transposes,
+                   steps.size(), prog->ops.size(), gates, prog->transposes,
                    counts[TO_MAT1] + counts[TO_MAT1_REAL] + counts[TO_MAT1_RX], counts[TO_FLIP], counts[TO_PHASE],
                    counts[TO_DENSE2] + counts[TO_DENSE3], counts[TO_RELABEL]);
       for (auto q : C_S_debug(S, n)) std::fprintf(stderr, "%u,", q);
       std::fprintf(stderr, "\n");
     }
+    Step s;
+    s.kind = Step::TileStep;
+    s.tile = std::move(prog);
     steps.push_back(std::move(s));
+  };
+
+  refresh();
+  emit_ready_opaque();
+  while (!rem.empty()) {
+    refresh();
+    uint64_t S = choose_tile_set(phys, rem, n <= m ? allmask : lowmask, m);
+    std::vector<char> tk(rem.size(), 0);
+    size_t cnt = scan(phys, rem, S, &tk);
+    if (cnt == 0) throw RuntimeError("tile planner made no progress");
+    const bool last = cnt == rem.size();
+    // pad S to exactly m qubits: on the last pass prefer displaced positions
+    // (so the layout can be restored for free), else the lowest unused
+    if (last && remap)
+      for (uint32_t q = 0; q < n && static_cast<uint32_t>(__builtin_popcountll(S)) < m; ++q)
+        if (inv[q] != q) S |= bit(q);
+    for (uint32_t q = 0; q < n && static_cast<uint32_t>(__builtin_popcountll(S)) < m; ++q) S |= bit(q);
+
+    std::vector<size_t> taken_pos;  // positions in rem, program order
+    for (size_t i = 0; i < rem.size(); ++i)
+      if (tk[i]) taken_pos.push_back(i);
+
+    // Any program-order prefix of the taken ops is dependency-closed, so a
+    // program too large for the parameter blob is cut to a fitting prefix.
+    size_t take = taken_pos.size();
+    std::shared_ptr<TileProgram> prog;
+    std::vector<std::pair<uint32_t, uint32_t>> swaps;
+    while (true) {
+      std::vector<const POp*> list;
+      std::vector<uint64_t> srcs;
+      for (size_t j = 0; j < take; ++j) {
+        list.push_back(&phys[rem[taken_pos[j]]]);
+        srcs.push_back(phys[rem[taken_pos[j]]].op.gate_index);
+      }
+      // layout change at the end of the pass (computed on copies of the map)
+      swaps.clear();
+      if (remap) {
+        std::vector<uint32_t> pm = perm, iv = inv;
+        auto sw = [&](uint32_t a, uint32_t b) {
+          std::swap(pm[iv[a]], pm[iv[b]]);
+          std::swap(iv[a], iv[b]);
+          swaps.push_back({a, b});
+        };
+        const bool all_taken = take == rem.size();
+        if (all_taken) {
+          // restore the identity on every position inside S
+          for (uint32_t p = 0; p < n; ++p) {
+            if (!((S >> p) & 1) || iv[p] == p) continue;
+            const uint32_t where = pm[p];  // physical position of logical p
+            if ((S >> where) & 1) sw(p, where);
+          }
+        } else {
+          // Belady: bring the logical qubits needed soonest into the low slots
+          std::vector<size_t> urg(n, SIZE_MAX);
+          std::vector<char> in_pass(rem.size(), 0);
+          for (size_t j = 0; j < take; ++j) in_pass[taken_pos[j]] = 1;
+          size_t k = 0;
+          for (size_t i = 0; i < rem.size(); ++i) {
+            if (in_pass[i]) continue;
+            uint64_t nm = pops[rem[i]].needmask;  // logical
+            while (nm) {
+              const uint32_t l = static_cast<uint32_t>(__builtin_ctzll(nm));
+              nm &= nm - 1;
+              if (urg[l] == SIZE_MAX) urg[l] = k;
+            }
+            ++k;
+          }
+          std::vector<uint32_t> cands;
+          for (uint32_t l = 0; l < n; ++l)
+            if (((S >> pm[l]) & 1) && urg[l] != SIZE_MAX) cands.push_back(l);
+          std::stable_sort(cands.begin(), cands.end(), [&](uint32_t a, uint32_t b) {
+            if (urg[a] != urg[b]) return urg[a] < urg[b];
+            return (pm[a] < L) > (pm[b] < L);
+          });
+          if (cands.size() > L) cands.resize(L);
+          std::vector<char> want(n, 0);
+          for (auto l : cands) want[l] = 1;
+          for (uint32_t p = 0; p < L; ++p) {
+            if (want[iv[p]]) continue;
+            for (auto l : cands)
+              if (pm[l] >= L) {
+                sw(p, pm[l]);
+                break;
+              }
+          }
+        }
+        extra.resize(0);
+        for (auto& [a, b] : swaps) extra.push_back(swap_rel(a, b));
+        for (const auto& e : extra) list.push_back(&e);
+      }
+      prog = compile_pass(S, list, srcs);
+      if (prog->h.bytes <= kTileBlobBytes || take == 1) break;
+      take = std::max<size_t>(1, take * 3 / 4);
+    }
+    if (prog->h.bytes > kTileBlobBytes) throw RuntimeError("tile program for one op exceeds the parameter blob");
+    for (auto& [a, b] : swaps) swap_phys(a, b);
+    std::vector<char> used(rem.size(), 0);
+    for (size_t j = 0; j < take; ++j) used[taken_pos[j]] = 1;
+    std::vector<uint32_t> keep;
+    for (size_t i = 0; i < rem.size(); ++i)
+      if (!used[i]) keep.push_back(rem[i]);
+    push_step(std::move(prog), S, take);
     rem.swap(keep);
+    refresh();
     emit_ready_opaque();
+  }
+  // Restore the logical layout if the last pass could not (or opaque ops ended
+  // the plan): relabel-only passes over the displaced positions.
+  while (remap && !identity()) {
+    uint64_t S = lowmask;
+    for (uint32_t p = 0; p < n && static_cast<uint32_t>(__builtin_popcountll(S)) < m; ++p)
+      if (inv[p] != p) {
+        S |= bit(p);
+        if (static_cast<uint32_t>(__builtin_popcountll(S)) < m) S |= bit(perm[p]);
+      }
+    for (uint32_t q = 0; q < n && static_cast<uint32_t>(__builtin_popcountll(S)) < m; ++q) S |= bit(q);
+    std::vector<std::pair<uint32_t, uint32_t>> swaps;
+    for (uint32_t p = 0; p < n; ++p) {
+      if (!((S >> p) & 1) || inv[p] == p) continue;
+      const uint32_t where = perm[p];
+      if ((S >> where) & 1) {
+        swaps.push_back({p, where});
+        swap_phys(p, where);
+      }
+    }
+    if (swaps.empty()) throw RuntimeError("layout restore made no progress");
+    extra.clear();
+    for (auto& [a, b] : swaps) extra.push_back(swap_rel(a, b));
+    std::vector<const POp*> list;
+    for (const auto& e : extra) list.push_back(&e);
+    push_step(compile_pass(S, list, {}), S, 0);
   }
 }
 
