@@ -278,10 +278,15 @@ def main():
     achieved = (2 * state_bytes) / (avg_pass_ms / 1e3) / 1e9 if avg_pass_ms else 0.0
     roofline = {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
                 "frac": round(achieved / peak, 4), "traffic": ncu_traffic(args.workload, args.plan),
-                "kernel": "k_tile<12>" if args.plan == "tiled" else "per-gate kernels",
+                "kernel": "qsb_tile_* (per-pass NVRTC sm_100a)" if args.plan == "tiled" else "per-gate kernels",
                 "algorithmic_bytes_per_launch": 2 * state_bytes, "launches_per_step": stats["launches"],
                 "avg_launch_ms": round(avg_pass_ms, 4), "peak_kind": peak_kind,
                 "pass_time_share": round(sum(pass_ms) / ms_per_step, 4) if ms_per_step else None}
+    if pass_ms:
+        srt = sorted(pass_ms)
+        roofline["launch_ms_min_median_max"] = [round(srt[0], 3), round(srt[len(srt) // 2], 3), round(srt[-1], 3)]
+        if os.environ.get("QSB_BENCH_PASSES"):
+            roofline["launch_ms"] = [round(x, 3) for x in per]
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
