@@ -1,0 +1,431 @@
+// CUDA source generator for one tile pass (included by jit.cpp only).
+//
+// Emits straight-line code over 16 SSA amplitude values per thread:
+//   * FLIPs on register bits (and register-controlled CNOTs) are renamings;
+//   * diagonal phases are deferred: a per-thread scalar (thread / tile-
+//     dependent factors) that commutes with every register-local gate, and
+//     per-slot constants (register-qubit factors) that commute with a 2x2 on a
+//     pair whenever both slots carry the same constant; both are applied only
+//     when data leaves the thread (transpose, store) or a gate mixes slots with
+//     different constants;
+//   * factors that depend only on thread bits are computed once per thread
+//     before the tile loop.
+#pragma once
+
+#include <complex>
+#include <cstring>
+#include <sstream>
+#include <string>
+#include <vector>
+
+#include "tile.hpp"
+
+namespace qsb {
+namespace jitgen {
+
+inline std::string hexll(unsigned long long v) {
+  char b[32];
+  std::snprintf(b, sizeof b, "0x%llxull", v);
+  return b;
+}
+
+struct Gen {
+  const TileProgram& tp;
+  std::ostringstream pro;   // before the tile loop (per-thread constants)
+  std::ostringstream s;     // tile-loop body
+  std::string name[16];
+  cd K[16];                 // pending per-slot constant factors
+  std::string Fp;           // pending per-thread scalar factor (empty = 1)
+  cd Kg = 1.0;              // pending tile-wide constant scalar
+  std::vector<double2> extra;  // coefficients appended after tp.coef
+  uint32_t cur_tq[kTileMaxT] = {};
+  int counter = 0;
+  bool prefetch = true;
+
+  explicit Gen(const TileProgram& p) : tp(p) {
+    for (auto& k : K) k = 1.0;
+  }
+
+  std::string fresh(const char* pfx = "v") { return pfx + std::to_string(counter++); }
+  std::string coef(uint32_t i) { return "P.c[" + std::to_string(i) + "]"; }
+  cd coefv(uint32_t i) const { return cd(tp.coef[i].x, tp.coef[i].y); }
+  std::string kconst(cd v) {
+    extra.push_back(make_double2(v.real(), v.imag()));
+    return coef(static_cast<uint32_t>(tp.coef.size() + extra.size() - 1));
+  }
+  static bool one(cd v) { return v == cd(1.0); }
+
+  void emit_G(const uint32_t* tq, bool decl) {
+    s << "    " << (decl ? "unsigned long long " : "") << "G = base";
+    for (uint32_t k = 0; k < tp.h.t; ++k) s << " | ((unsigned long long)((tid >> " << k << ") & 1u) << " << tq[k] << ")";
+    s << ";\n";
+    for (uint32_t k = 0; k < tp.h.t; ++k) cur_tq[k] = tq[k];
+  }
+
+  std::string pred(const TOp& o) {
+    if (!o.gmask) return "";
+    const std::string t = fresh("t");
+    s << "    const bool " << t << " = (G & " << hexll(o.gmask) << ") == " << hexll(o.gval) << ";\n";
+    return t;
+  }
+
+  void set(int p, const std::string& expr, const std::string& t) {
+    const std::string nv = fresh();
+    if (t.empty()) s << "    const double2 " << nv << " = " << expr << ";\n";
+    else s << "    const double2 " << nv << " = " << t << " ? " << expr << " : " << name[p] << ";\n";
+    name[p] = nv;
+  }
+
+  // --- deferred phases ----------------------------------------------------
+  void flush_const(int p) {
+    if (one(K[p])) return;
+    set(p, "cmul(" + name[p] + ", " + kconst(K[p]) + ")", "");
+    K[p] = 1.0;
+  }
+  void flush_pair(int p, int p1) {
+    if (K[p] != K[p1]) {
+      flush_const(p);
+      flush_const(p1);
+    }
+  }
+  // Applies the pending per-thread scalar and per-slot constants (and, at the
+  // store, the tile-wide scalar Kg).
+  void flush_all(bool with_global) {
+    const cd g = with_global ? Kg : cd(1.0);
+    for (int p = 0; p < 16; ++p) {
+      const cd kp = K[p] * g;
+      const bool k1 = one(kp);
+      if (k1 && Fp.empty()) continue;
+      std::string f;
+      if (k1) f = Fp;
+      else if (Fp.empty()) f = kconst(kp);
+      else f = "cmul(" + Fp + ", " + kconst(kp) + ")";
+      if (Fp.empty() && kp.imag() == 0.0)  // real scale: two multiplies
+        set(p, "make_double2(" + name[p] + ".x * " + f + ".x, " + name[p] + ".y * " + f + ".x)", "");
+      else
+        set(p, "cmul(" + name[p] + ", " + f + ")", "");
+      K[p] = 1.0;
+    }
+    Fp.clear();
+    if (with_global) Kg = 1.0;
+  }
+
+  // Unpredicated 2x2 whose rows share a pivot f (|m00| = |m11|, |m01| = |m10|:
+  // rotations, H): M = f * N with one entry of each row of N exactly +-1, so
+  // every output is a single fused multiply-add per real component; f joins
+  // the tile-wide scalar Kg (commutes with every linear op, applied at store).
+  bool mat1_factored(const TOp& o) {
+    if (o.rmask != 0 || o.gmask != 0) return false;
+    const cd m[4] = {coefv(o.coef), coefv(o.coef + 1), coefv(o.coef + 2), coefv(o.coef + 3)};
+    const cd f = std::abs(m[0]) >= std::abs(m[1]) ? m[0] : m[1];
+    if (f == cd(0)) return false;
+    const cd n[4] = {m[0] / f, m[1] / f, m[2] / f, m[3] / f};
+    auto unit = [](cd v) { return v.imag() == 0.0 && (v.real() == 1.0 || v.real() == -1.0); };
+    struct Row {
+      int piv;  // column holding +-1
+      double sign;
+      cd x;     // the other coefficient
+    } rows[2];
+    for (int r = 0; r < 2; ++r) {
+      const cd u = n[2 * r], w = n[2 * r + 1];
+      if (unit(u)) rows[r] = {0, u.real(), w};
+      else if (unit(w)) rows[r] = {1, w.real(), u};
+      else return false;
+    }
+    const int Kb = o.k;
+    std::string xc[2];
+    for (int r = 0; r < 2; ++r) xc[r] = kconst(rows[r].x);
+    for (int p = 0; p < 16; ++p) {
+      if ((p >> Kb) & 1) continue;
+      const int p1 = p | (1 << Kb);
+      flush_pair(p, p1);
+      const std::string in[2] = {name[p], name[p1]};
+      std::string out[2];
+      for (int r = 0; r < 2; ++r) {
+        const Row& R = rows[r];
+        const std::string& pv = in[R.piv];
+        const std::string& ot = in[1 - R.piv];
+        const std::string sg = R.sign < 0 ? "-" : "";
+        if (R.x.imag() == 0.0) {  // x real: (x*ot + s*pv)
+          out[r] = "make_double2(fma(" + xc[r] + ".x, " + ot + ".x, " + sg + pv + ".x), fma(" + xc[r] + ".x, " + ot +
+                   ".y, " + sg + pv + ".y))";
+        } else if (R.x.real() == 0.0) {  // x = i*y: (i*y*ot + s*pv)
+          out[r] = "make_double2(fma(-" + xc[r] + ".y, " + ot + ".y, " + sg + pv + ".x), fma(" + xc[r] + ".y, " + ot +
+                   ".x, " + sg + pv + ".y))";
+        } else {
+          out[r] = "caxpy(" + xc[r] + ", " + ot + ", " + (R.sign < 0 ? "cneg(" + pv + ")" : pv) + ")";
+        }
+      }
+      set(p, out[0], "");
+      set(p1, out[1], "");
+    }
+    Kg *= f;
+    return true;
+  }
+
+  // --- micro-ops ------------------------------------------------------------
+  void mat1(const TOp& o) {
+    if (mat1_factored(o)) return;
+    const std::string t = pred(o);
+    const int Kb = o.k;
+    const std::string m0 = coef(o.coef), m1 = coef(o.coef + 1), m2 = coef(o.coef + 2), m3 = coef(o.coef + 3);
+    for (int p = 0; p < 16; ++p) {
+      if ((p >> Kb) & 1) continue;
+      if ((p & o.rmask) != o.rval) continue;
+      const int p1 = p | (1 << Kb);
+      flush_pair(p, p1);
+      const std::string a = name[p], b = name[p1];
+      std::string e0, e1;
+      if (o.type == TO_MAT1) {
+        e0 = "cmv2(" + m0 + ", " + a + ", " + m1 + ", " + b + ")";
+        e1 = "cmv2(" + m2 + ", " + a + ", " + m3 + ", " + b + ")";
+      } else if (o.type == TO_MAT1_REAL) {
+        e0 = "rmv2(" + m0 + ".x, " + a + ", " + m1 + ".x, " + b + ")";
+        e1 = "rmv2(" + m2 + ".x, " + a + ", " + m3 + ".x, " + b + ")";
+      } else {
+        e0 = "xmv2(" + m0 + ".x, " + a + ", " + m1 + ".y, " + b + ")";
+        e1 = "xmv2(" + m3 + ".x, " + b + ", " + m2 + ".y, " + a + ")";
+      }
+      set(p, e0, t);
+      set(p1, e1, t);
+    }
+  }
+
+  void flip(const TOp& o) {
+    const int Kb = o.k;
+    const std::string t = o.gmask ? pred(o) : "";
+    for (int p = 0; p < 16; ++p) {
+      if ((p >> Kb) & 1) continue;
+      if ((p & o.rmask) != o.rval) continue;
+      const int p1 = p | (1 << Kb);
+      if (t.empty()) {
+        std::swap(name[p], name[p1]);  // pure renaming; pending constants travel along
+        std::swap(K[p], K[p1]);
+      } else {
+        flush_pair(p, p1);
+        const std::string a = name[p], b = name[p1];
+        const std::string na = fresh(), nb = fresh();
+        s << "    const double2 " << na << " = " << t << " ? " << b << " : " << a << ";\n";
+        s << "    const double2 " << nb << " = " << t << " ? " << a << " : " << b << ";\n";
+        name[p] = na;
+        name[p1] = nb;
+      }
+    }
+  }
+
+  void phase(const TOp& o) {
+    const std::string t = pred(o);
+    // split the non-register factors into thread-bit and tile (outside) ones
+    std::vector<std::pair<uint32_t, uint32_t>> thr;  // (tid bit, coef index)
+    std::vector<std::pair<uint32_t, uint32_t>> out;  // (qubit, coef index)
+    for (uint32_t j = 0; j < o.nlist; ++j) {
+      const uint32_t q = tp.meta[o.meta + j];
+      int tb = -1;
+      for (uint32_t k = 0; k < tp.h.t; ++k)
+        if (cur_tq[k] == q) tb = static_cast<int>(k);
+      if (tb >= 0) thr.push_back({static_cast<uint32_t>(tb), o.coef + 17 + j});
+      else out.push_back({q, o.coef + 17 + j});
+    }
+    std::string F;
+    if (!thr.empty()) {  // per-thread constant, hoisted out of the tile loop
+      F = fresh("FT");
+      pro << "  double2 " << F << " = make_double2(1.0, 0.0);\n";
+      for (auto& [b, ci] : thr) pro << "  if ((tid >> " << b << ") & 1u) " << F << " = cmul(" << F << ", " << coef(ci) << ");\n";
+    }
+    const bool c1 = one(coefv(o.coef + 16));
+    if (!c1 || !out.empty()) {
+      const std::string Fo = fresh("F");
+      s << "    double2 " << Fo << " = " << (F.empty() ? (c1 ? std::string("make_double2(1.0, 0.0)") : coef(o.coef + 16))
+                                                        : (c1 ? F : "cmul(" + F + ", " + coef(o.coef + 16) + ")"))
+        << ";\n";
+      for (auto& [q, ci] : out) s << "    if ((base >> " << q << ") & 1ull) " << Fo << " = cmul(" << Fo << ", " << coef(ci) << ");\n";
+      F = Fo;
+    }
+    if (!t.empty() && !F.empty()) {
+      const std::string Ft = fresh("F");
+      s << "    const double2 " << Ft << " = " << t << " ? " << F << " : make_double2(1.0, 0.0);\n";
+      F = Ft;
+    }
+    if (o.rmask == 0) {
+      // whole-thread factor: defer; register-qubit factors: pending constants
+      if (!F.empty()) {
+        if (Fp.empty()) {
+          Fp = F;
+        } else {
+          const std::string nf = fresh("FP");
+          s << "    const double2 " << nf << " = cmul(" << Fp << ", " << F << ");\n";
+          Fp = nf;
+        }
+      }
+      if (t.empty()) {
+        for (int p = 0; p < 16; ++p) K[p] *= coefv(o.coef + p);
+      } else {
+        // thread-predicated register factors cannot be folded into constants
+        for (int p = 0; p < 16; ++p) {
+          const cd g = coefv(o.coef + p);
+          if (!one(g)) set(p, "cmul(" + name[p] + ", " + coef(o.coef + p) + ")", t);
+        }
+      }
+      return;
+    }
+    // register-predicated phase: applies to a subset of slots right away
+    for (int p = 0; p < 16; ++p) {
+      if ((p & o.rmask) != o.rval) continue;
+      const cd g = coefv(o.coef + p);
+      std::string f;
+      if (F.empty() && one(g)) continue;
+      if (F.empty()) f = coef(o.coef + p);
+      else if (one(g)) f = F;
+      else f = "cmul(" + F + ", " + coef(o.coef + p) + ")";
+      set(p, "cmul(" + name[p] + ", " + f + ")", t);
+    }
+  }
+
+  void dense(const TOp& o) {
+    const std::string t = pred(o);
+    const int KD = o.type == TO_DENSE2 ? 2 : 3, Gd = 1 << KD;
+    for (int hi = 0; hi < (16 >> KD); ++hi) {
+      const int p0 = hi << KD;
+      if ((p0 & o.rmask) != o.rval) continue;
+      bool same = true;
+      for (int c = 1; c < Gd; ++c) same = same && K[p0 + c] == K[p0];
+      if (!same)
+        for (int c = 0; c < Gd; ++c) flush_const(p0 + c);
+      std::string in[8];
+      for (int c = 0; c < Gd; ++c) in[c] = name[p0 + c];
+      for (int r = 0; r < Gd; ++r) {
+        std::ostringstream x;
+        x << "dotrow" << Gd << "(P.c + " << (o.coef + r * Gd);
+        for (int c = 0; c < Gd; ++c) x << ", " << in[c];
+        x << ")";
+        set(p0 + r, x.str(), t);
+      }
+    }
+  }
+
+  void transpose(const TOp& o, int idx) {
+    flush_all(false);  // Kg (tile-wide) commutes with the exchange
+    const uint32_t TB = tp.h.t;
+    const uint32_t* mt = tp.meta.data() + o.meta;
+    const std::string Tw = "Tw" + std::to_string(idx), Tr = "Tr" + std::to_string(idx);
+    auto xorexpr = [&](const uint32_t* cols) {
+      std::ostringstream e;
+      e << "0u";
+      for (uint32_t k = 0; k < TB; ++k)
+        if (cols[k]) e << " ^ (((tid >> " << k << ") & 1u) * " << cols[k] << "u)";
+      return e.str();
+    };
+    s << "    __syncthreads();\n";
+    s << "    const unsigned " << Tw << " = " << xorexpr(mt) << ";\n";
+    for (int p = 0; p < 16; ++p) {
+      uint32_t a = 0;
+      for (int k = 0; k < 4; ++k)
+        if ((p >> k) & 1) a ^= mt[TB + k];
+      s << "    sm[" << Tw << " ^ " << a << "u] = " << name[p] << ";\n";
+    }
+    s << "    __syncthreads();\n";
+    s << "    const unsigned " << Tr << " = " << xorexpr(mt + TB + 4) << ";\n";
+    for (int p = 0; p < 16; ++p) {
+      uint32_t a = 0;
+      for (int k = 0; k < 4; ++k)
+        if ((p >> k) & 1) a ^= mt[2 * TB + 4 + k];
+      const std::string nv = fresh();
+      s << "    const double2 " << nv << " = sm[" << Tr << " ^ " << a << "u];\n";
+      name[p] = nv;
+    }
+    emit_G(mt + 2 * TB + 8, false);
+  }
+
+  std::string run(const std::string& kname, uint32_t threads, uint32_t minb) {
+    const TileHeader& h = tp.h;
+    const uint32_t T = 1u << h.t;
+    unsigned long long loff[16];
+    for (int p = 0; p < 16; ++p) {
+      loff[p] = 0;
+      for (int k = 0; k < 4; ++k)
+        if ((p >> k) & 1) loff[p] |= h.load.rs[k];
+    }
+    // ---- tile-loop body
+    if (prefetch) {
+      s << "    cp_async_wait_all();\n";
+      for (int p = 0; p < 16; ++p) {
+        name[p] = fresh();
+        s << "    const double2 " << name[p] << " = PB[" << p * T << " + tid];\n";
+      }
+      s << "    { const unsigned long long nt = tile + gridDim.x; if (nt < " << h.ntiles << "ull) prefetch(nt); }\n";
+    } else {
+      for (int p = 0; p < 16; ++p) {
+        name[p] = fresh();
+        s << "    const double2 " << name[p] << " = __ldcs(amps + (G | " << hexll(loff[p]) << "));\n";
+      }
+    }
+    for (uint32_t k = 0; k < h.t; ++k) cur_tq[k] = h.load.tq[k];
+    int ti = 0;
+    for (const TOp& o : tp.ops) {
+      switch (o.type) {
+        case TO_MAT1:
+        case TO_MAT1_REAL:
+        case TO_MAT1_RX: mat1(o); break;
+        case TO_FLIP: flip(o); break;
+        case TO_PHASE: phase(o); break;
+        case TO_DENSE2:
+        case TO_DENSE3: dense(o); break;
+        case TO_TRANSPOSE: transpose(o, ti++); break;
+        case TO_RELABEL: emit_G(tp.meta.data() + o.meta, false); break;
+        default: throw RuntimeError("jit: unknown micro-op");
+      }
+    }
+    flush_all(true);
+    // Relabels (free SWAPs) make threads store where other threads loaded; with
+    // no transpose barrier in the pass, every load must retire before any store.
+    if (ti == 0 && std::memcmp(&h.load, &h.store, sizeof(TileConfigAddr)) != 0) s << "    __syncthreads();\n";
+    for (int p = 0; p < 16; ++p) {
+      unsigned long long off = 0;
+      for (int k = 0; k < 4; ++k)
+        if ((p >> k) & 1) off |= h.store.rs[k];
+      s << "    __stcs(amps + (G | " << hexll(off) << "), " << name[p] << ");\n";
+    }
+
+    // ---- assemble
+    std::ostringstream k;
+    k << "struct __align__(16) QsbCoef { double2 c[" << std::max<size_t>(1, tp.coef.size() + extra.size()) << "]; };\n";
+    k << "extern \"C\" __global__ void __launch_bounds__(" << threads << ", " << minb << ") " << kname
+      << "(double2* __restrict__ amps, const __grid_constant__ QsbCoef P) {\n";
+    k << "  extern __shared__ double2 sm[];\n";
+    k << "  const unsigned tid = threadIdx.x;\n";
+    k << "  const unsigned long long TL = 0ull";
+    for (uint32_t b = 0; b < h.t; ++b) k << " | ((unsigned long long)((tid >> " << b << ") & 1u) << " << h.load.tq[b] << ")";
+    k << ";\n";
+    k << "  auto base_of = [&](unsigned long long b) {\n";
+    for (uint32_t b = 0; b < h.m && h.ntiles > 1; ++b) {
+      const uint32_t q = h.S[b];
+      k << "    b = ((b >> " << q << ") << " << (q + 1) << ") | (b & " << hexll((1ull << q) - 1) << ");\n";
+    }
+    k << "    return b;\n  };\n";
+    k << pro.str();
+    if (prefetch) {
+      // Each thread stages its own 16 amplitudes of the next tile in its own
+      // shared-memory slots (slot p*T + tid: conflict-free) with cp.async, so
+      // HBM reads of tile i+1 overlap the arithmetic of tile i.
+      k << "  double2* const PB = sm + " << (tp.transposes ? (1u << h.m) : 0u) << ";\n";
+      k << "  auto prefetch = [&](unsigned long long t) {\n";
+      k << "    const unsigned long long g = base_of(t) | TL;\n";
+      for (int p = 0; p < 16; ++p)
+        k << "    cp_async16(PB + " << p * T << " + tid, amps + (g | " << hexll(loff[p]) << "));\n";
+      k << "    cp_async_commit();\n  };\n";
+      k << "  unsigned long long tile = blockIdx.x;\n";
+      k << "  if (tile < " << h.ntiles << "ull) prefetch(tile);\n";
+      k << "  for (; tile < " << h.ntiles << "ull; tile += gridDim.x) {\n";
+    } else {
+      k << "  for (unsigned long long tile = blockIdx.x; tile < " << h.ntiles << "ull; tile += gridDim.x) {\n";
+    }
+    k << "    const unsigned long long base = base_of(tile);\n";
+    k << "    unsigned long long G = base | TL;\n";
+    k << s.str();
+    k << "  }\n}\n";
+    return k.str();
+  }
+};
+
+}  // namespace jitgen
+}  // namespace qsb

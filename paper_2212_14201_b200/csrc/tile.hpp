@@ -84,11 +84,14 @@ struct TileProgram {
   uint32_t transposes = 0;
   std::vector<uint64_t> source;  // gate indices, for diagnostics
   std::shared_ptr<struct JitModule> jit;  // specialised kernel (jit.hpp)
+  std::vector<double2> params;            // kernel parameter table (coef + generator constants)
 };
 
 // The coefficient table travels as a __grid_constant__ kernel parameter
 // (constant bank); the planner keeps every pass's tables below this size.
-constexpr uint32_t kTileBlobBytes = 30 * 1024;
+constexpr uint32_t kTileBlobBytes = 24 * 1024;
+// Hard limit of the __grid_constant__ parameter (CUDA 12.1+: 32764 bytes).
+constexpr uint32_t kParamLimitBytes = 32 * 1024 - 256;
 
 struct TileOptions {
   uint32_t m = 12;  // tile qubits
