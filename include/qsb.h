@@ -198,6 +198,54 @@ int qs_expect_pauli(qs_state_t s, const char* letters, uint32_t nterms, double* 
  * double accumulation                                  [statevector.hpp:544-552] */
 int qs_cumulative(qs_state_t s, double* cum_out, double* total_out);
 
+/* --- sharded state vectors (multi-GPU) -----------------------------------------
+ * The reference keeps one 2^n vector in host memory [statevector.hpp:111-118]
+ * and has no distributed mode; these entry points are the B200 extension the
+ * survey's section 8(e) calls for.  An n-qubit state is split over 2^g shards:
+ * the top g qubits are rank bits and shard r holds global indices
+ * [r*2^(n-g), (r+1)*2^(n-g)).  A plan built by qs_plan_create_sharded runs tile
+ * passes on every shard independently; a non-diagonal gate on a rank bit is
+ * preceded by a pairwise half-shard exchange (rank bit <-> local qubit).
+ *
+ *   qs_shards_create_local: all 2^g shards in this process on one device
+ *     (exchanges are device-local swaps; validates sharded plans on 1 GPU).
+ *   qs_shards_create_dist: this rank's shard, exchanges via NCCL send/recv
+ *     over NVLink.  libnccl.so.2 is loaded at run time (env QSB_NCCL_LIB
+ *     overrides the name).  The 128-byte unique id from qs_dist_unique_id on
+ *     one rank is broadcast by the caller (e.g. torch.distributed); world must
+ *     be a power of two.  Destroy the shards before their communicator.
+ *
+ * Amplitude I/O takes global indices; a distributed handle only serves the
+ * range of its own shard.  Reductions are summed in rank order on every rank
+ * (bit-identical across ranks and runs).                                      */
+typedef struct qs_dist* qs_dist_t;
+typedef struct qs_shards* qs_shards_t;
+int qs_dist_unique_id(unsigned char out[128]);
+int qs_dist_create(const unsigned char id[128], int world, int rank, int device, qs_dist_t* out);
+int qs_dist_destroy(qs_dist_t d);
+int qs_shards_create_local(uint32_t num_qubits, uint32_t global_qubits, int device, qs_shards_t* out);
+int qs_shards_create_dist(uint32_t num_qubits, qs_dist_t d, qs_shards_t* out);
+int qs_shards_destroy(qs_shards_t s);
+/* global_qubits = g; first_rank = lowest shard index held by this handle;
+ * local_count = shards held (2^g local, 1 distributed).                       */
+int qs_shards_info(qs_shards_t s, uint32_t* num_qubits, uint32_t* global_qubits, uint32_t* first_rank,
+                   uint32_t* local_count);
+void* qs_shards_stream(qs_shards_t s);
+int qs_shards_sync(qs_shards_t s);
+int qs_shards_set_basis_state(qs_shards_t s, uint64_t index);
+int qs_shards_set_amplitudes(qs_shards_t s, const double* data, uint64_t offset, uint64_t count);
+int qs_shards_get_amplitudes(qs_shards_t s, double* data, uint64_t offset, uint64_t count);
+/* Plans for a state with `global_qubits` rank bits (tile plans only).         */
+int qs_plan_create_sharded(uint32_t num_qubits, uint32_t global_qubits, const qs_gate* gates, uint64_t n,
+                           qs_plan_t* out);
+/* Number of rank-bit exchanges one execution performs.                      */
+int qs_plan_exchanges(qs_plan_t p, uint64_t* exchanges);
+int qs_shards_plan_enqueue(qs_shards_t s, qs_plan_t p);
+int qs_shards_plan_execute(qs_shards_t s, qs_plan_t p);
+int qs_shards_apply_circuit(qs_shards_t s, const qs_gate* gates, uint64_t n);
+int qs_shards_norm2(qs_shards_t s, double* out);
+int qs_shards_checksum(qs_shards_t s, double* out);
+
 #ifdef __cplusplus
 }
 #endif

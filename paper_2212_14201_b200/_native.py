@@ -108,6 +108,26 @@ _SIGS = {
     "qs_sample_seeded": (C.c_int, [_P, C.c_uint64, C.c_uint64, C.c_int, _U64P]),
     "qs_expect_pauli": (C.c_int, [_P, C.c_char_p, C.c_uint32, _DP]),
     "qs_cumulative": (C.c_int, [_P, _DP, _DP]),
+    # sharded state vectors
+    "qs_dist_unique_id": (C.c_int, [C.c_char_p]),
+    "qs_dist_create": (C.c_int, [C.c_char_p, C.c_int, C.c_int, C.c_int, C.POINTER(_P)]),
+    "qs_dist_destroy": (C.c_int, [_P]),
+    "qs_shards_create_local": (C.c_int, [C.c_uint32, C.c_uint32, C.c_int, C.POINTER(_P)]),
+    "qs_shards_create_dist": (C.c_int, [C.c_uint32, _P, C.POINTER(_P)]),
+    "qs_shards_destroy": (C.c_int, [_P]),
+    "qs_shards_info": (C.c_int, [_P, _UP, _UP, _UP, _UP]),
+    "qs_shards_stream": (C.c_void_p, [_P]),
+    "qs_shards_sync": (C.c_int, [_P]),
+    "qs_shards_set_basis_state": (C.c_int, [_P, C.c_uint64]),
+    "qs_shards_set_amplitudes": (C.c_int, [_P, _DP, C.c_uint64, C.c_uint64]),
+    "qs_shards_get_amplitudes": (C.c_int, [_P, _DP, C.c_uint64, C.c_uint64]),
+    "qs_plan_create_sharded": (C.c_int, [C.c_uint32, C.c_uint32, _GP, C.c_uint64, C.POINTER(_P)]),
+    "qs_plan_exchanges": (C.c_int, [_P, _U64P]),
+    "qs_shards_plan_enqueue": (C.c_int, [_P, _P]),
+    "qs_shards_plan_execute": (C.c_int, [_P, _P]),
+    "qs_shards_apply_circuit": (C.c_int, [_P, _GP, C.c_uint64]),
+    "qs_shards_norm2": (C.c_int, [_P, _DP]),
+    "qs_shards_checksum": (C.c_int, [_P, _DP]),
 }
 
 EXPORTED = tuple(_SIGS)

@@ -14,6 +14,7 @@
 #include "gates.hpp"
 #include "kernels.hpp"
 #include "plan.hpp"
+#include "shard.hpp"
 #include "tile.hpp"
 
 struct qs_state {
@@ -24,6 +25,12 @@ struct qs_plan {
 };
 struct qs_fused {
   std::vector<qsb::GateRec> gates;
+};
+struct qs_dist {
+  qsb::Dist* d = nullptr;
+};
+struct qs_shards {
+  std::unique_ptr<qsb::ShardSet> ss;
 };
 
 namespace qsb {
@@ -551,6 +558,171 @@ int qs_cumulative(qs_state_t h, double* cum_out, double* total_out) {
     }
     cudaFree(d);
     if (total_out) *total_out = total;
+  });
+}
+
+int qs_dist_unique_id(unsigned char out[128]) {
+  return guarded([&] {
+    if (!out) throw ValidationError("null id buffer");
+    dist_unique_id(out);
+  });
+}
+
+int qs_dist_create(const unsigned char id[128], int world, int rank, int device, qs_dist_t* out) {
+  return guarded([&] {
+    if (!id || !out) throw ValidationError("null id or output handle");
+    *out = nullptr;
+    int ndev = 0;
+    QSB_CUDA(cudaGetDeviceCount(&ndev));
+    if (device < 0 || device >= ndev) throw ValidationError("CUDA device " + std::to_string(device) + " not present");
+    auto* h = new qs_dist();
+    try {
+      h->d = dist_create(id, world, rank, device);
+    } catch (...) {
+      delete h;
+      throw;
+    }
+    *out = h;
+  });
+}
+
+int qs_dist_destroy(qs_dist_t d) {
+  return guarded([&] {
+    if (!d) return;
+    dist_destroy(d->d);
+    delete d;
+  });
+}
+
+static ShardSet& sh(qs_shards_t h) {
+  if (!h || !h->ss) throw ValidationError("null shard handle");
+  return *h->ss;
+}
+
+int qs_shards_create_local(uint32_t num_qubits, uint32_t global_qubits, int device, qs_shards_t* out) {
+  return guarded([&] {
+    if (!out) throw ValidationError("null output handle");
+    *out = nullptr;
+    if (num_qubits > 40) throw ValidationError("sharded states limited to 40 qubits");
+    int ndev = 0;
+    QSB_CUDA(cudaGetDeviceCount(&ndev));
+    if (device < 0 || device >= ndev) throw ValidationError("CUDA device " + std::to_string(device) + " not present");
+    auto h = std::make_unique<qs_shards>();
+    h->ss = make_local_shards(num_qubits, global_qubits, device);
+    *out = h.release();
+  });
+}
+
+int qs_shards_create_dist(uint32_t num_qubits, qs_dist_t d, qs_shards_t* out) {
+  return guarded([&] {
+    if (!out || !d) throw ValidationError("null communicator or output handle");
+    *out = nullptr;
+    if (num_qubits > 44) throw ValidationError("sharded states limited to 44 qubits");
+    auto h = std::make_unique<qs_shards>();
+    h->ss = make_dist_shard(num_qubits, d->d);
+    *out = h.release();
+  });
+}
+
+int qs_shards_destroy(qs_shards_t s) {
+  return guarded([&] { delete s; });
+}
+
+int qs_shards_info(qs_shards_t s, uint32_t* num_qubits, uint32_t* global_qubits, uint32_t* first_rank,
+                   uint32_t* local_count) {
+  return guarded([&] {
+    ShardSet& ss = sh(s);
+    if (num_qubits) *num_qubits = ss.n;
+    if (global_qubits) *global_qubits = ss.g;
+    if (first_rank) *first_rank = ss.shards.front()->rank;
+    if (local_count) *local_count = static_cast<uint32_t>(ss.shards.size());
+  });
+}
+
+void* qs_shards_stream(qs_shards_t s) { return (s && s->ss) ? static_cast<void*>(s->ss->stream) : nullptr; }
+
+int qs_shards_sync(qs_shards_t s) {
+  return guarded([&] { shard_sync(sh(s)); });
+}
+
+int qs_shards_set_basis_state(qs_shards_t s, uint64_t index) {
+  return guarded([&] {
+    ShardSet& ss = sh(s);
+    if (index >= (1ull << ss.n)) throw ValidationError("basis index out of range");
+    shard_fill_basis(ss, index);
+  });
+}
+
+int qs_shards_set_amplitudes(qs_shards_t s, const double* data, uint64_t offset, uint64_t count) {
+  return guarded([&] {
+    if (count && !data) throw ValidationError("null amplitude buffer");
+    shard_set(sh(s), data, offset, count);
+  });
+}
+
+int qs_shards_get_amplitudes(qs_shards_t s, double* data, uint64_t offset, uint64_t count) {
+  return guarded([&] {
+    if (count && !data) throw ValidationError("null amplitude buffer");
+    shard_get(sh(s), data, offset, count);
+  });
+}
+
+int qs_plan_create_sharded(uint32_t num_qubits, uint32_t global_qubits, const qs_gate* gates, uint64_t n,
+                           qs_plan_t* out) {
+  return guarded([&] {
+    if (!out) throw ValidationError("null output handle");
+    if (n && !gates) throw ValidationError("null gate array");
+    auto h = std::make_unique<qs_plan>();
+    h->p = make_plan(num_qubits, gates, n, QS_PLAN_TILED, 0, global_qubits);
+    *out = h.release();
+  });
+}
+
+int qs_plan_exchanges(qs_plan_t p, uint64_t* exchanges) {
+  return guarded([&] {
+    if (!p || !exchanges) throw ValidationError("null plan or output");
+    uint64_t c = 0;
+    for (const auto& st : p->p->steps) c += st.kind == Step::SwapStep;
+    *exchanges = c;
+  });
+}
+
+int qs_shards_plan_enqueue(qs_shards_t s, qs_plan_t p) {
+  return guarded([&] {
+    if (!p) throw ValidationError("null plan");
+    shard_execute(sh(s), *p->p);
+  });
+}
+
+int qs_shards_plan_execute(qs_shards_t s, qs_plan_t p) {
+  return guarded([&] {
+    if (!p) throw ValidationError("null plan");
+    shard_execute(sh(s), *p->p);
+    shard_sync(sh(s));
+  });
+}
+
+int qs_shards_apply_circuit(qs_shards_t s, const qs_gate* gates, uint64_t n) {
+  return guarded([&] {
+    ShardSet& ss = sh(s);
+    if (n && !gates) throw ValidationError("null gate array");
+    auto p = make_plan(ss.n, gates, n, QS_PLAN_TILED, 0, ss.g);
+    shard_execute(ss, *p);
+    shard_sync(ss);
+  });
+}
+
+int qs_shards_norm2(qs_shards_t s, double* out) {
+  return guarded([&] {
+    if (!out) throw ValidationError("null output");
+    *out = shard_norm2(sh(s));
+  });
+}
+
+int qs_shards_checksum(qs_shards_t s, double* out) {
+  return guarded([&] {
+    if (!out) throw ValidationError("null output");
+    *out = shard_checksum(sh(s));
   });
 }
 

@@ -48,9 +48,15 @@ void note_launch(int count = 1);
 
 // A state vector on one device: 2^n complex128 amplitudes, logical order.
 struct State {
-  uint32_t n = 0;
+  uint32_t n = 0;             // qubits of the whole state
   int device = 0;
-  uint64_t size = 0;          // 2^n
+  uint64_t size = 0;          // amplitudes held here: 2^(n-g)
+  // Sharded states: the top g qubits are rank bits; this object holds the
+  // shard with rank `rank` (global index = rank_base | local index).
+  uint32_t g = 0;
+  uint32_t rank = 0;
+  uint64_t rank_base = 0;
+  uint32_t local_qubits() const { return n - g; }
   double2* amps = nullptr;    // device
   cudaStream_t stream = nullptr;
   // scratch (grown on demand)

@@ -352,11 +352,11 @@ struct Gen {
         name[p] = fresh();
         s << "    const double2 " << name[p] << " = PB[" << p * T << " + tid];\n";
       }
-      s << "    { const unsigned long long nt = tile + gridDim.x; if (nt < " << h.ntiles << "ull) prefetch(nt); }\n";
+      s << "    { const unsigned long long nt = tile + gridDim.x; if (nt < ntiles) prefetch(nt); }\n";
     } else {
       for (int p = 0; p < 16; ++p) {
         name[p] = fresh();
-        s << "    const double2 " << name[p] << " = __ldcs(amps + (G | " << hexll(loff[p]) << "));\n";
+        s << "    const double2 " << name[p] << " = __ldcs(amps + ((G | " << hexll(loff[p]) << ") & lmask));\n";
       }
     }
     for (uint32_t k = 0; k < h.t; ++k) cur_tq[k] = h.load.tq[k];
@@ -383,21 +383,22 @@ struct Gen {
       unsigned long long off = 0;
       for (int k = 0; k < 4; ++k)
         if ((p >> k) & 1) off |= h.store.rs[k];
-      s << "    __stcs(amps + (G | " << hexll(off) << "), " << name[p] << ");\n";
+      s << "    __stcs(amps + ((G | " << hexll(off) << ") & lmask), " << name[p] << ");\n";
     }
 
     // ---- assemble
     std::ostringstream k;
     k << "struct __align__(16) QsbCoef { double2 c[" << std::max<size_t>(1, tp.coef.size() + extra.size()) << "]; };\n";
     k << "extern \"C\" __global__ void __launch_bounds__(" << threads << ", " << minb << ") " << kname
-      << "(double2* __restrict__ amps, const __grid_constant__ QsbCoef P) {\n";
+      << "(double2* __restrict__ amps, const unsigned long long rank_base, const unsigned long long lmask,\n"
+      << "    const unsigned long long ntiles, const __grid_constant__ QsbCoef P) {\n";
     k << "  extern __shared__ double2 sm[];\n";
     k << "  const unsigned tid = threadIdx.x;\n";
     k << "  const unsigned long long TL = 0ull";
     for (uint32_t b = 0; b < h.t; ++b) k << " | ((unsigned long long)((tid >> " << b << ") & 1u) << " << h.load.tq[b] << ")";
     k << ";\n";
     k << "  auto base_of = [&](unsigned long long b) {\n";
-    for (uint32_t b = 0; b < h.m && h.ntiles > 1; ++b) {
+    for (uint32_t b = 0; b < h.m; ++b) {
       const uint32_t q = h.S[b];
       k << "    b = ((b >> " << q << ") << " << (q + 1) << ") | (b & " << hexll((1ull << q) - 1) << ");\n";
     }
@@ -409,17 +410,17 @@ struct Gen {
       // HBM reads of tile i+1 overlap the arithmetic of tile i.
       k << "  double2* const PB = sm + " << (tp.transposes ? (1u << h.m) : 0u) << ";\n";
       k << "  auto prefetch = [&](unsigned long long t) {\n";
-      k << "    const unsigned long long g = base_of(t) | TL;\n";
+      k << "    const unsigned long long g = base_of(t) | rank_base | TL;\n";
       for (int p = 0; p < 16; ++p)
-        k << "    cp_async16(PB + " << p * T << " + tid, amps + (g | " << hexll(loff[p]) << "));\n";
+        k << "    cp_async16(PB + " << p * T << " + tid, amps + ((g | " << hexll(loff[p]) << ") & lmask));\n";
       k << "    cp_async_commit();\n  };\n";
       k << "  unsigned long long tile = blockIdx.x;\n";
-      k << "  if (tile < " << h.ntiles << "ull) prefetch(tile);\n";
-      k << "  for (; tile < " << h.ntiles << "ull; tile += gridDim.x) {\n";
+      k << "  if (tile < ntiles) prefetch(tile);\n";
+      k << "  for (; tile < ntiles; tile += gridDim.x) {\n";
     } else {
-      k << "  for (unsigned long long tile = blockIdx.x; tile < " << h.ntiles << "ull; tile += gridDim.x) {\n";
+      k << "  for (unsigned long long tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {\n";
     }
-    k << "    const unsigned long long base = base_of(tile);\n";
+    k << "    const unsigned long long base = base_of(tile) | rank_base;\n";
     k << "    unsigned long long G = base | TL;\n";
     k << s.str();
     k << "  }\n}\n";

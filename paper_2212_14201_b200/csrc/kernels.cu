@@ -223,7 +223,7 @@ __device__ __forceinline__ double block_sum(double v, double* sh) {
 
 // mode 0: sum |a|^2 ; 1: sum over i with bit q set ; 2: sum |a_i|^2 (i+1)
 __global__ void __launch_bounds__(kThreads) k_reduce(const double2* __restrict__ a, uint64_t n_items, int mode,
-                                                     uint64_t bit, double* __restrict__ partial) {
+                                                     uint64_t bit, uint64_t index_base, double* __restrict__ partial) {
   __shared__ double sh[kThreads / 32];
   const uint64_t chunk = (n_items + gridDim.x - 1) / gridDim.x;
   const uint64_t lo = blockIdx.x * chunk, hi = min(n_items, lo + chunk);
@@ -234,7 +234,7 @@ __global__ void __launch_bounds__(kThreads) k_reduce(const double2* __restrict__
       const uint64_t i = ((g & ~(bit - 1)) << 1) | bit | low;
       s += norm_ref(a[i]);
     } else if (mode == 2) {
-      s += norm_ref(a[g]) * (double)(g + 1);
+      s += norm_ref(a[g]) * (double)(index_base + g + 1);
     } else {
       s += norm_ref(a[g]);
     }
@@ -320,6 +320,42 @@ __global__ void __launch_bounds__(kThreads) k_scale(double2* __restrict__ a, uin
 __global__ void __launch_bounds__(kThreads) k_basis(double2* __restrict__ a, uint64_t size, uint64_t index) {
   for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < size; i += (uint64_t)gridDim.x * blockDim.x)
     a[i] = make_double2(i == index ? 1.0 : 0.0, 0.0);
+}
+
+// ------------------------------------------------- rank-bit exchanges
+// Swapping rank bit j with local bit p: the shard whose bit j is x keeps the
+// half with local bit p == x and trades the other half with its partner.
+
+// Both shards on this device (single-process shard groups): a holds x = 0
+// (sends its p == 1 half), b holds x = 1 (sends its p == 0 half).
+__global__ void __launch_bounds__(kThreads) k_swap_halves(double2* __restrict__ a, double2* __restrict__ b,
+                                                          uint64_t count, uint32_t p) {
+  const uint64_t bit = 1ull << p;
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < count; i += (uint64_t)gridDim.x * blockDim.x) {
+    const uint64_t l = ((i >> p) << (p + 1)) | (i & (bit - 1));
+    const double2 x = a[l | bit], y = b[l];
+    a[l | bit] = y;
+    b[l] = x;
+  }
+}
+
+// Gathers elements [off, off + cnt) of the half with local bit p == v.
+__global__ void __launch_bounds__(kThreads) k_pack_half(const double2* __restrict__ a, uint32_t p, uint32_t v,
+                                                        uint64_t off, uint64_t cnt, double2* __restrict__ out) {
+  const uint64_t bit = 1ull << p;
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < cnt; i += (uint64_t)gridDim.x * blockDim.x) {
+    const uint64_t k = off + i;
+    out[i] = a[((k >> p) << (p + 1)) | (v ? bit : 0) | (k & (bit - 1))];
+  }
+}
+
+__global__ void __launch_bounds__(kThreads) k_unpack_half(double2* __restrict__ a, uint32_t p, uint32_t v,
+                                                          uint64_t off, uint64_t cnt, const double2* __restrict__ in) {
+  const uint64_t bit = 1ull << p;
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < cnt; i += (uint64_t)gridDim.x * blockDim.x) {
+    const uint64_t k = off + i;
+    a[((k >> p) << (p + 1)) | (v ? bit : 0) | (k & (bit - 1))] = in[i];
+  }
 }
 
 // ------------------------------------------------- serial-equivalent scan
@@ -599,9 +635,25 @@ inline double2 d2(cd c) { return make_double2(c.real(), c.imag()); }
 
 // ------------------------------------------------------------ launchers
 
-void launch_op(State& s, const Op& op) {
+void launch_op(State& s, const Op& op_in) {
   DeviceGuard dg(s.device);
-  const uint32_t n = s.n;
+  const uint32_t n = s.local_qubits();
+  Op local;
+  const Op* opp = &op_in;
+  if (s.g) {
+    // Sharded: controls on rank bits are this shard's constants; targets are
+    // local (the planner exchanges rank bits in first).
+    local = op_in;
+    local.controls.clear();
+    for (auto c : op_in.controls) {
+      if (c < n) local.controls.push_back(c);
+      else if (!((s.rank >> (c - n)) & 1)) return;  // control is 0 on this shard
+    }
+    for (auto t : op_in.targets)
+      if (t >= n) throw RuntimeError("per-gate kernel on a rank bit (planner invariant)");
+    opp = &local;
+  }
+  const Op& op = *opp;
   switch (op.kind) {
     case OpKind::Identity: return;
     case OpKind::Mat1: {
@@ -670,6 +722,25 @@ void launch_op(State& s, const Op& op) {
   }
 }
 
+void swap_halves(State& a, State& b, uint32_t p) {
+  DeviceGuard dg(a.device);
+  const uint64_t count = a.size / 2;
+  k_swap_halves<<<grid_for(count, a.device), kThreads, 0, a.stream>>>(a.amps, b.amps, count, p);
+  QSB_LAUNCHED();
+}
+
+void pack_half(State& s, uint32_t p, uint32_t v, uint64_t off, uint64_t cnt, double2* out) {
+  DeviceGuard dg(s.device);
+  k_pack_half<<<grid_for(cnt, s.device), kThreads, 0, s.stream>>>(s.amps, p, v, off, cnt, out);
+  QSB_LAUNCHED();
+}
+
+void unpack_half(State& s, uint32_t p, uint32_t v, uint64_t off, uint64_t cnt, const double2* in) {
+  DeviceGuard dg(s.device);
+  k_unpack_half<<<grid_for(cnt, s.device), kThreads, 0, s.stream>>>(s.amps, p, v, off, cnt, in);
+  QSB_LAUNCHED();
+}
+
 void fill_basis(State& s, uint64_t index) {
   DeviceGuard dg(s.device);
   k_basis<<<grid_for(s.size, s.device), kThreads, 0, s.stream>>>(s.amps, s.size, index);
@@ -681,7 +752,7 @@ double reduce_mode(State& s, int mode, uint32_t q) {
   DeviceGuard dg(s.device);
   double* part = static_cast<double*>(s.get_scratch((kRedBlocks + 1) * sizeof(double)));
   const uint64_t items = mode == 1 ? s.size / 2 : s.size;
-  k_reduce<<<kRedBlocks, kThreads, 0, s.stream>>>(s.amps, items, mode, 1ull << q, part);
+  k_reduce<<<kRedBlocks, kThreads, 0, s.stream>>>(s.amps, items, mode, 1ull << q, s.rank_base, part);
   QSB_LAUNCHED();
   k_finalize<<<1, kThreads, 0, s.stream>>>(part, kRedBlocks, part + kRedBlocks);
   QSB_LAUNCHED();

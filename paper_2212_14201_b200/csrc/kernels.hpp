@@ -14,7 +14,12 @@ namespace qsb {
 // One HBM pass per op (the reference's per-gate kernels, statevector.hpp:268-467).
 void launch_op(State& s, const Op& op);
 
-void fill_basis(State& s, uint64_t index);                      // |index>
+void fill_basis(State& s, uint64_t index);                      // |index> (local index; out of range = all 0)
+
+// Rank-bit exchanges for sharded states (shard.cpp).
+void swap_halves(State& a, State& b, uint32_t p);                // a: rank bit 0, b: rank bit 1, same device
+void pack_half(State& s, uint32_t p, uint32_t v, uint64_t off, uint64_t cnt, double2* out);
+void unpack_half(State& s, uint32_t p, uint32_t v, uint64_t off, uint64_t cnt, const double2* in);
 double reduce_norm2(State& s);                                   // statevector.hpp:158-162
 double reduce_prob_one(State& s, uint32_t q);                    // :181-186
 double reduce_checksum(State& s);                                // bench.hpp:141-148

@@ -10,7 +10,7 @@ namespace qsb {
 uint64_t Plan::passes() const {
   uint64_t p = 0;
   for (const auto& s : steps)
-    if (s.kind == Step::TileStep || s.op.kind != OpKind::Identity) ++p;
+    if (s.kind != Step::OpStep || s.op.kind != OpKind::Identity) ++p;
   return p;
 }
 
@@ -24,9 +24,15 @@ uint64_t Plan::launches() const {
 }
 
 std::unique_ptr<Plan> make_plan(uint32_t n, const qs_gate* gates, uint64_t count, uint32_t mode,
-                                uint32_t max_fused_qubits) {
+                                uint32_t max_fused_qubits, uint32_t global_qubits) {
   auto plan = std::make_unique<Plan>();
   plan->n = n;
+  plan->g = global_qubits;
+  if (global_qubits) {
+    if (mode != QS_PLAN_DEFAULT && mode != QS_PLAN_TILED)
+      throw ValidationError("sharded states are planned with tile passes only");
+    if (global_qubits >= n || n - global_qubits < 6) throw ValidationError("each shard needs at least 6 local qubits");
+  }
   plan->mode = mode == QS_PLAN_DEFAULT ? QS_PLAN_TILED : mode;
   plan->gates = count;
   // validation first (validate_or_throw, circuit.hpp:523), in program order
@@ -49,7 +55,7 @@ std::unique_ptr<Plan> make_plan(uint32_t n, const qs_gate* gates, uint64_t count
     }
   }
   if (plan->mode == QS_PLAN_TILED) {
-    plan_tiles(n, ops, plan->steps);
+    plan_tiles(n, ops, plan->steps, global_qubits);
     compile_tile_steps(plan->steps);
   } else {
     for (auto& op : ops) {
@@ -65,12 +71,16 @@ std::unique_ptr<Plan> make_plan(uint32_t n, const qs_gate* gates, uint64_t count
 
 void execute_plan(State& s, const Plan& p) {
   if (p.n != s.n) throw ValidationError("plan was compiled for a different qubit count");
+  if (p.g != s.g) throw ValidationError("plan was compiled for a sharded state (use the shard API)");
   for (const auto& st : p.steps) execute_step(s, st);
 }
 
 void execute_step(State& s, const Step& st) {
-  if (st.kind == Step::OpStep) launch_op(s, st.op);
-  else launch_tile(s, *st.tile);
+  switch (st.kind) {
+    case Step::OpStep: launch_op(s, st.op); break;
+    case Step::TileStep: launch_tile(s, *st.tile); break;
+    case Step::SwapStep: throw ValidationError("rank-bit exchange outside a shard set");
+  }
 }
 
 }  // namespace qsb

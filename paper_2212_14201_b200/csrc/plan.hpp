@@ -15,13 +15,17 @@ namespace qsb {
 struct TileProgram;  // tile.hpp
 
 struct Step {
-  enum Kind { OpStep, TileStep } kind = OpStep;
+  enum Kind { OpStep, TileStep, SwapStep } kind = OpStep;
   Op op;                               // OpStep
   std::shared_ptr<TileProgram> tile;   // TileStep
+  // SwapStep (sharded states): exchange physical qubit n-g+gpos (a rank bit)
+  // with local physical qubit lpos -- a pairwise half-shard exchange.
+  uint32_t gpos = 0, lpos = 0;
 };
 
 struct Plan {
   uint32_t n = 0;
+  uint32_t g = 0;         // global (rank) qubits: the state is split over 2^g shards
   uint32_t mode = QS_PLAN_DEFAULT;
   uint64_t gates = 0;     // submitted gate count
   std::vector<Step> steps;
@@ -31,7 +35,7 @@ struct Plan {
 
 // Lowers and plans `count` gates for an n-qubit state.
 std::unique_ptr<Plan> make_plan(uint32_t n, const qs_gate* gates, uint64_t count, uint32_t mode,
-                                uint32_t max_fused_qubits);
+                                uint32_t max_fused_qubits, uint32_t global_qubits = 0);
 void execute_plan(State& s, const Plan& p);
 void execute_step(State& s, const Step& st);
 

@@ -1,0 +1,75 @@
+// Sharded state vectors: the top g qubits of an n-qubit state are
+// rank bits; shard r holds the 2^(n-g) amplitudes whose global index has
+// rank bits = r.  Tile passes run on every shard independently (rank bits are
+// outside every tile: diagonal gates and controls on them are per-shard
+// constants); a non-diagonal gate on a rank bit is preceded by a planner
+// SwapStep: rank bit j <-> local qubit p, a pairwise exchange of half a shard
+// between ranks r and r ^ 2^j.
+//
+// Two transports:
+//   * LocalTransport: all 2^g shards in one process on one device (the halves
+//     are swapped by one kernel).  Used to validate sharded plans on a single
+//     B200 and to run states larger than one allocation would allow.
+//   * NcclTransport: one shard per process/GPU; halves travel with grouped
+//     ncclSend/ncclRecv over NVLink in bounded chunks (libnccl is loaded at run
+//     time; the unique id is exchanged by the caller, e.g. torch.distributed).
+#pragma once
+
+#include <cstdint>
+#include <memory>
+#include <vector>
+
+#include "common.hpp"
+
+namespace qsb {
+
+struct Plan;
+
+struct Transport {
+  virtual ~Transport() = default;
+  virtual void exchange(std::vector<State*>& shards, uint32_t gpos, uint32_t lpos) = 0;
+  // sum of one double per shard over all ranks, in rank order (deterministic)
+  virtual double sum(const std::vector<double>& per_local_shard) = 0;
+  virtual void barrier() {}
+};
+
+struct ShardSet {
+  uint32_t n = 0, g = 0;
+  int device = 0;
+  std::vector<std::unique_ptr<State>> shards;  // the shards this process holds
+  std::unique_ptr<Transport> tr;
+  cudaStream_t stream = nullptr;               // shared by the local shards
+  bool owns_stream = true;
+
+  std::vector<State*> ptrs() {
+    std::vector<State*> v;
+    for (auto& s : shards) v.push_back(s.get());
+    return v;
+  }
+  ~ShardSet();
+};
+
+// Single-process group of 2^g shards on `device`.
+std::unique_ptr<ShardSet> make_local_shards(uint32_t n, uint32_t g, int device);
+
+// NCCL communicator handle (dist API).
+struct Dist;
+void dist_unique_id(unsigned char out[128]);
+Dist* dist_create(const unsigned char id[128], int world, int rank, int device);
+void dist_destroy(Dist* d);
+int dist_rank(const Dist* d);
+int dist_world(const Dist* d);
+// This process's shard of an n-qubit state over dist's world (a power of two).
+std::unique_ptr<ShardSet> make_dist_shard(uint32_t n, Dist* d);
+
+void shard_fill_basis(ShardSet& ss, uint64_t index);
+void shard_execute(ShardSet& ss, const Plan& p, uint64_t first = 0, uint64_t count = ~0ull);
+double shard_norm2(ShardSet& ss);
+double shard_checksum(ShardSet& ss);
+// Amplitude / probability I/O over [offset, offset+count) of the global index;
+// in a distributed set the range must lie inside this rank's shard.
+void shard_get(ShardSet& ss, double* out, uint64_t offset, uint64_t count);
+void shard_set(ShardSet& ss, const double* in, uint64_t offset, uint64_t count);
+void shard_sync(ShardSet& ss);
+
+}  // namespace qsb

@@ -98,14 +98,16 @@ struct TileOptions {
   uint32_t low = 4; // qubits 0..low-1 always in the tile: 256 B contiguous runs
                     // (measured: 128 B runs 70% of HBM per pass, 256 B 80%)
   bool remap = true;  // plan-level qubit relabelling (low slots hold the qubits needed next)
+  uint32_t global_qubits = 0;  // sharded states: top qubits are rank bits, never in a tile
 };
 TileOptions tile_options_from_env();
 
 void plan_tiles(uint32_t n, std::vector<Op>& ops, std::vector<Step>& steps, const TileOptions& opt);
 // Plans with and without qubit relabelling (unless fixed by QSB_TILE_REMAP)
 // and keeps the plan with fewer HBM passes.
-inline void plan_tiles(uint32_t n, std::vector<Op>& ops, std::vector<Step>& steps) {
+inline void plan_tiles(uint32_t n, std::vector<Op>& ops, std::vector<Step>& steps, uint32_t global_qubits = 0) {
   TileOptions o = tile_options_from_env();
+  o.global_qubits = global_qubits;
   if (std::getenv("QSB_TILE_REMAP")) {
     plan_tiles(n, ops, steps, o);
     return;

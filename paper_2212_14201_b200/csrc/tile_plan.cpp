@@ -39,6 +39,7 @@ std::vector<POp> preprocess(std::vector<Op>& ops) {
       case PK::Flip:
       case PK::SwapRel:
       case PK::Dense:
+      case PK::Opaque:
         for (auto q : op.targets) p.needmask |= bit(q);
         break;
       default: break;
@@ -696,7 +697,8 @@ POp swap_rel(uint32_t a, uint32_t b) {
 
 // Chooses the tile set S (physical qubits) for the next pass: starting from the
 // always-resident low qubits, add the qubit that lets the most pending ops run.
-uint64_t choose_tile_set(const std::vector<POp>& phys, const std::vector<uint32_t>& rem, uint64_t S0, uint32_t m) {
+uint64_t choose_tile_set(const std::vector<POp>& phys, const std::vector<uint32_t>& rem, uint64_t S0, uint32_t m,
+                         uint64_t allowed) {
   uint64_t S = S0;
   size_t cur = scan(phys, rem, S, nullptr);
   while (static_cast<uint32_t>(__builtin_popcountll(S)) < m) {
@@ -709,7 +711,7 @@ uint64_t choose_tile_set(const std::vector<POp>& phys, const std::vector<uint32_
       for (size_t i = 0; i < rem.size() && looked < 256; ++i) {
         if (tk[i]) continue;
         ++looked;
-        uint64_t nm = phys[rem[i]].needmask & ~seen;
+        uint64_t nm = phys[rem[i]].needmask & ~seen & allowed;
         while (nm) {
           const uint32_t q = static_cast<uint32_t>(__builtin_ctzll(nm));
           nm &= nm - 1;
@@ -736,7 +738,8 @@ uint64_t choose_tile_set(const std::vector<POp>& phys, const std::vector<uint32_
       for (size_t i = 0; i < rem.size(); ++i) {
         if (tk[i] || phys[rem[i]].k == PK::Opaque) continue;
         const uint64_t ns = S | phys[rem[i]].needmask;
-        if (static_cast<uint32_t>(__builtin_popcountll(ns)) <= m && scan(phys, rem, ns, nullptr) > cur) {
+        if (!(ns & ~allowed) && static_cast<uint32_t>(__builtin_popcountll(ns)) <= m &&
+            scan(phys, rem, ns, nullptr) > cur) {
           S = ns;
           cur = scan(phys, rem, S, nullptr);
           added = true;
@@ -766,11 +769,16 @@ void plan_tiles(uint32_t n, std::vector<Op>& ops, std::vector<Step>& steps, cons
     }
     return;
   }
-  const uint32_t m = std::min<uint32_t>(n, opt.m);
+  // Sharded states: physical qubits [nl, n) are rank bits.  Tiles only hold
+  // local qubits; a non-diagonal gate on a rank bit is preceded by a SwapStep
+  // (pairwise half-shard exchange) that brings that qubit into the shard.
+  const uint32_t nl = n - opt.global_qubits;
+  const uint32_t m = std::min<uint32_t>(nl, opt.m);
   const uint32_t L = std::min<uint32_t>(opt.low, m - kTileR);
   const uint64_t lowmask = (1ull << L) - 1;
-  const uint64_t allmask = n >= 64 ? ~0ull : (1ull << n) - 1;
-  const bool remap = opt.remap && n > m;
+  const uint64_t allmask = nl >= 64 ? ~0ull : (1ull << nl) - 1;  // every local position
+  const uint64_t gmask = (n >= 64 ? ~0ull : (1ull << n) - 1) & ~allmask;
+  const bool remap = opt.remap && nl > m;
 
   // Logical -> physical qubit map.  The low L physical qubits are in every
   // tile (coalescing); relabel SWAPs at pass ends move the qubits needed next
@@ -793,7 +801,7 @@ void plan_tiles(uint32_t n, std::vector<Op>& ops, std::vector<Step>& steps, cons
     keep.reserve(rem.size());
     for (auto idx : rem) {
       const POp& p = phys[idx];
-      if (p.k == PK::Opaque && !(p.qmask & blocked)) {
+      if (p.k == PK::Opaque && !(p.qmask & blocked) && !(p.needmask & gmask)) {
         Step s;
         s.kind = Step::OpStep;
         s.op = p.op;
@@ -814,6 +822,42 @@ void plan_tiles(uint32_t n, std::vector<Op>& ops, std::vector<Step>& steps, cons
     for (uint32_t q = 0; q < n; ++q)
       if (perm[q] != q) return false;
     return true;
+  };
+  auto emit_swap = [&](uint32_t j, uint32_t p) {  // rank bit j <-> local position p
+    Step s;
+    s.kind = Step::SwapStep;
+    s.gpos = j - nl;
+    s.lpos = p;
+    steps.push_back(std::move(s));
+    swap_phys(j, p);
+  };
+  // Brings every rank bit the op needs into the shard, evicting the local
+  // qubits needed furthest in the future (Belady); ties prefer the highest
+  // position (the exchanged half is then contiguous).
+  auto global_swaps_for = [&](const POp& op) {
+    std::vector<size_t> next(n, SIZE_MAX);
+    for (size_t k = 0; k < rem.size(); ++k) {
+      uint64_t nm = pops[rem[k]].needmask;  // logical
+      while (nm) {
+        const uint32_t l = static_cast<uint32_t>(__builtin_ctzll(nm));
+        nm &= nm - 1;
+        if (next[l] == SIZE_MAX) next[l] = k;
+      }
+    }
+    uint64_t need = op.needmask & gmask;
+    uint64_t taken = op.qmask;
+    while (need) {
+      const uint32_t j = static_cast<uint32_t>(__builtin_ctzll(need));
+      need &= need - 1;
+      int best = -1;
+      for (int p = static_cast<int>(nl) - 1; p >= 0; --p) {
+        if ((taken >> p) & 1) continue;
+        if (best < 0 || next[inv[p]] > next[inv[best]]) best = p;
+      }
+      if (best < 0) throw RuntimeError("no local qubit available for a rank-bit exchange");
+      emit_swap(j, static_cast<uint32_t>(best));
+      taken |= bit(static_cast<uint32_t>(best));
+    }
   };
 
   auto compile_pass = [&](uint64_t S, const std::vector<const POp*>& list, const std::vector<uint64_t>& srcs) {
@@ -852,7 +896,14 @@ void plan_tiles(uint32_t n, std::vector<Op>& ops, std::vector<Step>& steps, cons
   emit_ready_opaque();
   while (!rem.empty()) {
     refresh();
-    uint64_t S = choose_tile_set(phys, rem, n <= m ? allmask : lowmask, m);
+    // a non-diagonal gate on a rank bit at the head of the program: exchange first
+    if (gmask && (phys[rem[0]].needmask & gmask)) {
+      global_swaps_for(phys[rem[0]]);
+      refresh();
+      emit_ready_opaque();
+      continue;
+    }
+    uint64_t S = choose_tile_set(phys, rem, nl <= m ? allmask : lowmask, m, allmask);
     std::vector<char> tk(rem.size(), 0);
     size_t cnt = scan(phys, rem, S, &tk);
     if (cnt == 0) throw RuntimeError("tile planner made no progress");
@@ -860,9 +911,9 @@ void plan_tiles(uint32_t n, std::vector<Op>& ops, std::vector<Step>& steps, cons
     // pad S to exactly m qubits: on the last pass prefer displaced positions
     // (so the layout can be restored for free), else the lowest unused
     if (last && remap)
-      for (uint32_t q = 0; q < n && static_cast<uint32_t>(__builtin_popcountll(S)) < m; ++q)
+      for (uint32_t q = 0; q < nl && static_cast<uint32_t>(__builtin_popcountll(S)) < m; ++q)
         if (inv[q] != q) S |= bit(q);
-    for (uint32_t q = 0; q < n && static_cast<uint32_t>(__builtin_popcountll(S)) < m; ++q) S |= bit(q);
+    for (uint32_t q = 0; q < nl && static_cast<uint32_t>(__builtin_popcountll(S)) < m; ++q) S |= bit(q);
 
     std::vector<size_t> taken_pos;  // positions in rem, program order
     for (size_t i = 0; i < rem.size(); ++i)
@@ -952,18 +1003,28 @@ void plan_tiles(uint32_t n, std::vector<Op>& ops, std::vector<Step>& steps, cons
     refresh();
     emit_ready_opaque();
   }
-  // Restore the logical layout if the last pass could not (or opaque ops ended
-  // the plan): relabel-only passes over the displaced positions.
-  while (remap && !identity()) {
+  // Restore the logical layout: rank bits by exchanges, then relabel-only
+  // passes over the displaced local positions.
+  for (uint32_t j = nl; j < n; ++j) {
+    if (inv[j] == j) continue;
+    uint32_t src = perm[j];  // where logical j lives now
+    if (src >= nl) {         // on another rank bit: route through a local position
+      const uint32_t p = nl - 1;
+      emit_swap(src, p);
+      src = p;
+    }
+    emit_swap(j, src);
+  }
+  while (!identity()) {
     uint64_t S = lowmask;
-    for (uint32_t p = 0; p < n && static_cast<uint32_t>(__builtin_popcountll(S)) < m; ++p)
+    for (uint32_t p = 0; p < nl && static_cast<uint32_t>(__builtin_popcountll(S)) < m; ++p)
       if (inv[p] != p) {
         S |= bit(p);
         if (static_cast<uint32_t>(__builtin_popcountll(S)) < m) S |= bit(perm[p]);
       }
-    for (uint32_t q = 0; q < n && static_cast<uint32_t>(__builtin_popcountll(S)) < m; ++q) S |= bit(q);
+    for (uint32_t q = 0; q < nl && static_cast<uint32_t>(__builtin_popcountll(S)) < m; ++q) S |= bit(q);
     std::vector<std::pair<uint32_t, uint32_t>> swaps;
-    for (uint32_t p = 0; p < n; ++p) {
+    for (uint32_t p = 0; p < nl; ++p) {
       if (!((S >> p) & 1) || inv[p] == p) continue;
       const uint32_t where = perm[p];
       if ((S >> where) & 1) {

@@ -76,3 +76,19 @@ def test_emulated_golden_states(c):
         pytest.skip("tiles need >= 6 qubits")
     got, _ = emu_lib.run(circ.qubits, circ.gates, N.QS_PLAN_TILED, tile_m=min(12, max(8, circ.qubits - 2)))
     assert np.max(np.abs(got - gio.read_amps(c["name"] + ".amps"))) <= 1e-10
+
+
+@pytest.mark.parametrize("g", [1, 2, 3])
+@pytest.mark.parametrize("which", ["random", "qft", "mixed", "hea"])
+def test_emulated_sharded_plans(which, g):
+    # Sharded plans (rank bits never in a tile, SwapSteps before non-diagonal
+    # gates on them, identity layout restored) replayed on the full state.
+    n = 14
+    gates = {"random": lambda: Q.gen_random_circuit(n, 5, 424242).gates(),
+             "qft": lambda: Q.gen_qft(n, 0x2345).gates(),
+             "mixed": lambda: mixed_gates(n, 250, 77 + g),
+             "hea": lambda: Q.gen_hea(n, 3, 9).gates()}[which]()
+    want = ol.run_gates(n, gates)
+    for remap in (0, 1):
+        got, steps = emu_lib.run(n, gates, N.QS_PLAN_TILED, tile_m=9, low=3, global_qubits=g, remap=remap)
+        assert np.max(np.abs(got - want)) <= 1e-10, (remap, steps)

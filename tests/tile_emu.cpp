@@ -8,10 +8,12 @@
 #include <array>
 #include <cstdlib>
 #include <cstring>
+#include <memory>
 #include <vector>
 
 #include "../paper_2212_14201_b200/csrc/fusion.hpp"
 #include "../paper_2212_14201_b200/csrc/gates.hpp"
+#include "../paper_2212_14201_b200/csrc/plan.hpp"
 #include "../paper_2212_14201_b200/csrc/tile.hpp"
 
 using qsb::cd;
@@ -214,7 +216,7 @@ extern "C" {
 // Plans `gates` exactly as libqsb does and replays the plan on amps (2^n
 // complex, interleaved, in/out).  Returns 0, or -1 with the message in err.
 int te_run(uint32_t n, const qs_gate* gates, uint64_t count, uint32_t mode, uint32_t maxk, uint32_t tile_m,
-           uint32_t low, double* amps, char* err, uint64_t* passes) {
+           uint32_t low, double* amps, char* err, uint64_t* passes, uint32_t global_qubits, int remap) {
   try {
     std::vector<qsb::Op> ops;
     for (uint64_t i = 0; i < count; ++i) qsb::validate_gate(gates[i], n);
@@ -238,7 +240,19 @@ int te_run(uint32_t n, const qs_gate* gates, uint64_t count, uint32_t mode, uint
       qsb::TileOptions opt;
       opt.m = tile_m;
       opt.low = low;
-      qsb::plan_tiles(n, ops, steps, opt);
+      opt.global_qubits = global_qubits;
+      if (remap >= 0) {
+        opt.remap = remap != 0;
+        qsb::plan_tiles(n, ops, steps, opt);
+      } else {  // as the library does: keep the plan with fewer steps
+        std::vector<qsb::Op> copy = ops;
+        std::vector<qsb::Step> a1, a2;
+        opt.remap = false;
+        qsb::plan_tiles(n, copy, a1, opt);
+        opt.remap = true;
+        qsb::plan_tiles(n, ops, a2, opt);
+        steps = a2.size() < a1.size() ? std::move(a2) : std::move(a1);
+      }
     }
     std::vector<cd> a(size_t(1) << n);
     std::memcpy(a.data(), amps, a.size() * sizeof(cd));
@@ -246,8 +260,16 @@ int te_run(uint32_t n, const qs_gate* gates, uint64_t count, uint32_t mode, uint
     const size_t max_steps = lim ? static_cast<size_t>(std::atoll(lim)) : steps.size();
     for (size_t i = 0; i < steps.size() && i < max_steps; ++i) {
       const auto& s = steps[i];
-      if (s.kind == qsb::Step::OpStep) emu_op(a, n, s.op);
-      else emu_tile(a, *s.tile);
+      if (s.kind == qsb::Step::OpStep) {
+        emu_op(a, n, s.op);
+      } else if (s.kind == qsb::Step::SwapStep) {  // exchange = physical bit swap
+        qsb::Op sw;
+        sw.kind = qsb::OpKind::Swap;
+        sw.targets = {n - global_qubits + s.gpos, s.lpos};
+        emu_op(a, n, sw);
+      } else {
+        emu_tile(a, *s.tile);
+      }
     }
     std::memcpy(amps, a.data(), a.size() * sizeof(cd));
     if (passes) *passes = steps.size();
@@ -257,6 +279,61 @@ int te_run(uint32_t n, const qs_gate* gates, uint64_t count, uint32_t mode, uint
     err[255] = 0;
     return -1;
   }
+}
+
+// Step-wise access to a sharded plan, for the multi-process (gloo) tests: each
+// rank replays the non-exchange steps on its own shard and performs the
+// exchanges itself.
+struct te_plan {
+  std::unique_ptr<qsb::Plan> p;
+};
+
+int te_plan_create(uint32_t n, uint32_t g, const qs_gate* gates, uint64_t count, te_plan** out, char* err) {
+  try {
+    auto h = std::make_unique<te_plan>();
+    h->p = std::make_unique<qsb::Plan>();
+    h->p->n = n;
+    h->p->g = g;
+    std::vector<qsb::Op> ops;
+    for (uint64_t i = 0; i < count; ++i) qsb::validate_gate(gates[i], n);
+    for (uint64_t i = 0; i < count; ++i) ops.push_back(qsb::lower_gate(gates[i], n, false));
+    qsb::plan_tiles(n, ops, h->p->steps, g);
+    *out = h.release();
+    return 0;
+  } catch (const std::exception& e) {
+    std::strncpy(err, e.what(), 255);
+    err[255] = 0;
+    return -1;
+  }
+}
+
+void te_plan_free(te_plan* h) { delete h; }
+uint64_t te_plan_steps(te_plan* h) { return h->p->steps.size(); }
+int te_plan_step(te_plan* h, uint64_t i, uint32_t* gpos, uint32_t* lpos) {
+  const auto& s = h->p->steps[i];
+  *gpos = s.gpos;
+  *lpos = s.lpos;
+  return static_cast<int>(s.kind);
+}
+
+// Runs non-exchange step i on a local shard: `shard` holds the 2^(n-g)
+// amplitudes of rank `rank`.  The shard is embedded in a 2^n vector that is
+// zero elsewhere; a correct sharded plan never moves amplitude across rank
+// bits between exchanges, which the caller's comparison checks.
+int te_exec_step(te_plan* h, uint64_t i, uint32_t rank, double* shard) {
+  const auto& s = h->p->steps[i];
+  const uint32_t n = h->p->n, nl = n - h->p->g;
+  std::vector<cd> a(size_t(1) << n);
+  const size_t base = static_cast<size_t>(rank) << nl;
+  std::memcpy(a.data() + base, shard, (size_t(1) << nl) * sizeof(cd));
+  if (s.kind == qsb::Step::OpStep) emu_op(a, n, s.op);
+  else if (s.kind == qsb::Step::TileStep) emu_tile(a, *s.tile);
+  else return -1;
+  double leak = 0;
+  for (size_t k = 0; k < a.size(); ++k)
+    if ((k >> nl) != rank) leak += std::norm(a[k]);
+  std::memcpy(shard, a.data() + base, (size_t(1) << nl) * sizeof(cd));
+  return leak == 0 ? 0 : -2;
 }
 
 }  // extern "C"
