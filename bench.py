@@ -13,10 +13,13 @@ host gate array: planning + upload + execution + checksum read-back).
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
                     [--workload random30|random28|qft30|hea24|ghz20] [--plan tiled|dense|unfused]
 
-Under torchrun (N > 1) each rank runs an independent replica (the sharded
-34-qubit path is not in this bench yet); value sums all ranks, time is the max
-over ranks.  `--impl reference` times the reference CPU simulator
-(oracle/_ref/ref_driver, the unmodified qforge headers) on rank 0.
+Under torchrun (N > 1, a power of two) the same circuit runs on ONE state
+sharded over the N GPUs (top log2 N qubits = rank bits, half-shard exchanges
+over NCCL; strong scaling); `--replicas` runs independent copies instead.  The
+time is the max over ranks.  `--local-shards G` (N = 1) runs the sharded plan
+with 2^G shards on one GPU (diagnostic).  `--impl reference` times the
+reference CPU simulator (oracle/_ref/ref_driver, the unmodified qforge
+headers) on rank 0.
 """
 import argparse
 import json
@@ -37,6 +40,7 @@ WORKLOADS = {
     "qft30": ("qft", (30, 0x2AAAAAAA), 30),
     "hea24": ("hea", (24, 10, 2024), 24),
     "ghz20": ("ghz", (20,), 20),
+    "qft34": ("qft", (34, 0x2AAAAAAAA), 34),  # sharded over >= 2 GPUs (256 GiB state)
 }
 
 
@@ -144,6 +148,110 @@ def cpu_baseline_reference(workload, layers, reps, threads=None):
     return rows, None
 
 
+class SingleRunner:
+    """Whole state on one GPU (qs_state_t + qs_plan_t)."""
+
+    sharded = False
+
+    def __init__(self, n, gates, device, plan_mode):
+        from paper_2212_14201_b200 import _native as N
+        from paper_2212_14201_b200 import qforge as Q
+        self.N, self.L = N, N.lib()
+        t0 = time.time()
+        self.cc = Q.CompiledCircuit(n, gates, plan=plan_mode, max_fused_qubits=3)
+        self.plan_s = time.time() - t0
+        self.stats = self.cc.stats()
+        self.sv = Q.StateVector(n, device=device)
+        self.shard_amps = 1 << n
+        self.plan_mode = plan_mode
+        self.arr, self.keep = N.gate_array(gates)
+        self.G = len(gates)
+        self.cs = N.C.c_double()
+        self.e2e_path = "qs_apply_circuit(host qs_gate array) + qs_checksum"
+
+    def parallelism(self, world):
+        return "replicas" if world > 1 else "single"
+
+    def stream(self):
+        return self.L.qs_stream(self.sv.handle())
+
+    def reset(self):
+        self.N.check(self.L.qs_reset(self.sv.handle()))
+
+    def enqueue(self):
+        self.N.check(self.L.qs_plan_enqueue(self.sv.handle(), self.cc._h))
+
+    def checksum(self):
+        self.N.check(self.L.qs_checksum(self.sv.handle(), self.N.C.byref(self.cs)))
+        return self.cs.value
+
+    def apply_host(self):
+        self.N.check(self.L.qs_apply_circuit(self.sv.handle(), self.arr, self.G, self.plan_mode, 3))
+
+    def step_kinds(self):
+        return [1] * self.stats["launches"]
+
+    def timed(self):
+        buf = (self.N.C.c_float * max(1, self.stats["launches"]))()
+        self.N.check(self.L.qs_plan_execute_timed(self.sv.handle(), self.cc._h, buf))
+        return list(buf)[:self.stats["launches"]]
+
+
+class ShardedRunner:
+    """Amplitude-sharded state: one shard per rank over NCCL (dist_world > 1), or
+    2^local_g shards on this GPU (diagnostic: same plan, device-local exchanges)."""
+
+    sharded = True
+
+    def __init__(self, n, gates, device, dist_world=0, local_g=0):
+        from paper_2212_14201_b200 import _native as N
+        from paper_2212_14201_b200.sharded import DistComm, ShardedCircuit, ShardedState
+        self.N, self.L = N, N.lib()
+        self.g = (dist_world.bit_length() - 1) if dist_world else local_g
+        self.dist = bool(dist_world)
+        t0 = time.time()
+        self.sc = ShardedCircuit(n, self.g, gates)
+        self.plan_s = time.time() - t0
+        self.stats = self.sc.stats()
+        if self.dist:
+            self.comm = DistComm.from_torch(device)
+            self.st = ShardedState.distributed(n, self.comm)
+        else:
+            self.st = ShardedState.local(n, self.g, device)
+        # amplitudes one step sweeps on this GPU (all local shards)
+        self.shard_amps = 1 << (n - self.g) if self.dist else 1 << n
+        self.arr, self.keep = N.gate_array(gates)
+        self.G = len(gates)
+        self.kinds = [k for k, _, _ in self.sc.steps()]
+        self.e2e_path = "qs_shards_apply_circuit(host qs_gate array) + qs_shards_checksum"
+
+    def parallelism(self, world):
+        if self.dist:
+            return "amplitude-sharded over %d GPUs (%d rank qubits, NCCL exchanges)" % (world, self.g)
+        return "%d local shards on 1 GPU (diagnostic)" % (1 << self.g)
+
+    def stream(self):
+        return self.st.stream()
+
+    def reset(self):
+        self.st.reset(0)
+
+    def enqueue(self):
+        self.st.execute(self.sc, sync=False)
+
+    def checksum(self):
+        return self.st.checksum()
+
+    def apply_host(self):
+        self.N.check(self.L.qs_shards_apply_circuit(self.st.handle(), self.arr, self.G))
+
+    def step_kinds(self):
+        return self.kinds
+
+    def timed(self):
+        return self.st.execute_timed(self.sc)
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -155,6 +263,9 @@ def main():
     ap.add_argument("--cpu-layers", type=int, default=1)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--replicas", action="store_true", help="N>1: independent replicas instead of one sharded state")
+    ap.add_argument("--local-shards", type=int, default=0, metavar="G",
+                    help="N=1 diagnostic: split the state into 2^G shards on this GPU")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
 
@@ -174,28 +285,34 @@ def main():
     torch.cuda.set_device(local)
 
     from paper_2212_14201_b200 import _native as N
-    from paper_2212_14201_b200 import qforge as Q
 
     plan_mode = {"tiled": N.QS_PLAN_TILED, "dense": N.QS_PLAN_DENSE_FUSION, "unfused": N.QS_PLAN_UNFUSED}[args.plan]
     p, n = build_program(args.workload)
     gates = p.gates()
     G = len(gates)
-    t0 = time.time()
-    cc = Q.CompiledCircuit(n, gates, plan=plan_mode, max_fused_qubits=3)
-    plan_s = time.time() - t0
-    stats = cc.stats()
-    sv = Q.StateVector(n, device=local)
+    sharded = world > 1 and not args.replicas
+    if sharded and (world & (world - 1)):
+        sharded = False  # amplitude sharding needs a power-of-two world
+    if sharded:
+        runner = ShardedRunner(n, gates, local, dist_world=world)
+    elif args.local_shards:
+        runner = ShardedRunner(n, gates, local, local_g=args.local_shards)
+    else:
+        runner = SingleRunner(n, gates, local, plan_mode)
+    plan_s = runner.plan_s
+    stats = runner.stats
     L = N.lib()
-    stream = torch.cuda.ExternalStream(L.qs_stream(sv.handle()), device=torch.device("cuda", local))
-    cs = N.C.c_double()
+    stream = torch.cuda.ExternalStream(runner.stream(), device=torch.device("cuda", local))
+    # replicas: every rank runs the whole circuit; sharded: the ranks share one state
+    units = G * world if (world > 1 and not sharded) else G
 
     def step():
-        N.check(L.qs_reset(sv.handle()))
-        N.check(L.qs_plan_enqueue(sv.handle(), cc._h))
+        runner.reset()
+        runner.enqueue()
 
     for _ in range(args.warmup):
         step()
-        N.check(L.qs_checksum(sv.handle(), N.C.byref(cs)))
+        runner.checksum()
     torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
@@ -210,23 +327,21 @@ def main():
     ev0.record(stream)
     for _ in range(args.steps):
         step()
-        N.check(L.qs_checksum(sv.handle(), N.C.byref(cs)))  # device reduction + 8-byte read
+        checksum = runner.checksum()  # device reduction + 8-byte read (rank-ordered sum when sharded)
     ev1.record(stream)
     ev1.synchronize()
     torch.cuda.synchronize()
     launches = L.qs_kernel_launches() - launches0
     ms_total = ev0.elapsed_time(ev1)
-    checksum = cs.value
 
-    # per-pass device times (CUDA events between passes, same stream)
-    step_ms = (N.C.c_float * max(1, stats["launches"]))()
+    # per-step device times (CUDA events between steps, same stream)
     prof_runs = 2
-    per = [0.0] * stats["launches"]
+    per, kinds = None, runner.step_kinds()
     for _ in range(prof_runs):
-        N.check(L.qs_reset(sv.handle()))
-        N.check(L.qs_plan_execute_timed(sv.handle(), cc._h, step_ms))
-        for i in range(stats["launches"]):
-            per[i] += step_ms[i] / prof_runs
+        runner.reset()
+        t = runner.timed()
+        per = t if per is None else [a + b for a, b in zip(per, t)]
+    per = [x / prof_runs for x in per]
     clk = clocks.stop()
 
     ms_max = ms_total
@@ -235,16 +350,15 @@ def main():
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         ms_max = float(t.item())
     ms_per_step = ms_max / args.steps
-    value = G * world / (ms_per_step / 1e3)
+    value = units / (ms_per_step / 1e3)
 
     # e2e through the public API with host buffers (planning + upload + run + checksum read)
     e2e = None
     if not args.no_e2e:
-        arr, keep = N.gate_array(gates)
         h2d = N.C.sizeof(N.QsGate) * G
         for _ in range(2):
-            N.check(L.qs_reset(sv.handle()))
-            N.check(L.qs_apply_circuit(sv.handle(), arr, G, plan_mode, 3))
+            runner.reset()
+            runner.apply_host()
         torch.cuda.synchronize()
         if world > 1:
             dist.barrier()
@@ -254,9 +368,9 @@ def main():
         e1 = torch.cuda.Event(enable_timing=True)
         e0.record(stream)
         for _ in range(e_steps):
-            N.check(L.qs_reset(sv.handle()))
-            N.check(L.qs_apply_circuit(sv.handle(), arr, G, plan_mode, 3))
-            N.check(L.qs_checksum(sv.handle(), N.C.byref(cs)))
+            runner.reset()
+            runner.apply_host()
+            runner.checksum()
         e1.record(stream)
         e1.synchronize()
         wall = (time.perf_counter() - t0) * 1e3 / e_steps
@@ -266,22 +380,26 @@ def main():
             t = torch.tensor([e_ms], device="cuda")
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
             e_ms = float(t.item())
-        e2e = {"value": G * world / (e_ms / 1e3), "unit": "gates/s", "ms_per_step": e_ms,
-               "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": 8,
-               "path": "qs_apply_circuit(host qs_gate array) + qs_checksum"}
+        e2e = {"value": units / (e_ms / 1e3), "unit": "gates/s", "ms_per_step": e_ms,
+               "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": 8, "path": runner.e2e_path}
 
     peak, peak_kind = peaks()
-    state_bytes = 16 * (1 << n)
+    state_bytes = 16 * runner.shard_amps  # bytes of the state (or shard) one pass sweeps
     # dominant kernel: the tile pass (or the per-gate kernel in other plans)
-    pass_ms = [x for x in per if x > 0]
+    pass_ms = [x for x, k in zip(per, kinds) if k != 2 and x > 0]
+    xchg_ms = [x for x, k in zip(per, kinds) if k == 2]
     avg_pass_ms = sum(pass_ms) / len(pass_ms) if pass_ms else 0.0
     achieved = (2 * state_bytes) / (avg_pass_ms / 1e3) / 1e9 if avg_pass_ms else 0.0
     roofline = {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
-                "frac": round(achieved / peak, 4), "traffic": ncu_traffic(args.workload, args.plan),
+                "frac": round(achieved / peak, 4),
+                "traffic": ncu_traffic(args.workload, args.plan) if not runner.sharded else None,
                 "kernel": "qsb_tile_* (per-pass NVRTC sm_100a)" if args.plan == "tiled" else "per-gate kernels",
                 "algorithmic_bytes_per_launch": 2 * state_bytes, "launches_per_step": stats["launches"],
                 "avg_launch_ms": round(avg_pass_ms, 4), "peak_kind": peak_kind,
                 "pass_time_share": round(sum(pass_ms) / ms_per_step, 4) if ms_per_step else None}
+    if xchg_ms:
+        roofline["exchanges_per_step"] = len(xchg_ms)
+        roofline["exchange_ms_total"] = round(sum(xchg_ms), 3)
     if pass_ms:
         srt = sorted(pass_ms)
         roofline["launch_ms_min_median_max"] = [round(srt[0], 3), round(srt[len(srt) // 2], 3), round(srt[-1], 3)]
@@ -289,7 +407,7 @@ def main():
             roofline["launch_ms"] = [round(x, 3) for x in per]
 
     cpu = None
-    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+    if rank == 0 and world == 1 and not args.no_cpu_baseline and not args.local_shards:
         rows, err = cpu_baseline_reference(args.workload, args.cpu_layers, 1)
         if rows:
             r = rows[-1]
@@ -306,11 +424,13 @@ def main():
             "metric": "gates/sec (30q random layered circuit, d=20, complex128) vs HBM roofline",
             "value": round(value, 2), "unit": "gates/s", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": round(ms_per_step, 3), "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None, "dtype": "complex128 (f64)", "data": "synthetic",
+            "scaling": "strong" if runner.sharded else "weak", "vs_baseline": None, "dtype": "complex128 (f64)",
+            "data": "synthetic",
             "config": {"workload": "%s: %s%s" % (args.workload, WORKLOADS[args.workload][0], WORKLOADS[args.workload][1]),
                        "qubits": n, "gates": G, "plan": args.plan, "passes": stats["passes"],
-                       "plan_seconds": round(plan_s, 3), "parallelism": "replicas" if world > 1 else "single",
-                       "l2": "inputs larger than L2 (state %.1f GiB)" % (state_bytes / 2 ** 30),
+                       "plan_seconds": round(plan_s, 3), "parallelism": runner.parallelism(world),
+                       "l2": "inputs larger than L2 (%s %.1f GiB)" % ("shard" if runner.sharded else "state",
+                                                                    state_bytes / 2 ** 30),
                        "checksum": checksum},
             "e2e": e2e, "gpu_launches": int(launches), "roofline": roofline, "cpu_baseline": cpu,
             "clocks": clk,

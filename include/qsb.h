@@ -240,7 +240,12 @@ int qs_plan_create_sharded(uint32_t num_qubits, uint32_t global_qubits, const qs
                            qs_plan_t* out);
 /* Number of rank-bit exchanges one execution performs.                      */
 int qs_plan_exchanges(qs_plan_t p, uint64_t* exchanges);
+/* Step i of a plan: kind 0 = per-gate kernel, 1 = tile pass, 2 = rank-bit
+ * exchange of rank bit gpos (qubit n-g+gpos) with local qubit lpos.          */
+int qs_plan_step_info(qs_plan_t p, uint64_t i, int* kind, uint32_t* gpos, uint32_t* lpos);
 int qs_shards_plan_enqueue(qs_shards_t s, qs_plan_t p);
+/* Executes with a CUDA event around every step (step_ms[i], one per step).   */
+int qs_shards_plan_execute_timed(qs_shards_t s, qs_plan_t p, float* step_ms);
 int qs_shards_plan_execute(qs_shards_t s, qs_plan_t p);
 int qs_shards_apply_circuit(qs_shards_t s, const qs_gate* gates, uint64_t n);
 int qs_shards_norm2(qs_shards_t s, double* out);

@@ -687,6 +687,35 @@ int qs_plan_exchanges(qs_plan_t p, uint64_t* exchanges) {
   });
 }
 
+int qs_plan_step_info(qs_plan_t p, uint64_t i, int* kind, uint32_t* gpos, uint32_t* lpos) {
+  return guarded([&] {
+    if (!p || i >= p->p->steps.size()) throw ValidationError("bad plan step index");
+    const Step& st = p->p->steps[i];
+    if (kind) *kind = static_cast<int>(st.kind);
+    if (gpos) *gpos = st.gpos;
+    if (lpos) *lpos = st.lpos;
+  });
+}
+
+int qs_shards_plan_execute_timed(qs_shards_t s, qs_plan_t p, float* step_ms) {
+  return guarded([&] {
+    if (!p || !step_ms) throw ValidationError("null plan or output");
+    ShardSet& ss = sh(s);
+    DeviceGuard dg(ss.device);
+    const size_t ns = p->p->steps.size();
+    std::vector<cudaEvent_t> ev(ns + 1);
+    for (auto& e : ev) QSB_CUDA(cudaEventCreate(&e));
+    QSB_CUDA(cudaEventRecord(ev[0], ss.stream));
+    for (size_t i = 0; i < ns; ++i) {
+      shard_execute(ss, *p->p, i, 1);
+      QSB_CUDA(cudaEventRecord(ev[i + 1], ss.stream));
+    }
+    shard_sync(ss);
+    for (size_t i = 0; i < ns; ++i) QSB_CUDA(cudaEventElapsedTime(&step_ms[i], ev[i], ev[i + 1]));
+    for (auto& e : ev) cudaEventDestroy(e);
+  });
+}
+
 int qs_shards_plan_enqueue(qs_shards_t s, qs_plan_t p) {
   return guarded([&] {
     if (!p) throw ValidationError("null plan");

@@ -81,6 +81,15 @@ class ShardedCircuit:
     def handle(self):
         return self._h
 
+    def steps(self):
+        """[(kind, gpos, lpos)] per step; kind 0 per-gate kernel, 1 tile pass, 2 exchange."""
+        out = []
+        k, gp, lp = C.c_int(), C.c_uint32(), C.c_uint32()
+        for i in range(self.stats()["launches"] + self.stats()["exchanges"]):
+            N.check(N.lib().qs_plan_step_info(self._h, i, C.byref(k), C.byref(gp), C.byref(lp)))
+            out.append((k.value, gp.value, lp.value))
+        return out
+
     def stats(self):
         a, b, c, e = C.c_uint64(), C.c_uint64(), C.c_uint64(), C.c_uint64()
         N.check(N.lib().qs_plan_stats(self._h, C.byref(a), C.byref(b), C.byref(c)))
@@ -152,6 +161,13 @@ class ShardedState:
     def execute(self, circuit, sync=True):
         f = N.lib().qs_shards_plan_execute if sync else N.lib().qs_shards_plan_enqueue
         N.check(f(self._h, circuit.handle()))
+
+    def execute_timed(self, circuit):
+        """Per-step device times (ms) of one execution, CUDA events on the shard stream."""
+        n = len(circuit.steps())
+        buf = (C.c_float * max(1, n))()
+        N.check(N.lib().qs_shards_plan_execute_timed(self._h, circuit.handle(), buf))
+        return list(buf)[:n]
 
     def stream(self):
         return N.lib().qs_shards_stream(self._h)
