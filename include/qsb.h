@@ -241,8 +241,10 @@ int qs_plan_create_sharded(uint32_t num_qubits, uint32_t global_qubits, const qs
 /* Number of rank-bit exchanges one execution performs.                      */
 int qs_plan_exchanges(qs_plan_t p, uint64_t* exchanges);
 /* Step i of a plan: kind 0 = per-gate kernel, 1 = tile pass, 2 = rank-bit
- * exchange of rank bit gpos (qubit n-g+gpos) with local qubit lpos.          */
-int qs_plan_step_info(qs_plan_t p, uint64_t i, int* kind, uint32_t* gpos, uint32_t* lpos);
+ * exchange of rank bits gpos[b] (qubit n-g+gpos[b]) with local qubits
+ * lpos[b], b < *nbits (arrays of QS_MAX_EXCHANGE_BITS; nbits = 0 otherwise). */
+#define QS_MAX_EXCHANGE_BITS 16
+int qs_plan_step_info(qs_plan_t p, uint64_t i, int* kind, uint32_t* nbits, uint32_t* gpos, uint32_t* lpos);
 int qs_shards_plan_enqueue(qs_shards_t s, qs_plan_t p);
 /* Executes with a CUDA event around every step (step_ms[i], one per step).   */
 int qs_shards_plan_execute_timed(qs_shards_t s, qs_plan_t p, float* step_ms);

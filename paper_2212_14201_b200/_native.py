@@ -25,6 +25,7 @@ QS_PLAN_DENSE_FUSION = 2
 QS_PLAN_TILED = 3
 
 MAX_TARGETS = 8
+MAX_EXCHANGE_BITS = 16
 MAX_CONTROLS = 40
 
 
@@ -123,7 +124,7 @@ _SIGS = {
     "qs_shards_get_amplitudes": (C.c_int, [_P, _DP, C.c_uint64, C.c_uint64]),
     "qs_plan_create_sharded": (C.c_int, [C.c_uint32, C.c_uint32, _GP, C.c_uint64, C.POINTER(_P)]),
     "qs_plan_exchanges": (C.c_int, [_P, _U64P]),
-    "qs_plan_step_info": (C.c_int, [_P, C.c_uint64, C.POINTER(C.c_int), _UP, _UP]),
+    "qs_plan_step_info": (C.c_int, [_P, C.c_uint64, C.POINTER(C.c_int), _UP, _UP, _UP]),
     "qs_shards_plan_enqueue": (C.c_int, [_P, _P]),
     "qs_shards_plan_execute_timed": (C.c_int, [_P, _P, C.POINTER(C.c_float)]),
     "qs_shards_plan_execute": (C.c_int, [_P, _P]),

@@ -687,13 +687,16 @@ int qs_plan_exchanges(qs_plan_t p, uint64_t* exchanges) {
   });
 }
 
-int qs_plan_step_info(qs_plan_t p, uint64_t i, int* kind, uint32_t* gpos, uint32_t* lpos) {
+int qs_plan_step_info(qs_plan_t p, uint64_t i, int* kind, uint32_t* nbits, uint32_t* gpos, uint32_t* lpos) {
   return guarded([&] {
     if (!p || i >= p->p->steps.size()) throw ValidationError("bad plan step index");
     const Step& st = p->p->steps[i];
     if (kind) *kind = static_cast<int>(st.kind);
-    if (gpos) *gpos = st.gpos;
-    if (lpos) *lpos = st.lpos;
+    if (nbits) *nbits = static_cast<uint32_t>(st.gpos.size());
+    for (size_t b = 0; b < st.gpos.size() && b < QS_MAX_EXCHANGE_BITS; ++b) {
+      if (gpos) gpos[b] = st.gpos[b];
+      if (lpos) lpos[b] = st.lpos[b];
+    }
   });
 }
 

@@ -58,6 +58,7 @@ struct State {
   uint64_t rank_base = 0;
   uint32_t local_qubits() const { return n - g; }
   double2* amps = nullptr;    // device
+  double2* alt = nullptr;     // second buffer of a shard exchanged through peer memory
   cudaStream_t stream = nullptr;
   // scratch (grown on demand)
   void* scratch = nullptr;

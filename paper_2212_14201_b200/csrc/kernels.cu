@@ -339,23 +339,59 @@ __global__ void __launch_bounds__(kThreads) k_swap_halves(double2* __restrict__ 
   }
 }
 
-// Gathers elements [off, off + cnt) of the half with local bit p == v.
-__global__ void __launch_bounds__(kThreads) k_pack_half(const double2* __restrict__ a, uint32_t p, uint32_t v,
-                                                        uint64_t off, uint64_t cnt, double2* __restrict__ out) {
-  const uint64_t bit = 1ull << p;
-  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < cnt; i += (uint64_t)gridDim.x * blockDim.x) {
-    const uint64_t k = off + i;
-    out[i] = a[((k >> p) << (p + 1)) | (v ? bit : 0) | (k & (bit - 1))];
+struct ExchangeBits {
+  uint32_t lpos[kMaxExchangeBits];
+  unsigned long long pmask, aval;
+};
+
+// Multi-bit exchanges (all-to-all among 2^k ranks): block d of a shard is the
+// set of local indices whose bits at positions lpos[0..k) equal d's bits,
+// enumerated by the remaining bits in ascending order (both ends agree).
+struct BlockSpec {
+  uint32_t k;
+  uint32_t sorted[16];      // lpos ascending (zero-bit insertion order)
+  unsigned long long val;   // sum of d_i << lpos[i]
+};
+
+__device__ __forceinline__ uint64_t block_index(const BlockSpec& b, uint64_t i) {
+  for (uint32_t s = 0; s < b.k; ++s) {
+    const uint32_t p = b.sorted[s];
+    i = ((i >> p) << (p + 1)) | (i & ((1ull << p) - 1));
   }
+  return i | b.val;
 }
 
-__global__ void __launch_bounds__(kThreads) k_unpack_half(double2* __restrict__ a, uint32_t p, uint32_t v,
-                                                          uint64_t off, uint64_t cnt, const double2* __restrict__ in) {
-  const uint64_t bit = 1ull << p;
-  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < cnt; i += (uint64_t)gridDim.x * blockDim.x) {
-    const uint64_t k = off + i;
-    a[((k >> p) << (p + 1)) | (v ? bit : 0) | (k & (bit - 1))] = in[i];
+// Gathers elements [off, off + cnt) of block `b` into out.
+__global__ void __launch_bounds__(kThreads) k_pack_block(const double2* __restrict__ a, const BlockSpec b,
+                                                         uint64_t off, uint64_t cnt, double2* __restrict__ out) {
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < cnt; i += (uint64_t)gridDim.x * blockDim.x)
+    out[i] = a[block_index(b, off + i)];
+}
+
+__global__ void __launch_bounds__(kThreads) k_unpack_block(double2* __restrict__ a, const BlockSpec b, uint64_t off,
+                                                           uint64_t cnt, const double2* __restrict__ in) {
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < cnt; i += (uint64_t)gridDim.x * blockDim.x)
+    a[block_index(b, off + i)] = in[i];
+}
+
+// Peer-memory exchange (one kernel, no staging): every amplitude of this
+// shard is stored straight into its owner's second buffer after the swap of
+// rank bits gpos[i] <-> local bits lpos[i].  Local index l goes to the rank
+// whose exchanged bits equal l's bits at lpos (table slot d) at local index
+// l with those bits replaced by this rank's exchanged bits (aval).  Remote
+// slots are NVLink peer pointers (CUDA IPC) or sibling shards on this device.
+struct PeerTable {
+  double2* p[kMaxPeers];
+};
+
+__global__ void __launch_bounds__(kThreads) k_scatter_exchange(const double2* __restrict__ src, const PeerTable t,
+                                                               uint64_t size, uint32_t k, ExchangeBits eb) {
+  for (uint64_t l = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; l < size; l += (uint64_t)gridDim.x * blockDim.x) {
+    uint32_t d = 0;
+    for (uint32_t i = 0; i < k; ++i) d |= static_cast<uint32_t>((l >> eb.lpos[i]) & 1ull) << i;
+    t.p[d][(l & ~eb.pmask) | eb.aval] = src[l];
   }
+  __threadfence_system();
 }
 
 // ------------------------------------------------- serial-equivalent scan
@@ -729,15 +765,43 @@ void swap_halves(State& a, State& b, uint32_t p) {
   QSB_LAUNCHED();
 }
 
-void pack_half(State& s, uint32_t p, uint32_t v, uint64_t off, uint64_t cnt, double2* out) {
+static BlockSpec block_spec(const uint32_t* lpos, uint32_t k, uint32_t d) {
+  if (k > 16) throw ValidationError("too many exchange bits");
+  BlockSpec b{};
+  b.k = k;
+  for (uint32_t i = 0; i < k; ++i) {
+    b.sorted[i] = lpos[i];
+    if ((d >> i) & 1) b.val |= 1ull << lpos[i];
+  }
+  std::sort(b.sorted, b.sorted + k);
+  return b;
+}
+
+void pack_block(State& s, const uint32_t* lpos, uint32_t k, uint32_t d, uint64_t off, uint64_t cnt, double2* out) {
   DeviceGuard dg(s.device);
-  k_pack_half<<<grid_for(cnt, s.device), kThreads, 0, s.stream>>>(s.amps, p, v, off, cnt, out);
+  k_pack_block<<<grid_for(cnt, s.device), kThreads, 0, s.stream>>>(s.amps, block_spec(lpos, k, d), off, cnt, out);
   QSB_LAUNCHED();
 }
 
-void unpack_half(State& s, uint32_t p, uint32_t v, uint64_t off, uint64_t cnt, const double2* in) {
+void scatter_exchange(State& s, double2* const* peers, const uint32_t* lpos, uint32_t k, uint32_t aval) {
+  if (k > kMaxExchangeBits) throw ValidationError("peer exchange limited to 4 rank bits at once");
+  PeerTable t{};
+  for (uint32_t d = 0; d < (1u << k); ++d) t.p[d] = peers[d];
+  ExchangeBits eb{};
+  for (uint32_t i = 0; i < k; ++i) {
+    eb.lpos[i] = lpos[i];
+    eb.pmask |= 1ull << lpos[i];
+    if ((aval >> i) & 1) eb.aval |= 1ull << lpos[i];
+  }
   DeviceGuard dg(s.device);
-  k_unpack_half<<<grid_for(cnt, s.device), kThreads, 0, s.stream>>>(s.amps, p, v, off, cnt, in);
+  k_scatter_exchange<<<grid_for(s.size, s.device), kThreads, 0, s.stream>>>(s.amps, t, s.size, k, eb);
+  QSB_LAUNCHED();
+}
+
+void unpack_block(State& s, const uint32_t* lpos, uint32_t k, uint32_t d, uint64_t off, uint64_t cnt,
+                  const double2* in) {
+  DeviceGuard dg(s.device);
+  k_unpack_block<<<grid_for(cnt, s.device), kThreads, 0, s.stream>>>(s.amps, block_spec(lpos, k, d), off, cnt, in);
   QSB_LAUNCHED();
 }
 

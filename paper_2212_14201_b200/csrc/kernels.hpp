@@ -18,8 +18,18 @@ void fill_basis(State& s, uint64_t index);                      // |index> (loca
 
 // Rank-bit exchanges for sharded states (shard.cpp).
 void swap_halves(State& a, State& b, uint32_t p);                // a: rank bit 0, b: rank bit 1, same device
-void pack_half(State& s, uint32_t p, uint32_t v, uint64_t off, uint64_t cnt, double2* out);
-void unpack_half(State& s, uint32_t p, uint32_t v, uint64_t off, uint64_t cnt, const double2* in);
+// Peer-memory exchange of rank bits <-> local bits lpos[0..k): every amplitude
+// is written to peers[d] (d = its bits at lpos) at its new local index (those
+// bits replaced by aval).  peers[] are the owners' second buffers.
+constexpr uint32_t kMaxExchangeBits = 4;
+constexpr uint32_t kMaxPeers = 1u << kMaxExchangeBits;
+void scatter_exchange(State& s, double2* const* peers, const uint32_t* lpos, uint32_t k, uint32_t aval);
+
+// Block d of a k-bit exchange:local indices whose bits lpos[i] equal bit i of
+// d, enumerated by the remaining bits ascending; [off, off+cnt) of it.
+void pack_block(State& s, const uint32_t* lpos, uint32_t k, uint32_t d, uint64_t off, uint64_t cnt, double2* out);
+void unpack_block(State& s, const uint32_t* lpos, uint32_t k, uint32_t d, uint64_t off, uint64_t cnt,
+                  const double2* in);
 double reduce_norm2(State& s);                                   // statevector.hpp:158-162
 double reduce_prob_one(State& s, uint32_t q);                    // :181-186
 double reduce_checksum(State& s);                                // bench.hpp:141-148

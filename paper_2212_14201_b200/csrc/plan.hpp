@@ -18,9 +18,11 @@ struct Step {
   enum Kind { OpStep, TileStep, SwapStep } kind = OpStep;
   Op op;                               // OpStep
   std::shared_ptr<TileProgram> tile;   // TileStep
-  // SwapStep (sharded states): exchange physical qubit n-g+gpos (a rank bit)
-  // with local physical qubit lpos -- a pairwise half-shard exchange.
-  uint32_t gpos = 0, lpos = 0;
+  // SwapStep (sharded states): for every i, exchange physical qubit
+  // n-g+gpos[i] (a rank bit) with local physical qubit lpos[i].  One bit is a
+  // pairwise half-shard exchange; k bits are an all-to-all among the 2^k
+  // ranks that differ in those rank bits (each sends 1 - 2^-k of its shard).
+  std::vector<uint32_t> gpos, lpos;
 };
 
 struct Plan {

@@ -32,39 +32,61 @@ void alloc_shard(State& s, uint32_t n, uint32_t g, uint32_t rank, int device, cu
   }
 }
 
+bool alloc_alt(State& s) {
+  DeviceGuard dg(s.device);
+  if (cudaMalloc(&s.alt, s.size * sizeof(double2)) != cudaSuccess) {
+    cudaGetLastError();
+    s.alt = nullptr;
+    return false;
+  }
+  return true;
+}
+
 void free_shard(State& s) {
   DeviceGuard dg(s.device);
   if (s.amps) cudaFree(s.amps);
+  if (s.alt) cudaFree(s.alt);
   if (s.scratch) cudaFree(s.scratch);
   if (s.host_pinned) cudaFreeHost(s.host_pinned);
   s.amps = nullptr;
+  s.alt = nullptr;
   s.scratch = nullptr;
   s.host_pinned = nullptr;
 }
 
-// Exchange chunk (amplitudes per direction); QSB_SHARD_CHUNK overrides (tests).
-uint64_t exchange_chunk(uint64_t half) {
-  uint64_t c = 1ull << 26;  // 1 GiB per direction
+// QSB_SHARD_EXCHANGE: local sets "swap" (default) | "staged" | "peer";
+// distributed sets "peer" (default, falls back to NCCL) | "nccl".
+// QSB_SHARD_STAGED=1 is the older spelling of "staged".
+std::string exchange_mode() {
+  if (const char* e = std::getenv("QSB_SHARD_EXCHANGE")) return e;
+  const char* st = std::getenv("QSB_SHARD_STAGED");
+  if (st && *st && *st != '0') return "staged";
+  return "";
+}
+
+// Exchange chunk (amplitudes per block and peer); QSB_SHARD_CHUNK overrides (tests).
+uint64_t exchange_chunk(uint64_t block, uint32_t peers) {
+  uint64_t c = (1ull << 27) / std::max<uint32_t>(1, peers);  // <= 2 GiB in flight per direction
   if (const char* e = std::getenv("QSB_SHARD_CHUNK")) c = std::max<uint64_t>(1, std::strtoull(e, nullptr, 10));
-  return std::min(half, c);
+  return std::max<uint64_t>(1, std::min(block, c));
 }
 
 // Device staging buffer for pack/unpack exchanges (grown on demand).
 struct Staging {
   double2* buf = nullptr;
-  uint64_t elems = 0;  // per direction
+  uint64_t elems = 0;
   int device = 0;
-  double2* get(uint64_t chunk, int dev) {
-    if (elems < chunk) {
+  double2* get(uint64_t want, int dev) {
+    if (elems < want) {
       release();
       device = dev;
       DeviceGuard dg(dev);
-      if (cudaMalloc(&buf, 2 * chunk * sizeof(double2)) != cudaSuccess) {
+      if (cudaMalloc(&buf, want * sizeof(double2)) != cudaSuccess) {
         cudaGetLastError();
         buf = nullptr;
         throw MemoryError("cannot allocate exchange staging buffers");
       }
-      elems = chunk;
+      elems = want;
     }
     return buf;
   }
@@ -79,32 +101,62 @@ struct Staging {
   ~Staging() { release(); }
 };
 
+// Value of rank r's exchanged bits (bit i <- rank bit gpos[i]).
+uint32_t rank_bits(uint32_t r, const std::vector<uint32_t>& gpos) {
+  uint32_t a = 0;
+  for (size_t i = 0; i < gpos.size(); ++i) a |= ((r >> gpos[i]) & 1u) << i;
+  return a;
+}
+// r with its exchanged rank bits replaced by d.
+uint32_t with_bits(uint32_t r, const std::vector<uint32_t>& gpos, uint32_t d) {
+  for (size_t i = 0; i < gpos.size(); ++i) r = (r & ~(1u << gpos[i])) | (((d >> i) & 1u) << gpos[i]);
+  return r;
+}
+
 struct LocalTransport : Transport {
-  // staged: move halves through pack -> staging -> unpack like NcclTransport
-  // (with a device copy in place of send/recv) instead of one swap kernel.
-  bool staged = false;
+  // swap: one swap kernel per exchanged bit and shard pair (no extra memory);
+  // staged: the NCCL transport's protocol (pack block -> staging -> unpack at
+  //   the peer) with device copies in place of send/recv;
+  // peer: the peer-memory transport's scatter kernel into sibling shards'
+  //   second buffers (needs 2x memory).
+  enum Mode { Swap, Staged, Peer } mode = Swap;
   Staging stage;
-  void exchange(std::vector<State*>& shards, uint32_t gpos, uint32_t lpos) override {
-    const uint32_t bit = 1u << gpos;
-    for (uint32_t r = 0; r < shards.size(); ++r) {
-      if (r & bit) continue;
-      State& a = *shards[r];
-      State& b = *shards[r | bit];
-      if (!staged) {
-        swap_halves(a, b, lpos);
-        continue;
+  void exchange(std::vector<State*>& shards, const std::vector<uint32_t>& gpos,
+                const std::vector<uint32_t>& lpos) override {
+    const uint32_t k = static_cast<uint32_t>(gpos.size()), K = 1u << k;
+    const uint32_t P = static_cast<uint32_t>(shards.size());
+    if (mode == Peer && k <= kMaxExchangeBits) {
+      for (uint32_t r = 0; r < P; ++r) {
+        double2* peers[kMaxPeers];
+        for (uint32_t d = 0; d < K; ++d) peers[d] = shards[with_bits(r, gpos, d)]->alt;
+        scatter_exchange(*shards[r], peers, lpos.data(), k, rank_bits(r, gpos));
       }
-      // a (rank bit 0) sends its lpos=1 half, b sends its lpos=0 half
-      const uint64_t half = a.size / 2;
-      const uint64_t chunk = exchange_chunk(half);
-      double2* ab = stage.get(chunk, a.device);
-      double2* ba = ab + chunk;
-      for (uint64_t off = 0; off < half; off += chunk) {
-        const uint64_t c = std::min(chunk, half - off);
-        pack_half(a, lpos, 1, off, c, ab);
-        pack_half(b, lpos, 0, off, c, ba);
-        unpack_half(a, lpos, 1, off, c, ba);
-        unpack_half(b, lpos, 0, off, c, ab);
+      for (auto* s : shards) std::swap(s->amps, s->alt);
+      return;
+    }
+    if (mode != Staged) {  // disjoint transpositions commute: one bit at a time
+      for (size_t i = 0; i < gpos.size(); ++i) {
+        const uint32_t bit = 1u << gpos[i];
+        for (uint32_t r = 0; r < P; ++r)
+          if (!(r & bit)) swap_halves(*shards[r], *shards[r | bit], lpos[i]);
+      }
+      return;
+    }
+    const uint64_t B = shards[0]->size >> k;
+    const uint64_t chunk = exchange_chunk(B, K - 1);
+    double2* buf = stage.get(static_cast<uint64_t>(P) * K * chunk, shards[0]->device);
+    auto slot = [&](uint32_t r, uint32_t d) { return buf + (static_cast<uint64_t>(r) * K + d) * chunk; };
+    for (uint64_t off = 0; off < B; off += chunk) {
+      const uint64_t c = std::min(chunk, B - off);
+      for (uint32_t r = 0; r < P; ++r) {
+        const uint32_t a = rank_bits(r, gpos);
+        for (uint32_t d = 0; d < K; ++d)
+          if (d != a) pack_block(*shards[r], lpos.data(), k, d, off, c, slot(r, d));
+      }
+      for (uint32_t r = 0; r < P; ++r) {
+        const uint32_t a = rank_bits(r, gpos);
+        for (uint32_t d = 0; d < K; ++d)
+          if (d != a) unpack_block(*shards[r], lpos.data(), k, d, off, c, slot(with_bits(r, gpos, d), a));
       }
     }
   }
@@ -131,9 +183,12 @@ struct Nccl {
   int (*groupStart)() = nullptr;
   int (*groupEnd)() = nullptr;
   int (*allGather)(const void*, void*, size_t, int, ncclComm_t, cudaStream_t) = nullptr;
+  int (*allReduce)(const void*, void*, size_t, int, int, ncclComm_t, cudaStream_t) = nullptr;
   const char* (*errorString)(int) = nullptr;
 };
+constexpr int kNcclUint8 = 1;   // ncclUint8
 constexpr int kNcclDouble = 8;  // ncclFloat64
+constexpr int kNcclSum = 0, kNcclMin = 3;
 
 const Nccl& nccl() {
   static Nccl n;
@@ -157,6 +212,7 @@ const Nccl& nccl() {
     n.groupStart = reinterpret_cast<decltype(n.groupStart)>(sym("ncclGroupStart"));
     n.groupEnd = reinterpret_cast<decltype(n.groupEnd)>(sym("ncclGroupEnd"));
     n.allGather = reinterpret_cast<decltype(n.allGather)>(sym("ncclAllGather"));
+    n.allReduce = reinterpret_cast<decltype(n.allReduce)>(sym("ncclAllReduce"));
     n.errorString = reinterpret_cast<decltype(n.errorString)>(sym("ncclGetErrorString"));
   });
   if (!n.h || !n.send || !n.recv || !n.commInitRank) throw RuntimeError(err.empty() ? "incomplete libnccl" : err);
@@ -179,45 +235,181 @@ struct Dist {
 namespace {
 
 struct NcclTransport : Transport {
-  Dist* d;
-  Staging stage;              // send + recv chunks
-  double* red = nullptr;      // allgather buffer
-  explicit NcclTransport(Dist* dd) : d(dd) {}
-  ~NcclTransport() override {
-    DeviceGuard dg(d->device);
-    if (red) cudaFree(red);
+  Dist* d_;
+  Staging stage;              // send + recv chunks (staged mode)
+  double* red = nullptr;      // allgather / barrier buffer
+  // Peer mode: every rank's two shard buffers, mapped into this process
+  // (own: cudaMalloc; peers: CUDA IPC over NVLink).  cur = index of the
+  // buffer holding the state (identical on all ranks: same plan).
+  bool peer = false;
+  std::vector<double2*> bufs[2];
+  std::vector<char> opened;   // bufs[*][r] opened through IPC
+  int cur = 0;
+  explicit NcclTransport(Dist* dd) : d_(dd) {}
+  ~NcclTransport() override { close(); }
+
+  double* scratch() {
+    DeviceGuard dg(d_->device);
+    if (!red) QSB_CUDA(cudaMalloc(&red, (d_->world + 1) * sizeof(double)));
+    return red;
   }
-  void exchange(std::vector<State*>& shards, uint32_t gpos, uint32_t lpos) override {
+  // Stream-ordered barrier: completes on every rank only after every rank's
+  // prior work on its stream (incl. remote stores) has finished.
+  void stream_barrier(cudaStream_t st) {
+    double* r = scratch();
+    nccl_check(nccl().allReduce(r, r, 1, kNcclDouble, kNcclSum, d_->comm, st), "ncclAllReduce");
+  }
+  void barrier() override {
+    DeviceGuard dg(d_->device);
+    stream_barrier(nullptr);
+    QSB_CUDA(cudaDeviceSynchronize());
+  }
+
+  // Exports both buffers of this rank's shard and maps every peer's; all
+  // ranks agree (allreduce-min) before peer mode is used.
+  void setup_peer(State& s) {
+    DeviceGuard dg(d_->device);
+    const int W = d_->world;
+    int ok = alloc_alt(s) ? 1 : 0;
+    cudaIpcMemHandle_t h[2]{};
+    if (ok && (cudaIpcGetMemHandle(&h[0], s.amps) != cudaSuccess || cudaIpcGetMemHandle(&h[1], s.alt) != cudaSuccess)) {
+      cudaGetLastError();
+      ok = 0;
+    }
+    unsigned char* dev = nullptr;
+    const size_t hb = sizeof(h);
+    QSB_CUDA(cudaMalloc(&dev, hb * (W + 1)));
+    QSB_CUDA(cudaMemcpy(dev + hb * W, h, hb, cudaMemcpyHostToDevice));
+    nccl_check(nccl().allGather(dev + hb * W, dev, hb, kNcclUint8, d_->comm, nullptr), "ncclAllGather");
+    std::vector<cudaIpcMemHandle_t> all(2 * W);
+    QSB_CUDA(cudaMemcpy(all.data(), dev, hb * W, cudaMemcpyDeviceToHost));
+    cudaFree(dev);
+    bufs[0].assign(W, nullptr);
+    bufs[1].assign(W, nullptr);
+    opened.assign(W, 0);
+    for (int r = 0; r < W && ok; ++r) {
+      if (r == d_->rank) {
+        bufs[0][r] = s.amps;
+        bufs[1][r] = s.alt;
+        continue;
+      }
+      void* p0 = nullptr;
+      void* p1 = nullptr;
+      if (cudaIpcOpenMemHandle(&p0, all[2 * r], cudaIpcMemLazyEnablePeerAccess) != cudaSuccess) {
+        cudaGetLastError();
+        ok = 0;
+        break;
+      }
+      if (cudaIpcOpenMemHandle(&p1, all[2 * r + 1], cudaIpcMemLazyEnablePeerAccess) != cudaSuccess) {
+        cudaGetLastError();
+        cudaIpcCloseMemHandle(p0);
+        ok = 0;
+        break;
+      }
+      bufs[0][r] = static_cast<double2*>(p0);
+      bufs[1][r] = static_cast<double2*>(p1);
+      opened[r] = 1;
+    }
+    // agree on the mode
+    double* r = scratch();
+    double mine = ok;
+    QSB_CUDA(cudaMemcpy(r, &mine, sizeof(double), cudaMemcpyHostToDevice));
+    nccl_check(nccl().allReduce(r, r, 1, kNcclDouble, kNcclMin, d_->comm, nullptr), "ncclAllReduce");
+    double all_ok = 0;
+    QSB_CUDA(cudaMemcpy(&all_ok, r, sizeof(double), cudaMemcpyDeviceToHost));
+    peer = all_ok > 0.5;
+    if (!peer) close_peers(s);
+  }
+  void close_peers(State& s) {
+    DeviceGuard dg(d_->device);
+    for (size_t r = 0; r < opened.size(); ++r)
+      if (opened[r]) {
+        cudaIpcCloseMemHandle(bufs[0][r]);
+        cudaIpcCloseMemHandle(bufs[1][r]);
+        opened[r] = 0;
+      }
+    if (s.alt && !peer) {
+      cudaFree(s.alt);
+      s.alt = nullptr;
+    }
+  }
+  State* owner = nullptr;
+  void close() override {
+    if (!d_) return;
+    DeviceGuard dg(d_->device);
+    if (peer && owner) {
+      // no rank may free a buffer another rank still maps
+      try {
+        barrier();
+      } catch (...) {
+      }
+      for (size_t r = 0; r < opened.size(); ++r)
+        if (opened[r]) {
+          cudaIpcCloseMemHandle(bufs[0][r]);
+          cudaIpcCloseMemHandle(bufs[1][r]);
+          opened[r] = 0;
+        }
+      try {
+        barrier();
+      } catch (...) {
+      }
+      peer = false;
+    }
+    if (red) cudaFree(red);
+    red = nullptr;
+  }
+
+  void exchange(std::vector<State*>& shards, const std::vector<uint32_t>& gpos,
+                const std::vector<uint32_t>& lpos) override {
     State& s = *shards.at(0);
     const Nccl& N = nccl();
     DeviceGuard dg(s.device);
-    const int partner = static_cast<int>(s.rank ^ (1u << gpos));
-    const uint32_t v = 1u - ((s.rank >> gpos) & 1u);  // half that changes hands
-    const uint64_t half = s.size / 2;
-    const uint64_t chunk = exchange_chunk(half);
-    double2* sendb = stage.get(chunk, s.device);
-    double2* recvb = sendb + chunk;
-    for (uint64_t off = 0; off < half; off += chunk) {
-      const uint64_t c = std::min(chunk, half - off);
-      pack_half(s, lpos, v, off, c, sendb);
+    const uint32_t k = static_cast<uint32_t>(gpos.size()), K = 1u << k;
+    const uint32_t a = rank_bits(s.rank, gpos);
+    if (peer && k <= kMaxExchangeBits) {
+      // one kernel: every amplitude straight into its owner's free buffer over NVLink
+      double2* peers[kMaxPeers];
+      for (uint32_t d = 0; d < K; ++d) peers[d] = bufs[cur ^ 1][with_bits(s.rank, gpos, d)];
+      scatter_exchange(s, peers, lpos.data(), k, a);
+      stream_barrier(s.stream);
+      cur ^= 1;
+      s.amps = bufs[cur][s.rank];
+      s.alt = bufs[cur ^ 1][s.rank];
+      return;
+    }
+    // All-to-all among the 2^k ranks that differ in the exchanged rank bits:
+    // block d (local bits lpos = d) goes to the peer whose rank bits are d, and
+    // that peer's block a (a = our rank bits) lands in our block d.
+    const uint64_t B = s.size >> k;
+    const uint64_t chunk = exchange_chunk(B, K - 1);
+    double2* sendb = stage.get(2ull * K * chunk, s.device);
+    double2* recvb = sendb + static_cast<uint64_t>(K) * chunk;
+    for (uint64_t off = 0; off < B; off += chunk) {
+      const uint64_t c = std::min(chunk, B - off);
+      for (uint32_t d = 0; d < K; ++d)
+        if (d != a) pack_block(s, lpos.data(), k, d, off, c, sendb + d * chunk);
       nccl_check(N.groupStart(), "ncclGroupStart");
-      nccl_check(N.send(sendb, 2 * c, kNcclDouble, partner, d->comm, s.stream), "ncclSend");
-      nccl_check(N.recv(recvb, 2 * c, kNcclDouble, partner, d->comm, s.stream), "ncclRecv");
+      for (uint32_t d = 0; d < K; ++d) {
+        if (d == a) continue;
+        const int peer_rank = static_cast<int>(with_bits(s.rank, gpos, d));
+        nccl_check(N.send(sendb + d * chunk, 2 * c, kNcclDouble, peer_rank, d_->comm, s.stream), "ncclSend");
+        nccl_check(N.recv(recvb + d * chunk, 2 * c, kNcclDouble, peer_rank, d_->comm, s.stream), "ncclRecv");
+      }
       nccl_check(N.groupEnd(), "ncclGroupEnd");
-      unpack_half(s, lpos, v, off, c, recvb);
+      for (uint32_t d = 0; d < K; ++d)
+        if (d != a) unpack_block(s, lpos.data(), k, d, off, c, recvb + d * chunk);
     }
   }
   double sum(const std::vector<double>& v) override {
     const Nccl& N = nccl();
-    DeviceGuard dg(d->device);
-    if (!red) QSB_CUDA(cudaMalloc(&red, (d->world + 1) * sizeof(double)));
+    DeviceGuard dg(d_->device);
+    double* r = scratch();
     double mine = 0;
     for (double x : v) mine += x;
-    cudaStream_t st = nullptr;
-    QSB_CUDA(cudaMemcpy(red + d->world, &mine, sizeof(double), cudaMemcpyHostToDevice));
-    nccl_check(N.allGather(red + d->world, red, 1, kNcclDouble, d->comm, st), "ncclAllGather");
-    std::vector<double> all(d->world);
-    QSB_CUDA(cudaMemcpy(all.data(), red, d->world * sizeof(double), cudaMemcpyDeviceToHost));
+    QSB_CUDA(cudaMemcpy(r + d_->world, &mine, sizeof(double), cudaMemcpyHostToDevice));
+    nccl_check(N.allGather(r + d_->world, r, 1, kNcclDouble, d_->comm, nullptr), "ncclAllGather");
+    std::vector<double> all(d_->world);
+    QSB_CUDA(cudaMemcpy(all.data(), r, d_->world * sizeof(double), cudaMemcpyDeviceToHost));
     double t = 0;
     for (double x : all) t += x;  // rank order
     return t;
@@ -227,13 +419,13 @@ struct NcclTransport : Transport {
 }  // namespace
 
 ShardSet::~ShardSet() {
-  for (auto& s : shards) {
+  for (auto& s : shards)
     if (s->stream) {
       DeviceGuard dg(s->device);
       cudaStreamSynchronize(s->stream);
     }
-    free_shard(*s);
-  }
+  if (tr) tr->close();  // unmaps peer buffers (collective for distributed sets)
+  for (auto& s : shards) free_shard(*s);
   tr.reset();
   if (stream && owns_stream) {
     DeviceGuard dg(device);
@@ -256,8 +448,13 @@ std::unique_ptr<ShardSet> make_local_shards(uint32_t n, uint32_t g, int device) 
     ss->shards.push_back(std::move(s));
   }
   auto tr = std::make_unique<LocalTransport>();
-  const char* st = std::getenv("QSB_SHARD_STAGED");
-  tr->staged = st && *st && *st != '0';
+  const std::string mode = exchange_mode();
+  if (mode == "staged") tr->mode = LocalTransport::Staged;
+  if (mode == "peer") {
+    bool ok = true;
+    for (auto& s : ss->shards) ok = ok && alloc_alt(*s);
+    tr->mode = ok ? LocalTransport::Peer : LocalTransport::Swap;
+  }
   ss->tr = std::move(tr);
   shard_fill_basis(*ss, 0);
   return ss;
@@ -304,7 +501,11 @@ std::unique_ptr<ShardSet> make_dist_shard(uint32_t n, Dist* d) {
   auto s = std::make_unique<State>();
   alloc_shard(*s, n, g, static_cast<uint32_t>(d->rank), d->device, ss->stream);
   ss->shards.push_back(std::move(s));
-  ss->tr = std::make_unique<NcclTransport>(d);
+  auto tr = std::make_unique<NcclTransport>(d);
+  tr->owner = ss->shards[0].get();
+  // peer memory (CUDA IPC over NVLink) unless disabled; collective on all ranks
+  if (d->world > 1 && exchange_mode() != "nccl") tr->setup_peer(*ss->shards[0]);
+  ss->tr = std::move(tr);
   shard_fill_basis(*ss, 0);
   return ss;
 }

@@ -3,16 +3,25 @@
 // rank bits = r.  Tile passes run on every shard independently (rank bits are
 // outside every tile: diagonal gates and controls on them are per-shard
 // constants); a non-diagonal gate on a rank bit is preceded by a planner
-// SwapStep: rank bit j <-> local qubit p, a pairwise exchange of half a shard
-// between ranks r and r ^ 2^j.
+// SwapStep: rank bits j_i <-> local qubits p_i (i < k).  For k = 1 it is a
+// pairwise exchange of half a shard between ranks r and r ^ 2^j; for k > 1 an
+// all-to-all among the 2^k ranks that differ in those bits, each rank keeping
+// 1/2^k of its shard.
 //
 // Two transports:
-//   * LocalTransport: all 2^g shards in one process on one device (the halves
-//     are swapped by one kernel).  Used to validate sharded plans on a single
-//     B200 and to run states larger than one allocation would allow.
-//   * NcclTransport: one shard per process/GPU; halves travel with grouped
-//     ncclSend/ncclRecv over NVLink in bounded chunks (libnccl is loaded at run
-//     time; the unique id is exchanged by the caller, e.g. torch.distributed).
+//   * LocalTransport: all 2^g shards in one process on one device.  Used to
+//     validate sharded plans on a single B200 with each distributed data path:
+//     "swap" (one swap kernel per bit), "staged" (the NCCL fallback's
+//     pack/unpack protocol) and "peer" (the peer-memory scatter kernel into
+//     sibling shards' second buffers).
+//   * NcclTransport: one shard per process/GPU.  Default ("peer"): every
+//     rank maps every other rank's two shard buffers through CUDA IPC and an
+//     exchange is ONE kernel storing each amplitude straight into its new
+//     owner's free buffer over NVLink (no staging, no pack/unpack), followed
+//     by a stream-ordered NCCL barrier; buffers then flip.  Fallback ("nccl"):
+//     pack -> grouped ncclSend/ncclRecv in bounded chunks -> unpack.  libnccl
+//     is loaded at run time; the unique id is exchanged by the caller (e.g.
+//     torch.distributed).
 #pragma once
 
 #include <cstdint>
@@ -27,10 +36,14 @@ struct Plan;
 
 struct Transport {
   virtual ~Transport() = default;
-  virtual void exchange(std::vector<State*>& shards, uint32_t gpos, uint32_t lpos) = 0;
+  // Swaps rank bit gpos[i] with local qubit lpos[i] for every i (disjoint pairs).
+  virtual void exchange(std::vector<State*>& shards, const std::vector<uint32_t>& gpos,
+                        const std::vector<uint32_t>& lpos) = 0;
   // sum of one double per shard over all ranks, in rank order (deterministic)
   virtual double sum(const std::vector<double>& per_local_shard) = 0;
   virtual void barrier() {}
+  // Releases transport resources that reference the shards (before they are freed).
+  virtual void close() {}
 };
 
 struct ShardSet {

@@ -823,17 +823,28 @@ void plan_tiles(uint32_t n, std::vector<Op>& ops, std::vector<Step>& steps, cons
       if (perm[q] != q) return false;
     return true;
   };
-  auto emit_swap = [&](uint32_t j, uint32_t p) {  // rank bit j <-> local position p
+  // One exchange step for a set of disjoint (rank position j, local position p) pairs.
+  auto emit_swaps = [&](const std::vector<std::pair<uint32_t, uint32_t>>& pairs) {
+    if (pairs.empty()) return;
     Step s;
     s.kind = Step::SwapStep;
-    s.gpos = j - nl;
-    s.lpos = p;
+    for (auto [j, p] : pairs) {
+      s.gpos.push_back(j - nl);
+      s.lpos.push_back(p);
+    }
     steps.push_back(std::move(s));
-    swap_phys(j, p);
+    for (auto [j, p] : pairs) swap_phys(j, p);
   };
+  const bool batch_exchanges = [] {
+    const char* e = std::getenv("QSB_SHARD_BATCH");
+    return !e || std::atoi(e) != 0;
+  }();
   // Brings every rank bit the op needs into the shard, evicting the local
   // qubits needed furthest in the future (Belady); ties prefer the highest
-  // position (the exchanged half is then contiguous).
+  // position (the exchanged block is then contiguous).  Other rank bits whose
+  // qubit is needed before the evicted one's next use join the same exchange:
+  // a k-bit all-to-all moves 1 - 2^-k of a shard, so one more bit costs
+  // 2^-(k+1) of a shard instead of a later half-shard exchange.
   auto global_swaps_for = [&](const POp& op) {
     std::vector<size_t> next(n, SIZE_MAX);
     for (size_t k = 0; k < rem.size(); ++k) {
@@ -844,20 +855,34 @@ void plan_tiles(uint32_t n, std::vector<Op>& ops, std::vector<Step>& steps, cons
         if (next[l] == SIZE_MAX) next[l] = k;
       }
     }
-    uint64_t need = op.needmask & gmask;
+    std::vector<uint32_t> order;  // required rank positions, then optional by urgency
+    std::vector<uint32_t> optional;
+    for (uint32_t j = nl; j < n; ++j) {
+      if ((op.needmask >> j) & 1) order.push_back(j);
+      else if (batch_exchanges && next[inv[j]] != SIZE_MAX) optional.push_back(j);
+    }
+    const size_t required = order.size();
+    std::stable_sort(optional.begin(), optional.end(),
+                     [&](uint32_t a, uint32_t b) { return next[inv[a]] < next[inv[b]]; });
+    order.insert(order.end(), optional.begin(), optional.end());
     uint64_t taken = op.qmask;
-    while (need) {
-      const uint32_t j = static_cast<uint32_t>(__builtin_ctzll(need));
-      need &= need - 1;
+    std::vector<std::pair<uint32_t, uint32_t>> pairs;
+    for (size_t i = 0; i < order.size(); ++i) {
+      const uint32_t j = order[i];
       int best = -1;
       for (int p = static_cast<int>(nl) - 1; p >= 0; --p) {
         if ((taken >> p) & 1) continue;
         if (best < 0 || next[inv[p]] > next[inv[best]]) best = p;
       }
-      if (best < 0) throw RuntimeError("no local qubit available for a rank-bit exchange");
-      emit_swap(j, static_cast<uint32_t>(best));
+      if (best < 0) {
+        if (i < required) throw RuntimeError("no local qubit available for a rank-bit exchange");
+        break;
+      }
+      if (i >= required && !(next[inv[j]] < next[inv[best]])) break;
+      pairs.push_back({j, static_cast<uint32_t>(best)});
       taken |= bit(static_cast<uint32_t>(best));
     }
+    emit_swaps(pairs);
   };
 
   auto compile_pass = [&](uint64_t S, const std::vector<const POp*>& list, const std::vector<uint64_t>& srcs) {
@@ -1005,15 +1030,17 @@ void plan_tiles(uint32_t n, std::vector<Op>& ops, std::vector<Step>& steps, cons
   }
   // Restore the logical layout: rank bits by exchanges, then relabel-only
   // passes over the displaced local positions.
-  for (uint32_t j = nl; j < n; ++j) {
-    if (inv[j] == j) continue;
-    uint32_t src = perm[j];  // where logical j lives now
-    if (src >= nl) {         // on another rank bit: route through a local position
-      const uint32_t p = nl - 1;
-      emit_swap(src, p);
-      src = p;
+  while (true) {
+    std::vector<std::pair<uint32_t, uint32_t>> pairs;  // one all-to-all for every directly fixable bit
+    int misplaced = -1;
+    for (uint32_t j = nl; j < n; ++j) {
+      if (inv[j] == j) continue;
+      misplaced = static_cast<int>(j);
+      if (perm[j] < nl) pairs.push_back({j, perm[j]});  // logical j lives on local position perm[j]
     }
-    emit_swap(j, src);
+    if (misplaced < 0) break;
+    if (pairs.empty()) pairs.push_back({perm[misplaced], nl - 1});  // on another rank bit: route via a local one
+    emit_swaps(pairs);
   }
   while (!identity()) {
     uint64_t S = lowmask;

@@ -3,8 +3,10 @@
 The reference has no distributed mode: its StateVector is one host array
 (statevector.hpp:111-118).  Here an n-qubit state is split over 2^g shards --
 the top g qubits are rank bits -- and a plan compiled for g rank bits runs tile
-passes on every shard independently, with a pairwise half-shard exchange before
-each non-diagonal gate on a rank bit (paper_2212_14201_b200/csrc/shard.cpp).
+passes on every shard independently; before a non-diagonal gate on a rank bit
+the ranks exchange data so that rank bits and local qubits trade places (one
+bit: pairwise half-shard exchange; k bits: all-to-all among 2^k ranks;
+paper_2212_14201_b200/csrc/shard.cpp).
 
   * ``ShardedState.local(n, g)``: all 2^g shards in this process on one GPU
     (exchanges are device-local); validates sharded plans on a single B200.
@@ -82,12 +84,17 @@ class ShardedCircuit:
         return self._h
 
     def steps(self):
-        """[(kind, gpos, lpos)] per step; kind 0 per-gate kernel, 1 tile pass, 2 exchange."""
+        """[(kind, gpos, lpos)] per step; kind 0 per-gate kernel, 1 tile pass,
+        2 exchange of rank bits gpos[b] with local qubits lpos[b]."""
         out = []
-        k, gp, lp = C.c_int(), C.c_uint32(), C.c_uint32()
-        for i in range(self.stats()["launches"] + self.stats()["exchanges"]):
-            N.check(N.lib().qs_plan_step_info(self._h, i, C.byref(k), C.byref(gp), C.byref(lp)))
-            out.append((k.value, gp.value, lp.value))
+        k, nb = C.c_int(), C.c_uint32()
+        gp, lp = (C.c_uint32 * N.MAX_EXCHANGE_BITS)(), (C.c_uint32 * N.MAX_EXCHANGE_BITS)()
+        i = 0
+        total = self.stats()["launches"] + self.stats()["exchanges"]
+        while i < total:
+            N.check(N.lib().qs_plan_step_info(self._h, i, C.byref(k), C.byref(nb), gp, lp))
+            out.append((k.value, tuple(gp[:nb.value]), tuple(lp[:nb.value])))
+            i += 1
         return out
 
     def stats(self):

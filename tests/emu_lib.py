@@ -57,7 +57,8 @@ class Plan:
         L.te_plan_steps.restype = C.c_uint64
         L.te_plan_steps.argtypes = [C.c_void_p]
         L.te_plan_step.restype = C.c_int
-        L.te_plan_step.argtypes = [C.c_void_p, C.c_uint64, C.POINTER(C.c_uint32), C.POINTER(C.c_uint32)]
+        L.te_plan_step.argtypes = [C.c_void_p, C.c_uint64, C.POINTER(C.c_uint32), C.POINTER(C.c_uint32),
+                                   C.POINTER(C.c_uint32)]
         L.te_exec_step.restype = C.c_int
         L.te_exec_step.argtypes = [C.c_void_p, C.c_uint64, C.c_uint32, C.POINTER(C.c_double)]
         arr, keep = N.gate_array(gates)
@@ -75,9 +76,11 @@ class Plan:
         return lib().te_plan_steps(self._h)
 
     def step(self, i):
-        gp, lp = C.c_uint32(), C.c_uint32()
-        kind = lib().te_plan_step(self._h, i, C.byref(gp), C.byref(lp))
-        return kind, gp.value, lp.value
+        """(kind, gpos tuple, lpos tuple)."""
+        nb = C.c_uint32()
+        gp, lp = (C.c_uint32 * 16)(), (C.c_uint32 * 16)()
+        kind = lib().te_plan_step(self._h, i, C.byref(nb), gp, lp)
+        return kind, tuple(gp[:nb.value]), tuple(lp[:nb.value])
 
     def exec_step(self, i, rank, shard):
         """Runs non-exchange step i on `shard` (complex128, 2^(n-g), in place).

@@ -2,13 +2,28 @@
 
 Each rank holds only its shard (2^(n-g) amplitudes), replays the tile/op steps
 of the sharded plan on it with the host emulator, and performs every rank-bit
-exchange itself over torch.distributed (gloo): partner = rank ^ 2^gpos, the
-half with local bit lpos == 1 - (rank bit gpos) changes hands -- the protocol
-of NcclTransport::exchange (paper_2212_14201_b200/csrc/shard.cpp).
+exchange itself over torch.distributed (gloo) with the protocol of
+NcclTransport::exchange (paper_2212_14201_b200/csrc/shard.cpp): for exchanged
+rank bits gpos[b] <-> local bits lpos[b], block d (local bits = d) goes to the
+peer whose rank bits are d, and that peer's block a (a = our rank bits) lands
+in our block d.
 TEST INFRASTRUCTURE ONLY."""
 import os
 
 import numpy as np
+
+
+def block_indices(nl, lpos, d):
+    """Local indices whose bits lpos[b] equal bit b of d, ordered by the
+    remaining bits ascending (block_index in paper_2212_14201_b200/csrc/kernels.cu)."""
+    rest = [p for p in range(nl) if p not in lpos]
+    e = np.arange(1 << len(rest), dtype=np.int64)
+    idx = np.zeros_like(e)
+    for t, p in enumerate(rest):
+        idx |= ((e >> t) & 1) << p
+    for b, p in enumerate(lpos):
+        idx |= ((d >> b) & 1) << p
+    return idx
 
 
 def run(rank, world, port, n, which, seed, out_q):
@@ -40,15 +55,22 @@ def run(rank, world, port, n, which, seed, out_q):
         for i in range(len(plan)):
             kind, gpos, lpos = plan.step(i)
             if kind == emu_lib.Plan.SWAP:
-                partner = rank ^ (1 << gpos)
-                v = 1 - ((rank >> gpos) & 1)
-                view = shard.reshape(-1, 2, 1 << lpos)
-                send = torch.from_numpy(np.ascontiguousarray(view[:, v, :]).view(np.float64).ravel())
-                recv = torch.empty_like(send)
-                reqs = [dist.isend(send, partner), dist.irecv(recv, partner)]
+                k = len(gpos)
+                a = sum(((rank >> gpos[b]) & 1) << b for b in range(k))
+                reqs, recvs = [], {}
+                for d in range(1 << k):
+                    if d == a:
+                        continue
+                    peer = rank
+                    for b in range(k):
+                        peer = (peer & ~(1 << gpos[b])) | (((d >> b) & 1) << gpos[b])
+                    send = torch.from_numpy(shard[block_indices(nl, lpos, d)].view(np.float64).copy())
+                    recvs[d] = torch.empty_like(send)
+                    reqs += [dist.isend(send, peer), dist.irecv(recvs[d], peer)]
                 for r in reqs:
                     r.wait()
-                view[:, v, :] = recv.numpy().view(np.complex128).reshape(view[:, v, :].shape)
+                for d, buf in recvs.items():
+                    shard[block_indices(nl, lpos, d)] = buf.numpy().view(np.complex128)
                 exchanges += 1
             else:
                 rc = plan.exec_step(i, rank, shard)

@@ -31,7 +31,7 @@ def _launch(world, n, which, seed):
     return res
 
 
-@pytest.mark.parametrize("world,which", [(2, "mixed"), (2, "random"), (2, "qft"), (4, "hea"), (4, "mixed")])
+@pytest.mark.parametrize("world,which", [(2, "mixed"), (2, "random"), (2, "qft"), (4, "hea"), (4, "mixed"), (8, "random")])
 def test_sharded_protocol_gloo(world, which):
     n = 12
     res = _launch(world, n, which, 99 + world)

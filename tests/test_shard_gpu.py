@@ -3,8 +3,8 @@
 All 2^g shards live on one B200 (ShardedState.local): the plans, tile passes
 with rank bits, and half-shard exchanges are exactly those a distributed run
 executes, only the exchange transport differs (device-local swap instead of
-NCCL send/recv; the NCCL pack/unpack kernels are covered by
-test_staged_exchange_matches_oracle).  Results are compared with the C oracle and
+NCCL/peer-memory transfers; those kernels are covered by
+test_distributed_exchange_paths_match_oracle).  Results are compared with the C oracle and
 with the unsharded tile path."""
 import numpy as np
 import pytest
@@ -125,13 +125,15 @@ def test_sharded_qft_closed_form_large(n, g):
         assert np.max(np.abs(got - want)) <= TOL
 
 
-@pytest.mark.parametrize("g", [1, 3])
-def test_staged_exchange_matches_oracle(monkeypatch, g):
-    """QSB_SHARD_STAGED=1: local shards exchange through the NCCL transport's
-    pack -> staging buffer -> unpack kernels (chunked; only the send/recv is
-    replaced by a device copy), so the distributed data path is checked on one
-    GPU."""
-    monkeypatch.setenv("QSB_SHARD_STAGED", "1")
+@pytest.mark.parametrize("mode", ["staged", "peer"])
+@pytest.mark.parametrize("g", [1, 2, 3])
+def test_distributed_exchange_paths_match_oracle(monkeypatch, g, mode):
+    """The distributed transports' data paths on one GPU.  staged: the NCCL
+    fallback's pack -> staging buffer -> unpack kernels (chunked; only the
+    send/recv is replaced by a device copy).  peer: the peer-memory scatter
+    kernel writing every amplitude into its owner's second buffer (sibling
+    shards here, NVLink peers over CUDA IPC in a distributed run)."""
+    monkeypatch.setenv("QSB_SHARD_EXCHANGE", mode)
     monkeypatch.setenv("QSB_SHARD_CHUNK", "4096")  # force several chunks per exchange
     n = 15
     gates = mixed_gates(n, 200, 4242 + g)
@@ -143,8 +145,11 @@ def test_staged_exchange_matches_oracle(monkeypatch, g):
     st.set_amplitudes(a0, 0)
     circ = ShardedCircuit(n, g, gates)
     assert circ.stats()["exchanges"] >= 1
+    if g > 1:
+        assert max(len(gp) for k, gp, _ in circ.steps() if k == 2) > 1  # multi-bit all-to-all
     st.execute(circ)
     assert np.max(np.abs(st.amplitudes() - want)) <= TOL
+    assert abs(st.norm_squared() - 1.0) <= 1e-12
 
 
 def test_nccl_single_rank_communicator():
@@ -163,3 +168,26 @@ def test_nccl_single_rank_communicator():
     assert abs(st.checksum() - ol.checksum(want, n)) <= 1e-12 * (1 << n)
     st.close()
     comm.close()
+
+
+def test_checksum_invariant_across_shard_counts():
+    """SURVEY 8(d) config 4 parity: the 30-qubit random circuit's checksum does
+    not depend on the number of shards (P = 1, 2, 4, 8), nor on the transport."""
+    import os
+    n = 30
+    gates = Q.gen_random_circuit(n, 20, 424242).gates()
+    sv = Q.StateVector(n)
+    sv.apply_circuit(gates)
+    ref = sv.checksum()
+    probe = sv.amplitudes(12345678, 4096)
+    del sv
+    for g, mode in [(1, "swap"), (2, "peer"), (3, "swap"), (3, "peer")]:
+        os.environ["QSB_SHARD_EXCHANGE"] = mode
+        try:
+            st = ShardedState.local(n, g)
+        finally:
+            del os.environ["QSB_SHARD_EXCHANGE"]
+        st.apply_circuit(gates)
+        assert abs(st.checksum() - ref) <= 1e-12 * (1 << n)
+        assert np.max(np.abs(st.amplitudes(12345678, 4096) - probe)) <= 1e-12
+        st.close()

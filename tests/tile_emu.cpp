@@ -262,11 +262,13 @@ int te_run(uint32_t n, const qs_gate* gates, uint64_t count, uint32_t mode, uint
       const auto& s = steps[i];
       if (s.kind == qsb::Step::OpStep) {
         emu_op(a, n, s.op);
-      } else if (s.kind == qsb::Step::SwapStep) {  // exchange = physical bit swap
-        qsb::Op sw;
-        sw.kind = qsb::OpKind::Swap;
-        sw.targets = {n - global_qubits + s.gpos, s.lpos};
-        emu_op(a, n, sw);
+      } else if (s.kind == qsb::Step::SwapStep) {  // exchange = physical bit swaps
+        for (size_t b = 0; b < s.gpos.size(); ++b) {
+          qsb::Op sw;
+          sw.kind = qsb::OpKind::Swap;
+          sw.targets = {n - global_qubits + s.gpos[b], s.lpos[b]};
+          emu_op(a, n, sw);
+        }
       } else {
         emu_tile(a, *s.tile);
       }
@@ -309,10 +311,13 @@ int te_plan_create(uint32_t n, uint32_t g, const qs_gate* gates, uint64_t count,
 
 void te_plan_free(te_plan* h) { delete h; }
 uint64_t te_plan_steps(te_plan* h) { return h->p->steps.size(); }
-int te_plan_step(te_plan* h, uint64_t i, uint32_t* gpos, uint32_t* lpos) {
+int te_plan_step(te_plan* h, uint64_t i, uint32_t* nbits, uint32_t* gpos, uint32_t* lpos) {
   const auto& s = h->p->steps[i];
-  *gpos = s.gpos;
-  *lpos = s.lpos;
+  *nbits = static_cast<uint32_t>(s.gpos.size());
+  for (size_t b = 0; b < s.gpos.size(); ++b) {
+    gpos[b] = s.gpos[b];
+    lpos[b] = s.lpos[b];
+  }
   return static_cast<int>(s.kind);
 }
 
