@@ -41,6 +41,11 @@ struct Gen {
   uint32_t cur_tq[kTileMaxT] = {};
   int counter = 0;
   bool prefetch = true;
+  // single_buf: the prefetch buffer doubles as the transpose buffer (64 KiB
+  // per CTA, two resident CTAs per SM); the next tile's copies are issued
+  // after the last transpose has read the buffer.
+  bool single_buf = false;
+  int transposes_total = 0;
 
   explicit Gen(const TileProgram& p) : tp(p) {
     for (auto& k : K) k = 1.0;
@@ -336,8 +341,13 @@ struct Gen {
     emit_G(mt + 2 * TB + 8, false);
   }
 
+  static constexpr const char* kIssueNext =
+      "    { const unsigned long long nt = tile + gridDim.x; if (nt < ntiles) prefetch(nt); }\n";
+
   std::string run(const std::string& kname, uint32_t threads, uint32_t minb) {
     const TileHeader& h = tp.h;
+    transposes_total = 0;
+    for (const TOp& o : tp.ops) transposes_total += o.type == TO_TRANSPOSE;
     const uint32_t T = 1u << h.t;
     unsigned long long loff[16];
     for (int p = 0; p < 16; ++p) {
@@ -352,7 +362,7 @@ struct Gen {
         name[p] = fresh();
         s << "    const double2 " << name[p] << " = PB[" << p * T << " + tid];\n";
       }
-      s << "    { const unsigned long long nt = tile + gridDim.x; if (nt < ntiles) prefetch(nt); }\n";
+      if (!single_buf || transposes_total == 0) s << kIssueNext;
     } else {
       for (int p = 0; p < 16; ++p) {
         name[p] = fresh();
@@ -370,7 +380,10 @@ struct Gen {
         case TO_PHASE: phase(o); break;
         case TO_DENSE2:
         case TO_DENSE3: dense(o); break;
-        case TO_TRANSPOSE: transpose(o, ti++); break;
+        case TO_TRANSPOSE:
+          transpose(o, ti++);
+          if (prefetch && single_buf && ti == transposes_total) s << "    __syncthreads();\n" << kIssueNext;
+          break;
         case TO_RELABEL: emit_G(tp.meta.data() + o.meta, false); break;
         default: throw RuntimeError("jit: unknown micro-op");
       }
@@ -408,7 +421,7 @@ struct Gen {
       // Each thread stages its own 16 amplitudes of the next tile in its own
       // shared-memory slots (slot p*T + tid: conflict-free) with cp.async, so
       // HBM reads of tile i+1 overlap the arithmetic of tile i.
-      k << "  double2* const PB = sm + " << (tp.transposes ? (1u << h.m) : 0u) << ";\n";
+      k << "  double2* const PB = sm + " << (tp.transposes && !single_buf ? (1u << h.m) : 0u) << ";\n";
       k << "  auto prefetch = [&](unsigned long long t) {\n";
       k << "    const unsigned long long g = base_of(t) | rank_base | TL;\n";
       for (int p = 0; p < 16; ++p)
