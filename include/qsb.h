@@ -251,6 +251,17 @@ int qs_shards_plan_execute_timed(qs_shards_t s, qs_plan_t p, float* step_ms);
 int qs_shards_plan_execute(qs_shards_t s, qs_plan_t p);
 int qs_shards_apply_circuit(qs_shards_t s, const qs_gate* gates, uint64_t n);
 int qs_shards_norm2(qs_shards_t s, double* out);
+/* Marginal probabilities over distinct qubits (result bit b <-> qubits[b]),
+ * summed over shards in rank order                        [statevector.hpp:190-208] */
+int qs_shards_probs(qs_shards_t s, const uint32_t* qubits, uint32_t m, double* out);
+/* BasisSampler over the sharded state: the cumulative |a|^2 runs through the
+ * shards in rank order (each shard continues the previous one's running sum,
+ * so exact mode is bit-identical to the reference's serial loop); out_index
+ * holds global basis indices, identical on every rank     [statevector.hpp:542-570] */
+int qs_shards_sample(qs_shards_t s, const double* uniforms, uint64_t shots, int exact, uint64_t* out_index);
+int qs_shards_sample_seeded(qs_shards_t s, uint64_t seed, uint64_t shots, int exact, uint64_t* out_index);
+/* <psi|P_t|psi> (letters as in qs_expect_pauli); X on rank bits pairs shards. */
+int qs_shards_expect_pauli(qs_shards_t s, const char* letters, uint32_t nterms, double* out);
 int qs_shards_checksum(qs_shards_t s, double* out);
 
 #ifdef __cplusplus

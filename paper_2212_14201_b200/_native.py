@@ -130,6 +130,10 @@ _SIGS = {
     "qs_shards_plan_execute": (C.c_int, [_P, _P]),
     "qs_shards_apply_circuit": (C.c_int, [_P, _GP, C.c_uint64]),
     "qs_shards_norm2": (C.c_int, [_P, _DP]),
+    "qs_shards_probs": (C.c_int, [_P, _UP, C.c_uint32, _DP]),
+    "qs_shards_sample": (C.c_int, [_P, _DP, C.c_uint64, C.c_int, _U64P]),
+    "qs_shards_sample_seeded": (C.c_int, [_P, C.c_uint64, C.c_uint64, C.c_int, _U64P]),
+    "qs_shards_expect_pauli": (C.c_int, [_P, C.c_char_p, C.c_uint32, _DP]),
     "qs_shards_checksum": (C.c_int, [_P, _DP]),
 }
 

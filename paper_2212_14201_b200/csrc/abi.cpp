@@ -165,6 +165,7 @@ int qs_destroy(qs_state_t h) {
       DeviceGuard dg(s.device);
       cudaStreamSynchronize(s.stream);
       if (s.amps) cudaFree(s.amps);
+      if (s.alt) cudaFree(s.alt);
       if (s.scratch) cudaFree(s.scratch);
       if (s.host_pinned) cudaFreeHost(s.host_pinned);
       cudaStreamDestroy(s.stream);
@@ -512,28 +513,37 @@ int qs_sample_seeded(qs_state_t h, uint64_t seed, uint64_t shots, int exact, uin
   });
 }
 
+static void parse_pauli(const char* letters, uint32_t nterms, uint32_t n, std::vector<uint64_t>& xm,
+                        std::vector<uint64_t>& sm, std::vector<int>& ny) {
+  if (nterms && !letters) throw ValidationError("null Pauli letters");
+  xm.assign(nterms, 0);
+  sm.assign(nterms, 0);
+  ny.assign(nterms, 0);
+  for (uint32_t t = 0; t < nterms; ++t) {
+    uint64_t x = 0, z = 0;
+    int y = 0;
+    for (uint32_t q = 0; q < n; ++q) {
+      const char c = letters[static_cast<uint64_t>(t) * n + q];
+      switch (c) {
+        case 'I': break;
+        case 'X': x |= 1ull << q; break;
+        case 'Y': x |= 1ull << q; z |= 1ull << q; ++y; break;
+        case 'Z': z |= 1ull << q; break;
+        default: throw ValidationError(std::string("unknown Pauli letter '") + c + "'");
+      }
+    }
+    xm[t] = x;
+    sm[t] = z;
+    ny[t] = y;
+  }
+}
+
 int qs_expect_pauli(qs_state_t h, const char* letters, uint32_t nterms, double* out) {
   return guarded([&] {
     State& s = st(h);
-    std::vector<uint64_t> xm(nterms), sm(nterms);
-    std::vector<int> ny(nterms);
-    for (uint32_t t = 0; t < nterms; ++t) {
-      uint64_t x = 0, z = 0;
-      int y = 0;
-      for (uint32_t q = 0; q < s.n; ++q) {
-        const char c = letters[static_cast<uint64_t>(t) * s.n + q];
-        switch (c) {
-          case 'I': break;
-          case 'X': x |= 1ull << q; break;
-          case 'Y': x |= 1ull << q; z |= 1ull << q; ++y; break;
-          case 'Z': z |= 1ull << q; break;
-          default: throw ValidationError(std::string("unknown Pauli letter '") + c + "'");
-        }
-      }
-      xm[t] = x;
-      sm[t] = z;
-      ny[t] = y;
-    }
+    std::vector<uint64_t> xm, sm;
+    std::vector<int> ny;
+    parse_pauli(letters, nterms, s.n, xm, sm, ny);
     expect_pauli(s, xm, sm, ny, out);
   });
 }
@@ -741,6 +751,40 @@ int qs_shards_apply_circuit(qs_shards_t s, const qs_gate* gates, uint64_t n) {
     auto p = make_plan(ss.n, gates, n, QS_PLAN_TILED, 0, ss.g);
     shard_execute(ss, *p);
     shard_sync(ss);
+  });
+}
+
+int qs_shards_probs(qs_shards_t s, const uint32_t* qubits, uint32_t m, double* out) {
+  return guarded([&] {
+    if (!out || (m && !qubits)) throw ValidationError("null buffer");
+    shard_probs(sh(s), qubits, m, out);
+  });
+}
+
+int qs_shards_sample(qs_shards_t s, const double* uniforms, uint64_t shots, int exact, uint64_t* out_index) {
+  return guarded([&] {
+    if (shots && (!uniforms || !out_index)) throw ValidationError("null sample buffers");
+    shard_sample(sh(s), uniforms, shots, exact != 0, out_index);
+  });
+}
+
+int qs_shards_sample_seeded(qs_shards_t s, uint64_t seed, uint64_t shots, int exact, uint64_t* out_index) {
+  return guarded([&] {
+    if (shots && !out_index) throw ValidationError("null sample buffer");
+    std::vector<double> u(shots);  // Rng(seed).uniform() stream (rng.hpp:20-46)
+    std::mt19937_64 eng(seed);
+    for (uint64_t i = 0; i < shots; ++i) u[i] = static_cast<double>(eng() >> 11) * 0x1.0p-53;
+    shard_sample(sh(s), u.data(), shots, exact != 0, out_index);
+  });
+}
+
+int qs_shards_expect_pauli(qs_shards_t s, const char* letters, uint32_t nterms, double* out) {
+  return guarded([&] {
+    ShardSet& ss = sh(s);
+    std::vector<uint64_t> xm, sm;
+    std::vector<int> ny;
+    parse_pauli(letters, nterms, ss.n, xm, sm, ny);
+    shard_expect_pauli(ss, xm, sm, ny, out);
   });
 }
 

@@ -29,6 +29,11 @@ struct JitModule {
   uint32_t threads = 0;
   uint32_t min_blocks = 1;
   size_t smem = 0;      // dynamic shared memory per CTA
+  size_t spill_bytes = 0;  // ptxas-reported spill stores of the built variant
+  // 1-CTA variant used when the 2-CTA (128-register) build spills
+  std::string alt_source;
+  uint32_t alt_min_blocks = 1;
+  size_t alt_smem = 0;
   std::mutex mu;
   void* mod[64] = {};   // CUmodule per device
   void* fn[64] = {};    // CUfunction per device
@@ -36,7 +41,8 @@ struct JitModule {
 };
 
 // CUDA source of one tile pass (kernel name `name`).
-std::string tile_source(const TileProgram& tp, const std::string& name, std::vector<double2>* params);
+std::string tile_source(const TileProgram& tp, const std::string& name, std::vector<double2>* params,
+                        size_t* table_bytes = nullptr, int force_single = -1);
 
 // Generates and compiles every tile step of a plan (parallel, cached by source).
 void compile_tile_steps(std::vector<Step>& steps);

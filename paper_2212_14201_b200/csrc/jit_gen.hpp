@@ -14,6 +14,7 @@
 
 #include <complex>
 #include <cstring>
+#include <map>
 #include <sstream>
 #include <string>
 #include <vector>
@@ -46,6 +47,24 @@ struct Gen {
   // after the last transpose has read the buffer.
   bool single_buf = false;
   int transposes_total = 0;
+
+  // Tile-wide phase factors from qubits outside the tile: a product over up
+  // to n-m bits of the tile's global index.  Bits are grouped in chunks of 6
+  // of the compact tile index tix (tile | rank_base >> m); a chunk holding >= 2
+  // factors becomes a 64-entry table in shared memory, built once per CTA, so
+  // the per-tile cost is one lookup + one complex multiply per chunk.
+  struct Table {
+    uint32_t chunk, off;
+    std::vector<std::pair<uint32_t, uint32_t>> bits;  // (bit within chunk, coefficient index)
+  };
+  std::vector<Table> tables;
+  uint32_t table_entries = 0;
+  static constexpr uint32_t kChunk = 6, kMaxTableEntries = 32 * 64;
+  uint32_t tix_bit(uint32_t q) const {  // compact tile-index bit of an outside qubit
+    uint32_t below = 0;
+    for (uint32_t b = 0; b < tp.h.m; ++b) below += tp.h.S[b] < q;
+    return q - below;
+  }
 
   explicit Gen(const TileProgram& p) : tp(p) {
     for (auto& k : K) k = 1.0;
@@ -243,7 +262,20 @@ struct Gen {
       s << "    double2 " << Fo << " = " << (F.empty() ? (c1 ? std::string("make_double2(1.0, 0.0)") : coef(o.coef + 16))
                                                         : (c1 ? F : "cmul(" + F + ", " + coef(o.coef + 16) + ")"))
         << ";\n";
-      for (auto& [q, ci] : out) s << "    if ((base >> " << q << ") & 1ull) " << Fo << " = cmul(" << Fo << ", " << coef(ci) << ");\n";
+      std::map<uint32_t, std::vector<std::pair<uint32_t, uint32_t>>> by_chunk;
+      for (auto& [q, ci] : out) by_chunk[tix_bit(q) / kChunk].push_back({tix_bit(q) % kChunk, ci});
+      for (auto& [c, bits] : by_chunk) {
+        if (bits.size() >= 2 && table_entries + 64 <= kMaxTableEntries) {
+          tables.push_back({c, table_entries, bits});
+          s << "    " << Fo << " = cmul(" << Fo << ", TAB[" << table_entries << " + ((tix >> " << c * kChunk
+            << ") & 63u)]);\n";
+          table_entries += 64;
+        } else {
+          for (auto& [b, ci] : bits)
+            s << "    if ((tix >> " << c * kChunk + b << ") & 1ull) " << Fo << " = cmul(" << Fo << ", " << coef(ci)
+              << ");\n";
+        }
+      }
       F = Fo;
     }
     if (!t.empty() && !F.empty()) {
@@ -273,7 +305,17 @@ struct Gen {
       }
       return;
     }
-    // register-predicated phase: applies to a subset of slots right away
+    // register-predicated phase: the per-slot constants join the pending K
+    // (compile time); only the thread/tile factor F is applied now, to the
+    // selected slots (one complex multiply each)
+    if (t.empty()) {
+      for (int p = 0; p < 16; ++p) {
+        if ((p & o.rmask) != o.rval) continue;
+        K[p] *= coefv(o.coef + p);
+        if (!F.empty()) set(p, "cmul(" + name[p] + ", " + F + ")", "");
+      }
+      return;
+    }
     for (int p = 0; p < 16; ++p) {
       if ((p & o.rmask) != o.rval) continue;
       const cd g = coefv(o.coef + p);
@@ -417,6 +459,16 @@ struct Gen {
     }
     k << "    return b;\n  };\n";
     k << pro.str();
+    const uint32_t tile_bufs = single_buf ? 1u : (tp.transposes ? 1u : 0u) + (prefetch ? 1u : 0u);
+    if (!tables.empty()) {
+      k << "  double2* const TAB = sm + " << tile_bufs * (1u << h.m) << ";\n";
+      for (const Table& tb : tables) {
+        k << "  for (unsigned e = tid; e < 64u; e += " << threads << "u) {\n    double2 f = make_double2(1.0, 0.0);\n";
+        for (auto& [b, ci] : tb.bits) k << "    if ((e >> " << b << ") & 1u) f = cmul(f, " << coef(ci) << ");\n";
+        k << "    TAB[" << tb.off << " + e] = f;\n  }\n";
+      }
+      k << "  __syncthreads();\n";
+    }
     if (prefetch) {
       // Each thread stages its own 16 amplitudes of the next tile in its own
       // shared-memory slots (slot p*T + tid: conflict-free) with cp.async, so
@@ -434,6 +486,7 @@ struct Gen {
       k << "  for (unsigned long long tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {\n";
     }
     k << "    const unsigned long long base = base_of(tile) | rank_base;\n";
+    k << "    const unsigned long long tix = tile | (rank_base >> " << h.m << ");\n";
     k << "    unsigned long long G = base | TL;\n";
     k << s.str();
     k << "  }\n}\n";

@@ -394,6 +394,44 @@ __global__ void __launch_bounds__(kThreads) k_scatter_exchange(const double2* __
   __threadfence_system();
 }
 
+// ------------------------------------------------- qubit permutation
+// Out-of-place bit permutation of the index (the layout restore that ends a
+// plan whose SWAPs were absorbed as relabels): out[sigma(i)] = in[i], where
+// sigma moves index bit q to bit pos[q].  One HBM pass, coalesced on both
+// sides: a tile covers the 10 input bits A = {0..4} + sigma^-1({0..4}) (+ the
+// lowest others), staged in shared memory; reads run over input bits 0..4 and
+// writes over output bits 0..4.  Offsets come from 32-entry tables.
+constexpr uint32_t kPermTileBits = 10, kPermTile = 1u << kPermTileBits;
+
+struct PermSpec {
+  uint32_t nb;                              // base (tile-index) bits
+  uint8_t bin[64], bout[64];                // their input / output positions
+  unsigned long long in_lo[32], in_hi[32];  // input offset of local e (bits 0-4 / 5-9)
+  unsigned long long out_lo[32], out_hi[32];// output offset of local f
+  uint16_t e_lo[32], e_hi[32];              // local e feeding output local f
+};
+
+__global__ void __launch_bounds__(kThreads) k_permute(const double2* __restrict__ in, double2* __restrict__ out,
+                                                      const PermSpec ps, uint64_t ntiles) {
+  __shared__ double2 tile[kPermTile];
+  for (uint64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
+    uint64_t bi = 0, bo = 0;
+    for (uint32_t k = 0; k < ps.nb; ++k)
+      if ((t >> k) & 1ull) {
+        bi |= 1ull << ps.bin[k];
+        bo |= 1ull << ps.bout[k];
+      }
+    for (uint32_t e = threadIdx.x; e < kPermTile; e += kThreads)
+      tile[e ^ ((e >> 5) & 7u)] = __ldcs(in + (bi | ps.in_lo[e & 31u] | ps.in_hi[e >> 5]));
+    __syncthreads();
+    for (uint32_t f = threadIdx.x; f < kPermTile; f += kThreads) {
+      const uint32_t e = ps.e_lo[f & 31u] | ps.e_hi[f >> 5];
+      __stcs(out + (bo | ps.out_lo[f & 31u] | ps.out_hi[f >> 5]), tile[e ^ ((e >> 5) & 7u)]);
+    }
+    __syncthreads();
+  }
+}
+
 // ------------------------------------------------- serial-equivalent scan
 // The reference's BasisSampler accumulates acc += |a_i|^2 left to right in
 // double (statevector.hpp:544-552); counts depend on those exact roundings.
@@ -421,9 +459,10 @@ __global__ void __launch_bounds__(kThreads) k_chunk_sum(const double* __restrict
 }
 
 // exclusive scan of chunk sums (estimates only), single block
-__global__ void k_scan_estimate(const double* __restrict__ S, uint32_t nc, double* __restrict__ E) {
+__global__ void k_scan_estimate(const double* __restrict__ S, uint32_t nc, double* __restrict__ E,
+                                const double* __restrict__ carry) {
   if (threadIdx.x == 0) {
-    double acc = 0;
+    double acc = carry ? *carry : 0.0;
     for (uint32_t c = 0; c < nc; ++c) {
       E[c] = acc;
       acc += S[c];
@@ -498,9 +537,10 @@ __device__ __forceinline__ long long warp_incl_scan_ll(long long v) {
 // Phase C: one warp walks the chunks in order.
 __global__ void k_sequential(const double* __restrict__ p, uint64_t n, uint64_t C, uint32_t nc,
                              const ChunkInfo* __restrict__ info, double* __restrict__ start,
-                             unsigned char* __restrict__ fast, double* __restrict__ cum, double* __restrict__ total) {
+                             unsigned char* __restrict__ fast, double* __restrict__ cum, double* __restrict__ total,
+                             const double* __restrict__ carry) {
   const int lane = threadIdx.x & 31;
-  double A = 0.0;
+  double A = carry ? *carry : 0.0;  // sharded states: the previous shard's final running sum
   const double kMinNormalScaled = 2.2250738585072014e-308 * 4503599627370496.0;
   for (uint32_t c = 0; c < nc; ++c) {
     const ChunkInfo ci = info[c];
@@ -628,7 +668,58 @@ __global__ void __launch_bounds__(kThreads) k_search(const double* __restrict__ 
   }
 }
 
+// Sharded sampling: this shard answers the shots whose target lies in
+// [*lo, *hi) (lo = previous shards' total, null for the first shard; the last
+// shard also takes targets >= *hi, the reference's size-1 fallback).  Global
+// indices; other shots are left untouched.
+__global__ void __launch_bounds__(kThreads) k_search_range(const double* __restrict__ cum, uint64_t size,
+                                                           const double* __restrict__ total_p,
+                                                           const double* __restrict__ lo_p,
+                                                           const double* __restrict__ hi_p, int last,
+                                                           const double* __restrict__ u, uint64_t shots,
+                                                           uint64_t rank_base, unsigned long long* __restrict__ out) {
+  const double total = *total_p, hi = *hi_p;
+  for (uint64_t s = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; s < shots; s += (uint64_t)gridDim.x * blockDim.x) {
+    const double target = u[s] * total;
+    if (lo_p && target < *lo_p) continue;
+    if (!last && target >= hi) continue;
+    uint64_t a = 0, b = size - 1;
+    while (a < b) {
+      const uint64_t mid = (a + b) / 2;
+      if (cum[mid] > target) b = mid;
+      else a = mid + 1;
+    }
+    out[s] = rank_base | a;
+  }
+}
+
 // ---------------------------------------------------------- expectation
+// Pauli term whose X part crosses shards: sum_j conj(b[j ^ xl]) a[j] (-1)^popc(j & smask)
+// with b the partner shard (rank ^ X's rank bits).
+__global__ void __launch_bounds__(kThreads) k_pauli2(const double2* __restrict__ a, const double2* __restrict__ b,
+                                                     uint64_t size, uint64_t xmask, uint64_t smask,
+                                                     double2* __restrict__ partial) {
+  __shared__ double sh[kThreads / 32];
+  const uint64_t chunk = (size + gridDim.x - 1) / gridDim.x;
+  const uint64_t lo = blockIdx.x * chunk, hi = min(size, lo + chunk);
+  double re = 0, im = 0;
+  for (uint64_t j = lo + threadIdx.x; j < hi; j += blockDim.x) {
+    const double2 x = a[j];
+    const double2 y = b[j ^ xmask];
+    double pr = fma(y.x, x.x, y.y * x.y);
+    double pi = fma(y.x, x.y, -y.y * x.x);
+    if (__popcll(j & smask) & 1) {
+      pr = -pr;
+      pi = -pi;
+    }
+    re += pr;
+    im += pi;
+  }
+  const double tr = block_sum(re, sh);
+  const double ti = block_sum(im, sh);
+  if (threadIdx.x == 0) partial[blockIdx.x] = make_double2(tr, ti);
+}
+
 __global__ void __launch_bounds__(kThreads) k_pauli(const double2* __restrict__ a, uint64_t size, uint64_t xmask,
                                                     uint64_t smask, double2* __restrict__ partial) {
   __shared__ double sh[kThreads / 32];
@@ -805,6 +896,64 @@ void unpack_block(State& s, const uint32_t* lpos, uint32_t k, uint32_t d, uint64
   QSB_LAUNCHED();
 }
 
+void permute_qubits(State& s, const std::vector<uint32_t>& pos) {
+  const uint32_t n = s.local_qubits();
+  if (pos.size() != n) throw ValidationError("permutation size does not match the state");
+  if (n < kPermTileBits) throw ValidationError("qubit permutation needs at least 10 qubits");
+  std::vector<int> inv(n, -1);
+  for (uint32_t q = 0; q < n; ++q) {
+    if (pos[q] >= n || inv[pos[q]] >= 0) throw ValidationError("not a permutation");
+    inv[pos[q]] = static_cast<int>(q);
+  }
+  // tile bits A: input 0..4, the inputs that land on output 0..4, then the lowest others
+  std::vector<char> inA(n, 0);
+  for (uint32_t q = 0; q < 5; ++q) inA[q] = inA[inv[q]] = 1;
+  uint32_t cnt = 0;
+  for (uint32_t q = 0; q < n; ++q) cnt += inA[q];
+  for (uint32_t q = 0; q < n && cnt < kPermTileBits; ++q)
+    if (!inA[q]) {
+      inA[q] = 1;
+      ++cnt;
+    }
+  std::vector<uint32_t> A, B;
+  for (uint32_t q = 0; q < n; ++q) (inA[q] ? A : B).push_back(q);
+  std::vector<uint32_t> C;  // output positions of the tile, ascending
+  for (auto q : A) C.push_back(pos[q]);
+  std::sort(C.begin(), C.end());
+  PermSpec ps{};
+  ps.nb = static_cast<uint32_t>(B.size());
+  for (size_t k = 0; k < B.size(); ++k) {
+    ps.bin[k] = static_cast<uint8_t>(B[k]);
+    ps.bout[k] = static_cast<uint8_t>(pos[B[k]]);
+  }
+  for (uint32_t v = 0; v < 32; ++v) {
+    for (uint32_t j = 0; j < 5; ++j) {
+      if (!((v >> j) & 1)) continue;
+      ps.in_lo[v] |= 1ull << A[j];
+      ps.in_hi[v] |= 1ull << A[j + 5];
+      ps.out_lo[v] |= 1ull << C[j];
+      ps.out_hi[v] |= 1ull << C[j + 5];
+      // output bit C[j] comes from input bit inv[C[j]] = A[k]
+      const uint32_t klo = static_cast<uint32_t>(std::find(A.begin(), A.end(), static_cast<uint32_t>(inv[C[j]])) - A.begin());
+      const uint32_t khi =
+          static_cast<uint32_t>(std::find(A.begin(), A.end(), static_cast<uint32_t>(inv[C[j + 5]])) - A.begin());
+      ps.e_lo[v] |= static_cast<uint16_t>(1u << klo);
+      ps.e_hi[v] |= static_cast<uint16_t>(1u << khi);
+    }
+  }
+  DeviceGuard dg(s.device);
+  if (!s.alt && cudaMalloc(&s.alt, s.size * sizeof(double2)) != cudaSuccess) {
+    cudaGetLastError();
+    s.alt = nullptr;
+    throw MemoryError("cannot allocate the second state buffer for a qubit permutation");
+  }
+  const uint64_t ntiles = s.size >> kPermTileBits;
+  const uint32_t grid = static_cast<uint32_t>(std::min<uint64_t>(ntiles, num_sms(s.device) * 8ull));
+  k_permute<<<grid, kThreads, 0, s.stream>>>(s.amps, s.alt, ps, ntiles);
+  QSB_LAUNCHED();
+  std::swap(s.amps, s.alt);
+}
+
 void fill_basis(State& s, uint64_t index) {
   DeviceGuard dg(s.device);
   k_basis<<<grid_for(s.size, s.device), kThreads, 0, s.stream>>>(s.amps, s.size, index);
@@ -835,7 +984,7 @@ void marginal_probs(State& s, const uint32_t* qubits, uint32_t m, double* host_o
   DeviceGuard dg(s.device);
   std::vector<uint32_t> qs(qubits, qubits + m);
   const Slots sl = make_slots(qs, {});
-  const uint64_t per_bin = 1ull << (s.n - m);
+  const uint64_t per_bin = 1ull << (s.local_qubits() - m);
   const uint64_t bins = 1ull << m;
   const size_t out_bytes = bins * sizeof(double);
   if (m <= 12) {
@@ -928,18 +1077,18 @@ SamplerBuffers sampler_buffers(State& s, uint64_t extra_bytes, char** extra) {
   return b;
 }
 
-void build_cumulative(State& s, SamplerBuffers& b, bool exact) {
+void build_cumulative(State& s, SamplerBuffers& b, bool exact, const double* carry = nullptr) {
   const uint64_t N = s.size;
   k_probs<<<grid_for(N, s.device), kThreads, 0, s.stream>>>(s.amps, 0, N, b.p);
   QSB_LAUNCHED();
   k_chunk_sum<<<b.nc, kThreads, 0, s.stream>>>(b.p, N, b.C, b.S);
   QSB_LAUNCHED();
-  k_scan_estimate<<<1, 32, 0, s.stream>>>(b.S, b.nc, b.E);
+  k_scan_estimate<<<1, 32, 0, s.stream>>>(b.S, b.nc, b.E, carry);
   QSB_LAUNCHED();
   if (exact) {
     k_chunk_ints<<<b.nc, kThreads, 0, s.stream>>>(b.p, N, b.C, b.E, b.info);
     QSB_LAUNCHED();
-    k_sequential<<<1, 32, 0, s.stream>>>(b.p, N, b.C, b.nc, b.info, b.start, b.fast, b.cum, b.total);
+    k_sequential<<<1, 32, 0, s.stream>>>(b.p, N, b.C, b.nc, b.info, b.start, b.fast, b.cum, b.total, carry);
     QSB_LAUNCHED();
     k_expand<<<b.nc, kThreads, 0, s.stream>>>(b.p, N, b.C, b.info, b.start, b.fast, b.cum);
     QSB_LAUNCHED();
@@ -950,6 +1099,41 @@ void build_cumulative(State& s, SamplerBuffers& b, bool exact) {
   }
 }
 }  // namespace
+
+ShardCum shard_cumulative(State& s, bool exact, const double* carry_dev, uint64_t shots, double** u_dev,
+                          unsigned long long** out_dev) {
+  DeviceGuard dg(s.device);
+  char* extra;
+  SamplerBuffers b = sampler_buffers(s, shots * 16, &extra);
+  build_cumulative(s, b, exact, carry_dev);
+  if (u_dev) *u_dev = reinterpret_cast<double*>(extra);
+  if (out_dev) *out_dev = reinterpret_cast<unsigned long long*>(extra + shots * 8);
+  return ShardCum{b.cum, b.total};
+}
+
+void search_range(State& s, const ShardCum& c, const double* total_dev, const double* lo_dev, bool last,
+                  const double* u_dev, uint64_t shots, unsigned long long* out_dev) {
+  DeviceGuard dg(s.device);
+  if (!shots) return;
+  k_search_range<<<grid_for(shots, s.device), kThreads, 0, s.stream>>>(c.cum, s.size, total_dev, lo_dev, c.total, last,
+                                                                       u_dev, shots, s.rank_base, out_dev);
+  QSB_LAUNCHED();
+}
+
+void pauli_cross(State& s, const double2* a, const double2* partner, uint64_t size, uint64_t xl, uint64_t smask_local,
+                 double* out2) {
+  DeviceGuard dg(s.device);
+  double2* part = static_cast<double2*>(s.get_scratch((kRedBlocks + 1) * sizeof(double2)));
+  k_pauli2<<<kRedBlocks, kThreads, 0, s.stream>>>(a, partner, size, xl, smask_local, part);
+  QSB_LAUNCHED();
+  k_finalize2<<<1, kThreads, 0, s.stream>>>(part, kRedBlocks, part + kRedBlocks);
+  QSB_LAUNCHED();
+  double2 h;
+  QSB_CUDA(cudaMemcpyAsync(&h, part + kRedBlocks, sizeof(double2), cudaMemcpyDeviceToHost, s.stream));
+  QSB_CUDA(cudaStreamSynchronize(s.stream));
+  out2[0] = h.x;
+  out2[1] = h.y;
+}
 
 double exact_cumulative(State& s, double* d_probs, double* d_cum) {
   DeviceGuard dg(s.device);

@@ -14,6 +14,10 @@ namespace qsb {
 // One HBM pass per op (the reference's per-gate kernels, statevector.hpp:268-467).
 void launch_op(State& s, const Op& op);
 
+// Out-of-place qubit permutation: bit q of every index moves to bit pos[q]
+// (one HBM pass into the state's second buffer, then the buffers swap).
+void permute_qubits(State& s, const std::vector<uint32_t>& pos);
+
 void fill_basis(State& s, uint64_t index);                      // |index> (local index; out of range = all 0)
 
 // Rank-bit exchanges for sharded states (shard.cpp).
@@ -45,6 +49,23 @@ void sample(State& s, const double* uniforms_host, uint64_t shots, bool exact, u
 // <psi|P|psi> for Pauli strings given as (xmask, zmask, #Y) per term.
 void expect_pauli(State& s, const std::vector<uint64_t>& xmask, const std::vector<uint64_t>& zmask,
                   const std::vector<int>& ny, double* out);
+
+// Sharded sampling (shard.cpp): this shard's cumulative |a|^2 continuing from
+// *carry_dev (the previous shard's total; null = 0), plus device room for
+// `shots` uniforms and indices.
+struct ShardCum {
+  double* cum;
+  double* total;  // device: this shard's final running sum
+};
+ShardCum shard_cumulative(State& s, bool exact, const double* carry_dev, uint64_t shots, double** u_dev,
+                          unsigned long long** out_dev);
+// Writes global indices for the shots this shard owns (targets in [*lo, total)).
+void search_range(State& s, const ShardCum& c, const double* total_dev, const double* lo_dev, bool last,
+                  const double* u_dev, uint64_t shots, unsigned long long* out_dev);
+// sum_{j < size} conj(partner[j ^ xl]) a[j] (-1)^popc(j & smask) (host, synchronous; s
+// supplies stream and scratch).
+void pauli_cross(State& s, const double2* a, const double2* partner, uint64_t size, uint64_t xl, uint64_t smask_local,
+                 double* out2);
 
 // Exposed for tests of the exact scan (cum must hold s.size doubles on device).
 double exact_cumulative(State& s, double* d_probs, double* d_cum);

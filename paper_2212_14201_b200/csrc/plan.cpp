@@ -17,7 +17,7 @@ uint64_t Plan::passes() const {
 uint64_t Plan::launches() const {
   uint64_t l = 0;
   for (const auto& s : steps) {
-    if (s.kind == Step::TileStep) l += 1;
+    if (s.kind == Step::TileStep || s.kind == Step::PermStep) l += 1;
     else if (s.op.kind != OpKind::Identity) l += 1;
   }
   return l;
@@ -80,6 +80,7 @@ void execute_step(State& s, const Step& st) {
     case Step::OpStep: launch_op(s, st.op); break;
     case Step::TileStep: launch_tile(s, *st.tile); break;
     case Step::SwapStep: throw ValidationError("rank-bit exchange outside a shard set");
+    case Step::PermStep: permute_qubits(s, st.perm); break;
   }
 }
 

@@ -15,7 +15,7 @@ namespace qsb {
 struct TileProgram;  // tile.hpp
 
 struct Step {
-  enum Kind { OpStep, TileStep, SwapStep } kind = OpStep;
+  enum Kind { OpStep, TileStep, SwapStep, PermStep } kind = OpStep;
   Op op;                               // OpStep
   std::shared_ptr<TileProgram> tile;   // TileStep
   // SwapStep (sharded states): for every i, exchange physical qubit
@@ -23,6 +23,9 @@ struct Step {
   // pairwise half-shard exchange; k bits are an all-to-all among the 2^k
   // ranks that differ in those rank bits (each sends 1 - 2^-k of its shard).
   std::vector<uint32_t> gpos, lpos;
+  // PermStep: out-of-place qubit permutation, bit q of every index -> bit
+  // perm[q] (restores the logical layout after relabeling SWAPs in one pass).
+  std::vector<uint32_t> perm;
 };
 
 struct Plan {

@@ -188,7 +188,8 @@ struct Nccl {
 };
 constexpr int kNcclUint8 = 1;   // ncclUint8
 constexpr int kNcclDouble = 8;  // ncclFloat64
-constexpr int kNcclSum = 0, kNcclMin = 3;
+constexpr int kNcclUint64 = 5;  // ncclUint64
+constexpr int kNcclSum = 0, kNcclMax = 2, kNcclMin = 3;
 
 const Nccl& nccl() {
   static Nccl n;
@@ -532,6 +533,7 @@ void shard_execute(ShardSet& ss, const Plan& p, uint64_t first, uint64_t count) 
         for (auto* s : shards) launch_op(*s, st.op);
         break;
       case Step::SwapStep: ss.tr->exchange(shards, st.gpos, st.lpos); break;
+      case Step::PermStep: throw ValidationError("sharded plans restore their layout in place");
     }
   }
 }
@@ -588,6 +590,188 @@ void shard_set(ShardSet& ss, const double* in, uint64_t offset, uint64_t count) 
 void shard_sync(ShardSet& ss) {
   DeviceGuard dg(ss.device);
   QSB_CUDA(cudaStreamSynchronize(ss.stream));
+}
+
+
+// ------------------------------------------------------------ reductions
+namespace {
+NcclTransport* dist_of(ShardSet& ss) { return dynamic_cast<NcclTransport*>(ss.tr.get()); }
+
+struct DevBuf {  // small device buffer freed on scope exit
+  void* p = nullptr;
+  int dev = 0;
+  DevBuf(size_t bytes, int device) : dev(device) {
+    DeviceGuard dg(device);
+    if (cudaMalloc(&p, std::max<size_t>(bytes, 16)) != cudaSuccess) {
+      cudaGetLastError();
+      p = nullptr;
+      throw MemoryError("device allocation failed");
+    }
+  }
+  ~DevBuf() {
+    DeviceGuard dg(dev);
+    cudaFree(p);
+  }
+  template <class T>
+  T* as() {
+    return static_cast<T*>(p);
+  }
+};
+}  // namespace
+
+void shard_probs(ShardSet& ss, const uint32_t* qubits, uint32_t m, double* out) {
+  if (m == 0) throw ValidationError("probabilities: empty qubit subset");
+  if (m > 26) throw ValidationError("probabilities: at most 26 qubits for a sharded state");
+  uint64_t seen = 0;
+  for (uint32_t b = 0; b < m; ++b) {
+    if (qubits[b] >= ss.n) throw ValidationError("probabilities: qubit out of range");
+    if ((seen >> qubits[b]) & 1) throw ValidationError("probabilities: repeated qubit");
+    seen |= 1ull << qubits[b];
+  }
+  const uint32_t nl = ss.n - ss.g;
+  std::vector<uint32_t> lq, lb;  // local qubits of the subset and their result bits
+  for (uint32_t b = 0; b < m; ++b)
+    if (qubits[b] < nl) {
+      lq.push_back(qubits[b]);
+      lb.push_back(b);
+    }
+  const uint64_t R = 1ull << m;
+  // one full-size vector per held shard, summed in rank order
+  std::vector<double> mine(R * ss.shards.size(), 0.0);
+  for (size_t i = 0; i < ss.shards.size(); ++i) {
+    State& s = *ss.shards[i];
+    uint64_t fixed = 0;  // result bits set by this shard's rank bits
+    for (uint32_t b = 0; b < m; ++b)
+      if (qubits[b] >= nl && ((s.rank >> (qubits[b] - nl)) & 1)) fixed |= 1ull << b;
+    double* dst = mine.data() + i * R;
+    if (lq.empty()) {
+      dst[fixed] = reduce_norm2(s);
+      continue;
+    }
+    std::vector<double> loc(1ull << lq.size());
+    marginal_probs(s, lq.data(), static_cast<uint32_t>(lq.size()), loc.data());
+    for (uint64_t k = 0; k < loc.size(); ++k) {
+      uint64_t idx = fixed;
+      for (size_t j = 0; j < lq.size(); ++j)
+        if ((k >> j) & 1) idx |= 1ull << lb[j];
+      dst[idx] = loc[k];
+    }
+  }
+  std::vector<double> all;
+  if (NcclTransport* nt = dist_of(ss)) {
+    const int W = nt->d_->world;
+    DeviceGuard dg(ss.device);
+    DevBuf buf(R * 8 * (W + 1), ss.device);
+    double* d = buf.as<double>();
+    QSB_CUDA(cudaMemcpy(d + R * W, mine.data(), R * 8, cudaMemcpyHostToDevice));
+    nccl_check(nccl().allGather(d + R * W, d, R, kNcclDouble, nt->d_->comm, nullptr), "ncclAllGather");
+    all.resize(R * W);
+    QSB_CUDA(cudaMemcpy(all.data(), d, R * W * 8, cudaMemcpyDeviceToHost));
+  } else {
+    all = std::move(mine);
+  }
+  const size_t parts = all.size() / R;
+  for (uint64_t k = 0; k < R; ++k) {
+    double t = 0;
+    for (size_t r = 0; r < parts; ++r) t += all[r * R + k];  // rank order
+    out[k] = t;
+  }
+}
+
+void shard_sample(ShardSet& ss, const double* u_host, uint64_t shots, bool exact, uint64_t* out_host) {
+  if (!shots) return;
+  DeviceGuard dg(ss.device);
+  if (NcclTransport* nt = dist_of(ss)) {
+    State& s = *ss.shards[0];
+    const int W = nt->d_->world, r = nt->d_->rank;
+    DevBuf small(32, ss.device);
+    double* carry = small.as<double>();
+    double* total = carry + 1;
+    // serial chain: rank r continues the running sum of ranks < r (bit-exact serial order)
+    if (r > 0) nccl_check(nccl().recv(carry, 1, kNcclDouble, r - 1, nt->d_->comm, s.stream), "ncclRecv");
+    double* u = nullptr;
+    unsigned long long* out = nullptr;
+    ShardCum c = shard_cumulative(s, exact, r > 0 ? carry : nullptr, shots, &u, &out);
+    if (r + 1 < W) nccl_check(nccl().send(c.total, 1, kNcclDouble, r + 1, nt->d_->comm, s.stream), "ncclSend");
+    nccl_check(nccl().allReduce(c.total, total, 1, kNcclDouble, kNcclMax, nt->d_->comm, s.stream), "ncclAllReduce");
+    QSB_CUDA(cudaMemcpyAsync(u, u_host, shots * 8, cudaMemcpyHostToDevice, s.stream));
+    QSB_CUDA(cudaMemsetAsync(out, 0, shots * 8, s.stream));
+    search_range(s, c, total, r > 0 ? carry : nullptr, r + 1 == W, u, shots, out);
+    nccl_check(nccl().allReduce(out, out, shots, kNcclUint64, kNcclMax, nt->d_->comm, s.stream), "ncclAllReduce");
+    QSB_CUDA(cudaMemcpyAsync(out_host, out, shots * 8, cudaMemcpyDeviceToHost, s.stream));
+    QSB_CUDA(cudaStreamSynchronize(s.stream));
+    return;
+  }
+  const size_t P = ss.shards.size();
+  std::vector<ShardCum> c(P);
+  double* u = nullptr;
+  unsigned long long* out = nullptr;
+  for (size_t i = 0; i < P; ++i)
+    c[i] = shard_cumulative(*ss.shards[i], exact, i ? c[i - 1].total : nullptr, i ? 0 : shots, i ? nullptr : &u,
+                            i ? nullptr : &out);
+  QSB_CUDA(cudaMemcpyAsync(u, u_host, shots * 8, cudaMemcpyHostToDevice, ss.stream));
+  QSB_CUDA(cudaMemsetAsync(out, 0, shots * 8, ss.stream));
+  for (size_t i = 0; i < P; ++i)
+    search_range(*ss.shards[i], c[i], c[P - 1].total, i ? c[i - 1].total : nullptr, i + 1 == P, u, shots, out);
+  QSB_CUDA(cudaMemcpyAsync(out_host, out, shots * 8, cudaMemcpyDeviceToHost, ss.stream));
+  QSB_CUDA(cudaStreamSynchronize(ss.stream));
+}
+
+void shard_expect_pauli(ShardSet& ss, const std::vector<uint64_t>& xm, const std::vector<uint64_t>& zm,
+                        const std::vector<int>& ny, double* out) {
+  const uint32_t nl = ss.n - ss.g;
+  const uint64_t lmask = (1ull << nl) - 1;
+  NcclTransport* nt = dist_of(ss);
+  for (size_t t = 0; t < xm.size(); ++t) {
+    const uint64_t xl = xm[t] & lmask, xr = xm[t] >> nl, zl = zm[t] & lmask, zr = zm[t] >> nl;
+    std::vector<double> re, im;
+    for (auto& sp : ss.shards) {
+      State& s = *sp;
+      const double sg = (__builtin_popcountll(s.rank & zr) & 1) ? -1.0 : 1.0;
+      double v[2] = {0, 0};
+      if (!xr) {
+        expect_pauli(s, {xl}, {zl}, {0}, v);
+      } else if (!nt) {  // partner shard on this device
+        const uint32_t pr = s.rank ^ static_cast<uint32_t>(xr);
+        const State* partner = nullptr;
+        for (auto& q : ss.shards)
+          if (q->rank == pr) partner = q.get();
+        pauli_cross(s, s.amps, partner->amps, s.size, xl, zl, v);
+      } else if (nt->peer) {  // partner shard mapped over NVLink
+        const uint32_t pr = s.rank ^ static_cast<uint32_t>(xr);
+        pauli_cross(s, s.amps, nt->bufs[nt->cur][pr], s.size, xl, zl, v);
+      } else {  // stream the partner's shard in aligned chunks (X maps each chunk onto itself)
+        const uint32_t pr = s.rank ^ static_cast<uint32_t>(xr);
+        uint64_t C = exchange_chunk(s.size, 1);
+        const uint64_t need = xl ? (1ull << (64 - __builtin_clzll(xl))) : 1;
+        C = std::max(C, need);
+        C = std::min<uint64_t>(C, s.size);
+        double2* stg = nt->stage.get(2 * C, s.device);
+        for (uint64_t off = 0; off < s.size; off += C) {
+          nccl_check(nccl().groupStart(), "ncclGroupStart");
+          nccl_check(nccl().send(s.amps + off, 2 * C, kNcclDouble, static_cast<int>(pr), nt->d_->comm, s.stream),
+                     "ncclSend");
+          nccl_check(nccl().recv(stg, 2 * C, kNcclDouble, static_cast<int>(pr), nt->d_->comm, s.stream), "ncclRecv");
+          nccl_check(nccl().groupEnd(), "ncclGroupEnd");
+          double w[2];
+          pauli_cross(s, s.amps + off, stg, C, xl, zl, w);
+          const double so = (__builtin_popcountll(off & zl) & 1) ? -1.0 : 1.0;
+          v[0] += so * w[0];
+          v[1] += so * w[1];
+        }
+      }
+      re.push_back(sg * v[0]);
+      im.push_back(sg * v[1]);
+    }
+    double r = ss.tr->sum(re), i = ss.tr->sum(im);
+    for (int k = 0; k < (ny[t] & 3); ++k) {  // times i^ny
+      const double r2 = -i, i2 = r;
+      r = r2;
+      i = i2;
+    }
+    out[2 * t] = r;
+    out[2 * t + 1] = i;
+  }
 }
 
 }  // namespace qsb

@@ -84,5 +84,16 @@ double shard_checksum(ShardSet& ss);
 void shard_get(ShardSet& ss, double* out, uint64_t offset, uint64_t count);
 void shard_set(ShardSet& ss, const double* in, uint64_t offset, uint64_t count);
 void shard_sync(ShardSet& ss);
+// Marginal over distinct qubits (result bit b <-> qubits[b]); every rank gets
+// the full result, summed over shards in rank order.
+void shard_probs(ShardSet& ss, const uint32_t* qubits, uint32_t m, double* out);
+// BasisSampler over the whole sharded state: the cumulative sum runs serially
+// through the shards in rank order (exact mode: bit-identical to the
+// reference's serial loop); out[i] = global basis index for u[i], on every rank.
+void shard_sample(ShardSet& ss, const double* u, uint64_t shots, bool exact, uint64_t* out);
+// <psi|P_t|psi> for Pauli strings (xmask, zmask, #Y); X parts on rank bits pair
+// each shard with its partner (peer memory, sibling shard, or streamed chunks).
+void shard_expect_pauli(ShardSet& ss, const std::vector<uint64_t>& xm, const std::vector<uint64_t>& zm,
+                        const std::vector<int>& ny, double* out);
 
 }  // namespace qsb

@@ -98,6 +98,9 @@ struct TileOptions {
   uint32_t low = 4; // qubits 0..low-1 always in the tile: 256 B contiguous runs
                     // (measured: 128 B runs 70% of HBM per pass, 256 B 80%)
   bool remap = true;  // plan-level qubit relabelling (low slots hold the qubits needed next)
+  // End a plan whose layout was relabeled with one out-of-place permutation
+  // pass (needs a second state buffer) instead of in-place relabel passes.
+  bool perm_step = true;
   uint32_t global_qubits = 0;  // sharded states: top qubits are rank bits, never in a tile
 };
 TileOptions tile_options_from_env();

@@ -665,6 +665,7 @@ TileOptions tile_options_from_env() {
   if (const char* e = std::getenv("QSB_TILE_M")) o.m = static_cast<uint32_t>(std::atoi(e));
   if (const char* e = std::getenv("QSB_TILE_LOW")) o.low = static_cast<uint32_t>(std::atoi(e));
   if (const char* e = std::getenv("QSB_TILE_REMAP")) o.remap = std::atoi(e) != 0;
+  if (const char* e = std::getenv("QSB_PERM_STEP")) o.perm_step = std::atoi(e) != 0;
   o.m = std::max<uint32_t>(8, std::min<uint32_t>(kTileMaxM, o.m));
   o.low = std::min<uint32_t>(5, o.low);
   return o;
@@ -917,9 +918,38 @@ void plan_tiles(uint32_t n, std::vector<Op>& ops, std::vector<Step>& steps, cons
     steps.push_back(std::move(s));
   };
 
+  // With an out-of-place restore at the end, an uncontrolled SWAP whose qubits
+  // have no earlier pending op is absorbed into the logical->physical map (no
+  // data movement); the accumulated permutation costs one pass at the end
+  // (QFT's final bit reversal: 15 swaps -> 1 pass instead of 3-4).
+  const bool absorb_swaps = opt.perm_step && opt.global_qubits == 0 && n >= 10;
+  auto absorb_ready_swaps = [&]() {
+    if (!absorb_swaps) return;
+    uint64_t blocked = 0;
+    std::vector<uint32_t> keep;
+    keep.reserve(rem.size());
+    for (auto idx : rem) {
+      const POp& p = pops[idx];  // logical
+      if (p.k == PK::SwapRel && !(p.qmask & blocked)) {
+        swap_phys(perm[p.op.targets[0]], perm[p.op.targets[1]]);
+        continue;
+      }
+      blocked |= p.qmask;
+      keep.push_back(idx);
+    }
+    rem.swap(keep);
+  };
+  absorb_ready_swaps();
   refresh();
   emit_ready_opaque();
   while (!rem.empty()) {
+    for (size_t before = SIZE_MAX; before != rem.size() && !rem.empty();) {  // absorbing can free opaque ops
+      before = rem.size();
+      absorb_ready_swaps();
+      refresh();
+      emit_ready_opaque();
+    }
+    if (rem.empty()) break;
     refresh();
     // a non-diagonal gate on a rank bit at the head of the program: exchange first
     if (gmask && (phys[rem[0]].needmask & gmask)) {
@@ -1041,6 +1071,13 @@ void plan_tiles(uint32_t n, std::vector<Op>& ops, std::vector<Step>& steps, cons
     if (misplaced < 0) break;
     if (pairs.empty()) pairs.push_back({perm[misplaced], nl - 1});  // on another rank bit: route via a local one
     emit_swaps(pairs);
+  }
+  if (opt.perm_step && opt.global_qubits == 0 && n >= 10 && !identity()) {
+    Step s;
+    s.kind = Step::PermStep;
+    s.perm.assign(inv.begin(), inv.end());  // data at bit p belongs to logical inv[p]
+    steps.push_back(std::move(s));
+    for (uint32_t q = 0; q < n; ++q) perm[q] = inv[q] = q;
   }
   while (!identity()) {
     uint64_t S = lowmask;

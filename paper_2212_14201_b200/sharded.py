@@ -191,3 +191,28 @@ class ShardedState:
         out = C.c_double()
         N.check(N.lib().qs_shards_checksum(self._h, C.byref(out)))
         return out.value
+
+    def probabilities(self, qubits):
+        qubits = list(qubits)
+        out = np.empty(1 << len(qubits), dtype=np.float64)
+        q, m = N.uarr(qubits)
+        N.check(N.lib().qs_shards_probs(self._h, q, m, N.dptr(out)))
+        return out
+
+    def sample(self, uniforms, exact=True):
+        u = np.ascontiguousarray(uniforms, dtype=np.float64)
+        out = np.empty(u.size, dtype=np.uint64)
+        N.check(N.lib().qs_shards_sample(self._h, N.dptr(u), u.size, 1 if exact else 0, out.ctypes.data_as(N._U64P)))
+        return out
+
+    def sample_seeded(self, seed, shots, exact=True):
+        out = np.empty(shots, dtype=np.uint64)
+        N.check(N.lib().qs_shards_sample_seeded(self._h, seed, shots, 1 if exact else 0, out.ctypes.data_as(N._U64P)))
+        return out
+
+    def expect_pauli(self, words):
+        """words: per-qubit letter strings of length n -> complex array."""
+        letters = "".join(words).encode()
+        out = np.empty(2 * len(words), dtype=np.float64)
+        N.check(N.lib().qs_shards_expect_pauli(self._h, letters, len(words), N.dptr(out)))
+        return out.view(np.complex128)

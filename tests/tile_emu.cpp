@@ -269,6 +269,15 @@ int te_run(uint32_t n, const qs_gate* gates, uint64_t count, uint32_t mode, uint
           sw.targets = {n - global_qubits + s.gpos[b], s.lpos[b]};
           emu_op(a, n, sw);
         }
+      } else if (s.kind == qsb::Step::PermStep) {  // bit q of every index -> bit perm[q]
+        std::vector<cd> b(a.size());
+        for (uint64_t i = 0; i < a.size(); ++i) {
+          uint64_t o = 0;
+          for (uint32_t q = 0; q < n; ++q)
+            if ((i >> q) & 1) o |= 1ull << s.perm[q];
+          b[o] = a[i];
+        }
+        a.swap(b);
       } else {
         emu_tile(a, *s.tile);
       }
