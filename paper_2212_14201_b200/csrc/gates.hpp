@@ -22,6 +22,8 @@ struct Op {
   std::vector<uint32_t> controls;
   std::vector<cd> m;               // Diag: {d0, d1}; Mat1: 2x2; Dense: 2^k x 2^k (row-major)
   uint64_t gate_index = 0;         // position in the submitted gate list
+  uint64_t cneg = 0;               // controls that must be 0 (tile plans, diagonal ops only:
+                                   // produced by Pauli-X absorption, tile_plan.cpp)
 };
 
 // Row-major matrix of a named gate on its targets (defining controls in the

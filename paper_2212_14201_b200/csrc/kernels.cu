@@ -763,6 +763,7 @@ inline double2 d2(cd c) { return make_double2(c.real(), c.imag()); }
 // ------------------------------------------------------------ launchers
 
 void launch_op(State& s, const Op& op_in) {
+  if (op_in.cneg) throw RuntimeError("negated control in a per-gate kernel (planner invariant)");
   DeviceGuard dg(s.device);
   const uint32_t n = s.local_qubits();
   Op local;

@@ -101,6 +101,8 @@ struct TileOptions {
   // End a plan whose layout was relabeled with one out-of-place permutation
   // pass (needs a second state buffer) instead of in-place relabel passes.
   bool perm_step = true;
+  // Drop X gates whose flip can be folded into later gates (absorb_pauli_x).
+  bool absorb_x = true;
   uint32_t global_qubits = 0;  // sharded states: top qubits are rank bits, never in a tile
 };
 TileOptions tile_options_from_env();

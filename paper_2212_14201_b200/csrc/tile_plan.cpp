@@ -119,7 +119,8 @@ struct AOp {
   int cfg = 0;              // config index at this op
   uint32_t target = 0;      // MAT1 / FLIP qubit
   std::vector<uint32_t> dense_targets;
-  uint64_t pred = 0;        // control qubits (all must be 1)
+  uint64_t pred = 0;        // control qubits
+  uint64_t pred_val = ~0ull;  // their required values (bits of pred; default all 1)
   cd m[4];
   std::vector<cd> dense;    // row-major
   // PHASE
@@ -379,22 +380,34 @@ struct Compiler {
           const cd d0 = p.op.m[0], d1 = p.op.m[1];
           const uint64_t qm = ctrl | bit(tq);
           struct Rep {
-            uint64_t pred;
+            uint64_t pred, val;
             cd c;
             uint32_t q;
             cd w;
           };
+          // negated controls (Pauli-X absorption) must be 0
+          const uint64_t cval = ctrl & ~p.op.cneg;
           std::vector<Rep> reps;
-          if (d0 == cd(1.0)) {
-            reps.push_back({ctrl, 1.0, tq, d1});
-            for (auto cq : p.op.controls) reps.push_back({(ctrl & ~bit(cq)) | bit(tq), 1.0, cq, d1});
+          if (d0 == cd(1.0) || d1 == cd(1.0)) {
+            // one phase d on a conjunction of literals (b_q = v_q over the
+            // controls and the target); any literal can be the weight and the
+            // rest the predicate: d^[b=1] = d^b,  d^[b=0] = d * (1/d)^b
+            const cd d = d0 == cd(1.0) ? d1 : d0;
+            const uint64_t lits = ctrl | bit(tq);
+            const uint64_t vals = cval | (d0 == cd(1.0) ? bit(tq) : 0);
+            std::vector<uint32_t> order{tq};
+            order.insert(order.end(), p.op.controls.begin(), p.op.controls.end());
+            for (uint32_t q : order) {
+              const bool one = (vals >> q) & 1;
+              reps.push_back({lits & ~bit(q), vals & ~bit(q), one ? cd(1.0) : d, q, one ? d : 1.0 / d});
+            }
           } else {
-            reps.push_back({ctrl, d0, tq, d1 / d0});
+            reps.push_back({ctrl, cval, d0, tq, d1 / d0});
           }
           bool merged = false;
           if (open >= 0 && !(qm & x_open)) {
             for (auto& r : reps)
-              if (r.pred == aops[open].pred) {
+              if (r.pred == aops[open].pred && r.val == aops[open].pred_val) {
                 aops[open].c *= r.c;
                 auto it = aops[open].w.find(r.q);
                 if (it == aops[open].w.end()) aops[open].w[r.q] = r.w;
@@ -409,6 +422,7 @@ struct Compiler {
             a.type = TO_PHASE;
             a.cfg = cur;
             a.pred = r.pred;
+            a.pred_val = r.val;
             a.c = r.c;
             a.w[r.q] = r.w;
             aops.push_back(a);
@@ -545,19 +559,23 @@ std::shared_ptr<TileProgram> finalize(Compiler& C, uint64_t gates, const std::ve
   addr_of(C.cfgs[0], h.load);
   addr_of(C.cfgs[C.final_cfg], h.store);
 
-  auto split_pred = [&](const Cfg& c, uint64_t pred, TOp& o) {
+  auto split_pred = [&](const Cfg& c, uint64_t pred, TOp& o, uint64_t val = ~0ull) {
     o.rmask = 0;
     o.rval = 0;
     o.gmask = 0;
     o.gval = 0;
     for (uint32_t q = 0; q < 64; ++q) {
       if (!((pred >> q) & 1)) continue;
+      const bool one = (val >> q) & 1;
       int pos;
-      if (C.tb[q] >= 0 && C.has_reg(c, C.tb[q], &pos)) o.rmask |= static_cast<uint16_t>(1u << pos);
-      else o.gmask |= bit(q);
+      if (C.tb[q] >= 0 && C.has_reg(c, C.tb[q], &pos)) {
+        o.rmask |= static_cast<uint16_t>(1u << pos);
+        if (one) o.rval |= static_cast<uint16_t>(1u << pos);
+      } else {
+        o.gmask |= bit(q);
+        if (one) o.gval |= bit(q);
+      }
     }
-    o.rval = o.rmask;
-    o.gval = o.gmask;
   };
 
   for (const AOp& a : C.aops) {
@@ -594,7 +612,7 @@ std::shared_ptr<TileProgram> finalize(Compiler& C, uint64_t gates, const std::ve
         break;
       }
       case TO_PHASE: {
-        split_pred(c, a.pred, o);
+        split_pred(c, a.pred, o, a.pred_val);
         cd G[16];
         for (int p = 0; p < 16; ++p) G[p] = 1.0;
         std::vector<std::pair<uint32_t, cd>> list;
@@ -666,6 +684,7 @@ TileOptions tile_options_from_env() {
   if (const char* e = std::getenv("QSB_TILE_LOW")) o.low = static_cast<uint32_t>(std::atoi(e));
   if (const char* e = std::getenv("QSB_TILE_REMAP")) o.remap = std::atoi(e) != 0;
   if (const char* e = std::getenv("QSB_PERM_STEP")) o.perm_step = std::atoi(e) != 0;
+  if (const char* e = std::getenv("QSB_ABSORB_X")) o.absorb_x = std::atoi(e) != 0;
   o.m = std::max<uint32_t>(8, std::min<uint32_t>(kTileMaxM, o.m));
   o.low = std::min<uint32_t>(5, o.low);
   return o;
@@ -678,6 +697,8 @@ POp to_physical(const POp& p, const std::vector<uint32_t>& perm) {
   POp q = p;
   for (auto& t : q.op.targets) t = perm[t];
   for (auto& c : q.op.controls) c = perm[c];
+  q.op.cneg = 0;
+  for (uint64_t m = p.op.cneg; m; m &= m - 1) q.op.cneg |= bit(perm[__builtin_ctzll(m)]);
   q.qmask = 0;
   q.needmask = 0;
   for (auto c : q.op.controls) q.qmask |= bit(c);
@@ -758,7 +779,74 @@ uint64_t choose_tile_set(const std::vector<POp>& phys, const std::vector<uint32_
 
 }  // namespace
 
+namespace {
+bool is_diag(const Op& o) {
+  return o.kind == OpKind::Diag || (o.kind == OpKind::Mat1 && o.m[1] == cd(0) && o.m[2] == cd(0));
+}
+bool touches(const Op& o, uint32_t q) {
+  return std::find(o.targets.begin(), o.targets.end(), q) != o.targets.end() ||
+         std::find(o.controls.begin(), o.controls.end(), q) != o.controls.end();
+}
+}  // namespace
+
+// Pauli-X absorption (exact circuit identity).  An uncontrolled X on q is
+// dropped when the next non-diagonal use of q is an uncontrolled 1-qubit (or
+// dense) gate M on q: M becomes M.X, and the ops in between see q flipped --
+// a diagonal with target q swaps d0/d1, a diagonal controlled by q gets a
+// negated control (a tile predicate on q = 0); an X on q commutes.  Anything
+// else touching q in between keeps the X.  (QFT of a basis state: the preparation X's no longer
+// block the controlled phases, which then schedule like QFT|0>.)
+void absorb_pauli_x(std::vector<Op>& ops) {
+  for (size_t i = 0; i < ops.size(); ++i) {
+    const Op& x = ops[i];
+    if (x.kind != OpKind::Flip || !x.controls.empty()) continue;
+    const uint32_t q = x.targets[0];
+    size_t consumer = SIZE_MAX;
+    bool ok = true;
+    for (size_t j = i + 1; j < ops.size() && ok; ++j) {
+      const Op& o = ops[j];
+      if (!touches(o, q)) continue;
+      if (is_diag(o)) continue;  // target q: d0 <-> d1; control q: negated control
+      if (o.kind == OpKind::Flip && o.targets[0] == q &&
+          std::find(o.controls.begin(), o.controls.end(), q) == o.controls.end())
+        continue;  // X commutes with X (and controls elsewhere are unaffected)
+      if (o.controls.empty() && (o.kind == OpKind::Mat1 || o.kind == OpKind::Dense) &&
+          std::find(o.targets.begin(), o.targets.end(), q) != o.targets.end()) {
+        consumer = j;
+        break;
+      }
+      ok = false;
+    }
+    if (!ok || consumer == SIZE_MAX) continue;
+    for (size_t j = i + 1; j < consumer; ++j) {
+      Op& o = ops[j];
+      if (!touches(o, q) || !is_diag(o)) continue;
+      if (o.kind == OpKind::Mat1) {  // normalise to Diag
+        o.kind = OpKind::Diag;
+        o.m = {o.m[0], o.m[3]};
+      }
+      if (o.targets[0] == q) std::swap(o.m[0], o.m[1]);  // target q is flipped
+      else o.cneg ^= bit(q);                              // control q now selects 0
+    }
+    Op& c = ops[consumer];
+    if (c.kind == OpKind::Mat1) {
+      std::swap(c.m[0], c.m[1]);
+      std::swap(c.m[2], c.m[3]);
+    } else {  // dense: columns permuted by the flip of q's local bit
+      const size_t k = c.targets.size(), dim = size_t(1) << k;
+      const size_t b = k - 1 - static_cast<size_t>(std::find(c.targets.begin(), c.targets.end(), q) - c.targets.begin());
+      std::vector<cd> mm(c.m.size());
+      for (size_t r = 0; r < dim; ++r)
+        for (size_t cc = 0; cc < dim; ++cc) mm[r * dim + cc] = c.m[r * dim + (cc ^ (size_t(1) << b))];
+      c.m = std::move(mm);
+    }
+    ops[i].kind = OpKind::Identity;
+    ops[i].targets.clear();
+  }
+}
+
 void plan_tiles(uint32_t n, std::vector<Op>& ops, std::vector<Step>& steps, const TileOptions& opt) {
+  if (opt.absorb_x && n >= 6 && !std::getenv("QSB_NO_ABSORB_X")) absorb_pauli_x(ops);
   std::vector<POp> pops = preprocess(ops);
   // Tiny registers cannot host a 16-amplitude-per-thread tile: per-gate kernels.
   if (n < 6) {
