@@ -142,6 +142,12 @@ int qs_plan_enqueue(qs_state_t s, qs_plan_t p);
 /* Execute with a CUDA event around every step; step_ms[i] receives the device
  * time of step i (qs_plan_stats' launch count entries).                       */
 int qs_plan_execute_timed(qs_state_t s, qs_plan_t p, float* step_ms);
+/* Resets the state to the basis state |basis> and runs the plan (run() from
+ * |0...0>, simulator.hpp:147-159): when the plan starts with a tile pass the
+ * reset is fused into it -- that pass writes the state without reading it.
+ * The enqueue form does not wait.                                              */
+int qs_plan_execute_from_basis(qs_state_t s, qs_plan_t p, uint64_t basis);
+int qs_plan_enqueue_from_basis(qs_state_t s, qs_plan_t p, uint64_t basis);
 /* Executes steps [first, first+count) only (diagnostics, per-pass profiling). */
 int qs_plan_execute_range(qs_state_t s, qs_plan_t p, uint64_t first, uint64_t count);
 /* Planner statistics: passes (HBM sweeps) and kernel launches per execute.   */
@@ -246,6 +252,8 @@ int qs_plan_exchanges(qs_plan_t p, uint64_t* exchanges);
 #define QS_MAX_EXCHANGE_BITS 16
 int qs_plan_step_info(qs_plan_t p, uint64_t i, int* kind, uint32_t* nbits, uint32_t* gpos, uint32_t* lpos);
 int qs_shards_plan_enqueue(qs_shards_t s, qs_plan_t p);
+/* Reset to |basis> (global index) fused into the plan's first tile pass; no wait. */
+int qs_shards_plan_enqueue_from_basis(qs_shards_t s, qs_plan_t p, uint64_t basis);
 /* Executes with a CUDA event around every step (step_ms[i], one per step).   */
 int qs_shards_plan_execute_timed(qs_shards_t s, qs_plan_t p, float* step_ms);
 int qs_shards_plan_execute(qs_shards_t s, qs_plan_t p);

@@ -91,6 +91,8 @@ _SIGS = {
     "qs_plan_stats": (C.c_int, [_P, _U64P, _U64P, _U64P]),
     "qs_plan_enqueue": (C.c_int, [_P, _P]),
     "qs_plan_execute_range": (C.c_int, [_P, _P, C.c_uint64, C.c_uint64]),
+    "qs_plan_execute_from_basis": (C.c_int, [_P, _P, C.c_uint64]),
+    "qs_plan_enqueue_from_basis": (C.c_int, [_P, _P, C.c_uint64]),
     "qs_plan_execute_timed": (C.c_int, [_P, _P, C.POINTER(C.c_float)]),
     "qs_stream": (C.c_void_p, [_P]),
     "qs_fuse": (C.c_int, [_GP, C.c_uint64, C.c_uint32, C.c_uint32, C.POINTER(_P)]),
@@ -126,6 +128,7 @@ _SIGS = {
     "qs_plan_exchanges": (C.c_int, [_P, _U64P]),
     "qs_plan_step_info": (C.c_int, [_P, C.c_uint64, C.POINTER(C.c_int), _UP, _UP, _UP]),
     "qs_shards_plan_enqueue": (C.c_int, [_P, _P]),
+    "qs_shards_plan_enqueue_from_basis": (C.c_int, [_P, _P, C.c_uint64]),
     "qs_shards_plan_execute_timed": (C.c_int, [_P, _P, C.POINTER(C.c_float)]),
     "qs_shards_plan_execute": (C.c_int, [_P, _P]),
     "qs_shards_apply_circuit": (C.c_int, [_P, _GP, C.c_uint64]),

@@ -348,6 +348,21 @@ int qs_plan_enqueue(qs_state_t h, qs_plan_t p) {
   });
 }
 
+int qs_plan_enqueue_from_basis(qs_state_t h, qs_plan_t p, uint64_t basis) {
+  return guarded([&] {
+    if (!p) throw ValidationError("null plan");
+    execute_plan_from_basis(st(h), *p->p, basis);
+  });
+}
+
+int qs_plan_execute_from_basis(qs_state_t h, qs_plan_t p, uint64_t basis) {
+  return guarded([&] {
+    if (!p) throw ValidationError("null plan");
+    execute_plan_from_basis(st(h), *p->p, basis);
+    st(h).sync();
+  });
+}
+
 int qs_plan_execute_range(qs_state_t h, qs_plan_t p, uint64_t first, uint64_t count) {
   return guarded([&] {
     if (!p) throw ValidationError("null plan");
@@ -733,6 +748,13 @@ int qs_shards_plan_enqueue(qs_shards_t s, qs_plan_t p) {
   return guarded([&] {
     if (!p) throw ValidationError("null plan");
     shard_execute(sh(s), *p->p);
+  });
+}
+
+int qs_shards_plan_enqueue_from_basis(qs_shards_t s, qs_plan_t p, uint64_t basis) {
+  return guarded([&] {
+    if (!p) throw ValidationError("null plan");
+    shard_execute_from_basis(sh(s), *p->p, basis);
   });
 }
 

@@ -42,6 +42,9 @@ struct Gen {
   uint32_t cur_tq[kTileMaxT] = {};
   int counter = 0;
   bool prefetch = true;
+  // from_basis: the pass starts from the basis state |basis> (kernel
+  // parameter) instead of reading HBM -- the reset fused into the first pass.
+  bool from_basis = false;
   // single_buf: the prefetch buffer doubles as the transpose buffer (64 KiB
   // per CTA, two resident CTAs per SM); the next tile's copies are issued
   // after the last transpose has read the buffer.
@@ -398,7 +401,13 @@ struct Gen {
         if ((p >> k) & 1) loff[p] |= h.load.rs[k];
     }
     // ---- tile-loop body
-    if (prefetch) {
+    if (from_basis) {
+      for (int p = 0; p < 16; ++p) {
+        name[p] = fresh();
+        s << "    const double2 " << name[p] << " = make_double2(((G | " << hexll(loff[p])
+          << ") == basis) ? 1.0 : 0.0, 0.0);\n";
+      }
+    } else if (prefetch) {
       s << "    cp_async_wait_all();\n";
       for (int p = 0; p < 16; ++p) {
         name[p] = fresh();
@@ -446,7 +455,7 @@ struct Gen {
     k << "struct __align__(16) QsbCoef { double2 c[" << std::max<size_t>(1, tp.coef.size() + extra.size()) << "]; };\n";
     k << "extern \"C\" __global__ void __launch_bounds__(" << threads << ", " << minb << ") " << kname
       << "(double2* __restrict__ amps, const unsigned long long rank_base, const unsigned long long lmask,\n"
-      << "    const unsigned long long ntiles, const __grid_constant__ QsbCoef P) {\n";
+      << "    const unsigned long long ntiles, const unsigned long long basis, const __grid_constant__ QsbCoef P) {\n";
     k << "  extern __shared__ double2 sm[];\n";
     k << "  const unsigned tid = threadIdx.x;\n";
     k << "  const unsigned long long TL = 0ull";

@@ -75,6 +75,20 @@ void execute_plan(State& s, const Plan& p) {
   for (const auto& st : p.steps) execute_step(s, st);
 }
 
+void execute_plan_from_basis(State& s, const Plan& p, uint64_t basis) {
+  if (p.n != s.n) throw ValidationError("plan was compiled for a different qubit count");
+  if (p.g != s.g) throw ValidationError("plan was compiled for a sharded state (use the shard API)");
+  if (basis >> s.n) throw ValidationError("basis index out of range");
+  size_t i = 0;
+  if (!p.steps.empty() && p.steps[0].kind == Step::TileStep && !std::getenv("QSB_NO_FUSED_RESET")) {
+    launch_tile(s, *p.steps[0].tile, &basis);
+    i = 1;
+  } else {
+    fill_basis(s, basis);
+  }
+  for (; i < p.steps.size(); ++i) execute_step(s, p.steps[i]);
+}
+
 void execute_step(State& s, const Step& st) {
   switch (st.kind) {
     case Step::OpStep: launch_op(s, st.op); break;

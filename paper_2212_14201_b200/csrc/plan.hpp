@@ -42,6 +42,9 @@ struct Plan {
 std::unique_ptr<Plan> make_plan(uint32_t n, const qs_gate* gates, uint64_t count, uint32_t mode,
                                 uint32_t max_fused_qubits, uint32_t global_qubits = 0);
 void execute_plan(State& s, const Plan& p);
+// Resets to |basis> and runs the plan; when the plan starts with a tile pass
+// the reset is fused into it (no separate write pass, no read of the old state).
+void execute_plan_from_basis(State& s, const Plan& p, uint64_t basis);
 void execute_step(State& s, const Step& st);
 
 }  // namespace qsb

@@ -538,6 +538,22 @@ void shard_execute(ShardSet& ss, const Plan& p, uint64_t first, uint64_t count) 
   }
 }
 
+void shard_execute_from_basis(ShardSet& ss, const Plan& p, uint64_t basis) {
+  if (p.n != ss.n || p.g != ss.g) throw ValidationError("plan was compiled for a different state shape");
+  if (basis >> ss.n) throw ValidationError("basis index out of range");
+  uint64_t first = 0;
+  if (!p.steps.empty() && p.steps[0].kind == Step::TileStep) {
+    for (auto& s : ss.shards) launch_tile(*s, *p.steps[0].tile, &basis);  // global index: one shard holds it
+    first = 1;
+  } else {
+    for (auto& s : ss.shards) {
+      const bool mine = (basis >> s->local_qubits()) == s->rank;
+      fill_basis(*s, mine ? (basis & (s->size - 1)) : ~0ull);
+    }
+  }
+  shard_execute(ss, p, first);
+}
+
 double shard_norm2(ShardSet& ss) {
   std::vector<double> v;
   for (auto& s : ss.shards) v.push_back(reduce_norm2(*s));

@@ -77,6 +77,9 @@ std::unique_ptr<ShardSet> make_dist_shard(uint32_t n, Dist* d);
 
 void shard_fill_basis(ShardSet& ss, uint64_t index);
 void shard_execute(ShardSet& ss, const Plan& p, uint64_t first = 0, uint64_t count = ~0ull);
+// Resets to |basis> (global index) and runs the plan, the reset fused into a
+// leading tile pass.  Enqueued on the shard stream.
+void shard_execute_from_basis(ShardSet& ss, const Plan& p, uint64_t basis);
 double shard_norm2(ShardSet& ss);
 double shard_checksum(ShardSet& ss);
 // Amplitude / probability I/O over [offset, offset+count) of the global index;

@@ -84,6 +84,7 @@ struct TileProgram {
   uint32_t transposes = 0;
   std::vector<uint64_t> source;  // gate indices, for diagnostics
   std::shared_ptr<struct JitModule> jit;  // specialised kernel (jit.hpp)
+  mutable std::shared_ptr<struct JitModule> jit_basis;  // from-basis variant (first pass of a run), lazily built
   std::vector<double2> params;            // kernel parameter table (coef + generator constants)
 };
 
@@ -125,6 +126,8 @@ inline void plan_tiles(uint32_t n, std::vector<Op>& ops, std::vector<Step>& step
   plan_tiles(n, ops, remapped, o);
   steps = remapped.size() < plain.size() ? std::move(remapped) : std::move(plain);
 }
-void launch_tile(State& s, const TileProgram& tp);
+// basis != null: the pass starts from |*basis> (global index) instead of
+// reading the state -- a reset fused into the first pass.
+void launch_tile(State& s, const TileProgram& tp, const uint64_t* basis = nullptr);
 
 }  // namespace qsb

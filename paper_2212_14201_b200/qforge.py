@@ -311,8 +311,13 @@ class CompiledCircuit:
         if h is not None and N._lib is not None:
             N._lib.qs_plan_destroy(h)
 
-    def execute(self, state):
-        N.check(N.lib().qs_plan_execute(state.handle(), self._h))
+    def execute(self, state, from_basis=None):
+        """Runs the plan on `state`; with from_basis=b the state is first reset to
+        |b> (fused into the first pass)."""
+        if from_basis is None:
+            N.check(N.lib().qs_plan_execute(state.handle(), self._h))
+        else:
+            N.check(N.lib().qs_plan_execute_from_basis(state.handle(), self._h, from_basis))
 
     def stats(self):
         a, b, c = N.C.c_uint64(), N.C.c_uint64(), N.C.c_uint64()

@@ -165,7 +165,12 @@ class ShardedState:
         arr, keep = N.gate_array(gates)
         N.check(N.lib().qs_shards_apply_circuit(self._h, arr, len(gates)))
 
-    def execute(self, circuit, sync=True):
+    def execute(self, circuit, sync=True, from_basis=None):
+        if from_basis is not None:
+            N.check(N.lib().qs_shards_plan_enqueue_from_basis(self._h, circuit.handle(), from_basis))
+            if sync:
+                self.sync()
+            return
         f = N.lib().qs_shards_plan_execute if sync else N.lib().qs_shards_plan_enqueue
         N.check(f(self._h, circuit.handle()))
 

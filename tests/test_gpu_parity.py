@@ -239,3 +239,29 @@ def test_tile_path_random_mixed_vs_oracle(n):
         sv = Q.StateVector(n)
         sv.apply_circuit(gates, plan, 3)
         assert np.max(np.abs(sv.amplitudes() - want)) <= AMP_TOL, plan
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("which", ["random", "qft", "hea", "opaque_first"])
+def test_execute_from_basis_matches_reset_then_execute(which):
+    """qs_plan_execute_from_basis (reset fused into the first tile pass) equals
+    reset + execute, for basis states anywhere in the register."""
+    n = 14
+    if which == "opaque_first":  # plan starting with a per-gate kernel: plain reset path
+        rng = np.random.default_rng(2)
+        gates = [Q.make_custom_gate([0, 3, 5, 9], _random_unitary(4, rng))] + Q.gen_random_circuit(n, 2, 3).gates()
+    else:
+        gates = {"random": lambda: Q.gen_random_circuit(n, 5, 11), "qft": lambda: Q.gen_qft(n, 0),
+                 "hea": lambda: Q.gen_hea(n, 3, 5)}[which]().gates()
+    cc = Q.CompiledCircuit(n, gates, plan=N.QS_PLAN_TILED)
+    for b in (0, 1, (1 << n) - 1, 0x1A5B):
+        sv = Q.StateVector(n)
+        sv.reset(b)
+        cc.execute(sv)
+        want = sv.amplitudes()
+        sv2 = Q.StateVector(n)
+        sv2.apply_gate(Q.make_gate(Q.GateKind.H, [3]))  # dirty state: must be overwritten
+        cc.execute(sv2, from_basis=b)
+        assert np.max(np.abs(sv2.amplitudes() - want)) <= 1e-14
+        ref = ol.run_gates(n, gates, state=np.eye(1, 1 << n, b, dtype=np.complex128)[0])
+        assert np.max(np.abs(want - ref)) <= 1e-10

@@ -233,3 +233,19 @@ def test_sharded_sampling_matches_unsharded_30q():
     st = ShardedState.local(n, 3)
     st.apply_circuit(gates)
     assert np.array_equal(st.sample_seeded(5, 100000, exact=True), ref)
+
+
+@pytest.mark.parametrize("g", [1, 3])
+def test_sharded_execute_from_basis(g):
+    n = 15
+    gates = workload("qft", n)
+    circ = ShardedCircuit(n, g, gates)
+    for b in (0, (1 << n) - 1, 0x2C3A):
+        st = ShardedState.local(n, g)
+        st.reset(b)
+        st.execute(circ)
+        want = st.amplitudes()
+        st2 = ShardedState.local(n, g)
+        st2.set_amplitudes(np.full(1 << n, 0.5 + 0.25j), 0)  # dirty: must be overwritten
+        st2.execute(circ, from_basis=b)
+        assert np.max(np.abs(st2.amplitudes() - want)) <= 1e-14
