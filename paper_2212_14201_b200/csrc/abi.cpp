@@ -306,7 +306,7 @@ int qs_apply_circuit(qs_state_t h, const qs_gate* gates, uint64_t n, uint32_t pl
   return guarded([&] {
     State& s = st(h);
     if (n && !gates) throw ValidationError("null gate array");
-    auto p = make_plan(s.n, gates, n, plan, max_fused_qubits);
+    auto p = cached_plan(s.n, gates, n, plan, max_fused_qubits);
     execute_plan(s, *p);
     s.sync();
   });
@@ -770,7 +770,7 @@ int qs_shards_apply_circuit(qs_shards_t s, const qs_gate* gates, uint64_t n) {
   return guarded([&] {
     ShardSet& ss = sh(s);
     if (n && !gates) throw ValidationError("null gate array");
-    auto p = make_plan(ss.n, gates, n, QS_PLAN_TILED, 0, ss.g);
+    auto p = cached_plan(ss.n, gates, n, QS_PLAN_TILED, 0, ss.g);
     shard_execute(ss, *p);
     shard_sync(ss);
   });

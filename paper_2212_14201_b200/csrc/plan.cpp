@@ -1,5 +1,9 @@
 #include "plan.hpp"
 
+#include <list>
+#include <mutex>
+#include <string>
+
 #include "fusion.hpp"
 #include "jit.hpp"
 #include "kernels.hpp"
@@ -67,6 +71,68 @@ std::unique_ptr<Plan> make_plan(uint32_t n, const qs_gate* gates, uint64_t count
     }
   }
   return plan;
+}
+
+// ------------------------------------------------------------- plan cache
+// qs_apply_circuit re-submits the same gate list in loops (benchmarks,
+// repeated runs): plans are cached by the exact bytes of the submission.
+namespace {
+std::string plan_key(uint32_t n, const qs_gate* gates, uint64_t count, uint32_t mode, uint32_t maxk, uint32_t g) {
+  std::string k;
+  auto put = [&](const void* p, size_t b) { k.append(static_cast<const char*>(p), b); };
+  put(&n, 4);
+  put(&mode, 4);
+  put(&maxk, 4);
+  put(&g, 4);
+  put(&count, 8);
+  for (uint64_t i = 0; i < count; ++i) {
+    const qs_gate& q = gates[i];
+    put(&q.kind, 4);
+    put(&q.dagger, 4);
+    put(&q.num_targets, 4);
+    put(&q.num_controls, 4);
+    put(q.targets, 4 * std::min<uint32_t>(q.num_targets, QS_MAX_TARGETS));
+    put(q.controls, 4 * std::min<uint32_t>(q.num_controls, QS_MAX_CONTROLS));
+    put(q.params, sizeof(q.params));
+    if (q.kind == QS_CUSTOM && q.matrix && q.num_targets <= QS_MAX_TARGETS) {
+      const size_t dim = size_t(1) << q.num_targets;
+      put(q.matrix, dim * dim * 2 * sizeof(double));
+    }
+  }
+  return k;
+}
+struct PlanCache {
+  std::mutex mu;
+  std::list<std::pair<std::string, std::shared_ptr<const Plan>>> lru;  // front = most recent
+};
+PlanCache& plan_cache() {
+  static PlanCache c;
+  return c;
+}
+}  // namespace
+
+std::shared_ptr<const Plan> cached_plan(uint32_t n, const qs_gate* gates, uint64_t count, uint32_t mode,
+                                        uint32_t max_fused_qubits, uint32_t global_qubits) {
+  static const bool enabled = [] {
+    const char* e = std::getenv("QSB_PLAN_CACHE");
+    return !e || std::atoi(e) != 0;
+  }();
+  if (!enabled) return make_plan(n, gates, count, mode, max_fused_qubits, global_qubits);
+  const std::string key = plan_key(n, gates, count, mode, max_fused_qubits, global_qubits);
+  PlanCache& c = plan_cache();
+  {
+    std::lock_guard<std::mutex> lk(c.mu);
+    for (auto it = c.lru.begin(); it != c.lru.end(); ++it)
+      if (it->first == key) {
+        c.lru.splice(c.lru.begin(), c.lru, it);
+        return c.lru.front().second;
+      }
+  }
+  std::shared_ptr<const Plan> p = make_plan(n, gates, count, mode, max_fused_qubits, global_qubits);
+  std::lock_guard<std::mutex> lk(c.mu);
+  c.lru.emplace_front(key, p);
+  while (c.lru.size() > 8) c.lru.pop_back();
+  return p;
 }
 
 void execute_plan(State& s, const Plan& p) {

@@ -265,3 +265,24 @@ def test_execute_from_basis_matches_reset_then_execute(which):
         assert np.max(np.abs(sv2.amplitudes() - want)) <= 1e-14
         ref = ol.run_gates(n, gates, state=np.eye(1, 1 << n, b, dtype=np.complex128)[0])
         assert np.max(np.abs(want - ref)) <= 1e-10
+
+
+@pytest.mark.gpu
+def test_plan_cache_keys_on_every_byte():
+    """qs_apply_circuit caches plans by the submitted bytes: a changed angle or
+    custom-matrix entry must not reuse a stale plan."""
+    n = 12
+    rng = np.random.default_rng(8)
+    u = _random_unitary(2, rng)
+    base = Q.gen_random_circuit(n, 3, 4).gates() + [Q.make_custom_gate([2, 7], u)]
+    for variant in range(3):
+        gates = [Q.Gate(kind=g.kind, targets=list(g.targets), params=list(g.params), controls=list(g.controls),
+                        dagger=g.dagger, matrix=None if g.matrix is None else np.array(g.matrix)) for g in base]
+        if variant == 1:
+            gates[5].params = [gates[5].params[0] + 1e-3]
+        if variant == 2:
+            gates[-1].matrix = _random_unitary(2, rng)
+        for _ in range(2):  # second call hits the cache
+            sv = Q.StateVector(n)
+            sv.apply_circuit(gates)
+            assert np.max(np.abs(sv.amplitudes() - ol.run_gates(n, gates))) <= 1e-10
