@@ -442,25 +442,45 @@ struct Gen {
     flush_all(true);
     // Relabels (free SWAPs) make threads store where other threads loaded; with
     // no transpose barrier in the pass, every load must retire before any store.
-    if (ti == 0 && std::memcmp(&h.load, &h.store, sizeof(TileConfigAddr)) != 0) s << "    __syncthreads();\n";
-    for (int p = 0; p < 16; ++p) {
-      unsigned long long off = 0;
-      for (int k = 0; k < 4; ++k)
-        if ((p >> k) & 1) off |= h.store.rs[k];
-      s << "    __stcs(amps + ((G | " << hexll(off) << ") & lmask), " << name[p] << ");\n";
+    if (h.oop) {
+      // out of place through the final qubit permutation: the written index is
+      // sigma(base) | sigma(thread bits) | sigma(register bits)
+      s << "    unsigned long long GO = TLO;\n";
+      for (uint32_t i = 0; i + h.m < h.n; ++i)
+        s << "    if ((tix >> " << i << ") & 1ull) GO |= " << hexll(1ull << h.out_pos[i]) << ";\n";
+      for (int p = 0; p < 16; ++p) {
+        unsigned long long off = 0;
+        for (int k = 0; k < 4; ++k)
+          if ((p >> k) & 1) off |= h.store.rs[k];
+        s << "    __stcs(out + (GO | " << hexll(off) << "), " << name[p] << ");\n";
+      }
+    } else {
+      if (ti == 0 && std::memcmp(&h.load, &h.store, sizeof(TileConfigAddr)) != 0) s << "    __syncthreads();\n";
+      for (int p = 0; p < 16; ++p) {
+        unsigned long long off = 0;
+        for (int k = 0; k < 4; ++k)
+          if ((p >> k) & 1) off |= h.store.rs[k];
+        s << "    __stcs(amps + ((G | " << hexll(off) << ") & lmask), " << name[p] << ");\n";
+      }
     }
 
     // ---- assemble
     std::ostringstream k;
     k << "struct __align__(16) QsbCoef { double2 c[" << std::max<size_t>(1, tp.coef.size() + extra.size()) << "]; };\n";
     k << "extern \"C\" __global__ void __launch_bounds__(" << threads << ", " << minb << ") " << kname
-      << "(double2* __restrict__ amps, const unsigned long long rank_base, const unsigned long long lmask,\n"
+      << "(double2* __restrict__ amps, double2* __restrict__ out, const unsigned long long rank_base,\n"
+      << "    const unsigned long long lmask,\n"
       << "    const unsigned long long ntiles, const unsigned long long basis, const __grid_constant__ QsbCoef P) {\n";
     k << "  extern __shared__ double2 sm[];\n";
     k << "  const unsigned tid = threadIdx.x;\n";
     k << "  const unsigned long long TL = 0ull";
     for (uint32_t b = 0; b < h.t; ++b) k << " | ((unsigned long long)((tid >> " << b << ") & 1u) << " << h.load.tq[b] << ")";
     k << ";\n";
+    if (h.oop) {
+      k << "  const unsigned long long TLO = 0ull";
+      for (uint32_t b = 0; b < h.t; ++b) k << " | ((unsigned long long)((tid >> " << b << ") & 1u) << " << h.store.tq[b] << ")";
+      k << ";\n";
+    }
     k << "  auto base_of = [&](unsigned long long b) {\n";
     for (uint32_t b = 0; b < h.m; ++b) {
       const uint32_t q = h.S[b];

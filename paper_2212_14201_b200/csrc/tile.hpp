@@ -73,6 +73,11 @@ struct TileHeader {
   TileConfigAddr load, store;
   uint32_t ops_off, meta_off, coef_off, bytes;
   unsigned long long ntiles;
+  // Out-of-place pass (the plan's final qubit permutation folded in): stores
+  // go to the second buffer; store addressing above is already permuted and
+  // out_pos[i] is the output bit of tile-index bit i (non-tile qubits, ascending).
+  uint32_t oop = 0;
+  uint8_t out_pos[64] = {};
 };
 
 struct TileProgram {
@@ -104,6 +109,8 @@ struct TileOptions {
   bool perm_step = true;
   // Drop X gates whose flip can be folded into later gates (absorb_pauli_x).
   bool absorb_x = true;
+  // Fold that permutation into the last tile pass when possible (out of place).
+  bool fold_perm = true;
   uint32_t global_qubits = 0;  // sharded states: top qubits are rank bits, never in a tile
 };
 TileOptions tile_options_from_env();

@@ -146,17 +146,25 @@ struct Compiler {
     return false;
   }
 
-  // Fill thread bits: lanes 0..L-1 take tile bits 0..L-1 when those are not
-  // register bits; the rest ascending.
-  void fill_threads(Cfg& c) const {
+  // Tile bit that must sit in lane k (k < L) when the pass stores: its global
+  // position is the k-th lowest of the written index (coalescing).  Identity
+  // unless the pass stores out of place through a qubit permutation.
+  int lane[kTileMaxT] = {0, 1, 2, 3, 4, 5, 6, 7, 8};
+
+  // Fill thread bits: lanes 0..L-1 take the load lanes (tile bits 0..L-1, for
+  // the first configuration) or the store lanes when those are not register
+  // bits; the rest ascending.
+  void fill_threads(Cfg& c, bool load = false) const {
     std::vector<char> used(m, 0);
     for (int k = 0; k < kTileR; ++k) used[c.reg[k]] = 1;
     for (uint32_t k = 0; k < t; ++k) c.thr[k] = -1;
-    for (uint32_t k = 0; k < L; ++k)
-      if (!used[k]) {
-        c.thr[k] = static_cast<int>(k);
-        used[k] = 1;
+    for (uint32_t k = 0; k < L; ++k) {
+      const int y = load ? static_cast<int>(k) : lane[k];
+      if (!used[y]) {
+        c.thr[k] = y;
+        used[y] = 1;
       }
+    }
     uint32_t next = 0;
     for (uint32_t k = 0; k < t; ++k) {
       if (c.thr[k] >= 0) continue;
@@ -168,80 +176,12 @@ struct Compiler {
 
   bool store_ok(const Cfg& c) const {
     for (uint32_t k = 0; k < L; ++k)
-      if (c.thr[k] != static_cast<int>(k)) return false;
+      if (c.thr[k] != lane[k]) return false;
     return true;
   }
 
   // Register requirement of op i: exact positions for DENSE, else one tile bit.
   static bool needs_reg(const POp& p) { return p.k == PK::Mat1 || p.k == PK::Flip || p.k == PK::Dense; }
-
-  // Belady choice of the register set at op index `at` of the pass list.
-  Cfg choose(const Cfg* cur, const std::vector<const POp*>& list, size_t at, bool exclude_low) {
-    Cfg c;
-    for (int k = 0; k < kTileR; ++k) c.reg[k] = -1;
-    std::vector<char> placed(m, 0);
-    const POp& p = *list[at];
-    if (p.k == PK::Dense) {
-      const size_t kd = p.op.targets.size();
-      for (size_t b = 0; b < kd; ++b) {
-        const int x = tb[p.op.targets[kd - 1 - b]];
-        c.reg[b] = x;
-        placed[x] = 1;
-      }
-    } else {
-      const int x = tb[p.op.targets[0]];
-      int pos;
-      if (cur && has_reg(*cur, x, &pos)) c.reg[pos] = x;
-      else
-        for (int k = 0; k < kTileR; ++k)
-          if (c.reg[k] < 0) {
-            c.reg[k] = x;
-            break;
-          }
-      placed[x] = 1;
-    }
-    // next use of every tile bit from `at`
-    std::vector<size_t> next(m, SIZE_MAX);
-    for (size_t j = at; j < list.size(); ++j) {
-      const POp& q = *list[j];
-      if (!needs_reg(q)) continue;
-      for (auto tq : q.op.targets) {
-        const int x = tb[tq];
-        if (next[x] == SIZE_MAX) next[x] = j;
-      }
-    }
-    for (int k = 0; k < kTileR; ++k) {
-      if (c.reg[k] >= 0) continue;
-      // keep the current occupant when it is still useful
-      int best = -1;
-      if (cur) {
-        const int y = cur->reg[k];
-        if (y >= 0 && !placed[y] && next[y] != SIZE_MAX && !(exclude_low && y < static_cast<int>(L))) best = y;
-      }
-      if (best < 0) {
-        size_t bn = SIZE_MAX;
-        for (uint32_t y = 0; y < m; ++y) {
-          if (placed[y] || (exclude_low && y < L)) continue;
-          const size_t ny = next[y];
-          const bool better = best < 0 || ny < bn || (ny == bn && y >= L && best < static_cast<int>(L));
-          if (better) {
-            best = static_cast<int>(y);
-            bn = ny;
-          }
-        }
-      }
-      if (best < 0)  // everything placed (tiny tiles): any free bit
-        for (uint32_t y = 0; y < m; ++y)
-          if (!placed[y]) {
-            best = static_cast<int>(y);
-            break;
-          }
-      c.reg[k] = best;
-      placed[best] = 1;
-    }
-    fill_threads(c);
-    return c;
-  }
 
   void transpose_to(int& cur, const Cfg& next) {
     cfgs.push_back(next);
@@ -359,7 +299,7 @@ struct Compiler {
       c.reg[k] = best;
       placed[best] = 1;
     }
-    fill_threads(c);
+    fill_threads(c, /*load=*/cur == nullptr);  // the first configuration is the (coalesced) load
     return c;
   }
 
@@ -491,10 +431,10 @@ struct Compiler {
     }
     if (!store_ok(cfgs[cur])) {
       Cfg c = cfgs[cur];
-      bool low_in_reg = false;
+      bool lane_in_reg = false;
       for (int k = 0; k < kTileR; ++k)
-        if (c.reg[k] < static_cast<int>(L)) low_in_reg = true;
-      if (low_in_reg) c = default_cfg();
+        if (is_store_lane(c.reg[k])) lane_in_reg = true;
+      if (lane_in_reg) c = default_cfg();
       else fill_threads(c);
       transpose_to(cur, c);
     }
@@ -502,12 +442,18 @@ struct Compiler {
   }
   int final_cfg = 0;
 
+  bool is_store_lane(int y) const {
+    for (uint32_t k = 0; k < L; ++k)
+      if (lane[k] == y) return true;
+    return false;
+  }
+
   Cfg default_cfg() const {
     Cfg c;
-    // registers: the highest tile bits not reserved for lanes
+    // registers: the highest tile bits not reserved for the store lanes
     int k = 0;
     for (int y = static_cast<int>(m) - 1; y >= 0 && k < kTileR; --y)
-      if (y >= static_cast<int>(L) || m - L < kTileR) c.reg[k++] = y;
+      if (!is_store_lane(y) || m - L < kTileR) c.reg[k++] = y;
     fill_threads(c);
     return c;
   }
@@ -544,7 +490,11 @@ Swizzle pick_swizzle(const Cfg& a, const Cfg& b, uint32_t m, uint32_t t) {
   return Swizzle{};  // correct, possibly conflicted
 }
 
-std::shared_ptr<TileProgram> finalize(Compiler& C, uint64_t gates, const std::vector<uint64_t>& srcs) {
+// sigma (optional): the pass stores out of place, bit p of every written index
+// moved to bit sigma[p] (the plan's final layout restore folded into its last
+// pass); the compiler's store lanes must be sigma^-1 of the low positions.
+std::shared_ptr<TileProgram> finalize(Compiler& C, uint64_t gates, const std::vector<uint64_t>& srcs,
+                                      const std::vector<uint32_t>* sigma = nullptr) {
   auto tp = std::make_shared<TileProgram>();
   TileHeader& h = tp->h;
   h.n = C.n;
@@ -552,12 +502,19 @@ std::shared_ptr<TileProgram> finalize(Compiler& C, uint64_t gates, const std::ve
   h.t = C.t;
   for (uint32_t b = 0; b < C.m; ++b) h.S[b] = C.S[b];
   h.ntiles = 1ull << (C.n - C.m);
-  auto addr_of = [&](const Cfg& c, TileConfigAddr& a) {
-    for (uint32_t k = 0; k < C.t; ++k) a.tq[k] = C.S[c.thr[k]];
-    for (int k = 0; k < kTileR; ++k) a.rs[k] = 1ull << C.S[c.reg[k]];
+  auto sg = [&](uint32_t q) { return sigma ? (*sigma)[q] : q; };
+  auto addr_of = [&](const Cfg& c, TileConfigAddr& a, bool out) {
+    for (uint32_t k = 0; k < C.t; ++k) a.tq[k] = out ? sg(C.S[c.thr[k]]) : C.S[c.thr[k]];
+    for (int k = 0; k < kTileR; ++k) a.rs[k] = 1ull << (out ? sg(C.S[c.reg[k]]) : C.S[c.reg[k]]);
   };
-  addr_of(C.cfgs[0], h.load);
-  addr_of(C.cfgs[C.final_cfg], h.store);
+  addr_of(C.cfgs[0], h.load, false);
+  addr_of(C.cfgs[C.final_cfg], h.store, true);
+  if (sigma) {
+    h.oop = 1;
+    uint32_t i = 0;
+    for (uint32_t q = 0; q < C.n; ++q)
+      if (C.tb[q] < 0) h.out_pos[i++] = static_cast<uint8_t>(sg(q));
+  }
 
   auto split_pred = [&](const Cfg& c, uint64_t pred, TOp& o, uint64_t val = ~0ull) {
     o.rmask = 0;
@@ -685,6 +642,7 @@ TileOptions tile_options_from_env() {
   if (const char* e = std::getenv("QSB_TILE_REMAP")) o.remap = std::atoi(e) != 0;
   if (const char* e = std::getenv("QSB_PERM_STEP")) o.perm_step = std::atoi(e) != 0;
   if (const char* e = std::getenv("QSB_ABSORB_X")) o.absorb_x = std::atoi(e) != 0;
+  if (const char* e = std::getenv("QSB_FOLD_PERM")) o.fold_perm = std::atoi(e) != 0;
   o.m = std::max<uint32_t>(8, std::min<uint32_t>(kTileMaxM, o.m));
   o.low = std::min<uint32_t>(5, o.low);
   return o;
@@ -974,7 +932,8 @@ void plan_tiles(uint32_t n, std::vector<Op>& ops, std::vector<Step>& steps, cons
     emit_swaps(pairs);
   };
 
-  auto compile_pass = [&](uint64_t S, const std::vector<const POp*>& list, const std::vector<uint64_t>& srcs) {
+  auto compile_pass = [&](uint64_t S, const std::vector<const POp*>& list, const std::vector<uint64_t>& srcs,
+                          const std::vector<uint32_t>* sigma = nullptr) {
     Compiler C;
     C.n = n;
     C.m = m;
@@ -986,9 +945,18 @@ void plan_tiles(uint32_t n, std::vector<Op>& ops, std::vector<Step>& steps, cons
         C.tb[q] = static_cast<int>(C.S.size());
         C.S.push_back(q);
       }
+    if (sigma)  // store lane k holds the tile bit whose output position is k
+      for (uint32_t k = 0; k < L; ++k)
+        for (uint32_t q = 0; q < n; ++q)
+          if ((*sigma)[q] == k) C.lane[k] = C.tb[q];
     C.compile(list);
-    return finalize(C, list.size(), srcs);
+    return finalize(C, list.size(), srcs, sigma);
   };
+  // inputs of the most recent tile pass (to recompile it storing out of place)
+  uint64_t last_S = 0;
+  std::vector<POp> last_ops;
+  std::vector<uint64_t> last_srcs;
+  std::shared_ptr<TileProgram> last_prog;
   auto push_step = [&](std::shared_ptr<TileProgram> prog, uint64_t S, size_t gates) {
     if (std::getenv("QSB_PLAN_DEBUG")) {
       int counts[16] = {0};
@@ -1131,7 +1099,14 @@ void plan_tiles(uint32_t n, std::vector<Op>& ops, std::vector<Step>& steps, cons
         for (const auto& e : extra) list.push_back(&e);
       }
       prog = compile_pass(S, list, srcs);
-      if (prog->h.bytes <= kTileBlobBytes || take == 1) break;
+      if (prog->h.bytes <= kTileBlobBytes || take == 1) {
+        last_S = S;
+        last_ops.clear();
+        for (auto* op : list) last_ops.push_back(*op);
+        last_srcs = srcs;
+        last_prog = prog;
+        break;
+      }
       take = std::max<size_t>(1, take * 3 / 4);
     }
     if (prog->h.bytes > kTileBlobBytes) throw RuntimeError("tile program for one op exceeds the parameter blob");
@@ -1161,10 +1136,29 @@ void plan_tiles(uint32_t n, std::vector<Op>& ops, std::vector<Step>& steps, cons
     emit_swaps(pairs);
   }
   if (opt.perm_step && opt.global_qubits == 0 && n >= 10 && !identity()) {
-    Step s;
-    s.kind = Step::PermStep;
-    s.perm.assign(inv.begin(), inv.end());  // data at bit p belongs to logical inv[p]
-    steps.push_back(std::move(s));
+    const std::vector<uint32_t> sigma(inv.begin(), inv.end());  // data at bit p belongs to logical inv[p]
+    // Fold into the last tile pass (out-of-place store through sigma) when it
+    // ends the plan and holds the qubits that land on the low output bits.
+    bool folded = false;
+    if (opt.fold_perm && !steps.empty() && steps.back().kind == Step::TileStep && steps.back().tile == last_prog) {
+      bool lanes_in = true;
+      for (uint32_t k = 0; k < L; ++k) lanes_in = lanes_in && ((last_S >> perm[k]) & 1);
+      if (lanes_in) {
+        std::vector<const POp*> list;
+        for (const auto& o : last_ops) list.push_back(&o);
+        auto prog = compile_pass(last_S, list, last_srcs, &sigma);
+        if (prog->h.bytes <= kTileBlobBytes) {
+          steps.back().tile = std::move(prog);
+          folded = true;
+        }
+      }
+    }
+    if (!folded) {
+      Step s;
+      s.kind = Step::PermStep;
+      s.perm = sigma;
+      steps.push_back(std::move(s));
+    }
     for (uint32_t q = 0; q < n; ++q) perm[q] = inv[q] = q;
   }
   while (!identity()) {

@@ -94,6 +94,8 @@ void emu_tile(std::vector<cd>& a, const qsb::TileProgram& tp) {
   std::vector<cd> sm(size_t(1) << h.m);
   std::vector<std::array<cd, 16>> v(T);
   std::vector<uint64_t> G(T);
+  std::vector<cd> outbuf;  // out-of-place pass: written through the final permutation
+  if (h.oop) outbuf.assign(a.size(), cd(0));
   for (uint64_t tile = 0; tile < h.ntiles; ++tile) {
     uint64_t base = tile;
     for (uint32_t b = 0; b < h.m; ++b) {
@@ -204,9 +206,22 @@ void emu_tile(std::vector<cd>& a, const qsb::TileProgram& tp) {
       }
     }
     for (int k = 0; k < 4; ++k) rs[k] = h.store.rs[k];
+    if (h.oop) {
+      uint64_t bo = 0;
+      for (uint32_t i = 0; i + h.m < h.n; ++i)
+        if ((tile >> i) & 1) bo |= 1ull << h.out_pos[i];
+      for (int tid = 0; tid < T; ++tid) {
+        uint64_t go = bo;
+        for (uint32_t k = 0; k < h.t; ++k)
+          if ((tid >> k) & 1) go |= 1ull << h.store.tq[k];
+        for (int p = 0; p < 16; ++p) outbuf[go | regoff(p, rs)] = v[tid][p];
+      }
+      continue;
+    }
     for (int tid = 0; tid < T; ++tid)
       for (int p = 0; p < 16; ++p) a[G[tid] | regoff(p, rs)] = v[tid][p];
   }
+  if (h.oop) a.swap(outbuf);
 }
 
 }  // namespace
