@@ -274,6 +274,8 @@ def main():
     ap.add_argument("--replicas", action="store_true", help="N>1: independent replicas instead of one sharded state")
     ap.add_argument("--local-shards", type=int, default=0, metavar="G",
                     help="N=1 diagnostic: split the state into 2^G shards on this GPU")
+    ap.add_argument("--force-dist", action="store_true",
+                    help="run the distributed (NCCL) code path even at N=1 (smoke test of the N>1 path)")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
 
@@ -288,7 +290,11 @@ def main():
 
     import torch
     import torch.distributed as dist
-    if world > 1:
+    if world > 1 or args.force_dist:
+        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        os.environ.setdefault("MASTER_PORT", "29531")
+        os.environ.setdefault("RANK", "0")
+        os.environ.setdefault("WORLD_SIZE", "1")
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     torch.cuda.set_device(local)
 
@@ -298,7 +304,7 @@ def main():
     p, n = build_program(args.workload)
     gates = p.gates()
     G = len(gates)
-    sharded = world > 1 and not args.replicas
+    sharded = (world > 1 or args.force_dist) and not args.replicas
     if sharded and (world & (world - 1)):
         sharded = False  # amplitude sharding needs a power-of-two world
     if sharded:
@@ -443,7 +449,8 @@ def main():
             "clocks": clk,
         }
         print(json.dumps(line))
-    if world > 1:
+    if dist.is_initialized():
+        del runner  # shards and their communicator go before the process group
         dist.destroy_process_group()
     return 0
 
