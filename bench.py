@@ -169,7 +169,7 @@ class SingleRunner:
         self.arr, self.keep = N.gate_array(gates)
         self.G = len(gates)
         self.cs = N.C.c_double()
-        self.e2e_path = "qs_apply_circuit(host qs_gate array) + qs_checksum"
+        self.e2e_path = "qs_run_circuit(|0..0>, host qs_gate array) + qs_checksum"
 
     def parallelism(self, world):
         return "replicas" if world > 1 else "single"
@@ -190,8 +190,8 @@ class SingleRunner:
         self.N.check(self.L.qs_checksum(self.sv.handle(), self.N.C.byref(self.cs)))
         return self.cs.value
 
-    def apply_host(self):
-        self.N.check(self.L.qs_apply_circuit(self.sv.handle(), self.arr, self.G, self.plan_mode, 3))
+    def apply_host(self):  # run(): reset to |0...0> (fused) + the host gate list
+        self.N.check(self.L.qs_run_circuit(self.sv.handle(), 0, self.arr, self.G, self.plan_mode, 3))
 
     def step_kinds(self):
         return [1] * self.stats["launches"]
@@ -228,7 +228,7 @@ class ShardedRunner:
         self.arr, self.keep = N.gate_array(gates)
         self.G = len(gates)
         self.kinds = [k for k, _, _ in self.sc.steps()]
-        self.e2e_path = "qs_shards_apply_circuit(host qs_gate array) + qs_shards_checksum"
+        self.e2e_path = "qs_shards_set_basis_state + qs_shards_apply_circuit(host qs_gate array) + qs_shards_checksum"
 
     def parallelism(self, world):
         if self.dist:
@@ -250,7 +250,8 @@ class ShardedRunner:
     def checksum(self):
         return self.st.checksum()
 
-    def apply_host(self):
+    def apply_host(self):  # run(): reset to |0...0> + the host gate list
+        self.st.reset(0)
         self.N.check(self.L.qs_shards_apply_circuit(self.st.handle(), self.arr, self.G))
 
     def step_kinds(self):
@@ -370,7 +371,6 @@ def main():
     if not args.no_e2e:
         h2d = N.C.sizeof(N.QsGate) * G
         for _ in range(2):
-            runner.reset()
             runner.apply_host()
         torch.cuda.synchronize()
         if world > 1:
@@ -381,7 +381,6 @@ def main():
         e1 = torch.cuda.Event(enable_timing=True)
         e0.record(stream)
         for _ in range(e_steps):
-            runner.reset()
             runner.apply_host()
             runner.checksum()
         e1.record(stream)

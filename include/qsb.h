@@ -131,6 +131,13 @@ int qs_apply_matrix(qs_state_t s, const uint32_t* targets, uint32_t k, const dou
 int qs_apply_circuit(qs_state_t s, const qs_gate* gates, uint64_t n, uint32_t plan,
                      uint32_t max_fused_qubits);
 
+/* run() semantics: reset to the basis state |basis> and apply gates[0..n)
+ * (StateVector(n) + the gate loop, simulator.hpp:147-159).  The reset is
+ * fused into the first tile pass, which then writes the state without reading
+ * it.                                                                          */
+int qs_run_circuit(qs_state_t s, uint64_t basis, const qs_gate* gates, uint64_t n, uint32_t plan,
+                   uint32_t max_fused_qubits);
+
 /* Compiled circuit handle: plan once, run many times (bench / parameter sweeps). */
 typedef struct qs_plan* qs_plan_t;
 int qs_plan_create(uint32_t num_qubits, const qs_gate* gates, uint64_t n, uint32_t plan,

@@ -85,6 +85,7 @@ _SIGS = {
     "qs_apply_swap": (C.c_int, [_P, C.c_uint32, C.c_uint32, _UP, C.c_uint32]),
     "qs_apply_matrix": (C.c_int, [_P, _UP, C.c_uint32, _DP, _UP, C.c_uint32]),
     "qs_apply_circuit": (C.c_int, [_P, _GP, C.c_uint64, C.c_uint32, C.c_uint32]),
+    "qs_run_circuit": (C.c_int, [_P, C.c_uint64, _GP, C.c_uint64, C.c_uint32, C.c_uint32]),
     "qs_plan_create": (C.c_int, [C.c_uint32, _GP, C.c_uint64, C.c_uint32, C.c_uint32, C.POINTER(_P)]),
     "qs_plan_destroy": (C.c_int, [_P]),
     "qs_plan_execute": (C.c_int, [_P, _P]),

@@ -312,6 +312,17 @@ int qs_apply_circuit(qs_state_t h, const qs_gate* gates, uint64_t n, uint32_t pl
   });
 }
 
+int qs_run_circuit(qs_state_t h, uint64_t basis, const qs_gate* gates, uint64_t n, uint32_t plan,
+                   uint32_t max_fused_qubits) {
+  return guarded([&] {
+    State& s = st(h);
+    if (n && !gates) throw ValidationError("null gate array");
+    auto p = cached_plan(s.n, gates, n, plan, max_fused_qubits);
+    execute_plan_from_basis(s, *p, basis);
+    s.sync();
+  });
+}
+
 int qs_plan_create(uint32_t num_qubits, const qs_gate* gates, uint64_t n, uint32_t plan, uint32_t max_fused_qubits,
                    qs_plan_t* out) {
   return guarded([&] {

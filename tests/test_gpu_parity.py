@@ -286,3 +286,17 @@ def test_plan_cache_keys_on_every_byte():
             sv = Q.StateVector(n)
             sv.apply_circuit(gates)
             assert np.max(np.abs(sv.amplitudes() - ol.run_gates(n, gates))) <= 1e-10
+
+
+@pytest.mark.gpu
+def test_run_circuit_from_basis():
+    """qs_run_circuit = reset to |b> + apply (run() semantics), reset fused."""
+    n = 13
+    gates = Q.gen_qft(n, 0).gates()
+    for b in (0, 77):
+        sv = Q.StateVector(n)
+        sv.apply_gate(Q.make_gate(Q.GateKind.H, [0]))
+        arr, keep = N.gate_array(gates)
+        N.check(N.lib().qs_run_circuit(sv.handle(), b, arr, len(gates), N.QS_PLAN_DEFAULT, 3))
+        ref = ol.run_gates(n, gates, state=np.eye(1, 1 << n, b, dtype=np.complex128)[0])
+        assert np.max(np.abs(sv.amplitudes() - ref)) <= 1e-10
