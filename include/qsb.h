@@ -205,6 +205,17 @@ int qs_sample_seeded(qs_state_t s, uint64_t seed, uint64_t shots, int exact, uin
  * out[2t], out[2t+1] = real and imaginary part of <psi|P_t|psi>.            */
 int qs_expect_pauli(qs_state_t s, const char* letters, uint32_t nterms, double* out);
 
+/* Gradient of <psi|H|psi>, psi = gates[0..count) applied to |0...0>, with
+ * respect to the angle of each slot gate gates[slots[i]] (uncontrolled RX, RY
+ * or RZ): out[i] = dE/dtheta_i -- the value the reference's parameter-shift
+ * rule (E(t+pi/2) - E(t-pi/2)) / 2 yields for these gates
+ * [variational.hpp:139-155].  Computed by adjoint differentiation: one
+ * forward run, lambda = H psi, one backward sweep (2 state vectors resident).
+ * H = sum_t coeffs[t] * P_t, coeffs complex interleaved, letters as in
+ * qs_expect_pauli.  The state is used as workspace and is overwritten.       */
+int qs_gradient(qs_state_t s, const qs_gate* gates, uint64_t count, const uint64_t* slots, uint64_t nslots,
+                const char* letters, const double* coeffs, uint32_t nterms, double* out);
+
 /* BasisSampler's cumulative array cum_i = sum_{j<=i} |a_j|^2 (host copy,
  * 2^n doubles) and its total, computed on the device with the serial-
  * equivalent exact scan: bit-identical to the reference's left-to-right

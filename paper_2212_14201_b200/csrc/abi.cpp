@@ -15,6 +15,12 @@
 #include "kernels.hpp"
 #include "plan.hpp"
 #include "shard.hpp"
+
+namespace qsb {
+void gradient_adjoint(State& s, const qs_gate* gates, uint64_t count, const uint64_t* slots, uint64_t nslots,
+                      const std::vector<uint64_t>& xm, const std::vector<uint64_t>& zm, const std::vector<int>& ny,
+                      const double* coeffs, double* out);  // gradient.cpp
+}
 #include "tile.hpp"
 
 struct qs_state {
@@ -571,6 +577,20 @@ int qs_expect_pauli(qs_state_t h, const char* letters, uint32_t nterms, double* 
     std::vector<int> ny;
     parse_pauli(letters, nterms, s.n, xm, sm, ny);
     expect_pauli(s, xm, sm, ny, out);
+  });
+}
+
+int qs_gradient(qs_state_t h, const qs_gate* gates, uint64_t count, const uint64_t* slots, uint64_t nslots,
+                const char* letters, const double* coeffs, uint32_t nterms, double* out) {
+  return guarded([&] {
+    State& s = st(h);
+    if ((count && !gates) || (nslots && (!slots || !out)) || (nterms && !coeffs))
+      throw ValidationError("null gradient buffers");
+    for (uint64_t i = 0; i < count; ++i) validate_gate(gates[i], s.n);
+    std::vector<uint64_t> xm, zm;
+    std::vector<int> ny;
+    parse_pauli(letters, nterms, s.n, xm, zm, ny);
+    gradient_adjoint(s, gates, count, slots, nslots, xm, zm, ny, coeffs, out);
   });
 }
 

@@ -693,6 +693,19 @@ __global__ void __launch_bounds__(kThreads) k_search_range(const double* __restr
   }
 }
 
+// dst[k] += f * (-1)^popc((k ^ x) & z) * src[k ^ x]: dst += f * P src for the
+// Pauli string (X part x, Z part z; f carries the coefficient and i^#Y).
+__global__ void __launch_bounds__(kThreads) k_pauli_axpy(double2* __restrict__ dst, const double2* __restrict__ src,
+                                                         uint64_t size, uint64_t xmask, uint64_t zmask, double2 f) {
+  for (uint64_t k = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; k < size; k += (uint64_t)gridDim.x * blockDim.x) {
+    const uint64_t j = k ^ xmask;
+    double2 v = src[j];
+    if (__popcll(j & zmask) & 1) v = make_double2(-v.x, -v.y);
+    const double2 d = dst[k];
+    dst[k] = make_double2(fma(f.x, v.x, fma(-f.y, v.y, d.x)), fma(f.x, v.y, fma(f.y, v.x, d.y)));
+  }
+}
+
 // ---------------------------------------------------------- expectation
 // Pauli term whose X part crosses shards: sum_j conj(b[j ^ xl]) a[j] (-1)^popc(j & smask)
 // with b the partner shard (rank ^ X's rank bits).
@@ -1162,6 +1175,13 @@ void sample(State& s, const double* uniforms_host, uint64_t shots, bool exact, u
   QSB_LAUNCHED();
   QSB_CUDA(cudaMemcpyAsync(out_host, dout, shots * 8, cudaMemcpyDeviceToHost, s.stream));
   QSB_CUDA(cudaStreamSynchronize(s.stream));
+}
+
+void pauli_axpy(State& s, double2* dst, const double2* src, uint64_t xmask, uint64_t zmask, double fre, double fim) {
+  DeviceGuard dg(s.device);
+  k_pauli_axpy<<<grid_for(s.size, s.device), kThreads, 0, s.stream>>>(dst, src, s.size, xmask, zmask,
+                                                                      make_double2(fre, fim));
+  QSB_LAUNCHED();
 }
 
 void expect_pauli(State& s, const std::vector<uint64_t>& xmask, const std::vector<uint64_t>& smask,

@@ -67,6 +67,9 @@ void search_range(State& s, const ShardCum& c, const double* total_dev, const do
 void pauli_cross(State& s, const double2* a, const double2* partner, uint64_t size, uint64_t xl, uint64_t smask_local,
                  double* out2);
 
+// dst += f * P src (P = X^x Z^z, f complex incl. i^#Y), over s.size amplitudes.
+void pauli_axpy(State& s, double2* dst, const double2* src, uint64_t xmask, uint64_t zmask, double fre, double fim);
+
 // Exposed for tests of the exact scan (cum must hold s.size doubles on device).
 double exact_cumulative(State& s, double* d_probs, double* d_cum);
 

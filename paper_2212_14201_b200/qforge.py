@@ -635,3 +635,69 @@ def expectation(p, H, opts=None):
     if abs(acc.imag) > 1e-10:
         raise QforgeError("expectation has a non-real residue of %g; operator or state corrupt" % acc.imag)
     return acc.real
+
+
+class ParamCircuit:
+    """variational.hpp:56-130: a gate template with named rotation slots."""
+
+    def __init__(self, qubits, cbits=0):
+        self.tpl = Program(qubits, cbits)
+        self.slots = []  # (body index, name)
+        self.names = []
+
+    def add(self, g, targets=None, params=()):
+        self.tpl.add(g, targets, params)
+        return self
+
+    def add_param(self, kind, target, name):
+        kind = GateKind(kind)
+        if kind not in (GateKind.RX, GateKind.RY, GateKind.RZ):
+            raise QforgeError("parameter '%s' used in a non-rotation position (%s)" % (name, kind.name))
+        self.slots.append((len(self.tpl.body), name))
+        self.tpl.add(kind, [target], [0.0])
+        if name not in self.names:
+            self.names.append(name)
+        return self
+
+    def parameter_names(self):
+        return list(self.names)
+
+    def bind(self, values):
+        import copy
+        p = copy.deepcopy(self.tpl)
+        for idx, name in self.slots:
+            if name not in values:
+                raise ValidationError("parameter '%s' is unbound" % name)
+            p.body[idx].params = [float(values[name])]
+        return p
+
+
+def gradient(pc, H, at, opts=None):
+    """variational.hpp:139-155 values (shift rule) by adjoint differentiation on
+    the GPU: one forward run + one backward sweep for every slot (qs_gradient)."""
+    opts = opts or SimOptions()
+    opts.validate()
+    p = pc.bind(at)
+    if not H.is_hermitian():
+        raise ValidationError("expectation requires a Hermitian operator")
+    if H.num_qubits() > p.qubit_count:
+        raise ValidationError("operator touches qubits beyond the program")
+    if any(not isinstance(ins, Gate) for ins in p.body):
+        raise ValidationError("expectation requires a measurement-free gate program")
+    validate_or_throw(p)
+    arr, keep = N.gate_array(p.body)
+    slots = np.array([idx for idx, _ in pc.slots], dtype=np.uint64)
+    terms = list(H.terms().items())
+    words, coeffs = [], []
+    for key, c in terms:
+        letters = ["I"] * p.qubit_count
+        for q, l in key:
+            letters[q] = l
+        words.append("".join(letters))
+        coeffs += [complex(c).real, complex(c).imag]
+    coeffs = np.array(coeffs if coeffs else [0.0], dtype=np.float64)
+    work = StateVector(p.qubit_count, opts.device)
+    per = np.zeros(max(1, len(slots)), dtype=np.float64)
+    N.check(N.lib().qs_gradient(work.handle(), arr, len(p.body), slots.ctypes.data_as(N._U64P), len(slots),
+                                "".join(words).encode(), N.dptr(coeffs), len(terms), N.dptr(per)))
+    return [float(sum(per[i] for i, (_, nm) in enumerate(pc.slots) if nm == name)) for name in pc.names]

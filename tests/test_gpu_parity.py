@@ -300,3 +300,50 @@ def test_run_circuit_from_basis():
         N.check(N.lib().qs_run_circuit(sv.handle(), b, arr, len(gates), N.QS_PLAN_DEFAULT, 3))
         ref = ol.run_gates(n, gates, state=np.eye(1, 1 << n, b, dtype=np.complex128)[0])
         assert np.max(np.abs(sv.amplitudes() - ref)) <= 1e-10
+
+
+@pytest.mark.gpu
+def test_gradient_single_rotation_and_zero():
+    """variational_test.cpp:241-249, 285-292 analogues."""
+    pc = Q.ParamCircuit(1).add_param(Q.GateKind.RY, 0, "t")
+    g = Q.gradient(pc, Q.PauliOperator({"Z0": 1.0}), {"t": 0.3})
+    assert abs(g[0] + np.sin(0.3)) <= 1e-12
+    pc2 = Q.ParamCircuit(2).add_param(Q.GateKind.RX, 0, "a")
+    assert abs(Q.gradient(pc2, Q.PauliOperator({"Z1": 1.0}), {"a": 1.2})[0]) <= 1e-14
+
+
+@pytest.mark.gpu
+def test_gradient_matches_parameter_shift():
+    """Adjoint gradient == the reference's shift rule (two expectation() runs
+    per slot, variational.hpp:139-155) on a 10-qubit ansatz with shared names,
+    a dagger slot and a Hamiltonian with X/Y/Z terms."""
+    n = 10
+    rng = np.random.default_rng(21)
+    pc = Q.ParamCircuit(n)
+    names = ["a", "b", "c", "d", "e"]
+    for layer in range(3):
+        for q in range(n):
+            pc.add_param([Q.GateKind.RY, Q.GateKind.RZ, Q.GateKind.RX][(q + layer) % 3], q, names[(q * 7 + layer) % 5])
+        for q in range(n - 1):
+            pc.add(Q.GateKind.CNOT, [q, q + 1])
+        pc.add(Q.GateKind.H, [layer])
+    pc.tpl.body[4].dagger = True  # a slot applied as its adjoint
+    words = {}
+    for _ in range(9):
+        w = " ".join("%s%d" % (rng.choice(list("XYZ")), q) for q in sorted(rng.choice(n, 3, replace=False)))
+        words[w] = float(rng.normal())
+    H = Q.PauliOperator(words)
+    at = {nm: float(rng.uniform(0, 6.28)) for nm in names}
+    got = Q.gradient(pc, H, at)
+    want = []
+    for nm in pc.parameter_names():
+        acc = 0.0
+        for idx, (bi, sn) in enumerate(pc.slots):
+            if sn != nm:
+                continue
+            for sgn in (1, -1):
+                p = pc.bind(at)
+                p.body[bi].params = [p.body[bi].params[0] + sgn * np.pi / 2]
+                acc += 0.5 * sgn * Q.expectation(p, H)
+        want.append(acc)
+    assert np.max(np.abs(np.array(got) - np.array(want))) <= 1e-10
