@@ -144,7 +144,11 @@ struct Gen {
   bool mat1_factored(const TOp& o) {
     if (o.rmask != 0 || o.gmask != 0) return false;
     const cd m[4] = {coefv(o.coef), coefv(o.coef + 1), coefv(o.coef + 2), coefv(o.coef + 3)};
-    const cd f = std::abs(m[0]) >= std::abs(m[1]) ? m[0] : m[1];
+    // Pivot on the diagonal unless it is tiny: the generated code then does not
+    // depend on the rotation angle (parameter sweeps reuse compiled passes);
+    // the pending scale Kg is applied at the end of each pass, so the bounded
+    // growth (< 2^10 per gate) cannot overflow.
+    const cd f = std::abs(m[0]) >= 0x1p-10 * std::abs(m[1]) ? m[0] : m[1];
     if (f == cd(0)) return false;
     const cd n[4] = {m[0] / f, m[1] / f, m[2] / f, m[3] / f};
     auto unit = [](cd v) { return v.imag() == 0.0 && (v.real() == 1.0 || v.real() == -1.0); };
