@@ -205,6 +205,13 @@ int qs_sample_seeded(qs_state_t s, uint64_t seed, uint64_t shots, int exact, uin
  * out[2t], out[2t+1] = real and imaginary part of <psi|P_t|psi>.            */
 int qs_expect_pauli(qs_state_t s, const char* letters, uint32_t nterms, double* out);
 
+/* Reduced density matrix of 1..3 qubits (most significant first):
+ * out[r][c] = sum over the other qubits of a[.. r ..] conj(a[.. c ..]),
+ * 2^k x 2^k complex row-major interleaved.  One read pass.  The trajectory
+ * noise step takes every Kraus weight ||K_i psi||^2 = Tr(K_i rho K_i^dag)
+ * from it instead of one state copy per operator  [noise.hpp:259-311]. */
+int qs_reduced_density(qs_state_t s, const uint32_t* qubits, uint32_t k, double* out);
+
 /* Gradient of <psi|H|psi>, psi = gates[0..count) applied to |0...0>, with
  * respect to the angle of each slot gate gates[slots[i]] (uncontrolled RX, RY
  * or RZ): out[i] = dE/dtheta_i -- the value the reference's parameter-shift

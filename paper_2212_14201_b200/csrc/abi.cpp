@@ -580,6 +580,13 @@ int qs_expect_pauli(qs_state_t h, const char* letters, uint32_t nterms, double* 
   });
 }
 
+int qs_reduced_density(qs_state_t h, const uint32_t* qubits, uint32_t k, double* out) {
+  return guarded([&] {
+    if (!qubits || !out) throw ValidationError("null buffer");
+    reduced_density(st(h), qubits, k, out);
+  });
+}
+
 int qs_gradient(qs_state_t h, const qs_gate* gates, uint64_t count, const uint64_t* slots, uint64_t nslots,
                 const char* letters, const double* coeffs, uint32_t nterms, double* out) {
   return guarded([&] {

@@ -693,6 +693,54 @@ __global__ void __launch_bounds__(kThreads) k_search_range(const double* __restr
   }
 }
 
+// Reduced density matrix of qubits targets (msb first, local bit b <->
+// targets[K-1-b]): rho[r][c] = sum_rest a[rest|r] conj(a[rest|c]).  One read
+// pass; per-block partials (D*D complex) summed in block order afterwards.
+template <int K>
+__global__ void __launch_bounds__(kThreads) k_reduced_density(const double2* __restrict__ a, uint64_t groups, Slots sl,
+                                                              TargetMasks tm, double2* __restrict__ partial) {
+  constexpr int D = 1 << K;
+  __shared__ double sh[kThreads / 32];
+  double re[D * D], im[D * D];
+#pragma unroll
+  for (int i = 0; i < D * D; ++i) re[i] = im[i] = 0;
+  for (uint64_t g = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; g < groups; g += (uint64_t)gridDim.x * blockDim.x) {
+    const uint64_t base = deposit(g, sl);
+    double2 v[D];
+#pragma unroll
+    for (int r = 0; r < D; ++r) {
+      uint64_t off = 0;
+#pragma unroll
+      for (int b = 0; b < K; ++b)
+        if ((r >> b) & 1) off |= tm.m[b];
+      v[r] = a[base | off];
+    }
+#pragma unroll
+    for (int r = 0; r < D; ++r)
+#pragma unroll
+      for (int c = 0; c < D; ++c) {  // v_r * conj(v_c)
+        re[r * D + c] = fma(v[r].x, v[c].x, fma(v[r].y, v[c].y, re[r * D + c]));
+        im[r * D + c] = fma(v[r].y, v[c].x, fma(-v[r].x, v[c].y, im[r * D + c]));
+      }
+  }
+  for (int i = 0; i < D * D; ++i) {
+    const double tr = block_sum(re[i], sh);
+    const double ti = block_sum(im[i], sh);
+    if (threadIdx.x == 0) partial[(uint64_t)blockIdx.x * D * D + i] = make_double2(tr, ti);
+  }
+}
+
+__global__ void k_sum_partials(const double2* __restrict__ partial, int blocks, int width, double2* __restrict__ out) {
+  const int i = threadIdx.x;
+  if (i >= width) return;
+  double re = 0, im = 0;
+  for (int b = 0; b < blocks; ++b) {
+    re += partial[(uint64_t)b * width + i].x;
+    im += partial[(uint64_t)b * width + i].y;
+  }
+  out[i] = make_double2(re, im);
+}
+
 // dst[k] += f * (-1)^popc((k ^ x) & z) * src[k ^ x]: dst += f * P src for the
 // Pauli string (X part x, Z part z; f carries the coefficient and i^#Y).
 __global__ void __launch_bounds__(kThreads) k_pauli_axpy(double2* __restrict__ dst, const double2* __restrict__ src,
@@ -1174,6 +1222,33 @@ void sample(State& s, const double* uniforms_host, uint64_t shots, bool exact, u
   k_search<<<grid_for(shots, s.device), kThreads, 0, s.stream>>>(b.cum, s.size, b.total, du, shots, dout);
   QSB_LAUNCHED();
   QSB_CUDA(cudaMemcpyAsync(out_host, dout, shots * 8, cudaMemcpyDeviceToHost, s.stream));
+  QSB_CUDA(cudaStreamSynchronize(s.stream));
+}
+
+void reduced_density(State& s, const uint32_t* targets, uint32_t k, double* out) {
+  if (k < 1 || k > 3) throw ValidationError("reduced density matrix supports 1 to 3 qubits");
+  std::vector<uint32_t> tg(targets, targets + k);
+  for (auto q : tg)
+    if (q >= s.local_qubits()) throw ValidationError("reduced density: qubit out of range");
+  const Slots sl = make_slots(tg, {});
+  if (sl.count != k) throw ValidationError("reduced density: repeated qubit");
+  TargetMasks tm{};
+  for (uint32_t b = 0; b < k; ++b) tm.m[b] = 1ull << tg[k - 1 - b];
+  const uint64_t groups = 1ull << (s.local_qubits() - k);
+  const int width = 1 << (2 * k);
+  const int blocks = static_cast<int>(std::min<uint64_t>(kRedBlocks / 4, std::max<uint64_t>(1, groups / kThreads)));
+  DeviceGuard dg(s.device);
+  double2* part = static_cast<double2*>(s.get_scratch((static_cast<size_t>(blocks) + 1) * width * sizeof(double2)));
+  double2* res = part + static_cast<size_t>(blocks) * width;
+  switch (k) {
+    case 1: k_reduced_density<1><<<blocks, kThreads, 0, s.stream>>>(s.amps, groups, sl, tm, part); break;
+    case 2: k_reduced_density<2><<<blocks, kThreads, 0, s.stream>>>(s.amps, groups, sl, tm, part); break;
+    default: k_reduced_density<3><<<blocks, kThreads, 0, s.stream>>>(s.amps, groups, sl, tm, part); break;
+  }
+  QSB_LAUNCHED();
+  k_sum_partials<<<1, 64, 0, s.stream>>>(part, blocks, width, res);
+  QSB_LAUNCHED();
+  QSB_CUDA(cudaMemcpyAsync(out, res, width * sizeof(double2), cudaMemcpyDeviceToHost, s.stream));
   QSB_CUDA(cudaStreamSynchronize(s.stream));
 }
 

@@ -67,6 +67,10 @@ void search_range(State& s, const ShardCum& c, const double* total_dev, const do
 void pauli_cross(State& s, const double2* a, const double2* partner, uint64_t size, uint64_t xl, uint64_t smask_local,
                  double* out2);
 
+// Reduced density matrix over 1..3 qubits (msb first): out = 2^k x 2^k
+// complex, row-major interleaved (host, synchronous).
+void reduced_density(State& s, const uint32_t* targets, uint32_t k, double* out);
+
 // dst += f * P src (P = X^x Z^z, f complex incl. i^#Y), over s.size amplitudes.
 void pauli_axpy(State& s, double2* dst, const double2* src, uint64_t xmask, uint64_t zmask, double fre, double fim);
 

@@ -32,6 +32,29 @@ class NonTerminationGuard : public Error {
   using Error::Error;
 };
 
+// Text-format failures (noise configs here; same kinds as error.hpp:50-86).
+enum class ParseErrorKind { Syntax, UnknownMnemonic, ArityError, RangeError, UnterminatedBlock };
+
+inline const char* parse_error_kind_name(ParseErrorKind k) {
+  constexpr const char* names[] = {"Syntax", "UnknownMnemonic", "ArityError", "RangeError", "UnterminatedBlock"};
+  const auto i = static_cast<unsigned>(k);
+  return i < 5 ? names[i] : "?";
+}
+
+// line / column are 1-based; column 0 = the whole line.
+class ParseError : public Error {
+ public:
+  ParseError(ParseErrorKind k, std::uint32_t ln, std::uint32_t col, const std::string& msg)
+      : Error(std::string(parse_error_kind_name(k)) + " at line " + std::to_string(ln) +
+              (col ? ":" + std::to_string(col) : std::string()) + ": " + msg),
+        kind(k),
+        line(ln),
+        column(col) {}
+  ParseErrorKind kind;
+  std::uint32_t line;
+  std::uint32_t column;
+};
+
 namespace detail {
 // Converts a libqsb status into the matching qforge exception.
 inline void qs_check(int rc) {

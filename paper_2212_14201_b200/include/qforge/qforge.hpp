@@ -9,6 +9,7 @@
 #include "qforge/fusion.hpp"
 #include "qforge/gates.hpp"
 #include "qforge/linalg.hpp"
+#include "qforge/noise.hpp"
 #include "qforge/pauli.hpp"
 #include "qforge/rng.hpp"
 #include "qforge/simulator.hpp"

@@ -7,6 +7,7 @@
 #pragma once
 
 #include <cstdint>
+#include <functional>
 #include <map>
 #include <optional>
 #include <string>
@@ -68,10 +69,25 @@ inline bool trailing_measure_form(const Program& p) {
 }
 
 // Per-shot executor for programs with mid-circuit measurement / control flow.
+// Optional hooks (noise.hpp): gates for which `noisy` holds run one at a time
+// followed by `after_gate`; the others keep batching into planned runs;
+// `readout` maps each collapsed outcome to the recorded bit.
 class ShotExecutor {
  public:
-  ShotExecutor(const Program& p, const SimOptions& o, Rng rng)
-      : opts_(o), rng_(std::move(rng)), sv_(p.qubit_count), cbits_(p.cbit_count, 0) {}
+  using GateHook = std::function<void(const Gate&, StateVector&, Rng&)>;
+  using ReadoutHook = std::function<std::int64_t(std::uint32_t, std::int64_t, Rng&)>;
+
+  // `sv` is reused across shots (reset to |0...0> here): no allocation per shot.
+  ShotExecutor(const Program& p, const SimOptions& o, Rng rng, StateVector& sv)
+      : opts_(o), rng_(std::move(rng)), sv_(sv), cbits_(p.cbit_count, 0) {
+    sv_.reset_to_zero();
+  }
+
+  void set_gate_hook(std::function<bool(const Gate&)> noisy, GateHook after) {
+    noisy_ = std::move(noisy);
+    after_ = std::move(after);
+  }
+  void set_readout(ReadoutHook r) { readout_ = std::move(r); }
 
   void exec(const Program& p) {
     std::vector<Gate> pending;
@@ -82,12 +98,19 @@ class ShotExecutor {
     };
     for (const auto& ins : p.body) {
       if (const auto* g = std::get_if<GateOp>(&ins)) {
-        pending.push_back(g->gate);
+        if (noisy_ && noisy_(g->gate)) {
+          drain();
+          sv_.apply_gate(g->gate);
+          after_(g->gate, sv_, rng_);
+        } else {
+          pending.push_back(g->gate);
+        }
         continue;
       }
       drain();
       if (const auto* m = std::get_if<MeasureOp>(&ins)) {
-        cbits_[m->cbit] = sv_.measure_collapse(m->qubit, rng_.uniform());
+        const std::int64_t o = sv_.measure_collapse(m->qubit, rng_.uniform());
+        cbits_[m->cbit] = readout_ ? readout_(m->qubit, o, rng_) : o;
       } else if (const auto* f = std::get_if<IfOp>(&ins)) {
         if (f->condition.evaluate(cbits_) != 0) exec(*f->then_body);
         else if (f->else_body) exec(*f->else_body);
@@ -110,8 +133,11 @@ class ShotExecutor {
  private:
   const SimOptions& opts_;
   Rng rng_;
-  StateVector sv_;
+  StateVector& sv_;
   std::vector<std::int64_t> cbits_;
+  std::function<bool(const Gate&)> noisy_;
+  GateHook after_;
+  ReadoutHook readout_;
 };
 
 }  // namespace detail
@@ -157,12 +183,13 @@ inline RunResult run(const Program& p, const SimOptions& opts = {}, std::uint64_
     return result;
   }
   const std::uint64_t runs = shots > 0 ? shots : 1;
+  StateVector sv(p.qubit_count);
   for (std::uint64_t s = 0; s < runs; ++s) {
-    detail::ShotExecutor ex(p, opts, Rng::derive(opts.seed, s));
+    detail::ShotExecutor ex(p, opts, Rng::derive(opts.seed, s), sv);
     ex.exec(p);
     if (shots > 0) ++result.counts[detail::cbit_key(ex.cbits())];
-    if (s + 1 == runs) result.final_state = std::move(ex.state());
   }
+  result.final_state = std::move(sv);
   return result;
 }
 

@@ -168,6 +168,11 @@ class StateVector {
     detail::qs_check(qs_norm2(h_->h, &v));
     return v;
   }
+  // Back to |0...0> on the device (extension: per-shot executors reuse one state).
+  void reset_to_zero() {
+    device_op();
+    detail::qs_check(qs_reset(h_->h));
+  }
   void scale(cdouble f) {
     device_op();
     detail::qs_check(qs_scale(h_->h, f.real(), f.imag()));
