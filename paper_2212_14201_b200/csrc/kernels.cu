@@ -696,14 +696,16 @@ __global__ void __launch_bounds__(kThreads) k_search_range(const double* __restr
 // Reduced density matrix of qubits targets (msb first, local bit b <->
 // targets[K-1-b]): rho[r][c] = sum_rest a[rest|r] conj(a[rest|c]).  One read
 // pass; per-block partials (D*D complex) summed in block order afterwards.
-template <int K>
+// R = rows accumulated per launch (row0 .. row0+R-1): all D for K <= 2, one
+// row at a time for K = 3 (keeps the accumulators in registers).
+template <int K, int R>
 __global__ void __launch_bounds__(kThreads) k_reduced_density(const double2* __restrict__ a, uint64_t groups, Slots sl,
-                                                              TargetMasks tm, double2* __restrict__ partial) {
+                                                              TargetMasks tm, int row0, double2* __restrict__ partial) {
   constexpr int D = 1 << K;
   __shared__ double sh[kThreads / 32];
-  double re[D * D], im[D * D];
+  double re[R * D], im[R * D];
 #pragma unroll
-  for (int i = 0; i < D * D; ++i) re[i] = im[i] = 0;
+  for (int i = 0; i < R * D; ++i) re[i] = im[i] = 0;
   for (uint64_t g = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; g < groups; g += (uint64_t)gridDim.x * blockDim.x) {
     const uint64_t base = deposit(g, sl);
     double2 v[D];
@@ -716,17 +718,24 @@ __global__ void __launch_bounds__(kThreads) k_reduced_density(const double2* __r
       v[r] = a[base | off];
     }
 #pragma unroll
-    for (int r = 0; r < D; ++r)
+    for (int rr = 0; rr < R; ++rr) {
+      double2 vr = v[rr];
+      if constexpr (R < D) {  // rows picked at run time: select without dynamic indexing
+#pragma unroll
+        for (int c = 0; c < D; ++c)
+          if (c == row0 + rr) vr = v[c];
+      }
 #pragma unroll
       for (int c = 0; c < D; ++c) {  // v_r * conj(v_c)
-        re[r * D + c] = fma(v[r].x, v[c].x, fma(v[r].y, v[c].y, re[r * D + c]));
-        im[r * D + c] = fma(v[r].y, v[c].x, fma(-v[r].x, v[c].y, im[r * D + c]));
+        re[rr * D + c] = fma(vr.x, v[c].x, fma(vr.y, v[c].y, re[rr * D + c]));
+        im[rr * D + c] = fma(vr.y, v[c].x, fma(-vr.x, v[c].y, im[rr * D + c]));
       }
+    }
   }
-  for (int i = 0; i < D * D; ++i) {
+  for (int i = 0; i < R * D; ++i) {
     const double tr = block_sum(re[i], sh);
     const double ti = block_sum(im[i], sh);
-    if (threadIdx.x == 0) partial[(uint64_t)blockIdx.x * D * D + i] = make_double2(tr, ti);
+    if (threadIdx.x == 0) partial[(uint64_t)blockIdx.x * D * D + row0 * D + i] = make_double2(tr, ti);
   }
 }
 
@@ -781,28 +790,51 @@ __global__ void __launch_bounds__(kThreads) k_pauli2(const double2* __restrict__
   if (threadIdx.x == 0) partial[blockIdx.x] = make_double2(tr, ti);
 }
 
-__global__ void __launch_bounds__(kThreads) k_pauli(const double2* __restrict__ a, uint64_t size, uint64_t xmask,
-                                                    uint64_t smask, double2* __restrict__ partial) {
+// Pauli terms sharing one X mask in one read pass: v_j = conj(a[j^x]) a[j]
+// once, accumulated under each term's Z sign.  partial[block][t].
+constexpr int kPauliGroup = 8;
+struct ZMasks {
+  unsigned long long z[kPauliGroup];
+};
+__global__ void __launch_bounds__(kThreads) k_pauli_group(const double2* __restrict__ a, uint64_t size, uint64_t xmask,
+                                                          ZMasks zm, int T, double2* __restrict__ partial) {
   __shared__ double sh[kThreads / 32];
   const uint64_t chunk = (size + gridDim.x - 1) / gridDim.x;
   const uint64_t lo = blockIdx.x * chunk, hi = min(size, lo + chunk);
-  double re = 0, im = 0;
+  double re[kPauliGroup], im[kPauliGroup];
+#pragma unroll
+  for (int t = 0; t < kPauliGroup; ++t) re[t] = im[t] = 0;
   for (uint64_t j = lo + threadIdx.x; j < hi; j += blockDim.x) {
     const double2 x = a[j];
     const double2 y = xmask ? a[j ^ xmask] : x;
-    // conj(y) * x * sign(j)
-    double pr = fma(y.x, x.x, y.y * x.y);
-    double pi = fma(y.x, x.y, -y.y * x.x);
-    if (__popcll(j & smask) & 1) {
-      pr = -pr;
-      pi = -pi;
+    const double pr = fma(y.x, x.x, y.y * x.y);
+    const double pi = fma(y.x, x.y, -y.y * x.x);
+#pragma unroll
+    for (int t = 0; t < kPauliGroup; ++t) {
+      if (t >= T) break;
+      const bool neg = __popcll(j & zm.z[t]) & 1;
+      re[t] += neg ? -pr : pr;
+      im[t] += neg ? -pi : pi;
     }
-    re += pr;
-    im += pi;
+  }
+  for (int t = 0; t < T; ++t) {
+    const double tr = block_sum(re[t], sh);
+    const double ti = block_sum(im[t], sh);
+    if (threadIdx.x == 0) partial[(uint64_t)blockIdx.x * kPauliGroup + t] = make_double2(tr, ti);
+  }
+}
+
+__global__ void k_finalize2_strided(const double2* __restrict__ partial, int count, int stride,
+                                    double2* __restrict__ out) {
+  __shared__ double sh[kThreads / 32];
+  double re = 0, im = 0;
+  for (int i = threadIdx.x; i < count; i += blockDim.x) {
+    re += partial[(uint64_t)i * stride].x;
+    im += partial[(uint64_t)i * stride].y;
   }
   const double tr = block_sum(re, sh);
   const double ti = block_sum(im, sh);
-  if (threadIdx.x == 0) partial[blockIdx.x] = make_double2(tr, ti);
+  if (threadIdx.x == 0) *out = make_double2(tr, ti);
 }
 
 __global__ void k_finalize2(const double2* __restrict__ partial, int count, double2* __restrict__ out) {
@@ -1241,11 +1273,21 @@ void reduced_density(State& s, const uint32_t* targets, uint32_t k, double* out)
   double2* part = static_cast<double2*>(s.get_scratch((static_cast<size_t>(blocks) + 1) * width * sizeof(double2)));
   double2* res = part + static_cast<size_t>(blocks) * width;
   switch (k) {
-    case 1: k_reduced_density<1><<<blocks, kThreads, 0, s.stream>>>(s.amps, groups, sl, tm, part); break;
-    case 2: k_reduced_density<2><<<blocks, kThreads, 0, s.stream>>>(s.amps, groups, sl, tm, part); break;
-    default: k_reduced_density<3><<<blocks, kThreads, 0, s.stream>>>(s.amps, groups, sl, tm, part); break;
+    case 1:
+      k_reduced_density<1, 2><<<blocks, kThreads, 0, s.stream>>>(s.amps, groups, sl, tm, 0, part);
+      QSB_LAUNCHED();
+      break;
+    case 2:
+      k_reduced_density<2, 4><<<blocks, kThreads, 0, s.stream>>>(s.amps, groups, sl, tm, 0, part);
+      QSB_LAUNCHED();
+      break;
+    default:
+      for (int r = 0; r < 8; ++r) {
+        k_reduced_density<3, 1><<<blocks, kThreads, 0, s.stream>>>(s.amps, groups, sl, tm, r, part);
+        QSB_LAUNCHED();
+      }
+      break;
   }
-  QSB_LAUNCHED();
   k_sum_partials<<<1, 64, 0, s.stream>>>(part, blocks, width, res);
   QSB_LAUNCHED();
   QSB_CUDA(cudaMemcpyAsync(out, res, width * sizeof(double2), cudaMemcpyDeviceToHost, s.stream));
@@ -1263,13 +1305,32 @@ void expect_pauli(State& s, const std::vector<uint64_t>& xmask, const std::vecto
                   const std::vector<int>& ny, double* out) {
   DeviceGuard dg(s.device);
   const size_t T = xmask.size();
-  double2* part = static_cast<double2*>(s.get_scratch((kRedBlocks + T) * sizeof(double2)));
-  double2* res = part + kRedBlocks;
-  for (size_t t = 0; t < T; ++t) {
-    k_pauli<<<kRedBlocks, kThreads, 0, s.stream>>>(s.amps, s.size, xmask[t], smask[t], part);
+  // terms grouped by X mask (first-appearance order), up to kPauliGroup per pass
+  std::vector<std::vector<size_t>> groups;
+  {
+    std::vector<uint64_t> keys;
+    for (size_t t = 0; t < T; ++t) {
+      size_t g = 0;
+      while (g < keys.size() && (keys[g] != xmask[t] || groups[g].size() == kPauliGroup)) ++g;
+      if (g == keys.size()) {
+        keys.push_back(xmask[t]);
+        groups.emplace_back();
+      }
+      groups[g].push_back(t);
+    }
+  }
+  const uint32_t blocks = kRedBlocks / 2;
+  double2* part = static_cast<double2*>(s.get_scratch((static_cast<size_t>(blocks) * kPauliGroup + T) * sizeof(double2)));
+  double2* res = part + static_cast<size_t>(blocks) * kPauliGroup;
+  for (const auto& g : groups) {
+    ZMasks zm{};
+    for (size_t i = 0; i < g.size(); ++i) zm.z[i] = smask[g[i]];
+    k_pauli_group<<<blocks, kThreads, 0, s.stream>>>(s.amps, s.size, xmask[g[0]], zm, static_cast<int>(g.size()), part);
     QSB_LAUNCHED();
-    k_finalize2<<<1, kThreads, 0, s.stream>>>(part, kRedBlocks, res + t);
-    QSB_LAUNCHED();
+    for (size_t i = 0; i < g.size(); ++i) {
+      k_finalize2_strided<<<1, kThreads, 0, s.stream>>>(part + i, static_cast<int>(blocks), kPauliGroup, res + g[i]);
+      QSB_LAUNCHED();
+    }
   }
   std::vector<double2> h(T);
   QSB_CUDA(cudaMemcpyAsync(h.data(), res, T * sizeof(double2), cudaMemcpyDeviceToHost, s.stream));

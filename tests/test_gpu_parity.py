@@ -347,3 +347,37 @@ def test_gradient_matches_parameter_shift():
                 acc += 0.5 * sgn * Q.expectation(p, H)
         want.append(acc)
     assert np.max(np.abs(np.array(got) - np.array(want))) <= 1e-10
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("k", [1, 2, 3])
+def test_reduced_density_matches_numpy(k):
+    n = 11
+    st = Q.StateVector(n)
+    st.apply_circuit(Q.gen_random_circuit(n, 3, 5).gates())
+    a = st.amplitudes()
+    qs = [7, 2, 9][:k]
+    out = np.empty(2 * (1 << (2 * k)))
+    N.check(N.lib().qs_reduced_density(st.handle(), (N.C.c_uint32 * k)(*qs), k, N.dptr(out)))
+    rho = out.view(np.complex128).reshape(1 << k, 1 << k)
+    psi = a.reshape([2] * n)  # axis i <-> qubit n-1-i
+    axes = [n - 1 - q for q in qs]
+    rest = [i for i in range(n) if i not in axes]
+    m = np.transpose(psi, axes + rest).reshape(1 << k, -1)  # row index bits: qubits msb first
+    assert np.max(np.abs(rho - m @ m.conj().T)) <= 1e-13
+
+
+@pytest.mark.gpu
+def test_grouped_pauli_terms_match_oracle():
+    n = 12
+    st = Q.StateVector(n)
+    gates = Q.gen_random_circuit(n, 4, 17).gates()
+    st.apply_circuit(gates)
+    a = st.amplitudes()
+    rng = np.random.default_rng(3)
+    words = ["".join(rng.choice(list("IZ"), size=n)) for _ in range(11)]  # one X group (x = 0)
+    words += ["I" * 3 + "X" + "I" * (n - 4)] * 3 + ["Y" + "Z" * (n - 1), "X" * n, "I" * n]
+    got = st.expect_pauli(words)
+    for w, v in zip(words, got):
+        re, im = ol.expectation(a, n, [(w, 1.0)])
+        assert abs(v.real - re) <= 1e-12 and abs(v.imag - im) <= 1e-12
