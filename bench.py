@@ -113,12 +113,13 @@ def ncu_traffic(workload, plan):
     committed ncu --set full capture (profiles/), per launch; None if absent."""
     if workload != "random30" or plan != "tiled":
         return None
-    try:
-        with open(os.path.join(ROOT, "profiles", "r1", "ncu_full_tile30.json")) as f:
-            d = json.load(f)
-        rd = float(d["dram__bytes_read.sum"][0]) * {"Gbyte": 1e9, "Mbyte": 1e6}[d["dram__bytes_read.sum"][1]]
-        wr = float(d["dram__bytes_write.sum"][0]) * {"Gbyte": 1e9, "Mbyte": 1e6}[d["dram__bytes_write.sum"][1]]
-        return rd + wr
+    try:  # passes 1-3 of the current plan, one `ncu --set full` capture; average per launch
+        with open(os.path.join(ROOT, "profiles", "r1", "ncu_full_random30_passes1-3.json")) as f:
+            rows = json.load(f)
+        scale = {"Gbyte": 1e9, "Mbyte": 1e6}
+        tot = [float(d["dram__bytes_read.sum"][0]) * scale[d["dram__bytes_read.sum"][1]] +
+               float(d["dram__bytes_write.sum"][0]) * scale[d["dram__bytes_write.sum"][1]] for d in rows]
+        return sum(tot) / len(tot)
     except Exception:
         return None
 
