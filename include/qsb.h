@@ -88,7 +88,10 @@ int qs_destroy(qs_state_t s);
 int qs_clone(qs_state_t src, qs_state_t* out);
 uint32_t qs_num_qubits(qs_state_t s);
 int qs_device(qs_state_t s);
-/* Raw device pointer of the amplitudes (for zero-copy interop, e.g. torch).  */
+/* Raw device pointer of the amplitudes (for zero-copy interop, e.g. torch).
+ * Plans that end in a qubit permutation (relabelled SWAPs) write out of place
+ * into a second buffer of the same size and swap: query the pointer again
+ * after executing a plan.                                                     */
 void* qs_device_ptr(qs_state_t s);
 /* Resets to |0...0>. */
 int qs_reset(qs_state_t s);
