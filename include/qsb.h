@@ -215,6 +215,26 @@ int qs_expect_pauli(qs_state_t s, const char* letters, uint32_t nterms, double* 
  * from it instead of one state copy per operator  [noise.hpp:259-311]. */
 int qs_reduced_density(qs_state_t s, const uint32_t* qubits, uint32_t k, double* out);
 
+/* --- shot batches (per-shot paths of run() / run_noisy for small states) ----
+ * A state of n_total qubits holds B = 2^(n_total - shot_qubits) independent
+ * shot_qubits-qubit states; shot s owns [s * 2^shot_qubits, (s+1) * 2^...).
+ * Gates go through qs_apply_circuit (they never touch the shot bits); the
+ * per-shot steps below take one uniform per shot (the caller draws them from
+ * Rng::derive(seed, s) in program order, simulator.hpp:121-194):
+ *   qs_batch_reset:   every shot to |0...0>
+ *   qs_batch_measure: outcome_s = (u_s < 1 - P_s(1)) ? 0 : 1, collapse and
+ *                     renormalise each shot       [statevector.hpp:219-247]
+ *   qs_batch_kraus:   per shot, weights Tr(K_i rho_s K_i^dag) from the shot's
+ *                     reduced density matrix, the reference's pick with u_s,
+ *                     K_chosen / sqrt(w) applied  [noise.hpp:283-311]
+ *                     (1- or 2-qubit channels, <= 16 operators, ops
+ *                     nops x 2^k x 2^k complex row-major interleaved).       */
+int qs_batch_reset(qs_state_t s, uint32_t shot_qubits);
+int qs_batch_measure(qs_state_t s, uint32_t shot_qubits, uint32_t qubit, const double* uniforms, uint64_t shots,
+                     signed char* outcomes);
+int qs_batch_kraus(qs_state_t s, uint32_t shot_qubits, const uint32_t* qubits, uint32_t k, const double* ops,
+                   uint32_t nops, const double* uniforms, uint64_t shots, int32_t* chosen);
+
 /* Gradient of <psi|H|psi>, psi = gates[0..count) applied to |0...0>, with
  * respect to the angle of each slot gate gates[slots[i]] (uncontrolled RX, RY
  * or RZ): out[i] = dE/dtheta_i -- the value the reference's parameter-shift

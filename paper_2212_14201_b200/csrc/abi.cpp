@@ -580,6 +580,29 @@ int qs_expect_pauli(qs_state_t h, const char* letters, uint32_t nterms, double* 
   });
 }
 
+int qs_batch_reset(qs_state_t h, uint32_t shot_qubits) {
+  return guarded([&] {
+    batch_reset(st(h), shot_qubits);
+    st(h).sync();
+  });
+}
+
+int qs_batch_measure(qs_state_t h, uint32_t shot_qubits, uint32_t qubit, const double* uniforms, uint64_t shots,
+                     signed char* outcomes) {
+  return guarded([&] {
+    if (shots && (!uniforms || !outcomes)) throw ValidationError("null batch buffers");
+    batch_measure(st(h), shot_qubits, qubit, uniforms, shots, outcomes);
+  });
+}
+
+int qs_batch_kraus(qs_state_t h, uint32_t shot_qubits, const uint32_t* qubits, uint32_t k, const double* ops,
+                   uint32_t nops, const double* uniforms, uint64_t shots, int32_t* chosen) {
+  return guarded([&] {
+    if (!qubits || !ops || (shots && !uniforms)) throw ValidationError("null batch buffers");
+    batch_kraus(st(h), shot_qubits, qubits, k, ops, nops, uniforms, shots, chosen);
+  });
+}
+
 int qs_reduced_density(qs_state_t h, const uint32_t* qubits, uint32_t k, double* out) {
   return guarded([&] {
     if (!qubits || !out) throw ValidationError("null buffer");

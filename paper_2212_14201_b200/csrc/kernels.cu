@@ -750,6 +750,180 @@ __global__ void k_sum_partials(const double2* __restrict__ partial, int blocks, 
   out[i] = make_double2(re, im);
 }
 
+// ---------------------------------------------------------- shot batches
+// B independent n-qubit states held as one (n + b)-qubit vector: shot s owns
+// [s * 2^n, (s + 1) * 2^n).  Gates run through the ordinary planner (they
+// never touch the shot bits); measurements and Kraus choices differ per shot.
+__global__ void __launch_bounds__(kThreads) k_batch_basis(double2* __restrict__ a, uint64_t total, uint64_t lmask) {
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < total; i += (uint64_t)gridDim.x * blockDim.x)
+    a[i] = make_double2((i & lmask) == 0 ? 1.0 : 0.0, 0.0);
+}
+
+// p1[s] = sum over shot s of |a_i|^2 with bit set (one block per shot).
+__global__ void __launch_bounds__(kThreads) k_batch_prob_one(const double2* __restrict__ a, uint32_t n, uint64_t bit,
+                                                             uint64_t shots, double* __restrict__ p1) {
+  __shared__ double sh[kThreads / 32];
+  const uint64_t len = 1ull << n;
+  for (uint64_t s = blockIdx.x; s < shots; s += gridDim.x) {
+    const double2* b = a + s * len;
+    double acc = 0;
+    for (uint64_t i = threadIdx.x; i < len; i += blockDim.x)
+      if (i & bit) acc += norm_ref(b[i]);
+    const double t = block_sum(acc, sh);
+    if (threadIdx.x == 0) p1[s] = t;
+  }
+}
+
+// Per shot: outcome = (u < 1 - p1) ? 0 : 1 (statevector.hpp:219-225); keep and
+// rescale by 1/sqrt(prob) or zero.  A zero-probability pick raises *err.
+__global__ void __launch_bounds__(kThreads) k_batch_collapse(double2* __restrict__ a, uint32_t n, uint64_t bit,
+                                                             const double* __restrict__ p1, const double* __restrict__ u,
+                                                             uint64_t total, signed char* __restrict__ out,
+                                                             int* __restrict__ err) {
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < total; i += (uint64_t)gridDim.x * blockDim.x) {
+    const uint64_t s = i >> n;
+    const double q1 = p1[s], q0 = 1.0 - q1;
+    const int o = (u[s] < q0) ? 0 : 1;
+    const double prob = o ? q1 : q0;
+    if ((i & ((1ull << n) - 1)) == 0) {
+      out[s] = static_cast<signed char>(o);
+      if (prob <= 0.0) *err = 1;
+    }
+    if (((i & bit) != 0) == (o == 1)) {
+      const double inv = 1.0 / sqrt(prob);
+      const double2 x = a[i];
+      a[i] = make_double2(x.x * inv, x.y * inv);
+    } else {
+      a[i] = make_double2(0, 0);
+    }
+  }
+}
+
+// Reduced density matrix of K qubits per shot (one block per shot).
+template <int K>
+__global__ void __launch_bounds__(kThreads) k_batch_rdm(const double2* __restrict__ a, uint32_t n, Slots sl,
+                                                        TargetMasks tm, uint64_t shots, double2* __restrict__ rdm) {
+  constexpr int D = 1 << K;
+  __shared__ double sh[kThreads / 32];
+  const uint64_t groups = 1ull << (n - K);
+  for (uint64_t s = blockIdx.x; s < shots; s += gridDim.x) {
+    const double2* b = a + (s << n);
+    double re[D * D], im[D * D];
+#pragma unroll
+    for (int i = 0; i < D * D; ++i) re[i] = im[i] = 0;
+    for (uint64_t g = threadIdx.x; g < groups; g += blockDim.x) {
+      const uint64_t base = deposit(g, sl);
+      double2 v[D];
+#pragma unroll
+      for (int r = 0; r < D; ++r) {
+        uint64_t off = 0;
+#pragma unroll
+        for (int t = 0; t < K; ++t)
+          if ((r >> t) & 1) off |= tm.m[t];
+        v[r] = b[base | off];
+      }
+#pragma unroll
+      for (int r = 0; r < D; ++r)
+#pragma unroll
+        for (int c = 0; c < D; ++c) {
+          re[r * D + c] = fma(v[r].x, v[c].x, fma(v[r].y, v[c].y, re[r * D + c]));
+          im[r * D + c] = fma(v[r].y, v[c].x, fma(-v[r].x, v[c].y, im[r * D + c]));
+        }
+    }
+    for (int i = 0; i < D * D; ++i) {
+      const double tr = block_sum(re[i], sh);
+      const double ti = block_sum(im[i], sh);
+      if (threadIdx.x == 0) rdm[s * D * D + i] = make_double2(tr, ti);
+    }
+  }
+}
+
+// Per shot: w_i = Tr(K_i rho K_i^dag), the reference's pick (u * total against
+// the running sum, noise.hpp:290-305), scale = 1/sqrt(w_chosen).
+template <int K>
+__global__ void k_batch_choose(const double2* __restrict__ rdm, const double2* __restrict__ ops, int nops,
+                               const double* __restrict__ u, uint64_t shots, int* __restrict__ chosen,
+                               double* __restrict__ scale, int* __restrict__ err) {
+  constexpr int D = 1 << K;
+  for (uint64_t s = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; s < shots; s += (uint64_t)gridDim.x * blockDim.x) {
+    const double2* rho = rdm + s * D * D;
+    double w[16];
+    double total = 0;
+    for (int i = 0; i < nops; ++i) {
+      const double2* k = ops + (uint64_t)i * D * D;
+      double t = 0;
+      for (int r = 0; r < D; ++r)
+        for (int x = 0; x < D; ++x) {
+          double cr = 0, ci = 0;  // (K rho)[r][x]
+          for (int y = 0; y < D; ++y) {
+            const double2 kk = k[r * D + y], rr = rho[y * D + x];
+            cr = fma(kk.x, rr.x, fma(-kk.y, rr.y, cr));
+            ci = fma(kk.x, rr.y, fma(kk.y, rr.x, ci));
+          }
+          const double2 kc = k[r * D + x];  // times conj(K[r][x])
+          t = fma(cr, kc.x, fma(ci, kc.y, t));
+        }
+      w[i] = t > 0 ? t : 0.0;
+      total += w[i];
+    }
+    const double target = u[s] * total;
+    double acc = 0;
+    int pick = nops - 1;
+    for (int i = 0; i < nops; ++i) {
+      acc += w[i];
+      if (target < acc) {
+        pick = i;
+        break;
+      }
+    }
+    chosen[s] = pick;
+    if (w[pick] <= 0) {
+      *err = 1;
+      scale[s] = 0;
+    } else {
+      scale[s] = 1.0 / sqrt(w[pick]);
+    }
+  }
+}
+
+// a <- scale[s] * K_{chosen[s]} a on the K qubits, per shot.
+template <int K>
+__global__ void __launch_bounds__(kThreads) k_batch_apply(double2* __restrict__ a, uint32_t n, Slots sl, TargetMasks tm,
+                                                          uint64_t shots, const double2* __restrict__ ops,
+                                                          const int* __restrict__ chosen,
+                                                          const double* __restrict__ scale) {
+  constexpr int D = 1 << K;
+  const uint64_t groups = 1ull << (n - K), work = groups * shots;
+  for (uint64_t w = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; w < work; w += (uint64_t)gridDim.x * blockDim.x) {
+    const uint64_t s = w / groups, g = w % groups;
+    double2* b = a + (s << n);
+    const uint64_t base = deposit(g, sl);
+    const double2* k = ops + (uint64_t)chosen[s] * D * D;
+    const double f = scale[s];
+    uint64_t off[D];
+    double2 v[D];
+#pragma unroll
+    for (int r = 0; r < D; ++r) {
+      off[r] = 0;
+#pragma unroll
+      for (int t = 0; t < K; ++t)
+        if ((r >> t) & 1) off[r] |= tm.m[t];
+      v[r] = b[base | off[r]];
+    }
+#pragma unroll
+    for (int r = 0; r < D; ++r) {
+      double re = 0, im = 0;
+#pragma unroll
+      for (int c = 0; c < D; ++c) {
+        const double2 kk = k[r * D + c];
+        re = fma(kk.x, v[c].x, fma(-kk.y, v[c].y, re));
+        im = fma(kk.x, v[c].y, fma(kk.y, v[c].x, im));
+      }
+      b[base | off[r]] = make_double2(re * f, im * f);
+    }
+  }
+}
+
 // dst[k] += f * (-1)^popc((k ^ x) & z) * src[k ^ x]: dst += f * P src for the
 // Pauli string (X part x, Z part z; f carries the coefficient and i^#Y).
 __global__ void __launch_bounds__(kThreads) k_pauli_axpy(double2* __restrict__ dst, const double2* __restrict__ src,
@@ -1292,6 +1466,89 @@ void reduced_density(State& s, const uint32_t* targets, uint32_t k, double* out)
   QSB_LAUNCHED();
   QSB_CUDA(cudaMemcpyAsync(out, res, width * sizeof(double2), cudaMemcpyDeviceToHost, s.stream));
   QSB_CUDA(cudaStreamSynchronize(s.stream));
+}
+
+void batch_reset(State& s, uint32_t n) {
+  if (n > s.local_qubits()) throw ValidationError("batch: shot size exceeds the state");
+  DeviceGuard dg(s.device);
+  k_batch_basis<<<grid_for(s.size, s.device), kThreads, 0, s.stream>>>(s.amps, s.size, (1ull << n) - 1);
+  QSB_LAUNCHED();
+}
+
+void batch_measure(State& s, uint32_t n, uint32_t q, const double* u_host, uint64_t shots, signed char* out_host) {
+  if (n > s.local_qubits() || q >= n) throw ValidationError("batch measure: qubit out of range");
+  if (shots > (s.size >> n)) throw ValidationError("batch measure: more shots than the batch holds");
+  if (!shots) return;
+  DeviceGuard dg(s.device);
+  char* scr = static_cast<char*>(s.get_scratch(shots * 17 + 512));
+  double* p1 = reinterpret_cast<double*>(scr);
+  double* u = p1 + shots;
+  int* err = reinterpret_cast<int*>(u + shots);
+  signed char* out = reinterpret_cast<signed char*>(err + 4);
+  QSB_CUDA(cudaMemcpyAsync(u, u_host, shots * 8, cudaMemcpyHostToDevice, s.stream));
+  QSB_CUDA(cudaMemsetAsync(err, 0, sizeof(int), s.stream));
+  const uint32_t blocks = static_cast<uint32_t>(std::min<uint64_t>(shots, num_sms(s.device) * 8ull));
+  k_batch_prob_one<<<blocks, kThreads, 0, s.stream>>>(s.amps, n, 1ull << q, shots, p1);
+  QSB_LAUNCHED();
+  k_batch_collapse<<<grid_for(shots << n, s.device), kThreads, 0, s.stream>>>(s.amps, n, 1ull << q, p1, u, shots << n,
+                                                                              out, err);
+  QSB_LAUNCHED();
+  int h_err = 0;
+  QSB_CUDA(cudaMemcpyAsync(out_host, out, shots, cudaMemcpyDeviceToHost, s.stream));
+  QSB_CUDA(cudaMemcpyAsync(&h_err, err, sizeof(int), cudaMemcpyDeviceToHost, s.stream));
+  QSB_CUDA(cudaStreamSynchronize(s.stream));
+  if (h_err) throw RuntimeError("collapse onto a zero-probability outcome");
+}
+
+void batch_kraus(State& s, uint32_t n, const uint32_t* qubits, uint32_t k, const double* ops_host, uint32_t nops,
+                 const double* u_host, uint64_t shots, int* chosen_host) {
+  if (k < 1 || k > 2) throw ValidationError("batch Kraus step supports 1- and 2-qubit channels");
+  if (nops < 1 || nops > 16) throw ValidationError("batch Kraus step: 1 to 16 operators");
+  if (n > s.local_qubits() || shots > (s.size >> n)) throw ValidationError("batch Kraus step: bad batch shape");
+  std::vector<uint32_t> tg(qubits, qubits + k);
+  for (auto q : tg)
+    if (q >= n) throw ValidationError("batch Kraus step: qubit out of range");
+  const Slots sl = make_slots(tg, {});
+  if (sl.count != k) throw ValidationError("batch Kraus step: repeated qubit");
+  if (!shots) return;
+  TargetMasks tm{};
+  for (uint32_t b = 0; b < k; ++b) tm.m[b] = 1ull << tg[k - 1 - b];
+  const int D = 1 << k;
+  DeviceGuard dg(s.device);
+  const size_t ops_bytes = static_cast<size_t>(nops) * D * D * sizeof(double2);
+  char* scr = static_cast<char*>(s.get_scratch(ops_bytes + shots * (D * D * 16 + 8 + 8 + 4) + 1024));
+  double2* ops = reinterpret_cast<double2*>(scr);
+  double2* rdm = ops + static_cast<size_t>(nops) * D * D;
+  double* u = reinterpret_cast<double*>(rdm + shots * D * D);
+  double* scale = u + shots;
+  int* chosen = reinterpret_cast<int*>(scale + shots);
+  int* err = chosen + shots + 1;
+  QSB_CUDA(cudaMemcpyAsync(ops, ops_host, ops_bytes, cudaMemcpyHostToDevice, s.stream));
+  QSB_CUDA(cudaMemcpyAsync(u, u_host, shots * 8, cudaMemcpyHostToDevice, s.stream));
+  QSB_CUDA(cudaMemsetAsync(err, 0, sizeof(int), s.stream));
+  const uint32_t blocks = static_cast<uint32_t>(std::min<uint64_t>(shots, num_sms(s.device) * 8ull));
+  if (k == 1) {
+    k_batch_rdm<1><<<blocks, kThreads, 0, s.stream>>>(s.amps, n, sl, tm, shots, rdm);
+    QSB_LAUNCHED();
+    k_batch_choose<1><<<grid_for(shots, s.device), kThreads, 0, s.stream>>>(rdm, ops, nops, u, shots, chosen, scale, err);
+    QSB_LAUNCHED();
+    k_batch_apply<1><<<grid_for(shots << (n - 1), s.device), kThreads, 0, s.stream>>>(s.amps, n, sl, tm, shots, ops,
+                                                                                      chosen, scale);
+    QSB_LAUNCHED();
+  } else {
+    k_batch_rdm<2><<<blocks, kThreads, 0, s.stream>>>(s.amps, n, sl, tm, shots, rdm);
+    QSB_LAUNCHED();
+    k_batch_choose<2><<<grid_for(shots, s.device), kThreads, 0, s.stream>>>(rdm, ops, nops, u, shots, chosen, scale, err);
+    QSB_LAUNCHED();
+    k_batch_apply<2><<<grid_for(shots << (n - 2), s.device), kThreads, 0, s.stream>>>(s.amps, n, sl, tm, shots, ops,
+                                                                                      chosen, scale);
+    QSB_LAUNCHED();
+  }
+  int h_err = 0;
+  if (chosen_host) QSB_CUDA(cudaMemcpyAsync(chosen_host, chosen, shots * sizeof(int), cudaMemcpyDeviceToHost, s.stream));
+  QSB_CUDA(cudaMemcpyAsync(&h_err, err, sizeof(int), cudaMemcpyDeviceToHost, s.stream));
+  QSB_CUDA(cudaStreamSynchronize(s.stream));
+  if (h_err) throw RuntimeError("trajectory selected a zero-probability Kraus branch");
 }
 
 void pauli_axpy(State& s, double2* dst, const double2* src, uint64_t xmask, uint64_t zmask, double fre, double fim) {

@@ -71,6 +71,12 @@ void pauli_cross(State& s, const double2* a, const double2* partner, uint64_t si
 // complex, row-major interleaved (host, synchronous).
 void reduced_density(State& s, const uint32_t* targets, uint32_t k, double* out);
 
+// Shot batches: B n-qubit states as one vector (shot s at [s*2^n, (s+1)*2^n)).
+void batch_reset(State& s, uint32_t n);
+void batch_measure(State& s, uint32_t n, uint32_t q, const double* u_host, uint64_t shots, signed char* out_host);
+void batch_kraus(State& s, uint32_t n, const uint32_t* qubits, uint32_t k, const double* ops_host, uint32_t nops,
+                 const double* u_host, uint64_t shots, int* chosen_host);
+
 // dst += f * P src (P = X^x Z^z, f complex incl. i^#Y), over s.size amplitudes.
 void pauli_axpy(State& s, double2* dst, const double2* src, uint64_t xmask, uint64_t zmask, double fre, double fim);
 

@@ -7,6 +7,7 @@
 #pragma once
 
 #include <cstdint>
+#include <cstdlib>
 #include <functional>
 #include <map>
 #include <optional>
@@ -140,6 +141,132 @@ class ShotExecutor {
   ReadoutHook readout_;
 };
 
+// --- shot batches -------------------------------------------------------------
+// Flat programs (no QIf / QWhile) consume a data-independent sequence of
+// uniforms per shot, so many shots run together: B shots are one
+// (n + log2 B)-qubit state, gates go through the planner once for all shots,
+// measurements / Kraus choices are per-shot kernels (qs_batch_*), and the
+// draws of shot s come from Rng::derive(seed, s) in program order -- counts
+// equal the per-shot executor's (and the reference's).
+struct NoiseApplication {
+  const std::vector<CMatrix>* ops;
+  std::vector<std::uint32_t> qubits;
+};
+using NoiseOf = std::function<std::vector<NoiseApplication>(const Gate&)>;
+using ReadoutOf = std::function<const std::pair<double, double>*(std::uint32_t)>;  // (p01, p10) or null
+
+inline bool batchable(const Program& p, std::uint64_t shots, const NoiseOf* noise) {
+  if (std::getenv("QSB_NO_SHOT_BATCH")) return false;  // per-shot executor (cross-checks)
+  if (shots < 2 || !p.is_flat() || p.qubit_count > 22 || p.qubit_count < 1) return false;
+  if (noise)
+    for (const auto& ins : p.body)
+      if (const auto* g = std::get_if<GateOp>(&ins))
+        for (const auto& a : (*noise)(g->gate))
+          if (a.qubits.size() > 2 || a.ops->size() > 16) return false;
+  return true;
+}
+
+// Runs shots [first, first + count) of a flat program; returns their cbits.
+inline std::vector<std::vector<std::int64_t>> run_shot_batch(const Program& p, const SimOptions& opts,
+                                                             std::uint64_t first, std::uint64_t count,
+                                                             const NoiseOf* noise, const ReadoutOf* readout,
+                                                             StateVector* last) {
+  const std::uint32_t n = p.qubit_count;
+  std::uint32_t b = 0;
+  while ((std::uint64_t(1) << b) < count) ++b;
+  // draws per shot, in program order
+  std::size_t draws = 0;
+  for (const auto& ins : p.body) {
+    if (const auto* g = std::get_if<GateOp>(&ins)) {
+      if (noise) draws += (*noise)(g->gate).size();
+    } else if (const auto* m = std::get_if<MeasureOp>(&ins)) {
+      draws += 1 + ((readout && (*readout)(m->qubit)) ? 1 : 0);
+    }
+  }
+  std::vector<std::vector<double>> u(draws, std::vector<double>(count));
+  for (std::uint64_t s = 0; s < count; ++s) {
+    Rng r = Rng::derive(opts.seed, first + s);
+    for (std::size_t d = 0; d < draws; ++d) u[d][s] = r.uniform();
+  }
+  qs_state_t big = nullptr;
+  detail::qs_check(qs_create(n + b, 0, 40, &big));
+  struct Guard {
+    qs_state_t h;
+    ~Guard() { qs_destroy(h); }
+  } guard{big};
+  detail::qs_check(qs_batch_reset(big, n));
+  std::vector<std::vector<std::int64_t>> cbits(count, std::vector<std::int64_t>(p.cbit_count, 0));
+  detail::GateBatch pending;
+  auto drain = [&] {
+    if (pending.gates.empty()) return;
+    pending.rebind();
+    detail::qs_check(qs_apply_circuit(big, pending.gates.data(), pending.gates.size(), opts.plan, opts.max_fused_qubits));
+    pending = detail::GateBatch{};
+  };
+  std::size_t d = 0;
+  std::vector<signed char> outc(count);
+  for (const auto& ins : p.body) {
+    if (const auto* g = std::get_if<GateOp>(&ins)) {
+      pending.push(g->gate);
+      if (!noise) continue;
+      const auto apps = (*noise)(g->gate);
+      if (apps.empty()) continue;
+      drain();
+      for (const auto& a : apps) {
+        const std::size_t dim = std::size_t(1) << a.qubits.size();
+        std::vector<double> flat;
+        for (const auto& k : *a.ops)
+          for (std::size_t r = 0; r < dim; ++r)
+            for (std::size_t c = 0; c < dim; ++c) {
+              flat.push_back(k(static_cast<long>(r), static_cast<long>(c)).real());
+              flat.push_back(k(static_cast<long>(r), static_cast<long>(c)).imag());
+            }
+        detail::qs_check(qs_batch_kraus(big, n, a.qubits.data(), static_cast<std::uint32_t>(a.qubits.size()),
+                                        flat.data(), static_cast<std::uint32_t>(a.ops->size()), u[d++].data(), count,
+                                        nullptr));
+      }
+    } else if (const auto* m = std::get_if<MeasureOp>(&ins)) {
+      drain();
+      detail::qs_check(qs_batch_measure(big, n, m->qubit, u[d++].data(), count, outc.data()));
+      const std::pair<double, double>* ro = readout ? (*readout)(m->qubit) : nullptr;
+      for (std::uint64_t s = 0; s < count; ++s) {
+        std::int64_t o = outc[s];
+        if (ro) {
+          const double flip = o ? ro->second : ro->first;
+          if (u[d][s] < flip) o = o ? 0 : 1;
+        }
+        cbits[s][m->cbit] = o;
+      }
+      if (ro) ++d;
+    } else if (const auto* a = std::get_if<AssignOp>(&ins)) {
+      for (auto& c : cbits) c[a->cbit] = a->expr.evaluate(c);
+    }
+  }
+  drain();
+  if (last) {
+    std::vector<cdouble> amps(std::size_t(1) << n);
+    detail::qs_check(qs_get_amplitudes(big, reinterpret_cast<double*>(amps.data()), (count - 1) << n, amps.size()));
+    *last = StateVector::from_amplitudes(n, amps);
+  }
+  return cbits;
+}
+
+// Shots of a flat program in batches sized to ~2 GiB of device memory.
+inline std::vector<std::string> run_batched_keys(const Program& p, const SimOptions& opts, std::uint64_t shots,
+                                                 const NoiseOf* noise, const ReadoutOf* readout, StateVector* last) {
+  const std::uint32_t n = p.qubit_count;
+  const std::uint64_t cap = std::max<std::uint64_t>(2, (std::uint64_t(1) << 27) >> n);  // 2^27 amplitudes
+  std::vector<std::string> keys;
+  keys.reserve(shots);
+  for (std::uint64_t first = 0; first < shots; first += cap) {
+    const std::uint64_t count = std::min(cap, shots - first);
+    const bool tail = first + count == shots;
+    for (auto& c : run_shot_batch(p, opts, first, count, noise, readout, tail ? last : nullptr))
+      keys.push_back(cbit_key(c));
+  }
+  return keys;
+}
+
 }  // namespace detail
 
 inline RunResult run(const Program& p, const SimOptions& opts = {}, std::uint64_t shots = 0) {
@@ -180,6 +307,12 @@ inline RunResult run(const Program& p, const SimOptions& opts = {}, std::uint64_
       }
     }
     result.final_state = std::move(sv);
+    return result;
+  }
+  if (detail::batchable(p, shots, nullptr)) {
+    StateVector last(p.qubit_count);
+    for (auto& k : detail::run_batched_keys(p, opts, shots, nullptr, nullptr, &last)) ++result.counts[k];
+    result.final_state = std::move(last);
     return result;
   }
   const std::uint64_t runs = shots > 0 ? shots : 1;

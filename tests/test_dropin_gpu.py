@@ -33,3 +33,13 @@ def test_reference_suite_passes_against_dropin(suite):
     tail = (out.stdout[-3000:] + out.stderr[-3000:])
     assert out.returncode == 0, tail
     assert "[  PASSED  ]" in out.stdout, tail
+
+
+def test_shot_batches_match_per_shot_executor():
+    """Flat programs run all shots as one batched state; counts must equal the
+    per-shot executor's for the same seed (tests/shot_batch_check.cpp)."""
+    exe = os.path.join(DROP, "shot_batch_check")
+    assert os.path.exists(exe), "facade checks not built (make -C paper_2212_14201_b200/csrc facadechecks)"
+    out = subprocess.run([exe], capture_output=True, text=True, timeout=900)
+    assert out.returncode == 0, out.stdout[-3000:] + out.stderr[-3000:]
+    assert "PASSED" in out.stdout
