@@ -381,3 +381,24 @@ def test_grouped_pauli_terms_match_oracle():
     for w, v in zip(words, got):
         re, im = ol.expectation(a, n, [(w, 1.0)])
         assert abs(v.real - re) <= 1e-12 and abs(v.imag - im) <= 1e-12
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("n", list(range(1, 17)))
+def test_size_sweep_all_paths(n):
+    """Every register size through the tiled plan (per-gate kernels below 6
+    qubits, permutation passes from 10), the fused reset and the unfused plan."""
+    from test_planner_emu import mixed_gates
+    gates = mixed_gates(n, 60, 500 + n, max_controls=min(2, max(0, n - 3))) if n >= 4 else \
+        Q.gen_random_circuit(n, 3, n).gates()
+    gates += Q.gen_qft(n, (0x5A5A >> (16 - n)) % (1 << n)).gates() if n >= 2 else []
+    want = ol.run_gates(n, gates)
+    for plan in (N.QS_PLAN_TILED, N.QS_PLAN_UNFUSED):
+        sv = Q.StateVector(n)
+        sv.apply_circuit(gates, plan)
+        assert np.max(np.abs(sv.amplitudes() - want)) <= 1e-10, plan
+    cc = Q.CompiledCircuit(n, gates)
+    sv = Q.StateVector(n)
+    sv.apply_gate(Q.make_gate(Q.GateKind.H, [0]))
+    cc.execute(sv, from_basis=0)
+    assert np.max(np.abs(sv.amplitudes() - want)) <= 1e-10
