@@ -45,6 +45,12 @@ struct Gen {
   // from_basis: the pass starts from the basis state |basis> (kernel
   // parameter) instead of reading HBM -- the reset fused into the first pass.
   bool from_basis = false;
+  // exchange-fused variant (sharded plans): the pass's stores go straight to
+  // the owners' free buffers after the rank-bit exchange that follows it --
+  // destination shard = bits of the local index at xlpos, local index with
+  // those bits replaced by this rank's bits (xaval, a kernel parameter).
+  uint32_t xk = 0;
+  uint32_t xlpos[4] = {};
   // single_buf: the prefetch buffer doubles as the transpose buffer (64 KiB
   // per CTA, two resident CTAs per SM); the next tile's copies are issued
   // after the last transpose has read the buffer.
@@ -446,7 +452,18 @@ struct Gen {
     flush_all(true);
     // Relabels (free SWAPs) make threads store where other threads loaded; with
     // no transpose barrier in the pass, every load must retire before any store.
-    if (h.oop) {
+    if (xk) {
+      unsigned long long pmask = 0;
+      for (uint32_t i = 0; i < xk; ++i) pmask |= 1ull << xlpos[i];
+      for (int p = 0; p < 16; ++p) {
+        unsigned long long off = 0;
+        for (int k = 0; k < 4; ++k)
+          if ((p >> k) & 1) off |= h.store.rs[k];
+        s << "    { const unsigned long long L = (G | " << hexll(off) << ") & lmask; const unsigned d = 0u";
+        for (uint32_t i = 0; i < xk; ++i) s << " | ((unsigned)((L >> " << xlpos[i] << ") & 1ull) << " << i << ")";
+        s << "; __stcs(PEERS.p[d] + ((L & " << hexll(~pmask) << ") | xaval), " << name[p] << "); }\n";
+      }
+    } else if (h.oop) {
       // out of place through the final qubit permutation: the written index is
       // sigma(base) | sigma(thread bits) | sigma(register bits)
       s << "    unsigned long long GO = TLO;\n";
@@ -471,10 +488,12 @@ struct Gen {
     // ---- assemble
     std::ostringstream k;
     k << "struct __align__(16) QsbCoef { double2 c[" << std::max<size_t>(1, tp.coef.size() + extra.size()) << "]; };\n";
+    k << "struct QsbPeers { double2* p[16]; };\n";
     k << "extern \"C\" __global__ void __launch_bounds__(" << threads << ", " << minb << ") " << kname
       << "(double2* __restrict__ amps, double2* __restrict__ out, const unsigned long long rank_base,\n"
       << "    const unsigned long long lmask,\n"
-      << "    const unsigned long long ntiles, const unsigned long long basis, const __grid_constant__ QsbCoef P) {\n";
+      << "    const unsigned long long ntiles, const unsigned long long basis, const QsbPeers PEERS,\n"
+    << "    const unsigned long long xaval, const __grid_constant__ QsbCoef P) {\n";
     k << "  extern __shared__ double2 sm[];\n";
     k << "  const unsigned tid = threadIdx.x;\n";
     k << "  const unsigned long long TL = 0ull";

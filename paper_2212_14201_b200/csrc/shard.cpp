@@ -160,6 +160,24 @@ struct LocalTransport : Transport {
       }
     }
   }
+  bool fused_exchange(std::vector<State*>& shards, const TileProgram& tp, const std::vector<uint32_t>& gpos,
+                      const std::vector<uint32_t>& lpos) override {
+    const uint32_t k = static_cast<uint32_t>(gpos.size());
+    if (mode != Peer || k > kMaxExchangeBits) return false;
+    for (uint32_t r = 0; r < shards.size(); ++r) {
+      TileXchg x;
+      x.k = k;
+      const uint32_t a = rank_bits(r, gpos);
+      for (uint32_t i = 0; i < k; ++i) {
+        x.lpos[i] = lpos[i];
+        if ((a >> i) & 1) x.aval |= 1ull << lpos[i];
+      }
+      for (uint32_t d = 0; d < (1u << k); ++d) x.peers[d] = shards[with_bits(r, gpos, d)]->alt;
+      launch_tile(*shards[r], tp, nullptr, &x);
+    }
+    for (auto* s : shards) std::swap(s->amps, s->alt);
+    return true;
+  }
   double sum(const std::vector<double>& v) override {
     double t = 0;
     for (double x : v) t += x;
@@ -360,6 +378,28 @@ struct NcclTransport : Transport {
     red = nullptr;
   }
 
+  bool fused_exchange(std::vector<State*>& shards, const TileProgram& tp, const std::vector<uint32_t>& gpos,
+                      const std::vector<uint32_t>& lpos) override {
+    const uint32_t k = static_cast<uint32_t>(gpos.size());
+    if (!peer || k > kMaxExchangeBits) return false;
+    State& s = *shards.at(0);
+    DeviceGuard dg(s.device);
+    TileXchg x;
+    x.k = k;
+    const uint32_t a = rank_bits(s.rank, gpos);
+    for (uint32_t i = 0; i < k; ++i) {
+      x.lpos[i] = lpos[i];
+      if ((a >> i) & 1) x.aval |= 1ull << lpos[i];
+    }
+    for (uint32_t d = 0; d < (1u << k); ++d) x.peers[d] = bufs[cur ^ 1][with_bits(s.rank, gpos, d)];
+    launch_tile(s, tp, nullptr, &x);  // stores land in the owners' free buffers over NVLink
+    stream_barrier(s.stream);
+    cur ^= 1;
+    s.amps = bufs[cur][s.rank];
+    s.alt = bufs[cur ^ 1][s.rank];
+    return true;
+  }
+
   void exchange(std::vector<State*>& shards, const std::vector<uint32_t>& gpos,
                 const std::vector<uint32_t>& lpos) override {
     State& s = *shards.at(0);
@@ -523,10 +563,20 @@ void shard_execute(ShardSet& ss, const Plan& p, uint64_t first, uint64_t count) 
   if (p.n != ss.n || p.g != ss.g) throw ValidationError("plan was compiled for a different state shape");
   auto shards = ss.ptrs();
   const uint64_t last = std::min<uint64_t>(p.steps.size(), count == ~0ull ? p.steps.size() : first + count);
+  static const bool fuse = [] {
+    const char* e = std::getenv("QSB_FUSE_EXCHANGE");
+    return !e || std::atoi(e) != 0;
+  }();
   for (uint64_t i = first; i < last; ++i) {
     const Step& st = p.steps[i];
     switch (st.kind) {
       case Step::TileStep:
+        // a tile pass followed by an exchange: one kernel writing over peer memory
+        if (fuse && i + 1 < last && p.steps[i + 1].kind == Step::SwapStep &&
+            ss.tr->fused_exchange(shards, *st.tile, p.steps[i + 1].gpos, p.steps[i + 1].lpos)) {
+          ++i;
+          break;
+        }
         for (auto* s : shards) launch_tile(*s, *st.tile);
         break;
       case Step::OpStep:

@@ -44,6 +44,12 @@ struct Transport {
   virtual void barrier() {}
   // Releases transport resources that reference the shards (before they are freed).
   virtual void close() {}
+  // Runs tile pass tp with the following exchange fused into its stores
+  // (peer-memory transports); false = not supported, run them separately.
+  virtual bool fused_exchange(std::vector<State*>& shards, const struct TileProgram& tp,
+                              const std::vector<uint32_t>& gpos, const std::vector<uint32_t>& lpos) {
+    return false;
+  }
 };
 
 struct ShardSet {

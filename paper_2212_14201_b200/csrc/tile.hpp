@@ -23,6 +23,7 @@
 
 #include <cstdint>
 #include <cstdlib>
+#include <map>
 #include <memory>
 #include <vector>
 
@@ -90,6 +91,7 @@ struct TileProgram {
   std::vector<uint64_t> source;  // gate indices, for diagnostics
   std::shared_ptr<struct JitModule> jit;  // specialised kernel (jit.hpp)
   mutable std::shared_ptr<struct JitModule> jit_basis;  // from-basis variant (first pass of a run), lazily built
+  mutable std::map<uint64_t, std::shared_ptr<struct JitModule>> jit_xchg;  // exchange-fused variants, by local bits
   std::vector<double2> params;            // kernel parameter table (coef + generator constants)
 };
 
@@ -135,6 +137,14 @@ inline void plan_tiles(uint32_t n, std::vector<Op>& ops, std::vector<Step>& step
 }
 // basis != null: the pass starts from |*basis> (global index) instead of
 // reading the state -- a reset fused into the first pass.
-void launch_tile(State& s, const TileProgram& tp, const uint64_t* basis = nullptr);
+// Exchange fused into a pass (sharded plans, peer memory): after the pass,
+// rank bits gpos[i] trade places with local bits lpos[i].
+struct TileXchg {
+  uint32_t k = 0;
+  uint32_t lpos[4] = {};
+  double2* peers[16] = {};  // free buffer of the shard whose exchanged bits are d
+  unsigned long long aval = 0;  // this shard's exchanged rank bits, placed at lpos
+};
+void launch_tile(State& s, const TileProgram& tp, const uint64_t* basis = nullptr, const TileXchg* x = nullptr);
 
 }  // namespace qsb
