@@ -541,7 +541,10 @@ struct Gen {
     k << "    const unsigned long long tix = tile | (rank_base >> " << h.m << ");\n";
     k << "    unsigned long long G = base | TL;\n";
     k << s.str();
-    k << "  }\n}\n";
+    k << "  }\n";
+    // peer stores must be visible system-wide before the stream barrier that follows
+    if (xk) k << "  __threadfence_system();\n";
+    k << "}\n";
     return k.str();
   }
 };
