@@ -412,6 +412,30 @@ struct Gen {
     }
     // ---- tile-loop body
     if (from_basis) {
+      // Only the tile holding |basis> computes anything: every other tile
+      // starts (and so ends) at zero -- write zeros and move on.
+      unsigned long long smask = 0;
+      for (uint32_t b = 0; b < h.m; ++b) smask |= 1ull << h.S[b];
+      s << "    if ((basis & " << hexll(~smask) << ") != base) {\n";
+      if (h.oop) {
+        s << "      unsigned long long GZ = TLO;\n";
+        for (uint32_t i = 0; i + h.m < h.n; ++i)
+          s << "      if ((tix >> " << i << ") & 1ull) GZ |= " << hexll(1ull << h.out_pos[i]) << ";\n";
+        for (int p = 0; p < 16; ++p) {
+          unsigned long long off = 0;
+          for (int k = 0; k < 4; ++k)
+            if ((p >> k) & 1) off |= h.store.rs[k];
+          s << "      __stcs(out + (GZ | " << hexll(off) << "), make_double2(0.0, 0.0));\n";
+        }
+      } else {
+        for (int p = 0; p < 16; ++p) {
+          unsigned long long off = 0;
+          for (int k = 0; k < 4; ++k)
+            if ((p >> k) & 1) off |= h.store.rs[k];
+          s << "      __stcs(amps + ((base | TLS | " << hexll(off) << ") & lmask), make_double2(0.0, 0.0));\n";
+        }
+      }
+      s << "      continue;\n    }\n";
       for (int p = 0; p < 16; ++p) {
         name[p] = fresh();
         s << "    const double2 " << name[p] << " = make_double2(((G | " << hexll(loff[p])
@@ -499,6 +523,11 @@ struct Gen {
     k << "  const unsigned long long TL = 0ull";
     for (uint32_t b = 0; b < h.t; ++b) k << " | ((unsigned long long)((tid >> " << b << ") & 1u) << " << h.load.tq[b] << ")";
     k << ";\n";
+    if (from_basis && !h.oop) {
+      k << "  const unsigned long long TLS = 0ull";
+      for (uint32_t b = 0; b < h.t; ++b) k << " | ((unsigned long long)((tid >> " << b << ") & 1u) << " << h.store.tq[b] << ")";
+      k << ";\n";
+    }
     if (h.oop) {
       k << "  const unsigned long long TLO = 0ull";
       for (uint32_t b = 0; b < h.t; ++b) k << " | ((unsigned long long)((tid >> " << b << ") & 1u) << " << h.store.tq[b] << ")";
