@@ -411,13 +411,15 @@ struct Gen {
         if ((p >> k) & 1) loff[p] |= h.load.rs[k];
     }
     // ---- tile-loop body
-    if (from_basis) {
-      // Only the tile holding |basis> computes anything: every other tile
-      // starts (and so ends) at zero -- write zeros and move on.
-      unsigned long long smask = 0;
-      for (uint32_t b = 0; b < h.m; ++b) smask |= 1ull << h.S[b];
-      s << "    if ((basis & " << hexll(~smask) << ") != base) {\n";
-      if (h.oop) {
+    // Zero tiles of a run started from a basis state: a tile whose index
+    // disagrees with the still-definite outside qubits (dmask / dval, kernel
+    // parameters; dmask = 0 otherwise) is zero before and after the pass.  In
+    // place it is skipped outright; a pass that writes elsewhere (the reset
+    // fused into the first pass, an out-of-place pass) writes its zeros.
+    if (!xk) {
+      s << "    if ((base & dmask) != dval) {\n";
+      if (from_basis || h.oop) {
+        if (h.oop) {
         s << "      unsigned long long GZ = TLO;\n";
         for (uint32_t i = 0; i + h.m < h.n; ++i)
           s << "      if ((tix >> " << i << ") & 1ull) GZ |= " << hexll(1ull << h.out_pos[i]) << ";\n";
@@ -434,8 +436,12 @@ struct Gen {
             if ((p >> k) & 1) off |= h.store.rs[k];
           s << "      __stcs(amps + ((base | TLS | " << hexll(off) << ") & lmask), make_double2(0.0, 0.0));\n";
         }
+        }
       }
+      if (prefetch) s << "  " << kIssueNext;
       s << "      continue;\n    }\n";
+    }
+    if (from_basis) {
       for (int p = 0; p < 16; ++p) {
         name[p] = fresh();
         s << "    const double2 " << name[p] << " = make_double2(((G | " << hexll(loff[p])
@@ -517,13 +523,14 @@ struct Gen {
       << "(double2* __restrict__ amps, double2* __restrict__ out, const unsigned long long rank_base,\n"
       << "    const unsigned long long lmask,\n"
       << "    const unsigned long long ntiles, const unsigned long long basis, const QsbPeers PEERS,\n"
-    << "    const unsigned long long xaval, const __grid_constant__ QsbCoef P) {\n";
+    << "    const unsigned long long xaval, const unsigned long long dmask, const unsigned long long dval,\n"
+    << "    const __grid_constant__ QsbCoef P) {\n";
     k << "  extern __shared__ double2 sm[];\n";
     k << "  const unsigned tid = threadIdx.x;\n";
     k << "  const unsigned long long TL = 0ull";
     for (uint32_t b = 0; b < h.t; ++b) k << " | ((unsigned long long)((tid >> " << b << ") & 1u) << " << h.load.tq[b] << ")";
     k << ";\n";
-    if (from_basis && !h.oop) {
+    if (!h.oop) {
       k << "  const unsigned long long TLS = 0ull";
       for (uint32_t b = 0; b < h.t; ++b) k << " | ((unsigned long long)((tid >> " << b << ") & 1u) << " << h.store.tq[b] << ")";
       k << ";\n";
@@ -556,7 +563,9 @@ struct Gen {
       // HBM reads of tile i+1 overlap the arithmetic of tile i.
       k << "  double2* const PB = sm + " << (tp.transposes && !single_buf ? (1u << h.m) : 0u) << ";\n";
       k << "  auto prefetch = [&](unsigned long long t) {\n";
-      k << "    const unsigned long long g = base_of(t) | rank_base | TL;\n";
+      k << "    const unsigned long long tb = base_of(t) | rank_base;\n";
+      k << "    if ((tb & dmask) != dval) { cp_async_commit(); return; }  // zero tile: nothing to read\n";
+      k << "    const unsigned long long g = tb | TL;\n";
       for (int p = 0; p < 16; ++p)
         k << "    cp_async16(PB + " << p * T << " + tid, amps + ((g | " << hexll(loff[p]) << ") & lmask));\n";
       k << "    cp_async_commit();\n  };\n";

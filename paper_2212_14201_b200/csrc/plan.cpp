@@ -141,18 +141,39 @@ void execute_plan(State& s, const Plan& p) {
   for (const auto& st : p.steps) execute_step(s, st);
 }
 
+TileSkip zero_tiles(const Step& st, uint64_t basis) {
+  TileSkip k;
+  static const bool off = std::getenv("QSB_NO_ZERO_SKIP") != nullptr;
+  if (off) return k;
+  for (size_t i = 0; i < st.def_pos.size(); ++i) {
+    const unsigned long long bit = 1ull << st.def_pos[i];
+    k.mask |= bit;
+    if ((__builtin_popcountll(basis & st.def_mask[i]) & 1) ^ st.def_const[i]) k.val |= bit;
+  }
+  return k;
+}
+
 void execute_plan_from_basis(State& s, const Plan& p, uint64_t basis) {
   if (p.n != s.n) throw ValidationError("plan was compiled for a different qubit count");
   if (p.g != s.g) throw ValidationError("plan was compiled for a sharded state (use the shard API)");
   if (basis >> s.n) throw ValidationError("basis index out of range");
   size_t i = 0;
   if (!p.steps.empty() && p.steps[0].kind == Step::TileStep && !std::getenv("QSB_NO_FUSED_RESET")) {
-    launch_tile(s, *p.steps[0].tile, &basis);
+    const TileSkip k = zero_tiles(p.steps[0], basis);
+    launch_tile(s, *p.steps[0].tile, &basis, nullptr, &k);
     i = 1;
   } else {
     fill_basis(s, basis);
   }
-  for (; i < p.steps.size(); ++i) execute_step(s, p.steps[i]);
+  // tiles still provably zero (definite qubits outside the tile) are skipped
+  for (; i < p.steps.size(); ++i) {
+    if (p.steps[i].kind == Step::TileStep) {
+      const TileSkip k = zero_tiles(p.steps[i], basis);
+      launch_tile(s, *p.steps[i].tile, nullptr, nullptr, &k);
+    } else {
+      execute_step(s, p.steps[i]);
+    }
+  }
 }
 
 void execute_step(State& s, const Step& st) {

@@ -26,6 +26,14 @@ struct Step {
   // PermStep: out-of-place qubit permutation, bit q of every index -> bit
   // perm[q] (restores the logical layout after relabeling SWAPs in one pass).
   std::vector<uint32_t> perm;
+  // TileStep, runs started from a basis state |b> (qs_plan_execute_from_basis):
+  // qubits outside the tile that are still definite at the start of the pass,
+  // with their value as an affine GF(2) form of b (parity(b & mask) ^ c).  A
+  // tile whose index disagrees with those values is all zero and stays zero:
+  // the pass skips it (no HBM traffic in place; zeros written when out of place).
+  std::vector<uint32_t> def_pos;
+  std::vector<uint64_t> def_mask;
+  std::vector<uint8_t> def_const;
 };
 
 struct Plan {
@@ -49,6 +57,8 @@ void execute_plan(State& s, const Plan& p);
 // Resets to |basis> and runs the plan; when the plan starts with a tile pass
 // the reset is fused into it (no separate write pass, no read of the old state).
 void execute_plan_from_basis(State& s, const Plan& p, uint64_t basis);
+// The zero-tile mask of a tile step for a run started from |basis>.
+struct TileSkip zero_tiles(const Step& st, uint64_t basis);
 void execute_step(State& s, const Step& st);
 
 }  // namespace qsb

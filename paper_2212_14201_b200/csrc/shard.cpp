@@ -559,7 +559,7 @@ void shard_fill_basis(ShardSet& ss, uint64_t index) {
   shard_sync(ss);
 }
 
-void shard_execute(ShardSet& ss, const Plan& p, uint64_t first, uint64_t count) {
+void shard_execute(ShardSet& ss, const Plan& p, uint64_t first, uint64_t count, const uint64_t* basis) {
   if (p.n != ss.n || p.g != ss.g) throw ValidationError("plan was compiled for a different state shape");
   auto shards = ss.ptrs();
   const uint64_t last = std::min<uint64_t>(p.steps.size(), count == ~0ull ? p.steps.size() : first + count);
@@ -577,7 +577,12 @@ void shard_execute(ShardSet& ss, const Plan& p, uint64_t first, uint64_t count) 
           ++i;
           break;
         }
-        for (auto* s : shards) launch_tile(*s, *st.tile);
+        if (basis) {  // a run from |basis>: skip tiles that are still provably zero
+          const TileSkip k = zero_tiles(st, *basis);
+          for (auto* s : shards) launch_tile(*s, *st.tile, nullptr, nullptr, &k);
+        } else {
+          for (auto* s : shards) launch_tile(*s, *st.tile);
+        }
         break;
       case Step::OpStep:
         for (auto* s : shards) launch_op(*s, st.op);
@@ -593,7 +598,8 @@ void shard_execute_from_basis(ShardSet& ss, const Plan& p, uint64_t basis) {
   if (basis >> ss.n) throw ValidationError("basis index out of range");
   uint64_t first = 0;
   if (!p.steps.empty() && p.steps[0].kind == Step::TileStep) {
-    for (auto& s : ss.shards) launch_tile(*s, *p.steps[0].tile, &basis);  // global index: one shard holds it
+    const TileSkip k = zero_tiles(p.steps[0], basis);
+    for (auto& s : ss.shards) launch_tile(*s, *p.steps[0].tile, &basis, nullptr, &k);  // one shard holds |basis>
     first = 1;
   } else {
     for (auto& s : ss.shards) {
@@ -601,7 +607,7 @@ void shard_execute_from_basis(ShardSet& ss, const Plan& p, uint64_t basis) {
       fill_basis(*s, mine ? (basis & (s->size - 1)) : ~0ull);
     }
   }
-  shard_execute(ss, p, first);
+  shard_execute(ss, p, first, ~0ull, &basis);
 }
 
 double shard_norm2(ShardSet& ss) {

@@ -145,6 +145,12 @@ struct TileXchg {
   double2* peers[16] = {};  // free buffer of the shard whose exchanged bits are d
   unsigned long long aval = 0;  // this shard's exchanged rank bits, placed at lpos
 };
-void launch_tile(State& s, const TileProgram& tp, const uint64_t* basis = nullptr, const TileXchg* x = nullptr);
+// Zero-tile skip (runs from a basis state): tiles with (index & mask) != val
+// are zero and stay zero.
+struct TileSkip {
+  unsigned long long mask = 0, val = 0;
+};
+void launch_tile(State& s, const TileProgram& tp, const uint64_t* basis = nullptr, const TileXchg* x = nullptr,
+                 const TileSkip* skip = nullptr);
 
 }  // namespace qsb

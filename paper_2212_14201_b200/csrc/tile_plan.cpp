@@ -842,6 +842,67 @@ void plan_tiles(uint32_t n, std::vector<Op>& ops, std::vector<Step>& steps, cons
   auto refresh = [&]() {
     for (auto idx : rem) phys[idx] = to_physical(pops[idx], perm);
   };
+  // --- definite qubits of a run started from a basis state |b>: value of
+  // logical qubit q = parity(b & dmask[q]) ^ dconst[q] while ddef[q].
+  std::vector<char> ddef(n, 1), dconst(n, 0);
+  std::vector<uint64_t> dmask(n);
+  for (uint32_t q = 0; q < n; ++q) dmask[q] = 1ull << q;
+  auto undef = [&](uint32_t q) { ddef[q] = 0; };
+  auto apply_def = [&](const Op& op) {
+    // controls: all definite with a constant literal value 0 => the op is the identity
+    bool all_def = true, never = false;
+    for (auto c : op.controls) {
+      if (!ddef[c]) {
+        all_def = false;
+        continue;
+      }
+      const bool want_one = !((op.cneg >> c) & 1);
+      if (dmask[c] == 0 && dconst[c] != (want_one ? 1 : 0)) never = true;
+    }
+    if (never) return;
+    switch (op.kind) {
+      case OpKind::Identity:
+      case OpKind::Diag: return;
+      case OpKind::Flip: {
+        const uint32_t t = op.targets[0];
+        if (!ddef[t]) return;
+        if (!all_def) return undef(t);
+        if (op.controls.empty()) {
+          dconst[t] ^= 1;
+        } else if (op.controls.size() == 1) {  // t ^= (c == want)
+          const uint32_t c = op.controls[0];
+          dmask[t] ^= dmask[c];
+          dconst[t] ^= dconst[c] ^ (((op.cneg >> c) & 1) ? 1 : 0);
+        } else {
+          undef(t);  // AND of two forms is not affine
+        }
+        return;
+      }
+      case OpKind::Mat1: {
+        const uint32_t t = op.targets[0];
+        if (op.m[1] == cd(0) && op.m[2] == cd(0)) return;           // diagonal
+        if (op.m[0] == cd(0) && op.m[3] == cd(0) && op.controls.empty() && ddef[t]) {  // X up to phases
+          dconst[t] ^= 1;
+          return;
+        }
+        return undef(t);
+      }
+      case OpKind::Swap:
+        if (op.controls.empty()) {
+          const uint32_t a = op.targets[0], b2 = op.targets[1];
+          std::swap(ddef[a], ddef[b2]);
+          std::swap(dmask[a], dmask[b2]);
+          std::swap(dconst[a], dconst[b2]);
+        } else {
+          undef(op.targets[0]);
+          undef(op.targets[1]);
+        }
+        return;
+      case OpKind::Dense:
+        for (auto t : op.targets) undef(t);
+        return;
+    }
+  };
   auto emit_ready_opaque = [&]() {
     uint64_t blocked = 0;
     std::vector<uint32_t> keep;
@@ -849,6 +910,7 @@ void plan_tiles(uint32_t n, std::vector<Op>& ops, std::vector<Step>& steps, cons
     for (auto idx : rem) {
       const POp& p = phys[idx];
       if (p.k == PK::Opaque && !(p.qmask & blocked) && !(p.needmask & gmask)) {
+        apply_def(pops[idx].op);
         Step s;
         s.kind = Step::OpStep;
         s.op = p.op;
@@ -988,6 +1050,7 @@ void plan_tiles(uint32_t n, std::vector<Op>& ops, std::vector<Step>& steps, cons
       const POp& p = pops[idx];  // logical
       if (p.k == PK::SwapRel && !(p.qmask & blocked)) {
         swap_phys(perm[p.op.targets[0]], perm[p.op.targets[1]]);
+        apply_def(p.op);  // the logical SWAP exchanges the two qubits' states
         continue;
       }
       blocked |= p.qmask;
@@ -1110,13 +1173,28 @@ void plan_tiles(uint32_t n, std::vector<Op>& ops, std::vector<Step>& steps, cons
       take = std::max<size_t>(1, take * 3 / 4);
     }
     if (prog->h.bytes > kTileBlobBytes) throw RuntimeError("tile program for one op exceeds the parameter blob");
+    const std::vector<uint32_t> perm_at_start = perm;
     for (auto& [a, b] : swaps) swap_phys(a, b);
     std::vector<char> used(rem.size(), 0);
     for (size_t j = 0; j < take; ++j) used[taken_pos[j]] = 1;
     std::vector<uint32_t> keep;
     for (size_t i = 0; i < rem.size(); ++i)
       if (!used[i]) keep.push_back(rem[i]);
+    // definite outside qubits at the start of this pass, then the pass's effect
+    std::vector<uint32_t> dpos;
+    std::vector<uint64_t> dm;
+    std::vector<uint8_t> dc;
+    for (uint32_t q = 0; q < n; ++q)
+      if (ddef[q] && !((S >> perm_at_start[q]) & 1)) {
+        dpos.push_back(perm_at_start[q]);
+        dm.push_back(dmask[q]);
+        dc.push_back(static_cast<uint8_t>(dconst[q]));
+      }
+    for (size_t j = 0; j < take; ++j) apply_def(pops[rem[taken_pos[j]]].op);
     push_step(std::move(prog), S, take);
+    steps.back().def_pos = std::move(dpos);
+    steps.back().def_mask = std::move(dm);
+    steps.back().def_const = std::move(dc);
     rem.swap(keep);
     refresh();
     emit_ready_opaque();

@@ -402,3 +402,26 @@ def test_size_sweep_all_paths(n):
     sv.apply_gate(Q.make_gate(Q.GateKind.H, [0]))
     cc.execute(sv, from_basis=0)
     assert np.max(np.abs(sv.amplitudes() - want)) <= 1e-10
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("which", ["qft", "mixed", "random", "ghz", "hea"])
+def test_zero_tile_skip_from_basis(which):
+    """Runs from a basis state skip tiles that are provably zero (definite
+    qubits outside the tile); results must equal the oracle for many basis
+    states, including circuits with X / CNOT chains / controlled gates that keep
+    qubits definite for several passes."""
+    from test_planner_emu import mixed_gates
+    n = 18
+    gates = {"qft": lambda: Q.gen_qft(n, 0).gates(),
+             "mixed": lambda: mixed_gates(n, 120, 4242),
+             "random": lambda: Q.gen_random_circuit(n, 3, 7).gates(),
+             "ghz": lambda: Q.gen_ghz(n).gates(),
+             "hea": lambda: Q.gen_hea(n, 2, 3).gates()}[which]()
+    cc = Q.CompiledCircuit(n, gates)
+    rng = np.random.default_rng(1)
+    sv = Q.StateVector(n)
+    for b in [0, (1 << n) - 1] + [int(x) for x in rng.integers(0, 1 << n, 4)]:
+        cc.execute(sv, from_basis=b)
+        ref = ol.run_gates(n, gates, state=np.eye(1, 1 << n, b, dtype=np.complex128)[0])
+        assert np.max(np.abs(sv.amplitudes() - ref)) <= 1e-10, b
