@@ -759,7 +759,7 @@ int qs_plan_create_sharded(uint32_t num_qubits, uint32_t global_qubits, const qs
     if (!out) throw ValidationError("null output handle");
     if (n && !gates) throw ValidationError("null gate array");
     auto h = std::make_unique<qs_plan>();
-    h->p = make_plan(num_qubits, gates, n, QS_PLAN_TILED, 0, global_qubits);
+    h->p = make_plan(num_qubits, gates, n, QS_PLAN_TILED, 0, global_qubits, /*sharded=*/true);
     *out = h.release();
   });
 }

@@ -404,6 +404,25 @@ struct Gen {
     transposes_total = 0;
     for (const TOp& o : tp.ops) transposes_total += o.type == TO_TRANSPOSE;
     const uint32_t T = 1u << h.t;
+    const uint32_t TB = h.t;
+    // leading transpose out of the load layout: fused into the prefetch (the
+    // cp.async destinations are its write slots) or, from a basis state, into
+    // the register initialisation
+    const bool lead = leading_transpose(tp) && (prefetch || from_basis);
+    const uint32_t* mt0 = lead ? tp.meta.data() + tp.ops[0].meta : nullptr;
+    auto xorexpr = [&](const uint32_t* cols) {
+      std::ostringstream e;
+      e << "0u";
+      for (uint32_t k = 0; k < TB; ++k)
+        if (cols[k]) e << " ^ (((tid >> " << k << ") & 1u) * " << cols[k] << "u)";
+      return e.str();
+    };
+    auto slot_xor = [&](const uint32_t* cols, int p) {
+      uint32_t a = 0;
+      for (int k = 0; k < 4; ++k)
+        if ((p >> k) & 1) a ^= cols[k];
+      return a;
+    };
     unsigned long long loff[16];
     for (int p = 0; p < 16; ++p) {
       loff[p] = 0;
@@ -441,28 +460,54 @@ struct Gen {
       if (prefetch) s << "  " << kIssueNext;
       s << "      continue;\n    }\n";
     }
+    int ti = 0;
     if (from_basis) {
+      unsigned long long off[16];
+      for (int p = 0; p < 16; ++p) {
+        off[p] = loff[p];
+        if (lead) {  // registers start in the layout after the leading transpose
+          off[p] = 0;
+          for (int k = 0; k < 4; ++k)
+            if ((p >> k) & 1) off[p] |= 1ull << mt0[3 * TB + 8 + k];
+        }
+      }
+      if (lead) {
+        emit_G(mt0 + 2 * TB + 8, false);
+        ti = 1;
+      }
       for (int p = 0; p < 16; ++p) {
         name[p] = fresh();
-        s << "    const double2 " << name[p] << " = make_double2(((G | " << hexll(loff[p])
+        s << "    const double2 " << name[p] << " = make_double2(((G | " << hexll(off[p])
           << ") == basis) ? 1.0 : 0.0, 0.0);\n";
       }
     } else if (prefetch) {
       s << "    cp_async_wait_all();\n";
-      for (int p = 0; p < 16; ++p) {
-        name[p] = fresh();
-        s << "    const double2 " << name[p] << " = PB[" << p * T << " + tid];\n";
+      if (lead) {
+        s << "    __syncthreads();\n";
+        for (int p = 0; p < 16; ++p) {
+          name[p] = fresh();
+          s << "    const double2 " << name[p] << " = PB[R0 ^ " << slot_xor(mt0 + 2 * TB + 4, p) << "u];\n";
+        }
+        emit_G(mt0 + 2 * TB + 8, false);
+        ti = 1;
+        if (!single_buf || transposes_total == 1) s << "    __syncthreads();\n" << kIssueNext;
+      } else {
+        for (int p = 0; p < 16; ++p) {
+          name[p] = fresh();
+          s << "    const double2 " << name[p] << " = PB[" << p * T << " + tid];\n";
+        }
+        if (!single_buf || transposes_total == 0) s << kIssueNext;
       }
-      if (!single_buf || transposes_total == 0) s << kIssueNext;
     } else {
       for (int p = 0; p < 16; ++p) {
         name[p] = fresh();
         s << "    const double2 " << name[p] << " = __ldcs(amps + ((G | " << hexll(loff[p]) << ") & lmask));\n";
       }
     }
-    for (uint32_t k = 0; k < h.t; ++k) cur_tq[k] = h.load.tq[k];
-    int ti = 0;
-    for (const TOp& o : tp.ops) {
+    if (ti == 0)
+      for (uint32_t k = 0; k < h.t; ++k) cur_tq[k] = h.load.tq[k];
+    for (size_t oi = static_cast<size_t>(ti); oi < tp.ops.size(); ++oi) {
+      const TOp& o = tp.ops[oi];
       switch (o.type) {
         case TO_MAT1:
         case TO_MAT1_REAL:
@@ -547,7 +592,8 @@ struct Gen {
     }
     k << "    return b;\n  };\n";
     k << pro.str();
-    const uint32_t tile_bufs = single_buf ? 1u : (tp.transposes ? 1u : 0u) + (prefetch ? 1u : 0u);
+    const uint32_t tbuf = tp.transposes - (lead ? 1u : 0u);
+    const uint32_t tile_bufs = single_buf ? 1u : (tbuf ? 1u : 0u) + (prefetch ? 1u : 0u);
     if (!tables.empty()) {
       k << "  double2* const TAB = sm + " << tile_bufs * (1u << h.m) << ";\n";
       for (const Table& tb : tables) {
@@ -561,13 +607,22 @@ struct Gen {
       // Each thread stages its own 16 amplitudes of the next tile in its own
       // shared-memory slots (slot p*T + tid: conflict-free) with cp.async, so
       // HBM reads of tile i+1 overlap the arithmetic of tile i.
-      k << "  double2* const PB = sm + " << (tp.transposes && !single_buf ? (1u << h.m) : 0u) << ";\n";
+      k << "  double2* const PB = sm + " << (tbuf && !single_buf ? (1u << h.m) : 0u) << ";\n";
+      if (lead) {  // per-thread write / read offsets of the fused leading transpose
+        k << "  const unsigned W0 = " << xorexpr(mt0) << ";\n";
+        k << "  const unsigned R0 = " << xorexpr(mt0 + TB + 4) << ";\n";
+      }
       k << "  auto prefetch = [&](unsigned long long t) {\n";
       k << "    const unsigned long long tb = base_of(t) | rank_base;\n";
       k << "    if ((tb & dmask) != dval) { cp_async_commit(); return; }  // zero tile: nothing to read\n";
       k << "    const unsigned long long g = tb | TL;\n";
-      for (int p = 0; p < 16; ++p)
-        k << "    cp_async16(PB + " << p * T << " + tid, amps + ((g | " << hexll(loff[p]) << ") & lmask));\n";
+      for (int p = 0; p < 16; ++p) {
+        if (lead)
+          k << "    cp_async16(PB + (W0 ^ " << slot_xor(mt0 + TB, p) << "u), amps + ((g | " << hexll(loff[p])
+            << ") & lmask));\n";
+        else
+          k << "    cp_async16(PB + " << p * T << " + tid, amps + ((g | " << hexll(loff[p]) << ") & lmask));\n";
+      }
       k << "    cp_async_commit();\n  };\n";
       k << "  unsigned long long tile = blockIdx.x;\n";
       k << "  if (tile < ntiles) prefetch(tile);\n";

@@ -28,7 +28,7 @@ uint64_t Plan::launches() const {
 }
 
 std::unique_ptr<Plan> make_plan(uint32_t n, const qs_gate* gates, uint64_t count, uint32_t mode,
-                                uint32_t max_fused_qubits, uint32_t global_qubits) {
+                                uint32_t max_fused_qubits, uint32_t global_qubits, bool sharded) {
   auto plan = std::make_unique<Plan>();
   plan->n = n;
   plan->g = global_qubits;
@@ -59,7 +59,7 @@ std::unique_ptr<Plan> make_plan(uint32_t n, const qs_gate* gates, uint64_t count
     }
   }
   if (plan->mode == QS_PLAN_TILED) {
-    plan_tiles(n, ops, plan->steps, global_qubits);
+    plan_tiles(n, ops, plan->steps, global_qubits, sharded);
     compile_tile_steps(plan->steps);
   } else {
     for (auto& op : ops) {

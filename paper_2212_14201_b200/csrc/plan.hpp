@@ -47,8 +47,9 @@ struct Plan {
 };
 
 // Lowers and plans `count` gates for an n-qubit state.
+// sharded: a plan for ShardSets (layout restored in place, no permutation steps).
 std::unique_ptr<Plan> make_plan(uint32_t n, const qs_gate* gates, uint64_t count, uint32_t mode,
-                                uint32_t max_fused_qubits, uint32_t global_qubits = 0);
+                                uint32_t max_fused_qubits, uint32_t global_qubits = 0, bool sharded = false);
 // make_plan through a small LRU keyed by the exact submitted bytes (gates,
 // custom matrices, options); QSB_PLAN_CACHE=0 disables it.
 std::shared_ptr<const Plan> cached_plan(uint32_t n, const qs_gate* gates, uint64_t count, uint32_t mode,

@@ -83,6 +83,7 @@ struct TileHeader {
 
 struct TileProgram {
   TileHeader h{};
+
   std::vector<TOp> ops;
   std::vector<uint32_t> meta;
   std::vector<double2> coef;
@@ -94,6 +95,14 @@ struct TileProgram {
   mutable std::map<uint64_t, std::shared_ptr<struct JitModule>> jit_xchg;  // exchange-fused variants, by local bits
   std::vector<double2> params;            // kernel parameter table (coef + generator constants)
 };
+// A pass that starts with a transpose out of the (coalesced) load layout: with
+// prefetching, the cp.async writes land directly in the transpose's slots, so
+// that transpose needs no shared-memory buffer or write phase of its own.
+inline bool leading_transpose(const TileProgram& tp) { return !tp.ops.empty() && tp.ops[0].type == TO_TRANSPOSE; }
+inline uint32_t buffered_transposes(const TileProgram& tp, bool prefetch) {
+  return tp.transposes - ((prefetch && leading_transpose(tp)) ? 1u : 0u);
+}
+
 
 // The coefficient table travels as a __grid_constant__ kernel parameter
 // (constant bank); the planner keeps every pass's tables below this size.
@@ -113,28 +122,25 @@ struct TileOptions {
   bool absorb_x = true;
   // Fold that permutation into the last tile pass when possible (out of place).
   bool fold_perm = true;
+  // The first register configuration is free: the prefetch writes the tile to
+  // shared memory in the layout of the first transpose, so a pass may start
+  // with the low qubits in registers at the cost of one barrier.
+  bool free_load = true;
   uint32_t global_qubits = 0;  // sharded states: top qubits are rank bits, never in a tile
 };
 TileOptions tile_options_from_env();
 
 void plan_tiles(uint32_t n, std::vector<Op>& ops, std::vector<Step>& steps, const TileOptions& opt);
-// Plans with and without qubit relabelling (unless fixed by QSB_TILE_REMAP)
-// and keeps the plan with fewer HBM passes.
-inline void plan_tiles(uint32_t n, std::vector<Op>& ops, std::vector<Step>& steps, uint32_t global_qubits = 0) {
-  TileOptions o = tile_options_from_env();
-  o.global_qubits = global_qubits;
-  if (std::getenv("QSB_TILE_REMAP")) {
-    plan_tiles(n, ops, steps, o);
-    return;
-  }
-  std::vector<Op> copy = ops;
-  std::vector<Step> plain, remapped;
-  o.remap = false;
-  plan_tiles(n, copy, plain, o);
-  o.remap = true;
-  plan_tiles(n, ops, remapped, o);
-  steps = remapped.size() < plain.size() ? std::move(remapped) : std::move(plain);
-}
+// Estimated HBM time of a plan in units of one light 12-qubit tile pass
+// (measured on B200, 30 qubits: 12-qubit passes with <= 2 shared-memory
+// transposes 5.8 ms, with 3 or more 6.8 ms; 13-qubit passes -- one CTA per SM,
+// single buffer -- 6.85 ms).
+double plan_cost(const std::vector<Step>& steps);
+// Plans with and without qubit relabelling (unless fixed by QSB_TILE_REMAP),
+// with 12- and, for large unsharded states, 13-qubit tiles (unless fixed by
+// QSB_TILE_M), and keeps the cheapest plan.
+void plan_tiles(uint32_t n, std::vector<Op>& ops, std::vector<Step>& steps, uint32_t global_qubits = 0,
+                bool sharded = false);
 // basis != null: the pass starts from |*basis> (global index) instead of
 // reading the state -- a reset fused into the first pass.
 // Exchange fused into a pass (sharded plans, peer memory): after the pass,

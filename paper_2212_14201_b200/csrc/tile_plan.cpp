@@ -213,6 +213,7 @@ struct Compiler {
   // possible.
   std::vector<std::vector<int>> succ;
   std::vector<int> indeg;
+  std::vector<int> scratch_;
 
   void build_dag(const std::vector<const POp*>& list) {
     const size_t N = list.size();
@@ -303,11 +304,24 @@ struct Compiler {
     return c;
   }
 
+  bool free_load = false;
+
   void compile(const std::vector<const POp*>& list) {
     build_dag(list);
     std::vector<char> done(list.size(), 0);
     cfgs.push_back(choose_greedy(nullptr, list, done, /*exclude_low=*/true));
     int cur = 0;
+    if (free_load) {
+      // The load layout must keep the low qubits on lanes (coalesced reads);
+      // if the best first register set holds one of them, start with a
+      // transpose out of the load layout -- the GPU fuses it into the
+      // prefetch (the cp.async destinations are the transpose's write slots).
+      Cfg c1 = choose_greedy(&cfgs[0], list, done, /*exclude_low=*/false);
+      bool low_reg = false;
+      for (int k = 0; k < kTileR; ++k) low_reg |= c1.reg[k] < static_cast<int>(L);
+      if (low_reg && simulate(c1, list, done, scratch_).first > simulate(cfgs[0], list, done, scratch_).first)
+        transpose_to(cur, c1);
+    }
 
     int open = -1;           // open PHASE aop
     uint64_t x_open = 0;     // non-diagonal targets since it opened
@@ -604,6 +618,7 @@ std::shared_ptr<TileProgram> finalize(Compiler& C, uint64_t gates, const std::ve
         for (uint32_t k = 0; k < C.t; ++k) tp->meta.push_back(sw.phys(1u << fb.thr[k]));
         for (int k = 0; k < kTileR; ++k) tp->meta.push_back(sw.phys(1u << fb.reg[k]));
         for (uint32_t k = 0; k < C.t; ++k) tp->meta.push_back(C.S[fb.thr[k]]);
+        for (int k = 0; k < kTileR; ++k) tp->meta.push_back(C.S[fb.reg[k]]);
         ++tp->transposes;
         break;
       }
@@ -643,6 +658,7 @@ TileOptions tile_options_from_env() {
   if (const char* e = std::getenv("QSB_PERM_STEP")) o.perm_step = std::atoi(e) != 0;
   if (const char* e = std::getenv("QSB_ABSORB_X")) o.absorb_x = std::atoi(e) != 0;
   if (const char* e = std::getenv("QSB_FOLD_PERM")) o.fold_perm = std::atoi(e) != 0;
+  if (const char* e = std::getenv("QSB_FREE_LOAD")) o.free_load = std::atoi(e) != 0;
   o.m = std::max<uint32_t>(8, std::min<uint32_t>(kTileMaxM, o.m));
   o.low = std::min<uint32_t>(5, o.low);
   return o;
@@ -1001,6 +1017,7 @@ void plan_tiles(uint32_t n, std::vector<Op>& ops, std::vector<Step>& steps, cons
     C.m = m;
     C.t = m - kTileR;
     C.L = L;
+    C.free_load = opt.free_load;
     for (int q = 0; q < 64; ++q) C.tb[q] = -1;
     for (uint32_t q = 0; q < n; ++q)
       if ((S >> q) & 1) {
@@ -1023,8 +1040,8 @@ void plan_tiles(uint32_t n, std::vector<Op>& ops, std::vector<Step>& steps, cons
     if (std::getenv("QSB_PLAN_DEBUG")) {
       int counts[16] = {0};
       for (const auto& o : prog->ops) counts[o.type & 15]++;
-      std::fprintf(stderr, "pass %zu: ops=%zu gates=%zu transposes=%u mat1=%d flip=%d phase=%d dense=%d relabel=%d S=",
-                   steps.size(), prog->ops.size(), gates, prog->transposes,
+      std::fprintf(stderr, "pass %zu: ops=%zu gates=%zu lead=%d transposes=%u mat1=%d flip=%d phase=%d dense=%d relabel=%d S=",
+                   steps.size(), prog->ops.size(), gates, int(leading_transpose(*prog)), prog->transposes,
                    counts[TO_MAT1] + counts[TO_MAT1_REAL] + counts[TO_MAT1_RX], counts[TO_FLIP], counts[TO_PHASE],
                    counts[TO_DENSE2] + counts[TO_DENSE3], counts[TO_RELABEL]);
       for (auto q : C_S_debug(S, n)) std::fprintf(stderr, "%u,", q);
@@ -1263,6 +1280,49 @@ void plan_tiles(uint32_t n, std::vector<Op>& ops, std::vector<Step>& steps, cons
     for (const auto& e : extra) list.push_back(&e);
     push_step(compile_pass(S, list, {}), S, 0);
   }
+}
+
+double plan_cost(const std::vector<Step>& steps) {
+  double c = 0;
+  for (const Step& st : steps) {
+    if (st.kind != Step::TileStep) {
+      c += 1.0;
+      continue;
+    }
+    const TileProgram& tp = *st.tile;
+    if (tp.h.m >= 13) c += 1.18;
+    else c += buffered_transposes(tp, true) >= 3 ? 1.17 : 1.0;
+  }
+  return c;
+}
+
+void plan_tiles(uint32_t n, std::vector<Op>& ops, std::vector<Step>& steps, uint32_t global_qubits, bool sharded) {
+  TileOptions o = tile_options_from_env();
+  o.global_qubits = global_qubits;
+  if (sharded) o.perm_step = false;  // shards restore their layout in place
+  std::vector<uint32_t> ms{o.m};
+  // 13-qubit tiles: 2^13 tiles and more (enough CTAs), unsharded
+  if (!std::getenv("QSB_TILE_M") && !sharded && n >= 26) ms.push_back(13);
+  std::vector<int> remaps{0, 1};
+  if (const char* e = std::getenv("QSB_TILE_REMAP")) remaps = {std::atoi(e) != 0 ? 1 : 0};
+  const std::vector<Op> orig = ops;
+  double best = 0;
+  bool have = false;
+  for (uint32_t m : ms)
+    for (int r : remaps) {
+      std::vector<Op> copy = orig;
+      std::vector<Step> cand;
+      o.m = m;
+      o.remap = r != 0;
+      plan_tiles(n, copy, cand, o);
+      const double c = plan_cost(cand);
+      if (!have || c < best - 1e-9) {
+        best = c;
+        steps = std::move(cand);
+        ops = std::move(copy);
+        have = true;
+      }
+    }
 }
 
 }  // namespace qsb
