@@ -1,6 +1,6 @@
 // CUDA source generator for one tile pass (included by jit.cpp only).
 //
-// Emits straight-line code over 16 SSA amplitude values per thread:
+// Emits straight-line code over 2^r (16 or 32) SSA amplitude values per thread:
 //   * FLIPs on register bits (and register-controlled CNOTs) are renamings;
 //   * diagonal phases are deferred: a per-thread scalar (thread / tile-
 //     dependent factors) that commutes with every register-local gate, and
@@ -34,8 +34,10 @@ struct Gen {
   const TileProgram& tp;
   std::ostringstream pro;   // before the tile loop (per-thread constants)
   std::ostringstream s;     // tile-loop body
-  std::string name[16];
-  cd K[16];                 // pending per-slot constant factors
+  const int R;              // register bits
+  const int NS;             // register slots (2^R)
+  std::string name[kTileMaxSlots];
+  cd K[kTileMaxSlots];                 // pending per-slot constant factors
   std::string Fp;           // pending per-thread scalar factor (empty = 1)
   cd Kg = 1.0;              // pending tile-wide constant scalar
   std::vector<double2> extra;  // coefficients appended after tp.coef
@@ -55,6 +57,11 @@ struct Gen {
   // per CTA, two resident CTAs per SM); the next tile's copies are issued
   // after the last transpose has read the buffer.
   bool single_buf = false;
+  // early (single_buf only): the first `early` register slots of the next
+  // tile are staged in a second region PE and issued as soon as the current
+  // tile has read them (the rest follow the last transpose), so most of the
+  // next tile's HBM reads overlap this tile's transposes.
+  uint32_t early = 0;
   int transposes_total = 0;
 
   // Tile-wide phase factors from qubits outside the tile: a product over up
@@ -75,7 +82,7 @@ struct Gen {
     return q - below;
   }
 
-  explicit Gen(const TileProgram& p) : tp(p) {
+  explicit Gen(const TileProgram& p) : tp(p), R(static_cast<int>(p.h.r)), NS(1 << p.h.r) {
     for (auto& k : K) k = 1.0;
   }
 
@@ -125,7 +132,7 @@ struct Gen {
   // store, the tile-wide scalar Kg).
   void flush_all(bool with_global) {
     const cd g = with_global ? Kg : cd(1.0);
-    for (int p = 0; p < 16; ++p) {
+    for (int p = 0; p < NS; ++p) {
       const cd kp = K[p] * g;
       const bool k1 = one(kp);
       if (k1 && Fp.empty()) continue;
@@ -172,7 +179,7 @@ struct Gen {
     const int Kb = o.k;
     std::string xc[2];
     for (int r = 0; r < 2; ++r) xc[r] = kconst(rows[r].x);
-    for (int p = 0; p < 16; ++p) {
+    for (int p = 0; p < NS; ++p) {
       if ((p >> Kb) & 1) continue;
       const int p1 = p | (1 << Kb);
       flush_pair(p, p1);
@@ -206,7 +213,7 @@ struct Gen {
     const std::string t = pred(o);
     const int Kb = o.k;
     const std::string m0 = coef(o.coef), m1 = coef(o.coef + 1), m2 = coef(o.coef + 2), m3 = coef(o.coef + 3);
-    for (int p = 0; p < 16; ++p) {
+    for (int p = 0; p < NS; ++p) {
       if ((p >> Kb) & 1) continue;
       if ((p & o.rmask) != o.rval) continue;
       const int p1 = p | (1 << Kb);
@@ -231,7 +238,7 @@ struct Gen {
   void flip(const TOp& o) {
     const int Kb = o.k;
     const std::string t = o.gmask ? pred(o) : "";
-    for (int p = 0; p < 16; ++p) {
+    for (int p = 0; p < NS; ++p) {
       if ((p >> Kb) & 1) continue;
       if ((p & o.rmask) != o.rval) continue;
       const int p1 = p | (1 << Kb);
@@ -260,8 +267,8 @@ struct Gen {
       int tb = -1;
       for (uint32_t k = 0; k < tp.h.t; ++k)
         if (cur_tq[k] == q) tb = static_cast<int>(k);
-      if (tb >= 0) thr.push_back({static_cast<uint32_t>(tb), o.coef + 17 + j});
-      else out.push_back({q, o.coef + 17 + j});
+      if (tb >= 0) thr.push_back({static_cast<uint32_t>(tb), o.coef + NS + 1 + j});
+      else out.push_back({q, o.coef + NS + 1 + j});
     }
     std::string F;
     if (!thr.empty()) {  // per-thread constant, hoisted out of the tile loop
@@ -269,11 +276,11 @@ struct Gen {
       pro << "  double2 " << F << " = make_double2(1.0, 0.0);\n";
       for (auto& [b, ci] : thr) pro << "  if ((tid >> " << b << ") & 1u) " << F << " = cmul(" << F << ", " << coef(ci) << ");\n";
     }
-    const bool c1 = one(coefv(o.coef + 16));
+    const bool c1 = one(coefv(o.coef + NS));
     if (!c1 || !out.empty()) {
       const std::string Fo = fresh("F");
-      s << "    double2 " << Fo << " = " << (F.empty() ? (c1 ? std::string("make_double2(1.0, 0.0)") : coef(o.coef + 16))
-                                                        : (c1 ? F : "cmul(" + F + ", " + coef(o.coef + 16) + ")"))
+      s << "    double2 " << Fo << " = " << (F.empty() ? (c1 ? std::string("make_double2(1.0, 0.0)") : coef(o.coef + NS))
+                                                        : (c1 ? F : "cmul(" + F + ", " + coef(o.coef + NS) + ")"))
         << ";\n";
       std::map<uint32_t, std::vector<std::pair<uint32_t, uint32_t>>> by_chunk;
       for (auto& [q, ci] : out) by_chunk[tix_bit(q) / kChunk].push_back({tix_bit(q) % kChunk, ci});
@@ -308,10 +315,10 @@ struct Gen {
         }
       }
       if (t.empty()) {
-        for (int p = 0; p < 16; ++p) K[p] *= coefv(o.coef + p);
+        for (int p = 0; p < NS; ++p) K[p] *= coefv(o.coef + p);
       } else {
         // thread-predicated register factors cannot be folded into constants
-        for (int p = 0; p < 16; ++p) {
+        for (int p = 0; p < NS; ++p) {
           const cd g = coefv(o.coef + p);
           if (!one(g)) set(p, "cmul(" + name[p] + ", " + coef(o.coef + p) + ")", t);
         }
@@ -322,14 +329,14 @@ struct Gen {
     // (compile time); only the thread/tile factor F is applied now, to the
     // selected slots (one complex multiply each)
     if (t.empty()) {
-      for (int p = 0; p < 16; ++p) {
+      for (int p = 0; p < NS; ++p) {
         if ((p & o.rmask) != o.rval) continue;
         K[p] *= coefv(o.coef + p);
         if (!F.empty()) set(p, "cmul(" + name[p] + ", " + F + ")", "");
       }
       return;
     }
-    for (int p = 0; p < 16; ++p) {
+    for (int p = 0; p < NS; ++p) {
       if ((p & o.rmask) != o.rval) continue;
       const cd g = coefv(o.coef + p);
       std::string f;
@@ -344,7 +351,7 @@ struct Gen {
   void dense(const TOp& o) {
     const std::string t = pred(o);
     const int KD = o.type == TO_DENSE2 ? 2 : 3, Gd = 1 << KD;
-    for (int hi = 0; hi < (16 >> KD); ++hi) {
+    for (int hi = 0; hi < (NS >> KD); ++hi) {
       const int p0 = hi << KD;
       if ((p0 & o.rmask) != o.rval) continue;
       bool same = true;
@@ -377,27 +384,31 @@ struct Gen {
     };
     s << "    __syncthreads();\n";
     s << "    const unsigned " << Tw << " = " << xorexpr(mt) << ";\n";
-    for (int p = 0; p < 16; ++p) {
+    for (int p = 0; p < NS; ++p) {
       uint32_t a = 0;
-      for (int k = 0; k < 4; ++k)
+      for (int k = 0; k < R; ++k)
         if ((p >> k) & 1) a ^= mt[TB + k];
       s << "    sm[" << Tw << " ^ " << a << "u] = " << name[p] << ";\n";
     }
     s << "    __syncthreads();\n";
-    s << "    const unsigned " << Tr << " = " << xorexpr(mt + TB + 4) << ";\n";
-    for (int p = 0; p < 16; ++p) {
+    s << "    const unsigned " << Tr << " = " << xorexpr(mt + TB + R) << ";\n";
+    for (int p = 0; p < NS; ++p) {
       uint32_t a = 0;
-      for (int k = 0; k < 4; ++k)
-        if ((p >> k) & 1) a ^= mt[2 * TB + 4 + k];
+      for (int k = 0; k < R; ++k)
+        if ((p >> k) & 1) a ^= mt[2 * TB + R + k];
       const std::string nv = fresh();
       s << "    const double2 " << nv << " = sm[" << Tr << " ^ " << a << "u];\n";
       name[p] = nv;
     }
-    emit_G(mt + 2 * TB + 8, false);
+    emit_G(mt + 2 * TB + 2 * R, false);
   }
 
   static constexpr const char* kIssueNext =
       "    { const unsigned long long nt = tile + gridDim.x; if (nt < ntiles) prefetch(nt); }\n";
+  static constexpr const char* kIssueEarly =
+      "    { const unsigned long long nt = tile + gridDim.x; if (nt < ntiles) prefetch_e(nt); }\n";
+  static constexpr const char* kIssueLate =
+      "    { const unsigned long long nt = tile + gridDim.x; if (nt < ntiles) prefetch_l(nt); }\n";
 
   std::string run(const std::string& kname, uint32_t threads, uint32_t minb) {
     const TileHeader& h = tp.h;
@@ -408,7 +419,7 @@ struct Gen {
     // leading transpose out of the load layout: fused into the prefetch (the
     // cp.async destinations are its write slots) or, from a basis state, into
     // the register initialisation
-    const bool lead = leading_transpose(tp) && (prefetch || from_basis);
+    const bool lead = leading_transpose(tp) && (from_basis || (prefetch && early == 0));
     const uint32_t* mt0 = lead ? tp.meta.data() + tp.ops[0].meta : nullptr;
     auto xorexpr = [&](const uint32_t* cols) {
       std::ostringstream e;
@@ -419,14 +430,14 @@ struct Gen {
     };
     auto slot_xor = [&](const uint32_t* cols, int p) {
       uint32_t a = 0;
-      for (int k = 0; k < 4; ++k)
+      for (int k = 0; k < R; ++k)
         if ((p >> k) & 1) a ^= cols[k];
       return a;
     };
-    unsigned long long loff[16];
-    for (int p = 0; p < 16; ++p) {
+    unsigned long long loff[kTileMaxSlots];
+    for (int p = 0; p < NS; ++p) {
       loff[p] = 0;
-      for (int k = 0; k < 4; ++k)
+      for (int k = 0; k < R; ++k)
         if ((p >> k) & 1) loff[p] |= h.load.rs[k];
     }
     // ---- tile-loop body
@@ -442,16 +453,16 @@ struct Gen {
         s << "      unsigned long long GZ = TLO;\n";
         for (uint32_t i = 0; i + h.m < h.n; ++i)
           s << "      if ((tix >> " << i << ") & 1ull) GZ |= " << hexll(1ull << h.out_pos[i]) << ";\n";
-        for (int p = 0; p < 16; ++p) {
+        for (int p = 0; p < NS; ++p) {
           unsigned long long off = 0;
-          for (int k = 0; k < 4; ++k)
+          for (int k = 0; k < R; ++k)
             if ((p >> k) & 1) off |= h.store.rs[k];
           s << "      __stcs(out + (GZ | " << hexll(off) << "), make_double2(0.0, 0.0));\n";
         }
       } else {
-        for (int p = 0; p < 16; ++p) {
+        for (int p = 0; p < NS; ++p) {
           unsigned long long off = 0;
-          for (int k = 0; k < 4; ++k)
+          for (int k = 0; k < R; ++k)
             if ((p >> k) & 1) off |= h.store.rs[k];
           s << "      __stcs(amps + ((base | TLS | " << hexll(off) << ") & lmask), make_double2(0.0, 0.0));\n";
         }
@@ -462,20 +473,20 @@ struct Gen {
     }
     int ti = 0;
     if (from_basis) {
-      unsigned long long off[16];
-      for (int p = 0; p < 16; ++p) {
+      unsigned long long off[kTileMaxSlots];
+      for (int p = 0; p < NS; ++p) {
         off[p] = loff[p];
         if (lead) {  // registers start in the layout after the leading transpose
           off[p] = 0;
-          for (int k = 0; k < 4; ++k)
-            if ((p >> k) & 1) off[p] |= 1ull << mt0[3 * TB + 8 + k];
+          for (int k = 0; k < R; ++k)
+            if ((p >> k) & 1) off[p] |= 1ull << mt0[3 * TB + 2 * R + k];
         }
       }
       if (lead) {
-        emit_G(mt0 + 2 * TB + 8, false);
+        emit_G(mt0 + 2 * TB + 2 * R, false);
         ti = 1;
       }
-      for (int p = 0; p < 16; ++p) {
+      for (int p = 0; p < NS; ++p) {
         name[p] = fresh();
         s << "    const double2 " << name[p] << " = make_double2(((G | " << hexll(off[p])
           << ") == basis) ? 1.0 : 0.0, 0.0);\n";
@@ -484,22 +495,30 @@ struct Gen {
       s << "    cp_async_wait_all();\n";
       if (lead) {
         s << "    __syncthreads();\n";
-        for (int p = 0; p < 16; ++p) {
+        for (int p = 0; p < NS; ++p) {
           name[p] = fresh();
-          s << "    const double2 " << name[p] << " = PB[R0 ^ " << slot_xor(mt0 + 2 * TB + 4, p) << "u];\n";
+          s << "    const double2 " << name[p] << " = PB[R0 ^ " << slot_xor(mt0 + 2 * TB + R, p) << "u];\n";
         }
-        emit_G(mt0 + 2 * TB + 8, false);
+        emit_G(mt0 + 2 * TB + 2 * R, false);
         ti = 1;
         if (!single_buf || transposes_total == 1) s << "    __syncthreads();\n" << kIssueNext;
       } else {
-        for (int p = 0; p < 16; ++p) {
+        for (int p = 0; p < NS; ++p) {
           name[p] = fresh();
-          s << "    const double2 " << name[p] << " = PB[" << p * T << " + tid];\n";
+          if (static_cast<uint32_t>(p) < early)
+            s << "    const double2 " << name[p] << " = PE[" << p * T << " + tid];\n";
+          else
+            s << "    const double2 " << name[p] << " = PB[" << (p - static_cast<int>(early)) * T << " + tid];\n";
         }
-        if (!single_buf || transposes_total == 0) s << kIssueNext;
+        if (early) {  // own slots only: no barrier before re-filling them
+          s << kIssueEarly;
+          if (transposes_total == 0) s << kIssueLate;
+        } else if (!single_buf || transposes_total == 0) {
+          s << kIssueNext;
+        }
       }
     } else {
-      for (int p = 0; p < 16; ++p) {
+      for (int p = 0; p < NS; ++p) {
         name[p] = fresh();
         s << "    const double2 " << name[p] << " = __ldcs(amps + ((G | " << hexll(loff[p]) << ") & lmask));\n";
       }
@@ -518,7 +537,8 @@ struct Gen {
         case TO_DENSE3: dense(o); break;
         case TO_TRANSPOSE:
           transpose(o, ti++);
-          if (prefetch && single_buf && ti == transposes_total) s << "    __syncthreads();\n" << kIssueNext;
+          if (prefetch && single_buf && ti == transposes_total)
+            s << "    __syncthreads();\n" << (early ? kIssueLate : kIssueNext);
           break;
         case TO_RELABEL: emit_G(tp.meta.data() + o.meta, false); break;
         default: throw RuntimeError("jit: unknown micro-op");
@@ -530,9 +550,9 @@ struct Gen {
     if (xk) {
       unsigned long long pmask = 0;
       for (uint32_t i = 0; i < xk; ++i) pmask |= 1ull << xlpos[i];
-      for (int p = 0; p < 16; ++p) {
+      for (int p = 0; p < NS; ++p) {
         unsigned long long off = 0;
-        for (int k = 0; k < 4; ++k)
+        for (int k = 0; k < R; ++k)
           if ((p >> k) & 1) off |= h.store.rs[k];
         s << "    { const unsigned long long L = (G | " << hexll(off) << ") & lmask; const unsigned d = 0u";
         for (uint32_t i = 0; i < xk; ++i) s << " | ((unsigned)((L >> " << xlpos[i] << ") & 1ull) << " << i << ")";
@@ -544,17 +564,17 @@ struct Gen {
       s << "    unsigned long long GO = TLO;\n";
       for (uint32_t i = 0; i + h.m < h.n; ++i)
         s << "    if ((tix >> " << i << ") & 1ull) GO |= " << hexll(1ull << h.out_pos[i]) << ";\n";
-      for (int p = 0; p < 16; ++p) {
+      for (int p = 0; p < NS; ++p) {
         unsigned long long off = 0;
-        for (int k = 0; k < 4; ++k)
+        for (int k = 0; k < R; ++k)
           if ((p >> k) & 1) off |= h.store.rs[k];
         s << "    __stcs(out + (GO | " << hexll(off) << "), " << name[p] << ");\n";
       }
     } else {
       if (ti == 0 && std::memcmp(&h.load, &h.store, sizeof(TileConfigAddr)) != 0) s << "    __syncthreads();\n";
-      for (int p = 0; p < 16; ++p) {
+      for (int p = 0; p < NS; ++p) {
         unsigned long long off = 0;
-        for (int k = 0; k < 4; ++k)
+        for (int k = 0; k < R; ++k)
           if ((p >> k) & 1) off |= h.store.rs[k];
         s << "    __stcs(amps + ((G | " << hexll(off) << ") & lmask), " << name[p] << ");\n";
       }
@@ -594,8 +614,9 @@ struct Gen {
     k << pro.str();
     const uint32_t tbuf = tp.transposes - (lead ? 1u : 0u);
     const uint32_t tile_bufs = single_buf ? 1u : (tbuf ? 1u : 0u) + (prefetch ? 1u : 0u);
+    const uint32_t early_amps = prefetch ? early * T : 0u;
     if (!tables.empty()) {
-      k << "  double2* const TAB = sm + " << tile_bufs * (1u << h.m) << ";\n";
+      k << "  double2* const TAB = sm + " << tile_bufs * (1u << h.m) + early_amps << ";\n";
       for (const Table& tb : tables) {
         k << "  for (unsigned e = tid; e < 64u; e += " << threads << "u) {\n    double2 f = make_double2(1.0, 0.0);\n";
         for (auto& [b, ci] : tb.bits) k << "    if ((e >> " << b << ") & 1u) f = cmul(f, " << coef(ci) << ");\n";
@@ -610,20 +631,33 @@ struct Gen {
       k << "  double2* const PB = sm + " << (tbuf && !single_buf ? (1u << h.m) : 0u) << ";\n";
       if (lead) {  // per-thread write / read offsets of the fused leading transpose
         k << "  const unsigned W0 = " << xorexpr(mt0) << ";\n";
-        k << "  const unsigned R0 = " << xorexpr(mt0 + TB + 4) << ";\n";
+        k << "  const unsigned R0 = " << xorexpr(mt0 + TB + R) << ";\n";
       }
-      k << "  auto prefetch = [&](unsigned long long t) {\n";
-      k << "    const unsigned long long tb = base_of(t) | rank_base;\n";
-      k << "    if ((tb & dmask) != dval) { cp_async_commit(); return; }  // zero tile: nothing to read\n";
-      k << "    const unsigned long long g = tb | TL;\n";
-      for (int p = 0; p < 16; ++p) {
-        if (lead)
-          k << "    cp_async16(PB + (W0 ^ " << slot_xor(mt0 + TB, p) << "u), amps + ((g | " << hexll(loff[p])
-            << ") & lmask));\n";
-        else
-          k << "    cp_async16(PB + " << p * T << " + tid, amps + ((g | " << hexll(loff[p]) << ") & lmask));\n";
+      auto lambda = [&](const char* fname, int p0, int p1) {
+        k << "  auto " << fname << " = [&](unsigned long long t) {\n";
+        k << "    const unsigned long long tb = base_of(t) | rank_base;\n";
+        k << "    if ((tb & dmask) != dval) { cp_async_commit(); return; }  // zero tile: nothing to read\n";
+        k << "    const unsigned long long g = tb | TL;\n";
+        for (int p = p0; p < p1; ++p) {
+          if (lead)
+            k << "    cp_async16(PB + (W0 ^ " << slot_xor(mt0 + TB, p) << "u), amps + ((g | " << hexll(loff[p])
+              << ") & lmask));\n";
+          else if (static_cast<uint32_t>(p) < early)
+            k << "    cp_async16(PE + " << p * T << " + tid, amps + ((g | " << hexll(loff[p]) << ") & lmask));\n";
+          else
+            k << "    cp_async16(PB + " << (p - static_cast<int>(early)) * T << " + tid, amps + ((g | "
+              << hexll(loff[p]) << ") & lmask));\n";
+        }
+        k << "    cp_async_commit();\n  };\n";
+      };
+      if (early) {
+        k << "  double2* const PE = sm + " << tile_bufs * (1u << h.m) << ";\n";
+        lambda("prefetch_e", 0, static_cast<int>(early));
+        lambda("prefetch_l", static_cast<int>(early), NS);
+        k << "  auto prefetch = [&](unsigned long long t) { prefetch_e(t); prefetch_l(t); };\n";
+      } else {
+        lambda("prefetch", 0, NS);
       }
-      k << "    cp_async_commit();\n  };\n";
       k << "  unsigned long long tile = blockIdx.x;\n";
       k << "  if (tile < ntiles) prefetch(tile);\n";
       k << "  for (; tile < ntiles; tile += gridDim.x) {\n";

@@ -596,15 +596,26 @@ void shard_execute(ShardSet& ss, const Plan& p, uint64_t first, uint64_t count, 
 void shard_execute_from_basis(ShardSet& ss, const Plan& p, uint64_t basis) {
   if (p.n != ss.n || p.g != ss.g) throw ValidationError("plan was compiled for a different state shape");
   if (basis >> ss.n) throw ValidationError("basis index out of range");
-  uint64_t first = 0;
-  if (!p.steps.empty() && p.steps[0].kind == Step::TileStep) {
-    const TileSkip k = zero_tiles(p.steps[0], basis);
-    for (auto& s : ss.shards) launch_tile(*s, *p.steps[0].tile, &basis, nullptr, &k);  // one shard holds |basis>
-    first = 1;
+  // Exchanges before the first pass move a basis state to another basis state:
+  // start from that one instead (QFT: the qubits that receive H last start in
+  // the rank slots, SURVEY 8e -- one all-to-all fewer).
+  uint64_t b = basis, first = 0;
+  const uint32_t nl = ss.n - ss.g;
+  for (; first < p.steps.size() && p.steps[first].kind == Step::SwapStep; ++first) {
+    const Step& st = p.steps[first];
+    for (size_t i = 0; i < st.gpos.size(); ++i) {
+      const uint32_t hi = nl + st.gpos[i], lo = st.lpos[i];
+      if (((b >> hi) ^ (b >> lo)) & 1) b ^= (1ull << hi) | (1ull << lo);
+    }
+  }
+  if (first < p.steps.size() && p.steps[first].kind == Step::TileStep) {
+    const TileSkip k = zero_tiles(p.steps[first], basis);  // forms are in the submitted basis bits
+    for (auto& s : ss.shards) launch_tile(*s, *p.steps[first].tile, &b, nullptr, &k);  // one shard holds |b>
+    ++first;
   } else {
     for (auto& s : ss.shards) {
-      const bool mine = (basis >> s->local_qubits()) == s->rank;
-      fill_basis(*s, mine ? (basis & (s->size - 1)) : ~0ull);
+      const bool mine = (b >> s->local_qubits()) == s->rank;
+      fill_basis(*s, mine ? (b & (s->size - 1)) : ~0ull);
     }
   }
   shard_execute(ss, p, first, ~0ull, &basis);

@@ -33,9 +33,11 @@
 
 namespace qsb {
 
-constexpr int kTileR = 4;       // register bits: 16 amplitudes per thread
+constexpr int kTileMinR = 4;    // register bits: 16 amplitudes per thread ...
+constexpr int kTileMaxR = 5;    // ... or 32 (13-qubit tiles: fewer transposes)
 constexpr int kTileMaxM = 13;   // tile qubits (2^13 x 16 B = 128 KiB of smem)
-constexpr int kTileMaxT = kTileMaxM - kTileR;
+constexpr int kTileMaxT = kTileMaxM - kTileMinR;
+constexpr int kTileMaxSlots = 1 << kTileMaxR;
 
 enum TOpType : uint8_t {
   TO_MAT1 = 1,     // general 2x2 on register bit k
@@ -65,7 +67,7 @@ struct TOp {
 // register bit k holds qubit with stride rs[k].
 struct TileConfigAddr {
   uint32_t tq[kTileMaxT];
-  unsigned long long rs[kTileR];
+  unsigned long long rs[kTileMaxR];
 };
 
 struct TileHeader {
@@ -79,6 +81,7 @@ struct TileHeader {
   // out_pos[i] is the output bit of tile-index bit i (non-tile qubits, ascending).
   uint32_t oop = 0;
   uint8_t out_pos[64] = {};
+  uint32_t r = 4;  // register bits (2^r amplitudes per thread, t = m - r thread bits)
 };
 
 struct TileProgram {
@@ -112,6 +115,7 @@ constexpr uint32_t kParamLimitBytes = 32 * 1024 - 256;
 
 struct TileOptions {
   uint32_t m = 12;  // tile qubits
+  uint32_t r = 4;   // register qubits per thread
   uint32_t low = 4; // qubits 0..low-1 always in the tile: 256 B contiguous runs
                     // (measured: 128 B runs 70% of HBM per pass, 256 B 80%)
   bool remap = true;  // plan-level qubit relabelling (low slots hold the qubits needed next)

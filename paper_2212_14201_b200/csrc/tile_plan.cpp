@@ -109,7 +109,7 @@ size_t scan(const std::vector<POp>& pops, const std::vector<uint32_t>& rem, uint
 }
 
 struct Cfg {
-  int reg[kTileR];
+  int reg[kTileMaxR];
   int thr[kTileMaxT];
 };
 
@@ -132,13 +132,14 @@ struct AOp {
 
 struct Compiler {
   uint32_t n, m, t, L;
+  int R = 4;  // register bits
   std::vector<uint32_t> S;
   int tb[64];
   std::vector<Cfg> cfgs;
   std::vector<AOp> aops;
 
   bool has_reg(const Cfg& c, int x, int* pos = nullptr) const {
-    for (int k = 0; k < kTileR; ++k)
+    for (int k = 0; k < R; ++k)
       if (c.reg[k] == x) {
         if (pos) *pos = k;
         return true;
@@ -156,7 +157,7 @@ struct Compiler {
   // bits; the rest ascending.
   void fill_threads(Cfg& c, bool load = false) const {
     std::vector<char> used(m, 0);
-    for (int k = 0; k < kTileR; ++k) used[c.reg[k]] = 1;
+    for (int k = 0; k < R; ++k) used[c.reg[k]] = 1;
     for (uint32_t k = 0; k < t; ++k) c.thr[k] = -1;
     for (uint32_t k = 0; k < L; ++k) {
       const int y = load ? static_cast<int>(k) : lane[k];
@@ -259,7 +260,7 @@ struct Compiler {
   Cfg choose_greedy(const Cfg* cur, const std::vector<const POp*>& list, const std::vector<char>& done,
                     bool exclude_low) {
     Cfg c;
-    for (int k = 0; k < kTileR; ++k) c.reg[k] = -1;
+    for (int k = 0; k < R; ++k) c.reg[k] = -1;
     std::vector<char> placed(m, 0);
     // a blocked dense op at the front dictates exact slots
     for (size_t j = 0; j < list.size(); ++j) {
@@ -276,7 +277,7 @@ struct Compiler {
       break;
     }
     std::vector<int> scratch;
-    for (int k = 0; k < kTileR; ++k) {
+    for (int k = 0; k < R; ++k) {
       if (c.reg[k] >= 0) continue;
       int best = -1;
       std::pair<int, int> bs{-1, -2000000};
@@ -318,7 +319,7 @@ struct Compiler {
       // prefetch (the cp.async destinations are the transpose's write slots).
       Cfg c1 = choose_greedy(&cfgs[0], list, done, /*exclude_low=*/false);
       bool low_reg = false;
-      for (int k = 0; k < kTileR; ++k) low_reg |= c1.reg[k] < static_cast<int>(L);
+      for (int k = 0; k < R; ++k) low_reg |= c1.reg[k] < static_cast<int>(L);
       if (low_reg && simulate(c1, list, done, scratch_).first > simulate(cfgs[0], list, done, scratch_).first)
         transpose_to(cur, c1);
     }
@@ -388,7 +389,7 @@ struct Compiler {
         case PK::SwapRel: {
           const int a = tb[p.op.targets[0]], b = tb[p.op.targets[1]];
           Cfg c = cfgs[cur];
-          for (int k = 0; k < kTileR; ++k) c.reg[k] = c.reg[k] == a ? b : (c.reg[k] == b ? a : c.reg[k]);
+          for (int k = 0; k < R; ++k) c.reg[k] = c.reg[k] == a ? b : (c.reg[k] == b ? a : c.reg[k]);
           for (uint32_t k = 0; k < t; ++k) c.thr[k] = c.thr[k] == a ? b : (c.thr[k] == b ? a : c.thr[k]);
           cfgs.push_back(c);
           cur = static_cast<int>(cfgs.size() - 1);
@@ -446,7 +447,7 @@ struct Compiler {
     if (!store_ok(cfgs[cur])) {
       Cfg c = cfgs[cur];
       bool lane_in_reg = false;
-      for (int k = 0; k < kTileR; ++k)
+      for (int k = 0; k < R; ++k)
         if (is_store_lane(c.reg[k])) lane_in_reg = true;
       if (lane_in_reg) c = default_cfg();
       else fill_threads(c);
@@ -466,8 +467,8 @@ struct Compiler {
     Cfg c;
     // registers: the highest tile bits not reserved for the store lanes
     int k = 0;
-    for (int y = static_cast<int>(m) - 1; y >= 0 && k < kTileR; --y)
-      if (!is_store_lane(y) || m - L < kTileR) c.reg[k++] = y;
+    for (int y = static_cast<int>(m) - 1; y >= 0 && k < R; --y)
+      if (!is_store_lane(y) || m - L < static_cast<uint32_t>(R)) c.reg[k++] = y;
     fill_threads(c);
     return c;
   }
@@ -514,12 +515,13 @@ std::shared_ptr<TileProgram> finalize(Compiler& C, uint64_t gates, const std::ve
   h.n = C.n;
   h.m = C.m;
   h.t = C.t;
+  h.r = static_cast<uint32_t>(C.R);
   for (uint32_t b = 0; b < C.m; ++b) h.S[b] = C.S[b];
   h.ntiles = 1ull << (C.n - C.m);
   auto sg = [&](uint32_t q) { return sigma ? (*sigma)[q] : q; };
   auto addr_of = [&](const Cfg& c, TileConfigAddr& a, bool out) {
     for (uint32_t k = 0; k < C.t; ++k) a.tq[k] = out ? sg(C.S[c.thr[k]]) : C.S[c.thr[k]];
-    for (int k = 0; k < kTileR; ++k) a.rs[k] = 1ull << (out ? sg(C.S[c.reg[k]]) : C.S[c.reg[k]]);
+    for (int k = 0; k < C.R; ++k) a.rs[k] = 1ull << (out ? sg(C.S[c.reg[k]]) : C.S[c.reg[k]]);
   };
   addr_of(C.cfgs[0], h.load, false);
   addr_of(C.cfgs[C.final_cfg], h.store, true);
@@ -584,14 +586,15 @@ std::shared_ptr<TileProgram> finalize(Compiler& C, uint64_t gates, const std::ve
       }
       case TO_PHASE: {
         split_pred(c, a.pred, o, a.pred_val);
-        cd G[16];
-        for (int p = 0; p < 16; ++p) G[p] = 1.0;
+        const int NS = 1 << C.R;
+        cd G[kTileMaxSlots];
+        for (int p = 0; p < NS; ++p) G[p] = 1.0;
         std::vector<std::pair<uint32_t, cd>> list;
         for (const auto& [q, w] : a.w) {
           if (w == cd(1.0)) continue;
           int pos;
           if (C.tb[q] >= 0 && C.has_reg(c, C.tb[q], &pos)) {
-            for (int p = 0; p < 16; ++p)
+            for (int p = 0; p < NS; ++p)
               if ((p >> pos) & 1) G[p] *= w;
           } else {
             list.push_back({q, w});
@@ -600,7 +603,7 @@ std::shared_ptr<TileProgram> finalize(Compiler& C, uint64_t gates, const std::ve
         o.coef = static_cast<uint32_t>(tp->coef.size());
         o.meta = static_cast<uint32_t>(tp->meta.size());
         o.nlist = static_cast<uint16_t>(list.size());
-        for (int p = 0; p < 16; ++p) tp->coef.push_back(make_double2(G[p].real(), G[p].imag()));
+        for (int p = 0; p < NS; ++p) tp->coef.push_back(make_double2(G[p].real(), G[p].imag()));
         tp->coef.push_back(make_double2(a.c.real(), a.c.imag()));
         for (auto& [q, w] : list) {
           tp->coef.push_back(make_double2(w.real(), w.imag()));
@@ -614,11 +617,11 @@ std::shared_ptr<TileProgram> finalize(Compiler& C, uint64_t gates, const std::ve
         const Swizzle sw = pick_swizzle(fa, fb, C.m, C.t);
         o.meta = static_cast<uint32_t>(tp->meta.size());
         for (uint32_t k = 0; k < C.t; ++k) tp->meta.push_back(sw.phys(1u << fa.thr[k]));
-        for (int k = 0; k < kTileR; ++k) tp->meta.push_back(sw.phys(1u << fa.reg[k]));
+        for (int k = 0; k < C.R; ++k) tp->meta.push_back(sw.phys(1u << fa.reg[k]));
         for (uint32_t k = 0; k < C.t; ++k) tp->meta.push_back(sw.phys(1u << fb.thr[k]));
-        for (int k = 0; k < kTileR; ++k) tp->meta.push_back(sw.phys(1u << fb.reg[k]));
+        for (int k = 0; k < C.R; ++k) tp->meta.push_back(sw.phys(1u << fb.reg[k]));
         for (uint32_t k = 0; k < C.t; ++k) tp->meta.push_back(C.S[fb.thr[k]]);
-        for (int k = 0; k < kTileR; ++k) tp->meta.push_back(C.S[fb.reg[k]]);
+        for (int k = 0; k < C.R; ++k) tp->meta.push_back(C.S[fb.reg[k]]);
         ++tp->transposes;
         break;
       }
@@ -653,6 +656,7 @@ std::vector<uint32_t> C_S_debug(uint64_t S, uint32_t n) {
 TileOptions tile_options_from_env() {
   TileOptions o;
   if (const char* e = std::getenv("QSB_TILE_M")) o.m = static_cast<uint32_t>(std::atoi(e));
+  if (const char* e = std::getenv("QSB_TILE_R")) o.r = static_cast<uint32_t>(std::atoi(e));
   if (const char* e = std::getenv("QSB_TILE_LOW")) o.low = static_cast<uint32_t>(std::atoi(e));
   if (const char* e = std::getenv("QSB_TILE_REMAP")) o.remap = std::atoi(e) != 0;
   if (const char* e = std::getenv("QSB_PERM_STEP")) o.perm_step = std::atoi(e) != 0;
@@ -660,6 +664,7 @@ TileOptions tile_options_from_env() {
   if (const char* e = std::getenv("QSB_FOLD_PERM")) o.fold_perm = std::atoi(e) != 0;
   if (const char* e = std::getenv("QSB_FREE_LOAD")) o.free_load = std::atoi(e) != 0;
   o.m = std::max<uint32_t>(8, std::min<uint32_t>(kTileMaxM, o.m));
+  o.r = std::max<uint32_t>(kTileMinR, std::min<uint32_t>(kTileMaxR, o.r));
   o.low = std::min<uint32_t>(5, o.low);
   return o;
 }
@@ -837,7 +842,8 @@ void plan_tiles(uint32_t n, std::vector<Op>& ops, std::vector<Step>& steps, cons
   // (pairwise half-shard exchange) that brings that qubit into the shard.
   const uint32_t nl = n - opt.global_qubits;
   const uint32_t m = std::min<uint32_t>(nl, opt.m);
-  const uint32_t L = std::min<uint32_t>(opt.low, m - kTileR);
+  const uint32_t R = m >= opt.r + 4 ? opt.r : static_cast<uint32_t>(kTileMinR);  // register bits
+  const uint32_t L = std::min<uint32_t>(opt.low, m - R);
   const uint64_t lowmask = (1ull << L) - 1;
   const uint64_t allmask = nl >= 64 ? ~0ull : (1ull << nl) - 1;  // every local position
   const uint64_t gmask = (n >= 64 ? ~0ull : (1ull << n) - 1) & ~allmask;
@@ -1015,7 +1021,8 @@ void plan_tiles(uint32_t n, std::vector<Op>& ops, std::vector<Step>& steps, cons
     Compiler C;
     C.n = n;
     C.m = m;
-    C.t = m - kTileR;
+    C.R = static_cast<int>(R);
+    C.t = m - R;
     C.L = L;
     C.free_load = opt.free_load;
     for (int q = 0; q < 64; ++q) C.tb[q] = -1;
@@ -1301,8 +1308,8 @@ void plan_tiles(uint32_t n, std::vector<Op>& ops, std::vector<Step>& steps, uint
   o.global_qubits = global_qubits;
   if (sharded) o.perm_step = false;  // shards restore their layout in place
   std::vector<uint32_t> ms{o.m};
-  // 13-qubit tiles: 2^13 tiles and more (enough CTAs), unsharded
-  if (!std::getenv("QSB_TILE_M") && !sharded && n >= 26) ms.push_back(13);
+  // 13-qubit tiles when every shard has 2^13 tiles and more (enough CTAs)
+  if (!std::getenv("QSB_TILE_M") && n - global_qubits >= 26) ms.push_back(13);
   std::vector<int> remaps{0, 1};
   if (const char* e = std::getenv("QSB_TILE_REMAP")) remaps = {std::atoi(e) != 0 ? 1 : 0};
   const std::vector<Op> orig = ops;

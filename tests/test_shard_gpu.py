@@ -109,13 +109,17 @@ def qft_closed_form(n, x, idx):
     return np.exp(2j * np.pi * ph.astype(np.float64) / float(1 << n)) / np.sqrt(float(1 << n))
 
 
+@pytest.mark.parametrize("from_basis", [False, True])
 @pytest.mark.parametrize("n,g", [(26, 3), (30, 3)])
-def test_sharded_qft_closed_form_large(n, g):
+def test_sharded_qft_closed_form_large(n, g, from_basis):
+    """QFT|x> by X gates + QFT, or QFT run from the basis state x (the leading
+    all-to-all folded into the start index, reset fused, zero tiles skipped)."""
     x = 0x2A5A5A5 & ((1 << n) - 1)
-    gates = Q.gen_qft(n, x).gates()
     st = ShardedState.local(n, g)
-    circ = ShardedCircuit(n, g, gates)
-    st.execute(circ)
+    if from_basis:
+        st.execute(ShardedCircuit(n, g, Q.gen_qft(n, 0).gates()), from_basis=x)
+    else:
+        st.execute(ShardedCircuit(n, g, Q.gen_qft(n, x).gates()))
     assert abs(st.norm_squared() - 1.0) <= 1e-10
     size = 1 << n
     rng = np.random.default_rng(5)
@@ -235,10 +239,13 @@ def test_sharded_sampling_matches_unsharded_30q():
     assert np.array_equal(st.sample_seeded(5, 100000, exact=True), ref)
 
 
+@pytest.mark.parametrize("kind", ["qft", "random", "hea", "ghz"])
 @pytest.mark.parametrize("g", [1, 3])
-def test_sharded_execute_from_basis(g):
+def test_sharded_execute_from_basis(g, kind):
+    """Runs from a basis state: exchanges before the first pass are folded
+    into the start index, the reset into the first pass, zero tiles skipped."""
     n = 15
-    gates = workload("qft", n)
+    gates = workload(kind, n)
     circ = ShardedCircuit(n, g, gates)
     for b in (0, (1 << n) - 1, 0x2C3A):
         st = ShardedState.local(n, g)

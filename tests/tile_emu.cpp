@@ -81,9 +81,9 @@ void emu_op(std::vector<cd>& a, uint32_t n, const qsb::Op& op) {
   }
 }
 
-uint64_t regoff(int p, const unsigned long long (&rs)[4]) {
+uint64_t regoff(int p, const unsigned long long (&rs)[qsb::kTileMaxR], int R) {
   uint64_t o = 0;
-  for (int k = 0; k < 4; ++k)
+  for (int k = 0; k < R; ++k)
     if ((p >> k) & 1) o |= rs[k];
   return o;
 }
@@ -91,8 +91,9 @@ uint64_t regoff(int p, const unsigned long long (&rs)[4]) {
 void emu_tile(std::vector<cd>& a, const qsb::TileProgram& tp) {
   const qsb::TileHeader& h = tp.h;
   const int T = 1 << h.t;
+  const int R = static_cast<int>(h.r), NS = 1 << R;
   std::vector<cd> sm(size_t(1) << h.m);
-  std::vector<std::array<cd, 16>> v(T);
+  std::vector<std::array<cd, qsb::kTileMaxSlots>> v(T);
   std::vector<uint64_t> G(T);
   std::vector<cd> outbuf;  // out-of-place pass: written through the final permutation
   if (h.oop) outbuf.assign(a.size(), cd(0));
@@ -102,13 +103,13 @@ void emu_tile(std::vector<cd>& a, const qsb::TileProgram& tp) {
       const uint32_t p = h.S[b];
       base = ((base >> p) << (p + 1)) | (base & ((1ull << p) - 1));
     }
-    unsigned long long rs[4];
-    for (int k = 0; k < 4; ++k) rs[k] = h.load.rs[k];
+    unsigned long long rs[qsb::kTileMaxR] = {};
+    for (int k = 0; k < R; ++k) rs[k] = h.load.rs[k];
     for (int tid = 0; tid < T; ++tid) {
       G[tid] = base;
       for (uint32_t k = 0; k < h.t; ++k)
         if ((tid >> k) & 1) G[tid] |= 1ull << h.load.tq[k];
-      for (int p = 0; p < 16; ++p) v[tid][p] = a[G[tid] | regoff(p, rs)];
+      for (int p = 0; p < NS; ++p) v[tid][p] = a[G[tid] | regoff(p, rs, R)];
     }
     for (const qsb::TOp& o : tp.ops) {
       if (o.type == qsb::TO_TRANSPOSE) {
@@ -118,9 +119,9 @@ void emu_tile(std::vector<cd>& a, const qsb::TileProgram& tp) {
           uint32_t Tw = 0;
           for (uint32_t k = 0; k < TB; ++k)
             if ((tid >> k) & 1) Tw ^= mt[k];
-          for (int p = 0; p < 16; ++p) {
+          for (int p = 0; p < NS; ++p) {
             uint32_t ad = Tw;
-            for (int k = 0; k < 4; ++k)
+            for (int k = 0; k < R; ++k)
               if ((p >> k) & 1) ad ^= mt[TB + k];
             sm.at(ad) = v[tid][p];
           }
@@ -128,16 +129,16 @@ void emu_tile(std::vector<cd>& a, const qsb::TileProgram& tp) {
         for (int tid = 0; tid < T; ++tid) {
           uint32_t Tr = 0;
           for (uint32_t k = 0; k < TB; ++k)
-            if ((tid >> k) & 1) Tr ^= mt[TB + 4 + k];
-          for (int p = 0; p < 16; ++p) {
+            if ((tid >> k) & 1) Tr ^= mt[TB + R + k];
+          for (int p = 0; p < NS; ++p) {
             uint32_t ad = Tr;
-            for (int k = 0; k < 4; ++k)
-              if ((p >> k) & 1) ad ^= mt[2 * TB + 4 + k];
+            for (int k = 0; k < R; ++k)
+              if ((p >> k) & 1) ad ^= mt[2 * TB + R + k];
             v[tid][p] = sm.at(ad);
           }
           G[tid] = base;
           for (uint32_t k = 0; k < TB; ++k)
-            if ((tid >> k) & 1) G[tid] |= 1ull << mt[2 * TB + 8 + k];
+            if ((tid >> k) & 1) G[tid] |= 1ull << mt[2 * TB + 2 * R + k];
         }
         continue;
       }
@@ -158,7 +159,7 @@ void emu_tile(std::vector<cd>& a, const qsb::TileProgram& tp) {
           case qsb::TO_MAT1_REAL:
           case qsb::TO_MAT1_RX: {
             const int K = o.k;
-            for (int p = 0; p < 16; ++p) {
+            for (int p = 0; p < NS; ++p) {
               if (p & (1 << K)) continue;
               if ((p & o.rmask) != o.rval) continue;
               const int p1 = p | (1 << K);
@@ -170,7 +171,7 @@ void emu_tile(std::vector<cd>& a, const qsb::TileProgram& tp) {
           }
           case qsb::TO_FLIP: {
             const int K = o.k;
-            for (int p = 0; p < 16; ++p) {
+            for (int p = 0; p < NS; ++p) {
               if (p & (1 << K)) continue;
               if ((p & o.rmask) != o.rval) continue;
               std::swap(r[p], r[p | (1 << K)]);
@@ -178,17 +179,17 @@ void emu_tile(std::vector<cd>& a, const qsb::TileProgram& tp) {
             break;
           }
           case qsb::TO_PHASE: {
-            cd F = c2(c[16]);
+            cd F = c2(c[NS]);
             for (uint32_t j = 0; j < o.nlist; ++j)
-              if ((G[tid] >> tp.meta[o.meta + j]) & 1) F *= c2(c[17 + j]);
-            for (int p = 0; p < 16; ++p)
+              if ((G[tid] >> tp.meta[o.meta + j]) & 1) F *= c2(c[NS + 1 + j]);
+            for (int p = 0; p < NS; ++p)
               if ((p & o.rmask) == o.rval) r[p] *= F * c2(c[p]);
             break;
           }
           case qsb::TO_DENSE2:
           case qsb::TO_DENSE3: {
             const int KD = o.type == qsb::TO_DENSE2 ? 2 : 3, Gd = 1 << KD;
-            for (int hi = 0; hi < (16 >> KD); ++hi) {
+            for (int hi = 0; hi < (NS >> KD); ++hi) {
               const int p0 = hi << KD;
               if ((p0 & o.rmask) != o.rval) continue;
               cd in[8];
@@ -205,7 +206,7 @@ void emu_tile(std::vector<cd>& a, const qsb::TileProgram& tp) {
         }
       }
     }
-    for (int k = 0; k < 4; ++k) rs[k] = h.store.rs[k];
+    for (int k = 0; k < R; ++k) rs[k] = h.store.rs[k];
     if (h.oop) {
       uint64_t bo = 0;
       for (uint32_t i = 0; i + h.m < h.n; ++i)
@@ -214,12 +215,12 @@ void emu_tile(std::vector<cd>& a, const qsb::TileProgram& tp) {
         uint64_t go = bo;
         for (uint32_t k = 0; k < h.t; ++k)
           if ((tid >> k) & 1) go |= 1ull << h.store.tq[k];
-        for (int p = 0; p < 16; ++p) outbuf[go | regoff(p, rs)] = v[tid][p];
+        for (int p = 0; p < NS; ++p) outbuf[go | regoff(p, rs, R)] = v[tid][p];
       }
       continue;
     }
     for (int tid = 0; tid < T; ++tid)
-      for (int p = 0; p < 16; ++p) a[G[tid] | regoff(p, rs)] = v[tid][p];
+      for (int p = 0; p < NS; ++p) a[G[tid] | regoff(p, rs, R)] = v[tid][p];
   }
   if (h.oop) a.swap(outbuf);
 }
@@ -255,6 +256,7 @@ int te_run(uint32_t n, const qs_gate* gates, uint64_t count, uint32_t mode, uint
       qsb::TileOptions opt;
       opt.m = tile_m;
       opt.low = low;
+      if (const char* e = std::getenv("QSB_TILE_R")) opt.r = static_cast<uint32_t>(std::atoi(e));
       opt.global_qubits = global_qubits;
       if (remap >= 0) {
         opt.remap = remap != 0;
@@ -323,7 +325,7 @@ int te_plan_create(uint32_t n, uint32_t g, const qs_gate* gates, uint64_t count,
     std::vector<qsb::Op> ops;
     for (uint64_t i = 0; i < count; ++i) qsb::validate_gate(gates[i], n);
     for (uint64_t i = 0; i < count; ++i) ops.push_back(qsb::lower_gate(gates[i], n, false));
-    qsb::plan_tiles(n, ops, h->p->steps, g);
+    qsb::plan_tiles(n, ops, h->p->steps, g, /*sharded=*/g > 0);  // as qs_plan_create_sharded
     *out = h.release();
     return 0;
   } catch (const std::exception& e) {
