@@ -113,8 +113,8 @@ def ncu_traffic(workload, plan):
     committed ncu --set full capture (profiles/), per launch; None if absent."""
     if workload != "random30" or plan != "tiled":
         return None
-    try:  # passes 1-3 of the current plan, one `ncu --set full` capture; average per launch
-        with open(os.path.join(ROOT, "profiles", "r1", "ncu_full_random30_passes1-3.json")) as f:
+    try:  # passes 0-3 of the current (13-qubit tile) plan, one `ncu --set full` capture; average per launch
+        with open(os.path.join(ROOT, "profiles", "r1", "ncu_full_random30_m13_passes0-3.json")) as f:
             rows = json.load(f)
         scale = {"Gbyte": 1e9, "Mbyte": 1e6}
         tot = [float(d["dram__bytes_read.sum"][0]) * scale[d["dram__bytes_read.sum"][1]] +
