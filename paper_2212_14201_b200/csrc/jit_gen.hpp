@@ -39,6 +39,7 @@ struct Gen {
   std::string name[kTileMaxSlots];
   cd K[kTileMaxSlots];                 // pending per-slot constant factors
   std::string Fp;           // pending per-thread scalar factor (empty = 1)
+  std::string Fg;           // pending per-tile scalar (phases of qubits outside the tile; empty = 1)
   cd Kg = 1.0;              // pending tile-wide constant scalar
   std::vector<double2> extra;  // coefficients appended after tp.coef
   uint32_t cur_tq[kTileMaxT] = {};
@@ -89,9 +90,16 @@ struct Gen {
   std::string fresh(const char* pfx = "v") { return pfx + std::to_string(counter++); }
   std::string coef(uint32_t i) { return "P.c[" + std::to_string(i) + "]"; }
   cd coefv(uint32_t i) const { return cd(tp.coef[i].x, tp.coef[i].y); }
+  // compile-time constants, one coefficient slot per distinct value (equal
+  // expressions such as cmul(F, P.c[i]) are then common subexpressions)
+  std::map<std::pair<double, double>, uint32_t> kidx;
   std::string kconst(cd v) {
+    auto it = kidx.find({v.real(), v.imag()});
+    if (it != kidx.end()) return coef(it->second);
     extra.push_back(make_double2(v.real(), v.imag()));
-    return coef(static_cast<uint32_t>(tp.coef.size() + extra.size() - 1));
+    const uint32_t i = static_cast<uint32_t>(tp.coef.size() + extra.size() - 1);
+    kidx[{v.real(), v.imag()}] = i;
+    return coef(i);
   }
   static bool one(cd v) { return v == cd(1.0); }
 
@@ -132,6 +140,16 @@ struct Gen {
   // store, the tile-wide scalar Kg).
   void flush_all(bool with_global) {
     const cd g = with_global ? Kg : cd(1.0);
+    if (with_global && !Fg.empty()) {  // tile-wide factors wait for the store
+      if (Fp.empty()) {
+        Fp = Fg;
+      } else {
+        const std::string nf = fresh("FP");
+        s << "    const double2 " << nf << " = cmul(" << Fp << ", " << Fg << ");\n";
+        Fp = nf;
+      }
+      Fg.clear();
+    }
     for (int p = 0; p < NS; ++p) {
       const cd kp = K[p] * g;
       const bool k1 = one(kp);
@@ -277,11 +295,18 @@ struct Gen {
       for (auto& [b, ci] : thr) pro << "  if ((tid >> " << b << ") & 1u) " << F << " = cmul(" << F << ", " << coef(ci) << ");\n";
     }
     const bool c1 = one(coefv(o.coef + NS));
+    // Unpredicated whole-thread phase: the constant and the factors of qubits
+    // outside the tile form a per-tile scalar that commutes with everything up
+    // to the store (transposes included), so it joins Fg instead of Fp.
+    const bool tile_scalar = t.empty() && o.rmask == 0;
     if (!c1 || !out.empty()) {
       const std::string Fo = fresh("F");
-      s << "    double2 " << Fo << " = " << (F.empty() ? (c1 ? std::string("make_double2(1.0, 0.0)") : coef(o.coef + NS))
-                                                        : (c1 ? F : "cmul(" + F + ", " + coef(o.coef + NS) + ")"))
-        << ";\n";
+      if (tile_scalar)
+        s << "    double2 " << Fo << " = " << (c1 ? std::string("make_double2(1.0, 0.0)") : coef(o.coef + NS)) << ";\n";
+      else
+        s << "    double2 " << Fo << " = " << (F.empty() ? (c1 ? std::string("make_double2(1.0, 0.0)") : coef(o.coef + NS))
+                                                          : (c1 ? F : "cmul(" + F + ", " + coef(o.coef + NS) + ")"))
+          << ";\n";
       std::map<uint32_t, std::vector<std::pair<uint32_t, uint32_t>>> by_chunk;
       for (auto& [q, ci] : out) by_chunk[tix_bit(q) / kChunk].push_back({tix_bit(q) % kChunk, ci});
       for (auto& [c, bits] : by_chunk) {
@@ -296,7 +321,17 @@ struct Gen {
               << ");\n";
         }
       }
-      F = Fo;
+      if (tile_scalar) {
+        if (Fg.empty()) {
+          Fg = Fo;
+        } else {
+          const std::string nf = fresh("FG");
+          s << "    const double2 " << nf << " = cmul(" << Fg << ", " << Fo << ");\n";
+          Fg = nf;
+        }
+      } else {
+        F = Fo;
+      }
     }
     if (!t.empty() && !F.empty()) {
       const std::string Ft = fresh("F");
