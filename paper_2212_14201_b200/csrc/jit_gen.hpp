@@ -299,7 +299,9 @@ struct Gen {
     // outside the tile form a per-tile scalar that commutes with everything up
     // to the store (transposes included), so it joins Fg instead of Fp.
     const bool tile_scalar = t.empty() && o.rmask == 0;
-    if (!c1 || !out.empty()) {
+    if (tile_scalar && out.empty()) {  // a constant: joins the compile-time tile scalar
+      Kg *= coefv(o.coef + NS);
+    } else if (!c1 || !out.empty()) {
       const std::string Fo = fresh("F");
       if (tile_scalar)
         s << "    double2 " << Fo << " = " << (c1 ? std::string("make_double2(1.0, 0.0)") : coef(o.coef + NS)) << ";\n";
