@@ -7,6 +7,7 @@
 #include "qforge/circuit.hpp"
 #include "qforge/error.hpp"
 #include "qforge/fusion.hpp"
+#include "qforge/ir.hpp"
 #include "qforge/gates.hpp"
 #include "qforge/linalg.hpp"
 #include "qforge/noise.hpp"
