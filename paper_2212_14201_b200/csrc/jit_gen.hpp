@@ -63,6 +63,10 @@ struct Gen {
   // tile has read them (the rest follow the last transpose), so most of the
   // next tile's HBM reads overlap this tile's transposes.
   uint32_t early = 0;
+  // sparse: amplitudes whose definite tile qubits (imask / ival, kernel
+  // parameters) disagree are zero -- they are set, not read (runs from a
+  // basis state: the first passes touch only a sliver of each tile)
+  bool sparse = false;
   int transposes_total = 0;
 
   // Tile-wide phase factors from qubits outside the tile: a product over up
@@ -441,11 +445,11 @@ struct Gen {
   }
 
   static constexpr const char* kIssueNext =
-      "    { const unsigned long long nt = tile + gridDim.x; if (nt < ntiles) prefetch(nt); }\n";
+      "    { const unsigned long long nt = kk + gridDim.x; if (nt < ntiles) prefetch(expand(nt)); }\n";
   static constexpr const char* kIssueEarly =
-      "    { const unsigned long long nt = tile + gridDim.x; if (nt < ntiles) prefetch_e(nt); }\n";
+      "    { const unsigned long long nt = kk + gridDim.x; if (nt < ntiles) prefetch_e(expand(nt)); }\n";
   static constexpr const char* kIssueLate =
-      "    { const unsigned long long nt = tile + gridDim.x; if (nt < ntiles) prefetch_l(nt); }\n";
+      "    { const unsigned long long nt = kk + gridDim.x; if (nt < ntiles) prefetch_l(expand(nt)); }\n";
 
   std::string run(const std::string& kname, uint32_t threads, uint32_t minb) {
     const TileHeader& h = tp.h;
@@ -557,7 +561,11 @@ struct Gen {
     } else {
       for (int p = 0; p < NS; ++p) {
         name[p] = fresh();
-        s << "    const double2 " << name[p] << " = __ldcs(amps + ((G | " << hexll(loff[p]) << ") & lmask));\n";
+        if (sparse)
+          s << "    const double2 " << name[p] << " = (((G | " << hexll(loff[p]) << ") & imask) == ival) ? __ldcs(amps + ((G | "
+            << hexll(loff[p]) << ") & lmask)) : make_double2(0.0, 0.0);\n";
+        else
+          s << "    const double2 " << name[p] << " = __ldcs(amps + ((G | " << hexll(loff[p]) << ") & lmask));\n";
       }
     }
     if (ti == 0)
@@ -626,6 +634,8 @@ struct Gen {
       << "    const unsigned long long lmask,\n"
       << "    const unsigned long long ntiles, const unsigned long long basis, const QsbPeers PEERS,\n"
     << "    const unsigned long long xaval, const unsigned long long dmask, const unsigned long long dval,\n"
+    << "    const unsigned long long imask, const unsigned long long ival,\n"
+    << "    const unsigned long long tmask, const unsigned long long tval,\n"
     << "    const __grid_constant__ QsbCoef P) {\n";
     k << "  extern __shared__ double2 sm[];\n";
     k << "  const unsigned tid = threadIdx.x;\n";
@@ -642,6 +652,15 @@ struct Gen {
       for (uint32_t b = 0; b < h.t; ++b) k << " | ((unsigned long long)((tid >> " << b << ") & 1u) << " << h.store.tq[b] << ")";
       k << ";\n";
     }
+    // Runs from a basis state, in place: only the tiles that can be non-zero
+    // are visited -- the compact counter kk is spread over the tile-index bits
+    // outside tmask, whose values are tval (load balance: every CTA gets work)
+    k << "  auto expand = [&](unsigned long long c) {\n"
+         "    if (!tmask) return c;\n"
+         "    unsigned long long r = tval;\n"
+         "    for (unsigned long long m = ~tmask; c && m; m &= m - 1, c >>= 1)\n"
+         "      if (c & 1ull) r |= m & (0ull - m);\n"
+         "    return r;\n  };\n";
     k << "  auto base_of = [&](unsigned long long b) {\n";
     for (uint32_t b = 0; b < h.m; ++b) {
       const uint32_t q = h.S[b];
@@ -676,6 +695,15 @@ struct Gen {
         k << "    if ((tb & dmask) != dval) { cp_async_commit(); return; }  // zero tile: nothing to read\n";
         k << "    const unsigned long long g = tb | TL;\n";
         for (int p = p0; p < p1; ++p) {
+          if (sparse) {  // zero amplitudes: store the zero, skip the copy
+            std::string dst;
+            if (lead) dst = "PB + (W0 ^ " + std::to_string(slot_xor(mt0 + TB, p)) + "u)";
+            else if (static_cast<uint32_t>(p) < early) dst = "PE + " + std::to_string(p * T) + " + tid";
+            else dst = "PB + " + std::to_string((p - static_cast<int>(early)) * T) + " + tid";
+            k << "    { const unsigned long long a = g | " << hexll(loff[p]) << "; if ((a & imask) == ival) cp_async16("
+              << dst << ", amps + (a & lmask)); else *(" << dst << ") = make_double2(0.0, 0.0); }\n";
+            continue;
+          }
           if (lead)
             k << "    cp_async16(PB + (W0 ^ " << slot_xor(mt0 + TB, p) << "u), amps + ((g | " << hexll(loff[p])
               << ") & lmask));\n";
@@ -695,12 +723,13 @@ struct Gen {
       } else {
         lambda("prefetch", 0, NS);
       }
-      k << "  unsigned long long tile = blockIdx.x;\n";
-      k << "  if (tile < ntiles) prefetch(tile);\n";
-      k << "  for (; tile < ntiles; tile += gridDim.x) {\n";
+      k << "  unsigned long long kk = blockIdx.x;\n";
+      k << "  if (kk < ntiles) prefetch(expand(kk));\n";
+      k << "  for (; kk < ntiles; kk += gridDim.x) {\n";
     } else {
-      k << "  for (unsigned long long tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {\n";
+      k << "  for (unsigned long long kk = blockIdx.x; kk < ntiles; kk += gridDim.x) {\n";
     }
+    k << "    const unsigned long long tile = expand(kk);\n";
     k << "    const unsigned long long base = base_of(tile) | rank_base;\n";
     k << "    const unsigned long long tix = tile | (rank_base >> " << h.m << ");\n";
     k << "    unsigned long long G = base | TL;\n";

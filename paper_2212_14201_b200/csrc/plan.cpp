@@ -144,11 +144,21 @@ void execute_plan(State& s, const Plan& p) {
 TileSkip zero_tiles(const Step& st, uint64_t basis) {
   TileSkip k;
   static const bool off = std::getenv("QSB_NO_ZERO_SKIP") != nullptr;
-  if (off) return k;
+  static const bool no_sparse = std::getenv("QSB_NO_SPARSE_LOAD") != nullptr;
+  if (off || st.kind != Step::TileStep) return k;
+  unsigned long long tile_bits = 0;
+  for (uint32_t b = 0; b < st.tile->h.m; ++b) tile_bits |= 1ull << st.tile->h.S[b];
   for (size_t i = 0; i < st.def_pos.size(); ++i) {
     const unsigned long long bit = 1ull << st.def_pos[i];
-    k.mask |= bit;
-    if ((__builtin_popcountll(basis & st.def_mask[i]) & 1) ^ st.def_const[i]) k.val |= bit;
+    const bool one = (__builtin_popcountll(basis & st.def_mask[i]) & 1) ^ st.def_const[i];
+    if (bit & tile_bits) {
+      if (no_sparse) continue;
+      k.imask |= bit;
+      if (one) k.ival |= bit;
+    } else {
+      k.mask |= bit;
+      if (one) k.val |= bit;
+    }
   }
   return k;
 }

@@ -27,10 +27,11 @@ struct Step {
   // perm[q] (restores the logical layout after relabeling SWAPs in one pass).
   std::vector<uint32_t> perm;
   // TileStep, runs started from a basis state |b> (qs_plan_execute_from_basis):
-  // qubits outside the tile that are still definite at the start of the pass,
-  // with their value as an affine GF(2) form of b (parity(b & mask) ^ c).  A
-  // tile whose index disagrees with those values is all zero and stays zero:
-  // the pass skips it (no HBM traffic in place; zeros written when out of place).
+  // qubits that are still definite at the start of the pass, with their value
+  // as an affine GF(2) form of b (parity(b & mask) ^ c).  A tile whose index
+  // disagrees with the outside ones is all zero and stays zero: the pass skips
+  // it (no HBM traffic in place; zeros written when out of place); inside a
+  // tile, amplitudes that disagree with the inside ones are zero and not read.
   std::vector<uint32_t> def_pos;
   std::vector<uint64_t> def_mask;
   std::vector<uint8_t> def_const;

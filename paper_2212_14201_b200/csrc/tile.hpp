@@ -94,6 +94,7 @@ struct TileProgram {
   uint32_t transposes = 0;
   std::vector<uint64_t> source;  // gate indices, for diagnostics
   std::shared_ptr<struct JitModule> jit;  // specialised kernel (jit.hpp)
+  mutable std::shared_ptr<struct JitModule> jit_sparse;  // variant reading only non-zero amplitudes (runs from a basis state)
   mutable std::shared_ptr<struct JitModule> jit_basis;  // from-basis variant (first pass of a run), lazily built
   mutable std::map<uint64_t, std::shared_ptr<struct JitModule>> jit_xchg;  // exchange-fused variants, by local bits
   std::vector<double2> params;            // kernel parameter table (coef + generator constants)
@@ -158,7 +159,8 @@ struct TileXchg {
 // Zero-tile skip (runs from a basis state): tiles with (index & mask) != val
 // are zero and stay zero.
 struct TileSkip {
-  unsigned long long mask = 0, val = 0;
+  unsigned long long mask = 0, val = 0;    // definite qubits outside the tile: zero tiles
+  unsigned long long imask = 0, ival = 0;  // definite tile qubits: only matching amplitudes are read
 };
 void launch_tile(State& s, const TileProgram& tp, const uint64_t* basis = nullptr, const TileXchg* x = nullptr,
                  const TileSkip* skip = nullptr);

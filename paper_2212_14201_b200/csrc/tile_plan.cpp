@@ -1204,12 +1204,13 @@ void plan_tiles(uint32_t n, std::vector<Op>& ops, std::vector<Step>& steps, cons
     std::vector<uint32_t> keep;
     for (size_t i = 0; i < rem.size(); ++i)
       if (!used[i]) keep.push_back(rem[i]);
-    // definite outside qubits at the start of this pass, then the pass's effect
+    // definite qubits at the start of this pass (outside the tile: zero tiles;
+    // inside: zero amplitudes that need not be read), then the pass's effect
     std::vector<uint32_t> dpos;
     std::vector<uint64_t> dm;
     std::vector<uint8_t> dc;
     for (uint32_t q = 0; q < n; ++q)
-      if (ddef[q] && !((S >> perm_at_start[q]) & 1)) {
+      if (ddef[q]) {
         dpos.push_back(perm_at_start[q]);
         dm.push_back(dmask[q]);
         dc.push_back(static_cast<uint8_t>(dconst[q]));
