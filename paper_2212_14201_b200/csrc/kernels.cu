@@ -322,6 +322,14 @@ __global__ void __launch_bounds__(kThreads) k_basis(double2* __restrict__ a, uin
     a[i] = make_double2(i == index ? 1.0 : 0.0, 0.0);
 }
 
+// zeros every amplitude whose global index disagrees with (mask, val): the
+// part of a run from a basis state that no tile pass has written yet
+__global__ void __launch_bounds__(kThreads) k_zero_outside(double2* __restrict__ a, uint64_t size, uint64_t rank_base,
+                                                           uint64_t mask, uint64_t val) {
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < size; i += (uint64_t)gridDim.x * blockDim.x)
+    if (((i | rank_base) & mask) != val) a[i] = make_double2(0.0, 0.0);
+}
+
 // ------------------------------------------------- rank-bit exchanges
 // Swapping rank bit j with local bit p: the shard whose bit j is x keeps the
 // half with local bit p == x and trades the other half with its partner.
@@ -1225,6 +1233,12 @@ void permute_qubits(State& s, const std::vector<uint32_t>& pos) {
 void fill_basis(State& s, uint64_t index) {
   DeviceGuard dg(s.device);
   k_basis<<<grid_for(s.size, s.device), kThreads, 0, s.stream>>>(s.amps, s.size, index);
+  QSB_LAUNCHED();
+}
+
+void zero_outside(State& s, uint64_t mask, uint64_t val) {
+  DeviceGuard dg(s.device);
+  k_zero_outside<<<grid_for(s.size, s.device), kThreads, 0, s.stream>>>(s.amps, s.size, s.rank_base, mask, val);
   QSB_LAUNCHED();
 }
 

@@ -167,10 +167,25 @@ void execute_plan_from_basis(State& s, const Plan& p, uint64_t basis) {
   if (p.n != s.n) throw ValidationError("plan was compiled for a different qubit count");
   if (p.g != s.g) throw ValidationError("plan was compiled for a sharded state (use the shard API)");
   if (basis >> s.n) throw ValidationError("basis index out of range");
+  // Lazy zeros: the first pass writes only its possibly non-zero tiles; every
+  // later pass reads only amplitudes that can be non-zero (compact tile
+  // counter + sparse loads), and those lie inside what the previous pass
+  // wrote (a qubit definite outside a pass's tile stays definite through it).
+  // Before a step that reads everything, and at the end, the complement of
+  // the last pass's tiles is zeroed -- usually empty (every tile active).
+  static const bool lazy = !std::getenv("QSB_NO_LAZY_ZERO") && !std::getenv("QSB_NO_SPARSE_LOAD") &&
+                           !std::getenv("QSB_NO_ZERO_SKIP") && !std::getenv("QSB_NO_TILE_COMPACT");
+  TileSkip unwritten;  // amplitudes outside (mask, val) may hold stale data
+  auto settle = [&]() {
+    if (unwritten.mask) zero_outside(s, unwritten.mask, unwritten.val);
+    unwritten = TileSkip{};
+  };
   size_t i = 0;
   if (!p.steps.empty() && p.steps[0].kind == Step::TileStep && !std::getenv("QSB_NO_FUSED_RESET")) {
-    const TileSkip k = zero_tiles(p.steps[0], basis);
+    TileSkip k = zero_tiles(p.steps[0], basis);
+    k.lazy = lazy && !p.steps[0].tile->h.oop;
     launch_tile(s, *p.steps[0].tile, &basis, nullptr, &k);
+    if (k.lazy) unwritten = TileSkip{k.mask, k.val};
     i = 1;
   } else {
     fill_basis(s, basis);
@@ -180,10 +195,14 @@ void execute_plan_from_basis(State& s, const Plan& p, uint64_t basis) {
     if (p.steps[i].kind == Step::TileStep) {
       const TileSkip k = zero_tiles(p.steps[i], basis);
       launch_tile(s, *p.steps[i].tile, nullptr, nullptr, &k);
+      if (p.steps[i].tile->h.oop) unwritten = TileSkip{};  // the new buffer is written everywhere
+      else if (unwritten.mask) unwritten = TileSkip{k.mask, k.val};
     } else {
+      settle();
       execute_step(s, p.steps[i]);
     }
   }
+  settle();
 }
 
 void execute_step(State& s, const Step& st) {

@@ -161,6 +161,9 @@ struct TileXchg {
 struct TileSkip {
   unsigned long long mask = 0, val = 0;    // definite qubits outside the tile: zero tiles
   unsigned long long imask = 0, ival = 0;  // definite tile qubits: only matching amplitudes are read
+  // first pass of a run from a basis state: write only the tiles that can be
+  // non-zero (the rest is zeroed later, only if some step would read it)
+  bool lazy = false;
 };
 void launch_tile(State& s, const TileProgram& tp, const uint64_t* basis = nullptr, const TileXchg* x = nullptr,
                  const TileSkip* skip = nullptr);

@@ -425,3 +425,29 @@ def test_zero_tile_skip_from_basis(which):
         cc.execute(sv, from_basis=b)
         ref = ol.run_gates(n, gates, state=np.eye(1, 1 << n, b, dtype=np.complex128)[0])
         assert np.max(np.abs(sv.amplitudes() - ref)) <= 1e-10, b
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("which", ["low_block", "qft", "partial_ghz"])
+def test_from_basis_overwrites_stale_state(which):
+    """Runs from a basis state write only the tiles that can be non-zero and
+    zero the rest lazily: a state full of NaN beforehand must not leak into
+    the result, including qubits that stay definite to the end."""
+    from test_planner_emu import mixed_gates
+    n = 20
+    if which == "low_block":  # qubits 12..19 never touched: zeroed at the end
+        gates = [g for g in mixed_gates(12, 150, 99)]
+    elif which == "qft":
+        gates = Q.gen_qft(n, 0).gates()
+    else:  # GHZ on the top half only
+        gates = [Q.make_gate(Q.GateKind.H, [10])] + [Q.make_gate(Q.GateKind.CNOT, [q, q + 1]) for q in range(10, 19)]
+    cc = Q.CompiledCircuit(n, gates)
+    sv = Q.StateVector(n)
+    rng = np.random.default_rng(3)
+    for b in [0, (1 << n) - 1] + [int(x) for x in rng.integers(0, 1 << n, 3)]:
+        sv.set_amplitudes(np.full(1 << n, np.nan + 1j * np.nan))
+        cc.execute(sv, from_basis=b)
+        ref = ol.run_gates(n, gates, state=np.eye(1, 1 << n, b, dtype=np.complex128)[0])
+        got = sv.amplitudes()
+        assert np.all(np.isfinite(got)), b
+        assert np.max(np.abs(got - ref)) <= 1e-10, b
