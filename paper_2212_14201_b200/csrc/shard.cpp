@@ -559,9 +559,15 @@ void shard_fill_basis(ShardSet& ss, uint64_t index) {
   shard_sync(ss);
 }
 
-void shard_execute(ShardSet& ss, const Plan& p, uint64_t first, uint64_t count, const uint64_t* basis) {
+void shard_execute(ShardSet& ss, const Plan& p, uint64_t first, uint64_t count, const uint64_t* basis,
+                   TileSkip* unwritten) {
   if (p.n != ss.n || p.g != ss.g) throw ValidationError("plan was compiled for a different state shape");
   auto shards = ss.ptrs();
+  auto settle = [&]() {
+    if (!unwritten || !unwritten->mask) return;
+    for (auto* s : shards) zero_outside(*s, unwritten->mask, unwritten->val);
+    *unwritten = TileSkip{};
+  };
   const uint64_t last = std::min<uint64_t>(p.steps.size(), count == ~0ull ? p.steps.size() : first + count);
   static const bool fuse = [] {
     const char* e = std::getenv("QSB_FUSE_EXCHANGE");
@@ -572,22 +578,29 @@ void shard_execute(ShardSet& ss, const Plan& p, uint64_t first, uint64_t count, 
     switch (st.kind) {
       case Step::TileStep:
         // a tile pass followed by an exchange: one kernel writing over peer memory
-        if (fuse && i + 1 < last && p.steps[i + 1].kind == Step::SwapStep &&
-            ss.tr->fused_exchange(shards, *st.tile, p.steps[i + 1].gpos, p.steps[i + 1].lpos)) {
-          ++i;
-          break;
+        if (fuse && i + 1 < last && p.steps[i + 1].kind == Step::SwapStep) {
+          settle();  // the fused kernel reads every tile
+          if (ss.tr->fused_exchange(shards, *st.tile, p.steps[i + 1].gpos, p.steps[i + 1].lpos)) {
+            ++i;
+            break;
+          }
         }
         if (basis) {  // a run from |basis>: skip tiles that are still provably zero
           const TileSkip k = zero_tiles(st, *basis);
           for (auto* s : shards) launch_tile(*s, *st.tile, nullptr, nullptr, &k);
+          if (unwritten && unwritten->mask) *unwritten = TileSkip{k.mask, k.val};
         } else {
           for (auto* s : shards) launch_tile(*s, *st.tile);
         }
         break;
       case Step::OpStep:
+        settle();
         for (auto* s : shards) launch_op(*s, st.op);
         break;
-      case Step::SwapStep: ss.tr->exchange(shards, st.gpos, st.lpos); break;
+      case Step::SwapStep:
+        settle();
+        ss.tr->exchange(shards, st.gpos, st.lpos);
+        break;
       case Step::PermStep: throw ValidationError("sharded plans restore their layout in place");
     }
   }
@@ -608,9 +621,14 @@ void shard_execute_from_basis(ShardSet& ss, const Plan& p, uint64_t basis) {
       if (((b >> hi) ^ (b >> lo)) & 1) b ^= (1ull << hi) | (1ull << lo);
     }
   }
+  static const bool lazy = !std::getenv("QSB_NO_LAZY_ZERO") && !std::getenv("QSB_NO_SPARSE_LOAD") &&
+                           !std::getenv("QSB_NO_ZERO_SKIP") && !std::getenv("QSB_NO_TILE_COMPACT");
+  TileSkip unwritten;
   if (first < p.steps.size() && p.steps[first].kind == Step::TileStep) {
-    const TileSkip k = zero_tiles(p.steps[first], basis);  // forms are in the submitted basis bits
+    TileSkip k = zero_tiles(p.steps[first], basis);  // forms are in the submitted basis bits
+    k.lazy = lazy;  // write only the tiles that can be non-zero (see execute_plan_from_basis)
     for (auto& s : ss.shards) launch_tile(*s, *p.steps[first].tile, &b, nullptr, &k);  // one shard holds |b>
+    if (k.lazy) unwritten = TileSkip{k.mask, k.val};
     ++first;
   } else {
     for (auto& s : ss.shards) {
@@ -618,7 +636,9 @@ void shard_execute_from_basis(ShardSet& ss, const Plan& p, uint64_t basis) {
       fill_basis(*s, mine ? (b & (s->size - 1)) : ~0ull);
     }
   }
-  shard_execute(ss, p, first, ~0ull, &basis);
+  shard_execute(ss, p, first, ~0ull, &basis, &unwritten);
+  if (unwritten.mask)
+    for (auto& s : ss.shards) zero_outside(*s, unwritten.mask, unwritten.val);
 }
 
 double shard_norm2(ShardSet& ss) {

@@ -82,8 +82,11 @@ int dist_world(const Dist* d);
 std::unique_ptr<ShardSet> make_dist_shard(uint32_t n, Dist* d);
 
 void shard_fill_basis(ShardSet& ss, uint64_t index);
+// basis: the run started from |basis> (zero tiles skipped); unwritten: lazy
+// zeros of that run (amplitudes outside (mask, val) not yet written; zeroed
+// before any step that reads everything and at the end)
 void shard_execute(ShardSet& ss, const Plan& p, uint64_t first = 0, uint64_t count = ~0ull,
-                   const uint64_t* basis = nullptr);
+                   const uint64_t* basis = nullptr, struct TileSkip* unwritten = nullptr);
 // Resets to |basis> (global index) and runs the plan, the reset fused into a
 // leading tile pass.  Enqueued on the shard stream.
 void shard_execute_from_basis(ShardSet& ss, const Plan& p, uint64_t basis);
