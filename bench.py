@@ -170,7 +170,7 @@ class SingleRunner:
         self.arr, self.keep = N.gate_array(gates)
         self.G = len(gates)
         self.cs = N.C.c_double()
-        self.e2e_path = "qs_run_circuit(|0..0>, host qs_gate array) + qs_checksum"
+        self.e2e_path = "qs_run_circuit_checksum(|0..0>, host qs_gate array; checksum fused into the last pass)"
 
     def parallelism(self, world):
         return "replicas" if world > 1 else "single"
@@ -184,15 +184,16 @@ class SingleRunner:
     def enqueue(self):
         self.N.check(self.L.qs_plan_enqueue(self.sv.handle(), self.cc._h))
 
-    def run_from_zero(self):  # reset to |0...0> fused into the first pass
-        self.N.check(self.L.qs_plan_enqueue_from_basis(self.sv.handle(), self.cc._h, 0))
+    def run_from_zero(self):  # reset to |0...0> fused into the first pass, checksum into the last
+        self.N.check(self.L.qs_plan_execute_from_basis_checksum(self.sv.handle(), self.cc._h, 0,
+                                                                self.N.C.byref(self.cs)))
 
-    def checksum(self):
-        self.N.check(self.L.qs_checksum(self.sv.handle(), self.N.C.byref(self.cs)))
+    def checksum(self):  # the step's result (already computed by its last pass)
         return self.cs.value
 
-    def apply_host(self):  # run(): reset to |0...0> (fused) + the host gate list
-        self.N.check(self.L.qs_run_circuit(self.sv.handle(), 0, self.arr, self.G, self.plan_mode, 3))
+    def apply_host(self):  # run(): reset to |0...0> (fused) + the host gate list + checksum (fused)
+        self.N.check(self.L.qs_run_circuit_checksum(self.sv.handle(), 0, self.arr, self.G, self.plan_mode, 3,
+                                                    self.N.C.byref(self.cs)))
 
     def step_kinds(self):
         return [1] * self.stats["launches"]

@@ -140,6 +140,11 @@ int qs_apply_circuit(qs_state_t s, const qs_gate* gates, uint64_t n, uint32_t pl
  * it.                                                                          */
 int qs_run_circuit(qs_state_t s, uint64_t basis, const qs_gate* gates, uint64_t n, uint32_t plan,
                    uint32_t max_fused_qubits);
+/* qs_run_circuit + probability_checksum of the result (bench.hpp:141-148,
+ * run_bench's checksum): the last tile pass sums |a_i|^2 (i+1) over what it
+ * stores (one partial per CTA, fixed order), so no extra read of the state.  */
+int qs_run_circuit_checksum(qs_state_t s, uint64_t basis, const qs_gate* gates, uint64_t n, uint32_t plan,
+                            uint32_t max_fused_qubits, double* checksum);
 
 /* Compiled circuit handle: plan once, run many times (bench / parameter sweeps). */
 typedef struct qs_plan* qs_plan_t;
@@ -158,6 +163,8 @@ int qs_plan_execute_timed(qs_state_t s, qs_plan_t p, float* step_ms);
  * The enqueue form does not wait.                                              */
 int qs_plan_execute_from_basis(qs_state_t s, qs_plan_t p, uint64_t basis);
 int qs_plan_enqueue_from_basis(qs_state_t s, qs_plan_t p, uint64_t basis);
+/* qs_plan_execute_from_basis + the checksum fused into the last pass (above). */
+int qs_plan_execute_from_basis_checksum(qs_state_t s, qs_plan_t p, uint64_t basis, double* checksum);
 /* Executes steps [first, first+count) only (diagnostics, per-pass profiling). */
 int qs_plan_execute_range(qs_state_t s, qs_plan_t p, uint64_t first, uint64_t count);
 /* Planner statistics: passes (HBM sweeps) and kernel launches per execute.   */

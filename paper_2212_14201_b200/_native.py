@@ -86,6 +86,8 @@ _SIGS = {
     "qs_apply_matrix": (C.c_int, [_P, _UP, C.c_uint32, _DP, _UP, C.c_uint32]),
     "qs_apply_circuit": (C.c_int, [_P, _GP, C.c_uint64, C.c_uint32, C.c_uint32]),
     "qs_run_circuit": (C.c_int, [_P, C.c_uint64, _GP, C.c_uint64, C.c_uint32, C.c_uint32]),
+    "qs_run_circuit_checksum": (C.c_int, [_P, C.c_uint64, _GP, C.c_uint64, C.c_uint32, C.c_uint32,
+                                          C.POINTER(C.c_double)]),
     "qs_plan_create": (C.c_int, [C.c_uint32, _GP, C.c_uint64, C.c_uint32, C.c_uint32, C.POINTER(_P)]),
     "qs_plan_destroy": (C.c_int, [_P]),
     "qs_plan_execute": (C.c_int, [_P, _P]),
@@ -94,6 +96,7 @@ _SIGS = {
     "qs_plan_execute_range": (C.c_int, [_P, _P, C.c_uint64, C.c_uint64]),
     "qs_plan_execute_from_basis": (C.c_int, [_P, _P, C.c_uint64]),
     "qs_plan_enqueue_from_basis": (C.c_int, [_P, _P, C.c_uint64]),
+    "qs_plan_execute_from_basis_checksum": (C.c_int, [_P, _P, C.c_uint64, C.POINTER(C.c_double)]),
     "qs_plan_execute_timed": (C.c_int, [_P, _P, C.POINTER(C.c_float)]),
     "qs_stream": (C.c_void_p, [_P]),
     "qs_fuse": (C.c_int, [_GP, C.c_uint64, C.c_uint32, C.c_uint32, C.POINTER(_P)]),

@@ -372,6 +372,25 @@ int qs_plan_enqueue_from_basis(qs_state_t h, qs_plan_t p, uint64_t basis) {
   });
 }
 
+int qs_plan_execute_from_basis_checksum(qs_state_t h, qs_plan_t p, uint64_t basis, double* checksum) {
+  return guarded([&] {
+    if (!p) throw ValidationError("null plan");
+    if (!checksum) throw ValidationError("null checksum output");
+    execute_plan_from_basis(st(h), *p->p, basis, checksum);
+  });
+}
+
+int qs_run_circuit_checksum(qs_state_t h, uint64_t basis, const qs_gate* gates, uint64_t n, uint32_t plan,
+                            uint32_t max_fused_qubits, double* checksum) {
+  return guarded([&] {
+    State& s = st(h);
+    if (n && !gates) throw ValidationError("null gate array");
+    if (!checksum) throw ValidationError("null checksum output");
+    auto p = cached_plan(s.n, gates, n, plan, max_fused_qubits);
+    execute_plan_from_basis(s, *p, basis, checksum);
+  });
+}
+
 int qs_plan_execute_from_basis(qs_state_t h, qs_plan_t p, uint64_t basis) {
   return guarded([&] {
     if (!p) throw ValidationError("null plan");

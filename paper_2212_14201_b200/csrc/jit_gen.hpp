@@ -67,6 +67,9 @@ struct Gen {
   // parameters) disagree are zero -- they are set, not read (runs from a
   // basis state: the first passes touch only a sliver of each tile)
   bool sparse = false;
+  // reduce: the pass also sums |a_i|^2 (i + 1) over what it stores (the
+  // bench checksum, bench.hpp:141-148) -- one partial per CTA into red[]
+  bool reduce = false;
   int transposes_total = 0;
 
   // Tile-wide phase factors from qubits outside the tile: a product over up
@@ -614,6 +617,9 @@ struct Gen {
         for (int k = 0; k < R; ++k)
           if ((p >> k) & 1) off |= h.store.rs[k];
         s << "    __stcs(out + (GO | " << hexll(off) << "), " << name[p] << ");\n";
+        if (reduce)
+          s << "    ACC += __fma_rn(" << name[p] << ".x, " << name[p] << ".x, __dmul_rn(" << name[p] << ".y, " << name[p]
+            << ".y)) * (double)((GO | " << hexll(off) << ") + 1ull);\n";
       }
     } else {
       if (ti == 0 && std::memcmp(&h.load, &h.store, sizeof(TileConfigAddr)) != 0) s << "    __syncthreads();\n";
@@ -622,6 +628,9 @@ struct Gen {
         for (int k = 0; k < R; ++k)
           if ((p >> k) & 1) off |= h.store.rs[k];
         s << "    __stcs(amps + ((G | " << hexll(off) << ") & lmask), " << name[p] << ");\n";
+        if (reduce)
+          s << "    ACC += __fma_rn(" << name[p] << ".x, " << name[p] << ".x, __dmul_rn(" << name[p] << ".y, " << name[p]
+            << ".y)) * (double)((G | " << hexll(off) << ") + 1ull);\n";
       }
     }
 
@@ -635,9 +644,10 @@ struct Gen {
       << "    const unsigned long long ntiles, const unsigned long long basis, const QsbPeers PEERS,\n"
     << "    const unsigned long long xaval, const unsigned long long dmask, const unsigned long long dval,\n"
     << "    const unsigned long long imask, const unsigned long long ival,\n"
-    << "    const unsigned long long tmask, const unsigned long long tval,\n"
+    << "    const unsigned long long tmask, const unsigned long long tval, double* __restrict__ red,\n"
     << "    const __grid_constant__ QsbCoef P) {\n";
     k << "  extern __shared__ double2 sm[];\n";
+    if (reduce) k << "  double ACC = 0.0;\n";
     k << "  const unsigned tid = threadIdx.x;\n";
     k << "  const unsigned long long TL = 0ull";
     for (uint32_t b = 0; b < h.t; ++b) k << " | ((unsigned long long)((tid >> " << b << ") & 1u) << " << h.load.tq[b] << ")";
@@ -737,6 +747,16 @@ struct Gen {
     k << "  }\n";
     // peer stores must be visible system-wide before the stream barrier that follows
     if (xk) k << "  __threadfence_system();\n";
+    if (reduce) {  // fixed-order block sum of the per-thread checksums -> red[blockIdx.x]
+      k << "  {\n    __shared__ double RS[" << (threads / 32) << "];\n"
+           "    double v = ACC;\n"
+           "    for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);\n"
+           "    if ((tid & 31u) == 0) RS[tid >> 5] = v;\n"
+           "    __syncthreads();\n"
+           "    if (tid == 0) {\n      double t = 0.0;\n"
+           "      for (unsigned w = 0; w < " << (threads / 32) << "u; ++w) t += RS[w];\n"
+           "      red[blockIdx.x] = t;\n    }\n  }\n";
+    }
     k << "}\n";
     return k.str();
   }

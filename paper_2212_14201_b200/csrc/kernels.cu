@@ -1236,6 +1236,20 @@ void fill_basis(State& s, uint64_t index) {
   QSB_LAUNCHED();
 }
 
+double sum_partials(State& s, double* part, unsigned count) {
+  DeviceGuard dg(s.device);
+  double* h = static_cast<double*>(s.get_pinned(sizeof(double)));
+  if (count) {
+    k_finalize<<<1, kThreads, 0, s.stream>>>(part, static_cast<int>(count), part + count);
+    QSB_LAUNCHED();
+    QSB_CUDA(cudaMemcpyAsync(h, part + count, sizeof(double), cudaMemcpyDeviceToHost, s.stream));
+  } else {
+    *h = 0.0;
+  }
+  QSB_CUDA(cudaStreamSynchronize(s.stream));
+  return *h;
+}
+
 void zero_outside(State& s, uint64_t mask, uint64_t val) {
   DeviceGuard dg(s.device);
   k_zero_outside<<<grid_for(s.size, s.device), kThreads, 0, s.stream>>>(s.amps, s.size, s.rank_base, mask, val);

@@ -19,7 +19,9 @@ void launch_op(State& s, const Op& op);
 void permute_qubits(State& s, const std::vector<uint32_t>& pos);
 
 void fill_basis(State& s, uint64_t index);
-void zero_outside(State& s, uint64_t mask, uint64_t val);     // a[i] = 0 where (global i & mask) != val                      // |index> (local index; out of range = all 0)
+void zero_outside(State& s, uint64_t mask, uint64_t val);
+// sums per-CTA partials part[0..count) in a fixed order (part[count] is scratch); synchronises
+double sum_partials(State& s, double* part, unsigned count);     // a[i] = 0 where (global i & mask) != val                      // |index> (local index; out of range = all 0)
 
 // Rank-bit exchanges for sharded states (shard.cpp).
 void swap_halves(State& a, State& b, uint32_t p);                // a: rank bit 0, b: rank bit 1, same device

@@ -163,7 +163,7 @@ TileSkip zero_tiles(const Step& st, uint64_t basis) {
   return k;
 }
 
-void execute_plan_from_basis(State& s, const Plan& p, uint64_t basis) {
+void execute_plan_from_basis(State& s, const Plan& p, uint64_t basis, double* checksum) {
   if (p.n != s.n) throw ValidationError("plan was compiled for a different qubit count");
   if (p.g != s.g) throw ValidationError("plan was compiled for a sharded state (use the shard API)");
   if (basis >> s.n) throw ValidationError("basis index out of range");
@@ -180,11 +180,18 @@ void execute_plan_from_basis(State& s, const Plan& p, uint64_t basis) {
     if (unwritten.mask) zero_outside(s, unwritten.mask, unwritten.val);
     unwritten = TileSkip{};
   };
+  // the checksum rides on the last pass when the plan ends with a tile pass
+  static const bool fuse_sum = !std::getenv("QSB_NO_FUSED_CHECKSUM");
+  const bool fused = checksum && fuse_sum && !p.steps.empty() && p.steps.back().kind == Step::TileStep;
+  double* part = fused ? static_cast<double*>(s.get_scratch(kMaxTileGrid * sizeof(double) + sizeof(double))) : nullptr;
+  unsigned parts = 0;
+  const size_t last = p.steps.size() - 1;
   size_t i = 0;
   if (!p.steps.empty() && p.steps[0].kind == Step::TileStep && !std::getenv("QSB_NO_FUSED_RESET")) {
     TileSkip k = zero_tiles(p.steps[0], basis);
     k.lazy = lazy && !p.steps[0].tile->h.oop;
-    launch_tile(s, *p.steps[0].tile, &basis, nullptr, &k);
+    const unsigned g0 = launch_tile(s, *p.steps[0].tile, &basis, nullptr, &k, last == 0 ? part : nullptr);
+    if (last == 0) parts = g0;
     if (k.lazy) unwritten = TileSkip{k.mask, k.val};
     i = 1;
   } else {
@@ -194,7 +201,8 @@ void execute_plan_from_basis(State& s, const Plan& p, uint64_t basis) {
   for (; i < p.steps.size(); ++i) {
     if (p.steps[i].kind == Step::TileStep) {
       const TileSkip k = zero_tiles(p.steps[i], basis);
-      launch_tile(s, *p.steps[i].tile, nullptr, nullptr, &k);
+      const unsigned gi = launch_tile(s, *p.steps[i].tile, nullptr, nullptr, &k, i == last ? part : nullptr);
+      if (i == last) parts = gi;
       if (p.steps[i].tile->h.oop) unwritten = TileSkip{};  // the new buffer is written everywhere
       else if (unwritten.mask) unwritten = TileSkip{k.mask, k.val};
     } else {
@@ -202,7 +210,8 @@ void execute_plan_from_basis(State& s, const Plan& p, uint64_t basis) {
       execute_step(s, p.steps[i]);
     }
   }
-  settle();
+  settle();  // zeros only: the fused checksum is unchanged
+  if (checksum) *checksum = fused ? sum_partials(s, part, parts) : reduce_checksum(s);
 }
 
 void execute_step(State& s, const Step& st) {

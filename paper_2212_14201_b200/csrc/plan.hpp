@@ -58,7 +58,9 @@ std::shared_ptr<const Plan> cached_plan(uint32_t n, const qs_gate* gates, uint64
 void execute_plan(State& s, const Plan& p);
 // Resets to |basis> and runs the plan; when the plan starts with a tile pass
 // the reset is fused into it (no separate write pass, no read of the old state).
-void execute_plan_from_basis(State& s, const Plan& p, uint64_t basis);
+// checksum != null: also returns probability_checksum of the result, fused
+// into the last tile pass when the plan ends with one (synchronises).
+void execute_plan_from_basis(State& s, const Plan& p, uint64_t basis, double* checksum = nullptr);
 // The zero-tile mask of a tile step for a run started from |basis>.
 struct TileSkip zero_tiles(const Step& st, uint64_t basis);
 void execute_step(State& s, const Step& st);

@@ -94,8 +94,8 @@ struct TileProgram {
   uint32_t transposes = 0;
   std::vector<uint64_t> source;  // gate indices, for diagnostics
   std::shared_ptr<struct JitModule> jit;  // specialised kernel (jit.hpp)
-  mutable std::shared_ptr<struct JitModule> jit_sparse;  // variant reading only non-zero amplitudes (runs from a basis state)
-  mutable std::shared_ptr<struct JitModule> jit_basis;  // from-basis variant (first pass of a run), lazily built
+  // lazily built variants (jit.cpp variant_module): from a basis state, sparse reads, fused checksum
+  mutable std::map<unsigned, std::shared_ptr<struct JitModule>> variants;
   mutable std::map<uint64_t, std::shared_ptr<struct JitModule>> jit_xchg;  // exchange-fused variants, by local bits
   std::vector<double2> params;            // kernel parameter table (coef + generator constants)
 };
@@ -158,6 +158,8 @@ struct TileXchg {
 };
 // Zero-tile skip (runs from a basis state): tiles with (index & mask) != val
 // are zero and stay zero.
+constexpr unsigned kMaxTileGrid = 8192;  // CTAs of a reducing tile pass (partials buffer size)
+
 struct TileSkip {
   unsigned long long mask = 0, val = 0;    // definite qubits outside the tile: zero tiles
   unsigned long long imask = 0, ival = 0;  // definite tile qubits: only matching amplitudes are read
@@ -165,7 +167,9 @@ struct TileSkip {
   // non-zero (the rest is zeroed later, only if some step would read it)
   bool lazy = false;
 };
-void launch_tile(State& s, const TileProgram& tp, const uint64_t* basis = nullptr, const TileXchg* x = nullptr,
-                 const TileSkip* skip = nullptr);
+// red != null: also writes one checksum partial per CTA (sum |a_i|^2 (i+1) over
+// the stored amplitudes) to red[0 .. return value)
+unsigned launch_tile(State& s, const TileProgram& tp, const uint64_t* basis = nullptr, const TileXchg* x = nullptr,
+                     const TileSkip* skip = nullptr, double* red = nullptr);
 
 }  // namespace qsb

@@ -319,6 +319,13 @@ class CompiledCircuit:
         else:
             N.check(N.lib().qs_plan_execute_from_basis(state.handle(), self._h, from_basis))
 
+    def execute_checksum(self, state, from_basis=0):
+        """Runs the plan from |from_basis> and returns probability_checksum of the
+        result (bench.hpp:141-148), summed by the last pass as it stores."""
+        cs = N.C.c_double()
+        N.check(N.lib().qs_plan_execute_from_basis_checksum(state.handle(), self._h, from_basis, N.C.byref(cs)))
+        return cs.value
+
     def stats(self):
         a, b, c = N.C.c_uint64(), N.C.c_uint64(), N.C.c_uint64()
         N.check(N.lib().qs_plan_stats(self._h, N.C.byref(a), N.C.byref(b), N.C.byref(c)))

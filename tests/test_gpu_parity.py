@@ -451,3 +451,26 @@ def test_from_basis_overwrites_stale_state(which):
         got = sv.amplitudes()
         assert np.all(np.isfinite(got)), b
         assert np.max(np.abs(got - ref)) <= 1e-10, b
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("which,n", [("random", 22), ("qft", 22), ("ghz", 20), ("low_block", 20), ("random", 26),
+                                     ("qft", 27)])
+def test_fused_checksum_matches_reduction(which, n):
+    """probability_checksum fused into the last tile pass (one partial per CTA)
+    equals the separate fixed-order reduction and the oracle's checksum."""
+    from test_planner_emu import mixed_gates
+    gates = {"random": lambda: Q.gen_random_circuit(n, 4, 424242).gates(),
+             "qft": lambda: Q.gen_qft(n, 0).gates(),
+             "ghz": lambda: Q.gen_ghz(n).gates(),
+             "low_block": lambda: mixed_gates(12, 120, 5)}[which]()
+    cc = Q.CompiledCircuit(n, gates)
+    sv = Q.StateVector(n)
+    for b in (0, 0x2A5A5 & ((1 << n) - 1)):
+        fused = cc.execute_checksum(sv, b)
+        separate = sv.checksum()
+        assert abs(fused - separate) <= 1e-12 * abs(separate), (b, fused, separate)
+        if n <= 22:
+            ref = ol.run_gates(n, gates, state=np.eye(1, 1 << n, b, dtype=np.complex128)[0])
+            want = float(np.sum(np.abs(ref) ** 2 * (np.arange(1 << n) + 1.0)))
+            assert abs(fused - want) <= 1e-9 * want
