@@ -420,8 +420,10 @@ struct PermSpec {
 };
 
 __global__ void __launch_bounds__(kThreads) k_permute(const double2* __restrict__ in, double2* __restrict__ out,
-                                                      const PermSpec ps, uint64_t ntiles) {
+                                                      const PermSpec ps, uint64_t ntiles, double* __restrict__ red) {
   __shared__ double2 tile[kPermTile];
+  __shared__ double sh[kThreads / 32];
+  double acc = 0.0;  // red != null: checksum of what this block stores (bench.hpp:141-148)
   for (uint64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
     uint64_t bi = 0, bo = 0;
     for (uint32_t k = 0; k < ps.nb; ++k)
@@ -434,9 +436,16 @@ __global__ void __launch_bounds__(kThreads) k_permute(const double2* __restrict_
     __syncthreads();
     for (uint32_t f = threadIdx.x; f < kPermTile; f += kThreads) {
       const uint32_t e = ps.e_lo[f & 31u] | ps.e_hi[f >> 5];
-      __stcs(out + (bo | ps.out_lo[f & 31u] | ps.out_hi[f >> 5]), tile[e ^ ((e >> 5) & 7u)]);
+      const uint64_t o = bo | ps.out_lo[f & 31u] | ps.out_hi[f >> 5];
+      const double2 v = tile[e ^ ((e >> 5) & 7u)];
+      __stcs(out + o, v);
+      if (red) acc += norm_ref(v) * (double)(o + 1);
     }
     __syncthreads();
+  }
+  if (red) {
+    const double t = block_sum(acc, sh);
+    if (threadIdx.x == 0) red[blockIdx.x] = t;
   }
 }
 
@@ -1172,7 +1181,7 @@ void unpack_block(State& s, const uint32_t* lpos, uint32_t k, uint32_t d, uint64
   QSB_LAUNCHED();
 }
 
-void permute_qubits(State& s, const std::vector<uint32_t>& pos) {
+unsigned permute_qubits(State& s, const std::vector<uint32_t>& pos, double* red) {
   const uint32_t n = s.local_qubits();
   if (pos.size() != n) throw ValidationError("permutation size does not match the state");
   if (n < kPermTileBits) throw ValidationError("qubit permutation needs at least 10 qubits");
@@ -1225,9 +1234,10 @@ void permute_qubits(State& s, const std::vector<uint32_t>& pos) {
   }
   const uint64_t ntiles = s.size >> kPermTileBits;
   const uint32_t grid = static_cast<uint32_t>(std::min<uint64_t>(ntiles, num_sms(s.device) * 8ull));
-  k_permute<<<grid, kThreads, 0, s.stream>>>(s.amps, s.alt, ps, ntiles);
+  k_permute<<<grid, kThreads, 0, s.stream>>>(s.amps, s.alt, ps, ntiles, red);
   QSB_LAUNCHED();
   std::swap(s.amps, s.alt);
+  return grid;
 }
 
 void fill_basis(State& s, uint64_t index) {

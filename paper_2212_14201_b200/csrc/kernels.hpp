@@ -16,7 +16,8 @@ void launch_op(State& s, const Op& op);
 
 // Out-of-place qubit permutation: bit q of every index moves to bit pos[q]
 // (one HBM pass into the state's second buffer, then the buffers swap).
-void permute_qubits(State& s, const std::vector<uint32_t>& pos);
+// red != null: also one checksum partial per block into red[0 .. return value)
+unsigned permute_qubits(State& s, const std::vector<uint32_t>& pos, double* red = nullptr);
 
 void fill_basis(State& s, uint64_t index);
 void zero_outside(State& s, uint64_t mask, uint64_t val);

@@ -182,7 +182,8 @@ void execute_plan_from_basis(State& s, const Plan& p, uint64_t basis, double* ch
   };
   // the checksum rides on the last pass when the plan ends with a tile pass
   static const bool fuse_sum = !std::getenv("QSB_NO_FUSED_CHECKSUM");
-  const bool fused = checksum && fuse_sum && !p.steps.empty() && p.steps.back().kind == Step::TileStep;
+  const bool fused = checksum && fuse_sum && !p.steps.empty() &&
+                     (p.steps.back().kind == Step::TileStep || p.steps.back().kind == Step::PermStep);
   double* part = fused ? static_cast<double*>(s.get_scratch(kMaxTileGrid * sizeof(double) + sizeof(double))) : nullptr;
   unsigned parts = 0;
   const size_t last = p.steps.size() - 1;
@@ -205,6 +206,9 @@ void execute_plan_from_basis(State& s, const Plan& p, uint64_t basis, double* ch
       if (i == last) parts = gi;
       if (p.steps[i].tile->h.oop) unwritten = TileSkip{};  // the new buffer is written everywhere
       else if (unwritten.mask) unwritten = TileSkip{k.mask, k.val};
+    } else if (i == last && part && p.steps[i].kind == Step::PermStep) {
+      settle();
+      parts = permute_qubits(s, p.steps[i].perm, part);
     } else {
       settle();
       execute_step(s, p.steps[i]);

@@ -474,3 +474,21 @@ def test_fused_checksum_matches_reduction(which, n):
             ref = ol.run_gates(n, gates, state=np.eye(1, 1 << n, b, dtype=np.complex128)[0])
             want = float(np.sum(np.abs(ref) ** 2 * (np.arange(1 << n) + 1.0)))
             assert abs(fused - want) <= 1e-9 * want
+
+
+@pytest.mark.gpu
+def test_fused_checksum_through_final_permutation(monkeypatch):
+    """A plan ending with the out-of-place qubit permutation (QSB_FOLD_PERM=0:
+    QFT's final SWAPs as a k_permute step) sums the checksum in that step."""
+    monkeypatch.setenv("QSB_FOLD_PERM", "0")
+    n = 22
+    gates = Q.gen_qft(n, 0).gates()
+    cc = Q.CompiledCircuit(n, gates)
+    sv = Q.StateVector(n)
+    b = 0x1F2E3 & ((1 << n) - 1)
+    fused = cc.execute_checksum(sv, b)
+    assert abs(fused - sv.checksum()) <= 1e-12 * abs(fused)
+    ref = ol.run_gates(n, gates, state=np.eye(1, 1 << n, b, dtype=np.complex128)[0])
+    assert np.max(np.abs(sv.amplitudes() - ref)) <= 1e-10
+    want = float(np.sum(np.abs(ref) ** 2 * (np.arange(1 << n) + 1.0)))
+    assert abs(fused - want) <= 1e-9 * want
