@@ -241,6 +241,12 @@ int qs_batch_measure(qs_state_t s, uint32_t shot_qubits, uint32_t qubit, const d
                      signed char* outcomes);
 int qs_batch_kraus(qs_state_t s, uint32_t shot_qubits, const uint32_t* qubits, uint32_t k, const double* ops,
                    uint32_t nops, const double* uniforms, uint64_t shots, int32_t* chosen);
+/* Control flow in shot batches: a NEGATIVE uniform leaves that shot untouched
+ * in qs_batch_measure (outcome -1) and qs_batch_kraus (chosen -1); and
+ * qs_batch_apply applies one dense 2^k x 2^k matrix (k <= 3, qubits[0] most
+ * significant, row-major interleaved) only to the shots with mask[s] != 0. */
+int qs_batch_apply(qs_state_t s, uint32_t shot_qubits, const uint32_t* qubits, uint32_t k, const double* matrix,
+                   const signed char* mask, uint64_t shots);
 
 /* Gradient of <psi|H|psi>, psi = gates[0..count) applied to |0...0>, with
  * respect to the angle of each slot gate gates[slots[i]] (uncontrolled RX, RY

@@ -119,6 +119,7 @@ _SIGS = {
     "qs_batch_measure": (C.c_int, [_P, C.c_uint32, C.c_uint32, _DP, C.c_uint64, C.c_char_p]),
     "qs_batch_kraus": (C.c_int, [_P, C.c_uint32, _UP, C.c_uint32, _DP, C.c_uint32, _DP, C.c_uint64,
                                  C.POINTER(C.c_int32)]),
+    "qs_batch_apply": (C.c_int, [_P, C.c_uint32, _UP, C.c_uint32, _DP, C.c_char_p, C.c_uint64]),
     "qs_reduced_density": (C.c_int, [_P, _UP, C.c_uint32, _DP]),
     "qs_gradient": (C.c_int, [_P, _GP, C.c_uint64, _U64P, C.c_uint64, C.c_char_p, _DP, C.c_uint32, _DP]),
     # sharded state vectors

@@ -622,6 +622,14 @@ int qs_batch_kraus(qs_state_t h, uint32_t shot_qubits, const uint32_t* qubits, u
   });
 }
 
+int qs_batch_apply(qs_state_t h, uint32_t shot_qubits, const uint32_t* qubits, uint32_t k, const double* matrix,
+                   const signed char* mask, uint64_t shots) {
+  return guarded([&] {
+    if (!qubits || !matrix || (shots && !mask)) throw ValidationError("null batch buffers");
+    batch_apply(st(h), shot_qubits, qubits, k, matrix, mask, shots);
+  });
+}
+
 int qs_reduced_density(qs_state_t h, const uint32_t* qubits, uint32_t k, double* out) {
   return guarded([&] {
     if (!qubits || !out) throw ValidationError("null buffer");

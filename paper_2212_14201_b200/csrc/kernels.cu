@@ -799,6 +799,10 @@ __global__ void __launch_bounds__(kThreads) k_batch_collapse(double2* __restrict
                                                              int* __restrict__ err) {
   for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < total; i += (uint64_t)gridDim.x * blockDim.x) {
     const uint64_t s = i >> n;
+    if (u[s] < 0.0) {  // shot not on this path (control flow): untouched
+      if ((i & ((1ull << n) - 1)) == 0) out[s] = -1;
+      continue;
+    }
     const double q1 = p1[s], q0 = 1.0 - q1;
     const int o = (u[s] < q0) ? 0 : 1;
     const double prob = o ? q1 : q0;
@@ -863,6 +867,11 @@ __global__ void k_batch_choose(const double2* __restrict__ rdm, const double2* _
                                double* __restrict__ scale, int* __restrict__ err) {
   constexpr int D = 1 << K;
   for (uint64_t s = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; s < shots; s += (uint64_t)gridDim.x * blockDim.x) {
+    if (u[s] < 0.0) {  // shot not on this path (control flow)
+      chosen[s] = -1;
+      scale[s] = 1.0;
+      continue;
+    }
     const double2* rho = rdm + s * D * D;
     double w[16];
     double total = 0;
@@ -913,6 +922,7 @@ __global__ void __launch_bounds__(kThreads) k_batch_apply(double2* __restrict__ 
   const uint64_t groups = 1ull << (n - K), work = groups * shots;
   for (uint64_t w = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; w < work; w += (uint64_t)gridDim.x * blockDim.x) {
     const uint64_t s = w / groups, g = w % groups;
+    if (chosen[s] < 0) continue;  // shot not on this path
     double2* b = a + (s << n);
     const uint64_t base = deposit(g, sl);
     const double2* k = ops + (uint64_t)chosen[s] * D * D;
@@ -1536,6 +1546,40 @@ void batch_measure(State& s, uint32_t n, uint32_t q, const double* u_host, uint6
   QSB_CUDA(cudaMemcpyAsync(&h_err, err, sizeof(int), cudaMemcpyDeviceToHost, s.stream));
   QSB_CUDA(cudaStreamSynchronize(s.stream));
   if (h_err) throw RuntimeError("collapse onto a zero-probability outcome");
+}
+
+void batch_apply(State& s, uint32_t n, const uint32_t* qubits, uint32_t k, const double* m_host,
+                 const signed char* mask_host, uint64_t shots) {
+  if (k < 1 || k > 3) throw ValidationError("batch apply: 1 to 3 qubits");
+  if (n > s.local_qubits() || shots > (s.size >> n)) throw ValidationError("batch apply: bad batch shape");
+  std::vector<uint32_t> tg(qubits, qubits + k);
+  for (auto q : tg)
+    if (q >= n) throw ValidationError("batch apply: qubit out of range");
+  const Slots sl = make_slots(tg, {});
+  if (sl.count != k) throw ValidationError("batch apply: repeated qubit");
+  if (!shots) return;
+  TargetMasks tm{};
+  for (uint32_t b = 0; b < k; ++b) tm.m[b] = 1ull << tg[k - 1 - b];
+  const int D = 1 << k;
+  DeviceGuard dg(s.device);
+  const size_t mbytes = static_cast<size_t>(D) * D * sizeof(double2);
+  char* scr = static_cast<char*>(s.get_scratch(mbytes + shots * (4 + 8) + 256));
+  double2* m = reinterpret_cast<double2*>(scr);
+  double* scale = reinterpret_cast<double*>(scr + mbytes);
+  int* chosen = reinterpret_cast<int*>(scale + shots);
+  std::vector<int> ch(shots);
+  std::vector<double> one(shots, 1.0);
+  for (uint64_t i = 0; i < shots; ++i) ch[i] = mask_host[i] ? 0 : -1;
+  QSB_CUDA(cudaMemcpyAsync(m, m_host, mbytes, cudaMemcpyHostToDevice, s.stream));
+  QSB_CUDA(cudaMemcpyAsync(scale, one.data(), shots * 8, cudaMemcpyHostToDevice, s.stream));
+  QSB_CUDA(cudaMemcpyAsync(chosen, ch.data(), shots * 4, cudaMemcpyHostToDevice, s.stream));
+  switch (k) {
+    case 1: k_batch_apply<1><<<grid_for(shots << (n - 1), s.device), kThreads, 0, s.stream>>>(s.amps, n, sl, tm, shots, m, chosen, scale); break;
+    case 2: k_batch_apply<2><<<grid_for(shots << (n - 2), s.device), kThreads, 0, s.stream>>>(s.amps, n, sl, tm, shots, m, chosen, scale); break;
+    default: k_batch_apply<3><<<grid_for(shots << (n - 3), s.device), kThreads, 0, s.stream>>>(s.amps, n, sl, tm, shots, m, chosen, scale); break;
+  }
+  QSB_LAUNCHED();
+  QSB_CUDA(cudaStreamSynchronize(s.stream));  // host staging buffers go out of scope
 }
 
 void batch_kraus(State& s, uint32_t n, const uint32_t* qubits, uint32_t k, const double* ops_host, uint32_t nops,

@@ -78,6 +78,9 @@ void reduced_density(State& s, const uint32_t* targets, uint32_t k, double* out)
 // Shot batches: B n-qubit states as one vector (shot s at [s*2^n, (s+1)*2^n)).
 void batch_reset(State& s, uint32_t n);
 void batch_measure(State& s, uint32_t n, uint32_t q, const double* u_host, uint64_t shots, signed char* out_host);
+// m (2^k x 2^k, row-major interleaved; qubits[0] = most significant) applied to the shots with mask[s] != 0
+void batch_apply(State& s, uint32_t n, const uint32_t* qubits, uint32_t k, const double* m_host,
+                 const signed char* mask_host, uint64_t shots);
 void batch_kraus(State& s, uint32_t n, const uint32_t* qubits, uint32_t k, const double* ops_host, uint32_t nops,
                  const double* u_host, uint64_t shots, int* chosen_host);
 

@@ -155,15 +155,31 @@ struct NoiseApplication {
 using NoiseOf = std::function<std::vector<NoiseApplication>(const Gate&)>;
 using ReadoutOf = std::function<const std::pair<double, double>*(std::uint32_t)>;  // (p01, p10) or null
 
+// Programs with QIf / QWhile batch too: every instruction runs on the shots
+// whose path reaches it (a mask); gates on a strict subset go through
+// qs_batch_apply (<= 3 qubits incl. controls), measurements and Kraus steps
+// skip inactive shots (negative uniform), and each shot draws from its own
+// Rng::derive(seed, s) stream in its own program order.
 inline bool batchable(const Program& p, std::uint64_t shots, const NoiseOf* noise) {
   if (std::getenv("QSB_NO_SHOT_BATCH")) return false;  // per-shot executor (cross-checks)
-  if (shots < 2 || !p.is_flat() || p.qubit_count > 22 || p.qubit_count < 1) return false;
-  if (noise)
-    for (const auto& ins : p.body)
-      if (const auto* g = std::get_if<GateOp>(&ins))
-        for (const auto& a : (*noise)(g->gate))
-          if (a.qubits.size() > 2 || a.ops->size() > 16) return false;
-  return true;
+  if (shots < 2 || p.qubit_count > 22 || p.qubit_count < 1) return false;
+  if (!p.is_flat() && std::getenv("QSB_NO_CF_BATCH")) return false;
+  std::function<bool(const Program&, bool)> ok = [&](const Program& b, bool nested) {
+    for (const auto& ins : b.body) {
+      if (const auto* g = std::get_if<GateOp>(&ins)) {
+        if (nested && g->gate.qubits().size() > 3) return false;
+        if (noise)
+          for (const auto& a : (*noise)(g->gate))
+            if (a.qubits.size() > 2 || a.ops->size() > 16) return false;
+      } else if (const auto* f = std::get_if<IfOp>(&ins)) {
+        if (!ok(*f->then_body, true) || (f->else_body && !ok(*f->else_body, true))) return false;
+      } else if (const auto* w = std::get_if<WhileOp>(&ins)) {
+        if (!ok(*w->body, true)) return false;
+      }
+    }
+    return true;
+  };
+  return ok(p, false);
 }
 
 // Runs shots [first, first + count) of a flat program; returns their cbits.
@@ -251,7 +267,149 @@ inline std::vector<std::vector<std::int64_t>> run_shot_batch(const Program& p, c
   return cbits;
 }
 
-// Shots of a flat program in batches sized to ~2 GiB of device memory.
+// Shots [first, first + count) of a program with control flow (see batchable).
+class ControlFlowBatch {
+ public:
+  ControlFlowBatch(const Program& p, const SimOptions& opts, std::uint64_t first, std::uint64_t count,
+                   const NoiseOf* noise, const ReadoutOf* readout)
+      : opts_(opts), noise_(noise), readout_(readout), n_(p.qubit_count), count_(count),
+        cbits_(count, std::vector<std::int64_t>(p.cbit_count, 0)), outc_(count) {
+    while ((std::uint64_t(1) << b_) < count) ++b_;
+    rngs_.reserve(count);
+    for (std::uint64_t s = 0; s < count; ++s) rngs_.push_back(Rng::derive(opts.seed, first + s));
+    qs_check(qs_create(n_ + b_, 0, 40, &big_));
+    qs_check(qs_batch_reset(big_, n_));
+  }
+  ~ControlFlowBatch() { qs_destroy(big_); }
+  ControlFlowBatch(const ControlFlowBatch&) = delete;
+  ControlFlowBatch& operator=(const ControlFlowBatch&) = delete;
+
+  std::vector<std::vector<std::int64_t>> run(const Program& p, StateVector* last) {
+    exec(p, std::vector<signed char>(count_, 1));
+    drain();
+    if (last) {
+      std::vector<cdouble> amps(std::size_t(1) << n_);
+      qs_check(qs_get_amplitudes(big_, reinterpret_cast<double*>(amps.data()), (count_ - 1) << n_, amps.size()));
+      *last = StateVector::from_amplitudes(n_, amps);
+    }
+    return std::move(cbits_);
+  }
+
+ private:
+  const SimOptions& opts_;
+  const NoiseOf* noise_;
+  const ReadoutOf* readout_;
+  std::uint32_t n_, b_ = 0;
+  std::uint64_t count_;
+  qs_state_t big_ = nullptr;
+  std::vector<Rng> rngs_;
+  std::vector<std::vector<std::int64_t>> cbits_;
+  std::vector<signed char> outc_;
+  GateBatch pending_;
+
+  static bool any(const std::vector<signed char>& m) {
+    for (signed char x : m)
+      if (x) return true;
+    return false;
+  }
+  void drain() {
+    if (pending_.gates.empty()) return;
+    pending_.rebind();
+    qs_check(qs_apply_circuit(big_, pending_.gates.data(), pending_.gates.size(), opts_.plan, opts_.max_fused_qubits));
+    pending_ = GateBatch{};
+  }
+  std::vector<double> draws(const std::vector<signed char>& mask) {
+    std::vector<double> u(count_, -1.0);  // negative: shot not on this path
+    for (std::uint64_t s = 0; s < count_; ++s)
+      if (mask[s]) u[s] = rngs_[s].uniform();
+    return u;
+  }
+  void gate(const Gate& g, const std::vector<signed char>& mask, bool full) {
+    if (full) {
+      pending_.push(g);
+    } else {  // a strict subset of the shots: one dense matrix on its operands
+      drain();
+      const CMatrix m = gate_matrix(g);
+      std::vector<double> flat;
+      for (long r = 0; r < m.rows(); ++r)
+        for (long c = 0; c < m.cols(); ++c) {
+          flat.push_back(m(r, c).real());
+          flat.push_back(m(r, c).imag());
+        }
+      const std::vector<std::uint32_t> qs = g.qubits();
+      qs_check(qs_batch_apply(big_, n_, qs.data(), static_cast<std::uint32_t>(qs.size()), flat.data(), mask.data(),
+                              count_));
+    }
+    if (!noise_) return;
+    const auto apps = (*noise_)(g);
+    if (apps.empty()) return;
+    drain();
+    for (const auto& a : apps) {
+      const std::size_t dim = std::size_t(1) << a.qubits.size();
+      std::vector<double> flat;
+      for (const auto& k : *a.ops)
+        for (std::size_t r = 0; r < dim; ++r)
+          for (std::size_t c = 0; c < dim; ++c) {
+            flat.push_back(k(static_cast<long>(r), static_cast<long>(c)).real());
+            flat.push_back(k(static_cast<long>(r), static_cast<long>(c)).imag());
+          }
+      const std::vector<double> u = draws(mask);
+      qs_check(qs_batch_kraus(big_, n_, a.qubits.data(), static_cast<std::uint32_t>(a.qubits.size()), flat.data(),
+                              static_cast<std::uint32_t>(a.ops->size()), u.data(), count_, nullptr));
+    }
+  }
+  void measure(const MeasureOp& m, const std::vector<signed char>& mask) {
+    drain();
+    const std::vector<double> u = draws(mask);
+    qs_check(qs_batch_measure(big_, n_, m.qubit, u.data(), count_, outc_.data()));
+    const std::pair<double, double>* ro = readout_ ? (*readout_)(m.qubit) : nullptr;
+    for (std::uint64_t s = 0; s < count_; ++s) {
+      if (!mask[s]) continue;
+      std::int64_t o = outc_[s];
+      if (ro) {
+        const double flip = o ? ro->second : ro->first;
+        if (rngs_[s].uniform() < flip) o = o ? 0 : 1;
+      }
+      cbits_[s][m.cbit] = o;
+    }
+  }
+  void exec(const Program& b, const std::vector<signed char>& mask) {
+    bool full = true;
+    for (signed char x : mask) full = full && x;
+    for (const auto& ins : b.body) {
+      if (const auto* g = std::get_if<GateOp>(&ins)) {
+        gate(g->gate, mask, full);
+      } else if (const auto* m = std::get_if<MeasureOp>(&ins)) {
+        measure(*m, mask);
+      } else if (const auto* f = std::get_if<IfOp>(&ins)) {
+        drain();
+        std::vector<signed char> yes(count_, 0), no(count_, 0);
+        for (std::uint64_t s = 0; s < count_; ++s)
+          if (mask[s]) (f->condition.evaluate(cbits_[s]) != 0 ? yes : no)[s] = 1;
+        if (any(yes)) exec(*f->then_body, yes);
+        if (f->else_body && any(no)) exec(*f->else_body, no);
+      } else if (const auto* w = std::get_if<WhileOp>(&ins)) {
+        drain();
+        std::vector<signed char> cur = mask;
+        for (std::uint64_t iters = 0;;) {
+          for (std::uint64_t s = 0; s < count_; ++s)
+            if (cur[s] && w->condition.evaluate(cbits_[s]) == 0) cur[s] = 0;  // this shot leaves the loop
+          if (!any(cur)) break;
+          if (++iters > opts_.max_while_iterations)
+            throw NonTerminationGuard("QWhile exceeded " + std::to_string(opts_.max_while_iterations) + " iterations");
+          exec(*w->body, cur);
+          drain();
+        }
+      } else if (const auto* a = std::get_if<AssignOp>(&ins)) {
+        for (std::uint64_t s = 0; s < count_; ++s)
+          if (mask[s]) cbits_[s][a->cbit] = a->expr.evaluate(cbits_[s]);
+      }
+    }
+  }
+  static void qs_check(int rc) { detail::qs_check(rc); }
+};
+
+// Shots in batches sized to ~2 GiB of device memory.
 inline std::vector<std::string> run_batched_keys(const Program& p, const SimOptions& opts, std::uint64_t shots,
                                                  const NoiseOf* noise, const ReadoutOf* readout, StateVector* last) {
   const std::uint32_t n = p.qubit_count;
@@ -261,8 +419,10 @@ inline std::vector<std::string> run_batched_keys(const Program& p, const SimOpti
   for (std::uint64_t first = 0; first < shots; first += cap) {
     const std::uint64_t count = std::min(cap, shots - first);
     const bool tail = first + count == shots;
-    for (auto& c : run_shot_batch(p, opts, first, count, noise, readout, tail ? last : nullptr))
-      keys.push_back(cbit_key(c));
+    std::vector<std::vector<std::int64_t>> cb;
+    if (p.is_flat()) cb = run_shot_batch(p, opts, first, count, noise, readout, tail ? last : nullptr);
+    else cb = ControlFlowBatch(p, opts, first, count, noise, readout).run(p, tail ? last : nullptr);
+    for (auto& c : cb) keys.push_back(cbit_key(c));
   }
   return keys;
 }

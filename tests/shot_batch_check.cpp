@@ -64,6 +64,45 @@ int main() {
   nm.set_readout(0, {0.02, 0.0});
   both("noisy", [&] { return run_noisy(p, nm, o, 4000); });
 
+  // control flow in shot batches: divergent branches (gates on subsets of the
+  // shots, incl. 2- and 3-qubit operands), nested QIF, repeat-until-success
+  // QWHILE, measurement inside branches, classical assignments
+  const Program cf = parse_ir(R"(QINIT 5
+CREG 5
+H q[0]
+RY q[1],(0.9)
+MEASURE q[0],c[0]
+QIF c[0] == 1
+  X q[2]
+  CNOT q[1],q[3]
+  MEASURE q[1],c[1]
+  QIF c[1]
+    TOFFOLI q[1],q[2],q[4]
+  ELSE
+    CONTROL q[2]
+    RX q[4],(0.4)
+    ENDCONTROL
+  ENDQIF
+ELSE
+  RY q[2],(1.3)
+  CZ q[0],q[2]
+ENDQIF
+c[3] = 0
+QWHILE c[3] == 0
+  H q[3]
+  MEASURE q[3],c[3]
+  c[4] = c[4] + 1
+ENDQWHILE
+U3 q[4],(0.3,0.2,0.1)
+MEASURE q[2],c[2]
+MEASURE q[4],c[1]
+)");
+  both("control-flow", [&] { return run(cf, o, 3000); });
+  SimOptions o2;
+  o2.seed = 4242;
+  both("control-flow-seed2", [&] { return run(cf, o2, 1500); });
+  both("control-flow-noisy", [&] { return run_noisy(cf, nm, o, 2500); });
+
   std::printf(failures ? "FAILED\n" : "PASSED\n");
   return failures ? 1 : 0;
 }
