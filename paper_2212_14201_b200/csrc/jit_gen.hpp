@@ -623,11 +623,14 @@ struct Gen {
       }
     } else {
       if (ti == 0 && std::memcmp(&h.load, &h.store, sizeof(TileConfigAddr)) != 0) s << "    __syncthreads();\n";
+      // (G | off) & lmask == (G & lmask) + off: the register strides are local
+      // bits that G does not have -- one base pointer, constant offsets
+      s << "    double2* const SP = amps + (G & lmask);\n";
       for (int p = 0; p < NS; ++p) {
         unsigned long long off = 0;
         for (int k = 0; k < R; ++k)
           if ((p >> k) & 1) off |= h.store.rs[k];
-        s << "    __stcs(amps + ((G | " << hexll(off) << ") & lmask), " << name[p] << ");\n";
+        s << "    __stcs(SP + " << hexll(off) << ", " << name[p] << ");\n";
         if (reduce)
           s << "    ACC += __fma_rn(" << name[p] << ".x, " << name[p] << ".x, __dmul_rn(" << name[p] << ".y, " << name[p]
             << ".y)) * (double)((G | " << hexll(off) << ") + 1ull);\n";
@@ -671,12 +674,31 @@ struct Gen {
          "    for (unsigned long long m = ~tmask; c && m; m &= m - 1, c >>= 1)\n"
          "      if (c & 1ull) r |= m & (0ull - m);\n"
          "    return r;\n  };\n";
-    k << "  auto base_of = [&](unsigned long long b) {\n";
-    for (uint32_t b = 0; b < h.m; ++b) {
-      const uint32_t q = h.S[b];
-      k << "    b = ((b >> " << q << ") << " << (q + 1) << ") | (b & " << hexll((1ull << q) - 1) << ");\n";
+    // tile index -> index with zeros at the tile qubits: the non-tile positions
+    // form a few contiguous runs, each a shift-and-mask of the tile index
+    k << "  auto base_of = [&](unsigned long long b) {\n    return 0ull";
+    {
+      bool in_tile[64] = {};
+      for (uint32_t b = 0; b < h.m; ++b) in_tile[h.S[b]] = true;
+      uint32_t c = 0;  // compact bit of the next run
+      for (uint32_t q = 0; q < 64;) {
+        if (in_tile[q]) {
+          ++q;
+          continue;
+        }
+        uint32_t e = q;
+        while (e < 64 && !in_tile[e]) ++e;
+        const uint32_t len = e - q;
+        if (e >= 64 || len >= 64 - c) {  // last run: everything above
+          k << " | ((b >> " << c << ") << " << q << ")";
+          break;
+        }
+        k << " | (((b >> " << c << ") & " << hexll((1ull << len) - 1) << ") << " << q << ")";
+        c += len;
+        q = e;
+      }
     }
-    k << "    return b;\n  };\n";
+    k << ";\n  };\n";
     k << pro.str();
     const uint32_t tbuf = tp.transposes - (lead ? 1u : 0u);
     const uint32_t tile_bufs = single_buf ? 1u : (tbuf ? 1u : 0u) + (prefetch ? 1u : 0u);
@@ -704,6 +726,7 @@ struct Gen {
         k << "    const unsigned long long tb = base_of(t) | rank_base;\n";
         k << "    if ((tb & dmask) != dval) { cp_async_commit(); return; }  // zero tile: nothing to read\n";
         k << "    const unsigned long long g = tb | TL;\n";
+        k << "    const double2* const gp = amps + (g & lmask);  // + loff[p] == (g | loff[p]) & lmask\n";
         for (int p = p0; p < p1; ++p) {
           if (sparse) {  // zero amplitudes: store the zero, skip the copy
             std::string dst;
@@ -715,13 +738,12 @@ struct Gen {
             continue;
           }
           if (lead)
-            k << "    cp_async16(PB + (W0 ^ " << slot_xor(mt0 + TB, p) << "u), amps + ((g | " << hexll(loff[p])
-              << ") & lmask));\n";
+            k << "    cp_async16(PB + (W0 ^ " << slot_xor(mt0 + TB, p) << "u), gp + " << hexll(loff[p]) << ");\n";
           else if (static_cast<uint32_t>(p) < early)
-            k << "    cp_async16(PE + " << p * T << " + tid, amps + ((g | " << hexll(loff[p]) << ") & lmask));\n";
+            k << "    cp_async16(PE + " << p * T << " + tid, gp + " << hexll(loff[p]) << ");\n";
           else
-            k << "    cp_async16(PB + " << (p - static_cast<int>(early)) * T << " + tid, amps + ((g | "
-              << hexll(loff[p]) << ") & lmask));\n";
+            k << "    cp_async16(PB + " << (p - static_cast<int>(early)) * T << " + tid, gp + " << hexll(loff[p])
+              << ");\n";
         }
         k << "    cp_async_commit();\n  };\n";
       };
