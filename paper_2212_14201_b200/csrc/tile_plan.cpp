@@ -452,6 +452,7 @@ struct Compiler {
       if (lane_in_reg) c = default_cfg();
       else fill_threads(c);
       transpose_to(cur, c);
+      if (std::getenv("QSB_PLAN_DEBUG")) std::fprintf(stderr, "store-fix transpose (lanes %s)\n", lane_in_reg ? "in registers" : "on other thread bits");
     }
     final_cfg = cur;
   }
