@@ -858,7 +858,7 @@ int qs_shards_apply_circuit(qs_shards_t s, const qs_gate* gates, uint64_t n) {
   return guarded([&] {
     ShardSet& ss = sh(s);
     if (n && !gates) throw ValidationError("null gate array");
-    auto p = cached_plan(ss.n, gates, n, QS_PLAN_TILED, 0, ss.g);
+    auto p = cached_plan(ss.n, gates, n, QS_PLAN_TILED, 0, ss.g, /*sharded=*/true);
     shard_execute(ss, *p);
     shard_sync(ss);
   });

@@ -112,13 +112,13 @@ PlanCache& plan_cache() {
 }  // namespace
 
 std::shared_ptr<const Plan> cached_plan(uint32_t n, const qs_gate* gates, uint64_t count, uint32_t mode,
-                                        uint32_t max_fused_qubits, uint32_t global_qubits) {
+                                        uint32_t max_fused_qubits, uint32_t global_qubits, bool sharded) {
   static const bool enabled = [] {
     const char* e = std::getenv("QSB_PLAN_CACHE");
     return !e || std::atoi(e) != 0;
   }();
-  if (!enabled) return make_plan(n, gates, count, mode, max_fused_qubits, global_qubits);
-  const std::string key = plan_key(n, gates, count, mode, max_fused_qubits, global_qubits);
+  if (!enabled) return make_plan(n, gates, count, mode, max_fused_qubits, global_qubits, sharded);
+  const std::string key = plan_key(n, gates, count, mode, max_fused_qubits, global_qubits) + (sharded ? "S" : "");
   PlanCache& c = plan_cache();
   {
     std::lock_guard<std::mutex> lk(c.mu);
@@ -128,7 +128,7 @@ std::shared_ptr<const Plan> cached_plan(uint32_t n, const qs_gate* gates, uint64
         return c.lru.front().second;
       }
   }
-  std::shared_ptr<const Plan> p = make_plan(n, gates, count, mode, max_fused_qubits, global_qubits);
+  std::shared_ptr<const Plan> p = make_plan(n, gates, count, mode, max_fused_qubits, global_qubits, sharded);
   std::lock_guard<std::mutex> lk(c.mu);
   c.lru.emplace_front(key, p);
   while (c.lru.size() > 8) c.lru.pop_back();

@@ -54,7 +54,7 @@ std::unique_ptr<Plan> make_plan(uint32_t n, const qs_gate* gates, uint64_t count
 // make_plan through a small LRU keyed by the exact submitted bytes (gates,
 // custom matrices, options); QSB_PLAN_CACHE=0 disables it.
 std::shared_ptr<const Plan> cached_plan(uint32_t n, const qs_gate* gates, uint64_t count, uint32_t mode,
-                                        uint32_t max_fused_qubits, uint32_t global_qubits = 0);
+                                        uint32_t max_fused_qubits, uint32_t global_qubits = 0, bool sharded = false);
 void execute_plan(State& s, const Plan& p);
 // Resets to |basis> and runs the plan; when the plan starts with a tile pass
 // the reset is fused into it (no separate write pass, no read of the old state).

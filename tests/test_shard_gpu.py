@@ -170,6 +170,12 @@ def test_nccl_single_rank_communicator():
     assert np.max(np.abs(st.amplitudes() - want)) <= TOL
     assert abs(st.norm_squared() - 1.0) <= 1e-12
     assert abs(st.checksum() - ol.checksum(want, n)) <= 1e-12 * (1 << n)
+    # the host gate-list path plans for shards too (no permutation steps):
+    # QFT's final SWAPs on a one-rank world
+    qft = workload("qft", n)
+    st.reset(0)
+    st.apply_circuit(qft)
+    assert np.max(np.abs(st.amplitudes() - ol.run_gates(n, qft))) <= TOL
     st.close()
     comm.close()
 
