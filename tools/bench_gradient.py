@@ -47,3 +47,20 @@ err = max(abs(a - b) for a, b in zip(g[:sample], shift))
 print({"slots": len(pc.slots), "terms": len(terms), "adjoint_s": round(adj, 4),
        "shift_rule_gpu_s_est": round(per_slot * len(pc.slots), 2), "speedup": round(per_slot * len(pc.slots) / adj, 1),
        "max_abs_diff_first_%d" % sample: err})
+
+# Config 5's sampling sweep: the bound ansatz with every qubit measured,
+# run(p, seed=s, 10^6 shots) for s = 0..9 (trailing measurements: one state
+# evolution + the exact serial-equivalent sampler on the device).
+prog = Q.Program(n, n)
+prog.body.extend(pc.bind(at).body)
+for q in range(n):
+    prog.measure(q, q)
+Q.run(prog, Q.SimOptions(seed=0), 1000)  # warm-up
+t0 = time.perf_counter()
+keys = 0
+for s in range(10):
+    r = Q.run(prog, Q.SimOptions(seed=s), 1_000_000)
+    keys += len(r.counts)
+sweep = time.perf_counter() - t0
+print({"sampling_sweep": "10 seeds x 1e6 shots, 24 qubits measured", "seconds": round(sweep, 3),
+       "per_run_s": round(sweep / 10, 4), "distinct_keys_total": keys})
