@@ -230,7 +230,7 @@ class ShardedRunner:
         self.arr, self.keep = N.gate_array(gates)
         self.G = len(gates)
         self.kinds = [k for k, _, _ in self.sc.steps()]
-        self.e2e_path = "qs_shards_set_basis_state + qs_shards_apply_circuit(host qs_gate array) + qs_shards_checksum"
+        self.e2e_path = "qs_shards_run_circuit(|0..0>, host qs_gate array) + qs_shards_checksum"
 
     def parallelism(self, world):
         if self.dist:
@@ -252,9 +252,8 @@ class ShardedRunner:
     def checksum(self):
         return self.st.checksum()
 
-    def apply_host(self):  # run(): reset to |0...0> + the host gate list
-        self.st.reset(0)
-        self.N.check(self.L.qs_shards_apply_circuit(self.st.handle(), self.arr, self.G))
+    def apply_host(self):  # run(): reset to |0...0> (fused) + the host gate list
+        self.N.check(self.L.qs_shards_run_circuit(self.st.handle(), 0, self.arr, self.G))
 
     def step_kinds(self):
         return self.kinds

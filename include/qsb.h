@@ -319,6 +319,10 @@ int qs_shards_plan_enqueue_from_basis(qs_shards_t s, qs_plan_t p, uint64_t basis
 int qs_shards_plan_execute_timed(qs_shards_t s, qs_plan_t p, float* step_ms);
 int qs_shards_plan_execute(qs_shards_t s, qs_plan_t p);
 int qs_shards_apply_circuit(qs_shards_t s, const qs_gate* gates, uint64_t n);
+/* run() on a sharded state: reset to |basis> fused into the first pass (runs
+ * from a basis state skip provably zero tiles / shards), then the host gate
+ * list; waits.                                                                 */
+int qs_shards_run_circuit(qs_shards_t s, uint64_t basis, const qs_gate* gates, uint64_t n);
 int qs_shards_norm2(qs_shards_t s, double* out);
 /* Marginal probabilities over distinct qubits (result bit b <-> qubits[b]),
  * summed over shards in rank order                        [statevector.hpp:190-208] */

@@ -143,6 +143,7 @@ _SIGS = {
     "qs_shards_plan_execute_timed": (C.c_int, [_P, _P, C.POINTER(C.c_float)]),
     "qs_shards_plan_execute": (C.c_int, [_P, _P]),
     "qs_shards_apply_circuit": (C.c_int, [_P, _GP, C.c_uint64]),
+    "qs_shards_run_circuit": (C.c_int, [_P, C.c_uint64, _GP, C.c_uint64]),
     "qs_shards_norm2": (C.c_int, [_P, _DP]),
     "qs_shards_probs": (C.c_int, [_P, _UP, C.c_uint32, _DP]),
     "qs_shards_sample": (C.c_int, [_P, _DP, C.c_uint64, C.c_int, _U64P]),

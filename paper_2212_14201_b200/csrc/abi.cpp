@@ -864,6 +864,16 @@ int qs_shards_apply_circuit(qs_shards_t s, const qs_gate* gates, uint64_t n) {
   });
 }
 
+int qs_shards_run_circuit(qs_shards_t s, uint64_t basis, const qs_gate* gates, uint64_t n) {
+  return guarded([&] {
+    ShardSet& ss = sh(s);
+    if (n && !gates) throw ValidationError("null gate array");
+    auto p = cached_plan(ss.n, gates, n, QS_PLAN_TILED, 0, ss.g, /*sharded=*/true);
+    shard_execute_from_basis(ss, *p, basis);
+    shard_sync(ss);
+  });
+}
+
 int qs_shards_probs(qs_shards_t s, const uint32_t* qubits, uint32_t m, double* out) {
   return guarded([&] {
     if (!out || (m && !qubits)) throw ValidationError("null buffer");

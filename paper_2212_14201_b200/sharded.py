@@ -165,6 +165,11 @@ class ShardedState:
         arr, keep = N.gate_array(gates)
         N.check(N.lib().qs_shards_apply_circuit(self._h, arr, len(gates)))
 
+    def run_circuit(self, gates, basis=0):
+        """run(): reset to |basis> fused into the first pass, then `gates`."""
+        arr, keep = N.gate_array(gates)
+        N.check(N.lib().qs_shards_run_circuit(self._h, basis, arr, len(gates)))
+
     def execute(self, circuit, sync=True, from_basis=None):
         if from_basis is not None:
             N.check(N.lib().qs_shards_plan_enqueue_from_basis(self._h, circuit.handle(), from_basis))

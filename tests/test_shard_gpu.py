@@ -176,6 +176,9 @@ def test_nccl_single_rank_communicator():
     st.reset(0)
     st.apply_circuit(qft)
     assert np.max(np.abs(st.amplitudes() - ol.run_gates(n, qft))) <= TOL
+    st.run_circuit(gates, basis=5)  # run() from |5>: reset fused, lazy zeros
+    want5 = ol.run_gates(n, gates, state=np.eye(1, 1 << n, 5, dtype=np.complex128)[0])
+    assert np.max(np.abs(st.amplitudes() - want5)) <= TOL
     st.close()
     comm.close()
 
@@ -197,7 +200,7 @@ def test_checksum_invariant_across_shard_counts():
             st = ShardedState.local(n, g)
         finally:
             del os.environ["QSB_SHARD_EXCHANGE"]
-        st.apply_circuit(gates)
+        st.run_circuit(gates) if mode == "peer" else st.apply_circuit(gates)
         assert abs(st.checksum() - ref) <= 1e-12 * (1 << n)
         assert np.max(np.abs(st.amplitudes(12345678, 4096) - probe)) <= 1e-12
         st.close()
