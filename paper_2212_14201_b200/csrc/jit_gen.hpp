@@ -71,6 +71,12 @@ struct Gen {
   // bench checksum, bench.hpp:141-148) -- one partial per CTA into red[]
   bool reduce = false;
   int transposes_total = 0;
+  // Warp-local transposes: when the qubits on thread bits >= 5 stay put, every
+  // warp exchanges only its own amplitudes (each has a fixed smem slot), so
+  // __syncwarp suffices -- except before the first exchange of a tile, whose
+  // block barrier separates it from the previous tile's reads of the buffer.
+  bool tile_barrier_done = false;
+  bool warp_local_ok = true;
 
   // Tile-wide phase factors from qubits outside the tile: a product over up
   // to n-m bits of the tile's global index.  Bits are grouped in chunks of 6
@@ -426,7 +432,10 @@ struct Gen {
         if (cols[k]) e << " ^ (((tid >> " << k << ") & 1u) * " << cols[k] << "u)";
       return e.str();
     };
-    s << "    __syncthreads();\n";
+    bool warp_local = warp_local_ok && TB > 5;
+    for (uint32_t k = 5; warp_local && k < TB; ++k) warp_local = cur_tq[k] == mt[2 * TB + 2 * R + k];
+    s << ((warp_local && tile_barrier_done) ? "    __syncwarp();\n" : "    __syncthreads();\n");
+    tile_barrier_done = true;
     s << "    const unsigned " << Tw << " = " << xorexpr(mt) << ";\n";
     for (int p = 0; p < NS; ++p) {
       uint32_t a = 0;
@@ -434,7 +443,7 @@ struct Gen {
         if ((p >> k) & 1) a ^= mt[TB + k];
       s << "    sm[" << Tw << " ^ " << a << "u] = " << name[p] << ";\n";
     }
-    s << "    __syncthreads();\n";
+    s << (warp_local ? "    __syncwarp();\n" : "    __syncthreads();\n");
     s << "    const unsigned " << Tr << " = " << xorexpr(mt + TB + R) << ";\n";
     for (int p = 0; p < NS; ++p) {
       uint32_t a = 0;
@@ -516,6 +525,7 @@ struct Gen {
       s << "      continue;\n    }\n";
     }
     int ti = 0;
+    tile_barrier_done = lead && !from_basis;  // the fused leading exchange has its own block barrier
     if (from_basis) {
       unsigned long long off[kTileMaxSlots];
       for (int p = 0; p < NS; ++p) {
