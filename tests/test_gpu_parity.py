@@ -492,3 +492,36 @@ def test_fused_checksum_through_final_permutation(monkeypatch):
     assert np.max(np.abs(sv.amplitudes() - ref)) <= 1e-10
     want = float(np.sum(np.abs(ref) ** 2 * (np.arange(1 << n) + 1.0)))
     assert abs(fused - want) <= 1e-9 * want
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("knobs", [
+    {"QSB_TILE_M": "13", "QSB_TILE_R": "5"},
+    {"QSB_TILE_M": "13", "QSB_TILE_EARLY": "8"},
+    {"QSB_TILE_EARLY": "12"},
+    {"QSB_TILE_SINGLEBUF": "1", "QSB_NO_WARP_TRANSPOSE": "1"},
+    {"QSB_TILE_PREFETCH": "0"},
+    {"QSB_FREE_LOAD": "0", "QSB_NO_SPARSE_LOAD": "1", "QSB_NO_TILE_COMPACT": "1"},
+])
+def test_tile_knobs_keep_parity(monkeypatch, knobs):
+    """The diagnostic / experimental tile knobs (DESIGN 6e) still produce the
+    oracle's state: 5 register bits, early prefetch issue, forced single
+    buffer, no prefetch, no free load / sparse reads / compaction."""
+    from test_planner_emu import mixed_gates
+    for k, v in knobs.items():
+        monkeypatch.setenv(k, v)
+    n = 18
+    for gates in (Q.gen_random_circuit(n, 3, 11).gates(), Q.gen_qft(n, 0).gates(), mixed_gates(n, 150, 17)):
+        cc = Q.CompiledCircuit(n, gates)
+        sv = Q.StateVector(n)
+        b = 0x2B1C5 & ((1 << n) - 1)
+        cs = cc.execute_checksum(sv, b)
+        ref = ol.run_gates(n, gates, state=np.eye(1, 1 << n, b, dtype=np.complex128)[0])
+        assert np.max(np.abs(sv.amplitudes() - ref)) <= 1e-10
+        want = float(np.sum(np.abs(ref) ** 2 * (np.arange(1 << n) + 1.0)))
+        assert abs(cs - want) <= 1e-9 * want
+        sv2 = Q.StateVector(n)
+        sv2.set_amplitudes(ref)
+        cc.execute(sv2)  # in place from an arbitrary state
+        ref2 = ol.run_gates(n, gates, state=ref)
+        assert np.max(np.abs(sv2.amplitudes() - ref2)) <= 1e-10
