@@ -136,10 +136,9 @@ struct TileOptions {
 TileOptions tile_options_from_env();
 
 void plan_tiles(uint32_t n, std::vector<Op>& ops, std::vector<Step>& steps, const TileOptions& opt);
-// Estimated HBM time of a plan in units of one light 12-qubit tile pass
-// (measured on B200, 30 qubits: 12-qubit passes with <= 2 shared-memory
-// transposes 5.8 ms, with 3 or more 6.8 ms; 13-qubit passes -- one CTA per SM,
-// single buffer -- 6.85 ms).
+// Estimated time of a plan in units of one HBM sweep (measured on B200, 30
+// qubits, profiles/r1/random30_per_pass.txt: 12- and 13-qubit passes with <= 2
+// shared-memory exchanges 5.8 ms, each further exchange +17%).
 double plan_cost(const std::vector<Step>& steps);
 // Plans with and without qubit relabelling (unless fixed by QSB_TILE_REMAP),
 // with 12- and, for large unsharded states, 13-qubit tiles (unless fixed by
