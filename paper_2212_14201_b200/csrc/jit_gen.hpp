@@ -72,9 +72,9 @@ struct Gen {
   bool reduce = false;
   int transposes_total = 0;
   // Warp-local transposes: when the qubits on thread bits >= 5 stay put, every
-  // warp exchanges only its own amplitudes (each has a fixed smem slot), so
-  // __syncwarp suffices -- except before the first exchange of a tile, whose
-  // block barrier separates it from the previous tile's reads of the buffer.
+  // warp exchanges only its own amplitudes (under one exchange's swizzle each
+  // has its own smem slot), so the barrier between the writes and the reads
+  // is a __syncwarp; the barrier before the writes stays block-wide.
   bool tile_barrier_done = false;
   bool warp_local_ok = true;
 
@@ -434,7 +434,10 @@ struct Gen {
     };
     bool warp_local = warp_local_ok && TB > 5;
     for (uint32_t k = 5; warp_local && k < TB; ++k) warp_local = cur_tq[k] == mt[2 * TB + 2 * R + k];
-    s << ((warp_local && tile_barrier_done) ? "    __syncwarp();\n" : "    __syncthreads();\n");
+    // the leading barrier stays block-wide: each exchange picks its own
+    // swizzle, so this exchange's writes may hit slots other warps are still
+    // reading from the previous one
+    s << "    __syncthreads();\n";
     tile_barrier_done = true;
     s << "    const unsigned " << Tw << " = " << xorexpr(mt) << ";\n";
     for (int p = 0; p < NS; ++p) {
