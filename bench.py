@@ -409,7 +409,9 @@ def main():
                 "kernel": "qsb_tile_* (per-pass NVRTC sm_100a)" if args.plan == "tiled" else "per-gate kernels",
                 "algorithmic_bytes_per_launch": 2 * state_bytes, "launches_per_step": stats["launches"],
                 "avg_launch_ms": round(avg_pass_ms, 4), "peak_kind": peak_kind,
-                "pass_time_share": round(sum(pass_ms) / ms_per_step, 4) if ms_per_step else None}
+                # tile passes' share of the per-step-timed run (full passes, not started
+                # from a basis state, so its total exceeds the timed step's)
+                "pass_time_share": round(sum(pass_ms) / sum(per), 4) if per and sum(per) else None}
     if xchg_ms:
         roofline["exchanges_per_step"] = len(xchg_ms)
         roofline["exchange_ms_total"] = round(sum(xchg_ms), 3)
