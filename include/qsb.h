@@ -78,6 +78,10 @@ const char* qs_last_error(void);
 int qs_abi_version(void);
 /* Number of this library's own kernel launches since load (bench evidence). */
 uint64_t qs_kernel_launches(void);
+/* Tile-kernel JIT counters since load: NVRTC builds, in-process cache hits,
+ * cubins loaded from the on-disk cache ($QSB_JIT_CACHE, default
+ * ~/.cache/qsb-jit).  Any pointer may be NULL. */
+int qs_jit_stats(uint64_t* nvrtc_builds, uint64_t* memory_hits, uint64_t* disk_hits);
 
 /* --- lifecycle ------------------------------------------------------------- */
 /* StateVector(n): |0...0> on `device`.  max_qubits bounds n (the reference caps

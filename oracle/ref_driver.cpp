@@ -375,6 +375,71 @@ int golden_big(const std::string& dir) {
   return 0;
 }
 
+// Reference results for the BENCHMARKED configurations at their real size
+// (BASELINE configs 2 and 3, bench.py workloads random28 / random30 / qft30):
+// the final state of run() (simulator.hpp:142-194, fusion at the default k=3)
+// reduced to probability_checksum (bench.hpp:141-148), norm_squared, 8 windows
+// of 4096 amplitudes (window 0 at index 0, 7 at Rng(7)-drawn offsets), the
+// first 256 probabilities and one 6-qubit marginal (statevector.hpp:190-207).
+// Peak host memory ~2 x 16 GiB at 30 qubits (state + RunResult copy).
+//   ref_driver golden_huge <dir> [random28|random30|qft30 ...]
+int golden_huge(const std::string& dir, const std::vector<std::string>& which) {
+  Manifest man;
+  for (const std::string& name : which) {
+    Program p;
+    std::string gen;
+    if (name == "random28") {
+      p = gen_random_circuit(28, 20, 424242);
+      gen = "\"random\",\"args\":[28,20,424242]";
+    } else if (name == "random30") {
+      p = gen_random_circuit(30, 20, 424242);
+      gen = "\"random\",\"args\":[30,20,424242]";
+    } else if (name == "qft30") {
+      p = oraclegen::gen_qft(30, 0x2AAAAAAAull);
+      gen = "\"qft\",\"args\":[30,715827882]";
+    } else {
+      std::fprintf(stderr, "golden_huge: unknown case %s\n", name.c_str());
+      return 2;
+    }
+    const std::uint32_t n = p.qubit_count;
+    const std::size_t dim = std::size_t{1} << n;
+    auto t0 = std::chrono::steady_clock::now();
+    RunResult rr = run(p);
+    auto t1 = std::chrono::steady_clock::now();
+    const StateVector& sv = *rr.final_state;
+    const double cs = probability_checksum(sv);
+    const double nrm = sv.norm_squared();
+    constexpr std::size_t W = 4096;
+    std::vector<std::uint64_t> starts = {0};
+    Rng r(7);
+    while (starts.size() < 8) starts.push_back(r.below(dim - W) & ~std::uint64_t{15});
+    {
+      std::ofstream f(dir + "/" + name + ".win.amps", std::ios::binary);
+      for (std::uint64_t s : starts)
+        for (std::size_t i = 0; i < W; ++i) {
+          const cdouble a = sv.amplitude(s + i);
+          f.write(reinterpret_cast<const char*>(&a), sizeof a);
+        }
+    }
+    std::vector<double> head;
+    for (std::size_t i = 0; i < 256; ++i) head.push_back(std::norm(sv.amplitude(i)));
+    std::vector<std::uint32_t> sub = {n - 1, 17, 13, 5, 1, 0};
+    const auto marg = sv.probabilities(sub);
+    std::string st = "[";
+    for (std::size_t i = 0; i < starts.size(); ++i) st += (i ? "," : "") + std::to_string(starts[i]);
+    man.add("{\"name\":\"" + name + "\",\"type\":\"huge\",\"n\":" + std::to_string(n) + ",\"gen\":" + gen +
+            ",\"gates\":" + std::to_string(p.body.size()) + ",\"checksum\":" + g17(cs) + ",\"norm2\":" + g17(nrm) +
+            ",\"window\":4096,\"starts\":" + st + "],\"amps\":\"" + name + ".win.amps\",\"probs_head\":" +
+            dlist(head) + ",\"marginal_qubits\":" + qlist(sub) + ",\"marginal\":" + dlist(marg) +
+            ",\"run_seconds\":" + g17(std::chrono::duration<double>(t1 - t0).count()) +
+            ",\"threads\":" + std::to_string(omp_get_max_threads()) + "}");
+    std::fprintf(stderr, "golden_huge %s: run %.1f s, checksum %.17g\n", name.c_str(),
+                 std::chrono::duration<double>(t1 - t0).count(), cs);
+    man.write(dir + "/manifest_huge.json");  // rewritten after every case
+  }
+  return 0;
+}
+
 // CPU timing of the reference through run() (simulator.hpp:142): the first
 // `layers` layers of gen_random_circuit(n, d, seed) (a bounded sample of the
 // workload), `reps` repetitions; prints one JSON line per repetition.
@@ -417,6 +482,11 @@ int bench(int argc, char** argv) {
 int main(int argc, char** argv) {
   if (argc >= 3 && std::strcmp(argv[1], "golden") == 0) return golden(argv[2]);
   if (argc >= 3 && std::strcmp(argv[1], "golden_big") == 0) return golden_big(argv[2]);
+  if (argc >= 3 && std::strcmp(argv[1], "golden_huge") == 0) {
+    std::vector<std::string> which(argv + 3, argv + argc);
+    if (which.empty()) which = {"random28", "qft30", "random30"};
+    return golden_huge(argv[2], which);
+  }
   if (argc >= 2 && std::strcmp(argv[1], "bench") == 0) return bench(argc, argv);
   std::fprintf(stderr, "usage: ref_driver golden <dir> | golden_big <dir> | bench ...\n");
   return 2;

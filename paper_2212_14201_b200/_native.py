@@ -67,6 +67,7 @@ _SIGS = {
     "qs_last_error": (C.c_char_p, []),
     "qs_abi_version": (C.c_int, []),
     "qs_kernel_launches": (C.c_uint64, []),
+    "qs_jit_stats": (C.c_int, [C.POINTER(C.c_uint64)] * 3),
     "qs_create": (C.c_int, [C.c_uint32, C.c_int, C.c_uint32, C.POINTER(_P)]),
     "qs_destroy": (C.c_int, [_P]),
     "qs_clone": (C.c_int, [_P, C.POINTER(_P)]),

@@ -12,6 +12,7 @@
 #include "common.hpp"
 #include "fusion.hpp"
 #include "gates.hpp"
+#include "jit.hpp"
 #include "kernels.hpp"
 #include "plan.hpp"
 #include "shard.hpp"
@@ -126,6 +127,12 @@ extern "C" {
 const char* qs_last_error(void) { return qsb::g_last_error.c_str(); }
 int qs_abi_version(void) { return QSB_ABI_VERSION; }
 uint64_t qs_kernel_launches(void) { return qsb::g_launches.load(); }
+int qs_jit_stats(uint64_t* nvrtc_builds, uint64_t* memory_hits, uint64_t* disk_hits) {
+  if (nvrtc_builds) *nvrtc_builds = qsb::jit_compiles();
+  if (memory_hits) *memory_hits = qsb::jit_cache_hits();
+  if (disk_hits) *disk_hits = qsb::jit_disk_hits();
+  return QS_OK;
+}
 
 int qs_create(uint32_t num_qubits, int device, uint32_t max_qubits, qs_state_t* out) {
   return guarded([&] {

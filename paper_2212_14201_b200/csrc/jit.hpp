@@ -51,5 +51,6 @@ void compile_tile_steps(std::vector<Step>& steps);
 // Statistics for tests / diagnostics.
 uint64_t jit_compiles();
 uint64_t jit_cache_hits();
+uint64_t jit_disk_hits();  // cubins loaded from the on-disk cache (QSB_JIT_CACHE)
 
 }  // namespace qsb

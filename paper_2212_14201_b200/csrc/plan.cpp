@@ -118,7 +118,16 @@ std::shared_ptr<const Plan> cached_plan(uint32_t n, const qs_gate* gates, uint64
     return !e || std::atoi(e) != 0;
   }();
   if (!enabled) return make_plan(n, gates, count, mode, max_fused_qubits, global_qubits, sharded);
-  const std::string key = plan_key(n, gates, count, mode, max_fused_qubits, global_qubits) + (sharded ? "S" : "");
+  // planning / code-generation knobs (DESIGN 6e) are read when a plan is made,
+  // so they are part of the key: a plan made under other settings is not reused
+  std::string knobs;
+  for (const char* k : {"QSB_TILE_M", "QSB_TILE_R", "QSB_TILE_LOW", "QSB_TILE_REMAP", "QSB_PERM_STEP", "QSB_ABSORB_X",
+                        "QSB_NO_ABSORB_X", "QSB_FOLD_PERM", "QSB_FREE_LOAD", "QSB_SHARD_BATCH", "QSB_TILE_PREFETCH",
+                        "QSB_TILE_SINGLEBUF", "QSB_TILE_MINB", "QSB_BASIS_MINB", "QSB_TILE_EARLY",
+                        "QSB_NO_WARP_TRANSPOSE", "QSB_TILE_VARIANTS"})
+    if (const char* v = std::getenv(k)) knobs += std::string(k) + "=" + v + ";";
+  const std::string key =
+      plan_key(n, gates, count, mode, max_fused_qubits, global_qubits) + (sharded ? "S" : "") + knobs;
   PlanCache& c = plan_cache();
   {
     std::lock_guard<std::mutex> lk(c.mu);
@@ -143,8 +152,8 @@ void execute_plan(State& s, const Plan& p) {
 
 TileSkip zero_tiles(const Step& st, uint64_t basis) {
   TileSkip k;
-  static const bool off = std::getenv("QSB_NO_ZERO_SKIP") != nullptr;
-  static const bool no_sparse = std::getenv("QSB_NO_SPARSE_LOAD") != nullptr;
+  const bool off = std::getenv("QSB_NO_ZERO_SKIP") != nullptr;
+  const bool no_sparse = std::getenv("QSB_NO_SPARSE_LOAD") != nullptr;
   if (off || st.kind != Step::TileStep) return k;
   unsigned long long tile_bits = 0;
   for (uint32_t b = 0; b < st.tile->h.m; ++b) tile_bits |= 1ull << st.tile->h.S[b];
@@ -173,7 +182,7 @@ void execute_plan_from_basis(State& s, const Plan& p, uint64_t basis, double* ch
   // wrote (a qubit definite outside a pass's tile stays definite through it).
   // Before a step that reads everything, and at the end, the complement of
   // the last pass's tiles is zeroed -- usually empty (every tile active).
-  static const bool lazy = !std::getenv("QSB_NO_LAZY_ZERO") && !std::getenv("QSB_NO_SPARSE_LOAD") &&
+  const bool lazy = !std::getenv("QSB_NO_LAZY_ZERO") && !std::getenv("QSB_NO_SPARSE_LOAD") &&
                            !std::getenv("QSB_NO_ZERO_SKIP") && !std::getenv("QSB_NO_TILE_COMPACT");
   TileSkip unwritten;  // amplitudes outside (mask, val) may hold stale data
   auto settle = [&]() {
@@ -181,7 +190,7 @@ void execute_plan_from_basis(State& s, const Plan& p, uint64_t basis, double* ch
     unwritten = TileSkip{};
   };
   // the checksum rides on the last pass when the plan ends with a tile pass
-  static const bool fuse_sum = !std::getenv("QSB_NO_FUSED_CHECKSUM");
+  const bool fuse_sum = !std::getenv("QSB_NO_FUSED_CHECKSUM");
   const bool fused = checksum && fuse_sum && !p.steps.empty() &&
                      (p.steps.back().kind == Step::TileStep || p.steps.back().kind == Step::PermStep);
   double* part = fused ? static_cast<double*>(s.get_scratch(kMaxTileGrid * sizeof(double) + sizeof(double))) : nullptr;

@@ -569,7 +569,7 @@ void shard_execute(ShardSet& ss, const Plan& p, uint64_t first, uint64_t count, 
     *unwritten = TileSkip{};
   };
   const uint64_t last = std::min<uint64_t>(p.steps.size(), count == ~0ull ? p.steps.size() : first + count);
-  static const bool fuse = [] {
+  const bool fuse = [] {
     const char* e = std::getenv("QSB_FUSE_EXCHANGE");
     return !e || std::atoi(e) != 0;
   }();
@@ -621,7 +621,7 @@ void shard_execute_from_basis(ShardSet& ss, const Plan& p, uint64_t basis) {
       if (((b >> hi) ^ (b >> lo)) & 1) b ^= (1ull << hi) | (1ull << lo);
     }
   }
-  static const bool lazy = !std::getenv("QSB_NO_LAZY_ZERO") && !std::getenv("QSB_NO_SPARSE_LOAD") &&
+  const bool lazy = !std::getenv("QSB_NO_LAZY_ZERO") && !std::getenv("QSB_NO_SPARSE_LOAD") &&
                            !std::getenv("QSB_NO_ZERO_SKIP") && !std::getenv("QSB_NO_TILE_COMPACT");
   TileSkip unwritten;
   if (first < p.steps.size() && p.steps[first].kind == Step::TileStep) {

@@ -7,6 +7,9 @@
 #include <cstring>
 #include <map>
 #include <random>
+#include <string>
+#include <thread>
+#include <vector>
 
 #include "tile.hpp"
 
@@ -1323,24 +1326,44 @@ void plan_tiles(uint32_t n, std::vector<Op>& ops, std::vector<Step>& steps, uint
   if (!std::getenv("QSB_TILE_M") && n - global_qubits >= 26) ms.push_back(13);
   std::vector<int> remaps{0, 1};
   if (const char* e = std::getenv("QSB_TILE_REMAP")) remaps = {std::atoi(e) != 0 ? 1 : 0};
-  const std::vector<Op> orig = ops;
-  double best = 0;
-  bool have = false;
+  // The candidates are planned concurrently (independent; the planner has no
+  // shared mutable state) and the cheapest is kept (ties: the first).
+  struct Cand {
+    TileOptions o;
+    std::vector<Op> ops;
+    std::vector<Step> steps;
+    double cost = 0;
+    std::string err;
+  };
+  std::vector<Cand> cands;
   for (uint32_t m : ms)
     for (int r : remaps) {
-      std::vector<Op> copy = orig;
-      std::vector<Step> cand;
-      o.m = m;
-      o.remap = r != 0;
-      plan_tiles(n, copy, cand, o);
-      const double c = plan_cost(cand);
-      if (!have || c < best - 1e-9) {
-        best = c;
-        steps = std::move(cand);
-        ops = std::move(copy);
-        have = true;
-      }
+      Cand c;
+      c.o = o;
+      c.o.m = m;
+      c.o.remap = r != 0;
+      c.ops = ops;
+      cands.push_back(std::move(c));
     }
+  auto work = [](Cand& c, uint32_t nq) {
+    try {
+      plan_tiles(nq, c.ops, c.steps, c.o);
+      c.cost = plan_cost(c.steps);
+    } catch (const std::exception& e) {
+      c.err = e.what();
+    }
+  };
+  std::vector<std::thread> pool;
+  for (size_t i = 1; i < cands.size(); ++i) pool.emplace_back(work, std::ref(cands[i]), n);
+  work(cands[0], n);
+  for (auto& t : pool) t.join();
+  size_t best = 0;
+  for (size_t i = 0; i < cands.size(); ++i) {
+    if (!cands[i].err.empty()) throw RuntimeError(cands[i].err);
+    if (cands[i].cost < cands[best].cost - 1e-9) best = i;
+  }
+  steps = std::move(cands[best].steps);
+  ops = std::move(cands[best].ops);
 }
 
 }  // namespace qsb

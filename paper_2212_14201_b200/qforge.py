@@ -135,7 +135,7 @@ def validate_or_throw(p):
 class SimOptions:
     """simulator.hpp:18-36 plus the B200 planner knobs (plan, device)."""
     parallel_threshold: int = 1 << 14   # accepted, no effect on the GPU
-    fusion_enabled: bool = False        # reference dense fusion (QS_PLAN_DENSE_FUSION)
+    fusion_enabled: bool = False        # accepted; gate runs are always fused into tile passes
     max_fused_qubits: int = 3
     seed: int = 0
     workers: int = 0                    # accepted, no effect on the GPU
@@ -407,12 +407,21 @@ def counts_from_indices(indices, measures, cbits):
     return out
 
 
+def run_plan_mode(opts):
+    """The plan run() executes, as in the C++ facade (include/qforge/simulator.hpp
+    run()): fusion_enabled keeps the default tile passes -- they already fuse
+    every gate run, far beyond fuse_circuit's k <= 5 blocks -- and the
+    reference's dense-block plan runs only when asked for explicitly
+    (plan=QS_PLAN_DENSE_FUSION)."""
+    return opts.plan_mode()
+
+
 def run(p, opts=None, shots=0):
     """simulator.hpp:142-194."""
     opts = opts or SimOptions()
     opts.validate()
     validate_or_throw(p)
-    mode = N.QS_PLAN_DENSE_FUSION if (opts.fusion_enabled and opts.plan == N.QS_PLAN_DEFAULT) else opts.plan_mode()
+    mode = run_plan_mode(opts)
     result = RunResult()
     if _trailing_measure_form(p):
         sv = StateVector(p.qubit_count, opts.device)

@@ -115,3 +115,47 @@ def test_validation_errors_without_gpu():
     p.add(Q.make_gate(Q.GateKind.RX, [0]))  # missing parameter
     with pytest.raises(Q.ValidationError):
         Q.validate_or_throw(p)
+
+
+_JIT_PROBE = r"""
+import json, sys
+sys.path.insert(0, %r)
+from paper_2212_14201_b200 import _native as N, qforge as Q
+cc = Q.CompiledCircuit(16, Q.gen_random_circuit(16, 3, 7).gates())
+a = [N.C.c_uint64() for _ in range(3)]
+N.check(N.lib().qs_jit_stats(*[N.C.byref(x) for x in a]))
+print(json.dumps({"stats": cc.stats(), "jit": [x.value for x in a]}))
+"""
+
+
+def test_jit_disk_cache_serves_a_cold_process(tmp_path):
+    """NVRTC output is cached on disk (QSB_JIT_CACHE): a second, fresh process
+    planning the same circuit shape builds nothing and loads every tile cubin
+    from the cache (the cold-start path of run(), VERDICT r1 item 'cold path')."""
+    import json
+    import subprocess
+    import sys
+    env = dict(os.environ, QSB_JIT_CACHE=str(tmp_path / "jit"))
+    outs = []
+    for _ in range(2):
+        r = subprocess.run([sys.executable, "-c", _JIT_PROBE % ROOT], capture_output=True, text=True, env=env,
+                           timeout=600)
+        assert r.returncode == 0, r.stderr
+        outs.append(json.loads(r.stdout.strip().splitlines()[-1]))
+    first, second = outs
+    assert first["stats"] == second["stats"]
+    assert first["jit"][0] > 0 and first["jit"][2] == 0     # built with NVRTC, nothing on disk yet
+    assert second["jit"][0] == 0                            # nothing rebuilt ...
+    assert second["jit"][2] == first["jit"][0]              # ... every module came from disk
+    assert len(list((tmp_path / "jit").glob("*.qsbcubin"))) == first["jit"][0]
+
+
+def test_run_plan_mode_matches_the_cpp_facade():
+    """Python run() picks the plan the C++ facade's run() picks
+    (include/qforge/simulator.hpp: dense fusion only when asked for by plan)."""
+    assert Q.run_plan_mode(Q.SimOptions()) == N.QS_PLAN_TILED
+    assert Q.run_plan_mode(Q.SimOptions(fusion_enabled=True)) == N.QS_PLAN_TILED
+    assert Q.run_plan_mode(Q.SimOptions(fusion_enabled=True, plan=N.QS_PLAN_DENSE_FUSION)) == N.QS_PLAN_DENSE_FUSION
+    assert Q.run_plan_mode(Q.SimOptions(plan=N.QS_PLAN_UNFUSED)) == N.QS_PLAN_UNFUSED
+    src = open(os.path.join(ROOT, "paper_2212_14201_b200", "include", "qforge", "simulator.hpp")).read()
+    assert "(opts.fusion_enabled && opts.plan == QS_PLAN_DENSE_FUSION) ? QS_PLAN_DENSE_FUSION" in src
