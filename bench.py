@@ -6,22 +6,27 @@ on complex128 state vectors in HBM.
 One step = one full circuit execution from |0...0>: reset the state, run every
 planned pass (gen_random_circuit(30, 20, 424242): 1200 gates), reduce the
 probability checksum (bench.hpp:141-148).  The reset is fused into the first
-tile pass (qs_plan_enqueue_from_basis: that pass writes the state without
-reading it).  `value` is original (unfused)
-gates per second of device time with the circuit plan already resident;
-`e2e` is the same metric through the public API (qs_apply_circuit with the
-host gate array: planning + upload + execution + checksum read-back).
+tile pass (that pass writes the state without reading it) and the checksum
+into the last (qs_plan_execute_from_basis_checksum).  `value` is original
+(unfused) gates per second of device time with the circuit plan resident;
+`e2e` is the same metric through the public API with host buffers
+(qs_run_circuit_checksum: validation, plan-cache lookup, upload, execution,
+checksum read-back), and `e2e.cold` the same call in a fresh process (planning
+and tile-kernel build or on-disk cubin load included).  `parity` compares the
+step's checksum with the unmodified reference's (tests/golden/huge).
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
-                    [--workload random30|random28|qft30|hea24|ghz20] [--plan tiled|dense|unfused]
+                    [--workload random30|random28|qft30|hea24|ghz20|qft34|random34]
+                    [--plan tiled|dense|unfused]
 
 Under torchrun (N > 1, a power of two) the same circuit runs on ONE state
-sharded over the N GPUs (top log2 N qubits = rank bits, half-shard exchanges
-over NCCL; strong scaling); `--replicas` runs independent copies instead.  The
-time is the max over ranks.  `--local-shards G` (N = 1) runs the sharded plan
-with 2^G shards on one GPU (diagnostic).  `--impl reference` times the
-reference CPU simulator (oracle/_ref/ref_driver, the unmodified qforge
-headers) on rank 0.
+sharded over the N GPUs (top log2 N qubits = rank bits, batched all-to-all
+exchanges over peer memory / NCCL; strong scaling), and the config-4 34-qubit
+lines (qft34, random34) are added under "config4"; `--replicas` runs
+independent copies instead.  The time is the max over ranks.
+`--local-shards G` (N = 1) runs the sharded plan with 2^G shards on one GPU
+(diagnostic).  `--impl reference` times the reference CPU simulator
+(oracle/_ref/ref_driver, the unmodified qforge headers) on rank 0.
 """
 import argparse
 import json
@@ -42,8 +47,12 @@ WORKLOADS = {
     "qft30": ("qft", (30, 0x2AAAAAAA), 30),
     "hea24": ("hea", (24, 10, 2024), 24),
     "ghz20": ("ghz", (20,), 20),
-    "qft34": ("qft", (34, 0x2AAAAAAAA), 34),  # sharded over >= 2 GPUs (256 GiB state)
+    "qft34": ("qft", (34, 0x2AAAAAAAA), 34),  # config 4: sharded over >= 2 GPUs (256 GiB state)
+    "random34": ("random", (34, 20, 424242), 34),  # config 4: sharded over >= 2 GPUs
 }
+# reference results of the unmodified qforge run() for these workloads
+# (oracle/_ref/ref_driver golden_huge; tests/test_bench_parity.py)
+HUGE = os.path.join(ROOT, "tests", "golden", "huge", "manifest_huge.json")
 
 
 def peaks():
@@ -131,24 +140,40 @@ def build_program(workload):
     return p, n
 
 
-def cpu_baseline_reference(workload, layers, reps, threads=None):
-    """Times the reference (oracle/_ref/ref_driver: unmodified qforge run()) on
-    a bounded sample: the first `layers` layers of the workload, fusion on."""
+def ref_steps(workload, per_step, steps, threads=None, fusion=True):
+    """Times the reference (oracle/_ref/ref_driver bench_steps: the unmodified
+    qforge run() body -- fuse_circuit + StateVector::apply_gate per block,
+    simulator.hpp:147-159 -- on ONE resident state, so neither its per-run()
+    allocation/zero fill nor its final-state copy is inside a step).  A step =
+    the next `per_step` gates of the workload's circuit.  Returns (alloc row,
+    step rows) or (None, error)."""
     exe = os.path.join(ROOT, "oracle", "_ref", "ref_driver")
     if not os.path.exists(exe):
         return None, "oracle/_ref/ref_driver not built"
     gen, args, n = WORKLOADS[workload]
-    if gen != "random":
-        return None, "cpu baseline implemented for the random workloads"
+    if gen not in ("random", "qft") or n > 30:
+        return None, "the reference caps states at 30 qubits (statevector.hpp:137)"
+    a = (str(args[0]), str(args[1]), str(args[2])) if gen == "random" else (str(args[0]), str(args[1]), "0")
     env = dict(os.environ)
-    if threads:
-        env["OMP_NUM_THREADS"] = str(threads)
-    out = subprocess.run([exe, "bench", "random", str(args[0]), str(args[1]), str(args[2]), str(layers), "1",
-                          str(reps)], capture_output=True, text=True, env=env, timeout=3600)
+    env["OMP_NUM_THREADS"] = str(threads or os.cpu_count() or 1)
+    out = subprocess.run([exe, "bench_steps", gen, *a, str(per_step), str(steps), "1" if fusion else "0"],
+                         capture_output=True, text=True, env=env, timeout=3600)
     if out.returncode != 0:
         return None, out.stderr.strip()[-200:]
     rows = [json.loads(l) for l in out.stdout.splitlines() if l.startswith("{")]
-    return rows, None
+    alloc = [r for r in rows if "alloc_seconds" in r]
+    return (alloc[0] if alloc else {}, [r for r in rows if "seconds" in r]), None
+
+
+def reference_checksum(workload):
+    try:
+        with open(HUGE) as f:
+            for c in json.load(f):
+                if c["name"] == workload:
+                    return c["checksum"]
+    except OSError:
+        pass
+    return None
 
 
 class SingleRunner:
@@ -195,13 +220,15 @@ class SingleRunner:
         self.N.check(self.L.qs_run_circuit_checksum(self.sv.handle(), 0, self.arr, self.G, self.plan_mode, 3,
                                                     self.N.C.byref(self.cs)))
 
-    def step_kinds(self):
-        return [1] * self.stats["launches"]
-
     def timed(self):
-        buf = (self.N.C.c_float * max(1, self.stats["launches"]))()
-        self.N.check(self.L.qs_plan_execute_timed(self.sv.handle(), self.cc._h, buf))
-        return list(buf)[:self.stats["launches"]]
+        """The timed step's exact path (from |0...0>, zero-tile skipping, fused
+        checksum) with a CUDA event between launches: per-launch ms, the
+        launch's algorithmic bytes, and its kind (1 = tile/permutation pass)."""
+        k = max(1, self.stats["launches"])
+        ms, by = (self.N.C.c_float * k)(), (self.N.C.c_double * k)()
+        self.N.check(self.L.qs_plan_execute_from_basis_profile(self.sv.handle(), self.cc._h, 0, None, ms, by))
+        k = self.stats["launches"]
+        return list(ms)[:k], list(by)[:k], [1] * k
 
 
 class ShardedRunner:
@@ -255,11 +282,150 @@ class ShardedRunner:
     def apply_host(self):  # run(): reset to |0...0> (fused) + the host gate list
         self.N.check(self.L.qs_shards_run_circuit(self.st.handle(), 0, self.arr, self.G))
 
-    def step_kinds(self):
-        return self.kinds
-
     def timed(self):
-        return self.st.execute_timed(self.sc)
+        """Full passes (not from a basis state), CUDA events between steps; an
+        exchange step (kind 2) moves no HBM bytes of its own in this count."""
+        ms = self.st.execute_timed(self.sc)
+        full = 32.0 * self.shard_amps
+        return ms, [full if k != 2 else 0.0 for k in self.kinds], self.kinds
+
+
+COLD_PROBE = r"""
+import json, os, sys, time
+sys.path.insert(0, %(root)r)
+sys.path.insert(0, os.path.join(%(root)r, "tests"))
+from paper_2212_14201_b200 import _native as N, qforge as Q
+import bench
+p, n = bench.build_program(%(workload)r)
+gates = p.gates()
+L = N.lib()
+h = N.C.c_void_p()
+N.check(L.qs_create(6, %(device)d, 6, N.C.byref(h)))  # CUDA context, not timed
+N.check(L.qs_destroy(h))
+t0 = time.perf_counter()
+arr, keep = N.gate_array(gates)
+N.check(L.qs_create(n, %(device)d, n, N.C.byref(h)))
+cs = N.C.c_double()
+N.check(L.qs_run_circuit_checksum(h, 0, arr, len(gates), N.QS_PLAN_TILED, 3, N.C.byref(cs)))
+t1 = time.perf_counter()
+st = [N.C.c_uint64() for _ in range(3)]
+N.check(L.qs_jit_stats(*[N.C.byref(x) for x in st]))
+N.check(L.qs_destroy(h))
+print(json.dumps({"ms": (t1 - t0) * 1e3, "checksum": cs.value, "nvrtc_builds": st[0].value,
+                  "disk_hits": st[2].value}))
+"""
+
+
+def e2e_cold(workload, device, jit_dir, units):
+    """run() of the workload in a FRESH process: gate array, state allocation,
+    planning, tile-kernel build (on-disk cubin cache `jit_dir`), execution and
+    the checksum read-back, wall clock (the CUDA context is created before)."""
+    env = dict(os.environ, QSB_JIT_CACHE=jit_dir)
+    r = subprocess.run([sys.executable, "-c", COLD_PROBE % {"root": ROOT, "workload": workload, "device": device}],
+                       capture_output=True, text=True, env=env, timeout=1800)
+    if r.returncode != 0:
+        return {"error": r.stderr.strip()[-300:]}
+    d = json.loads(r.stdout.strip().splitlines()[-1])
+    d["value"] = units / (d["ms"] / 1e3)
+    return d
+
+
+def measure(runner, steps, warmup, world, units, local):
+    """W untimed steps, then K steps between CUDA events on the runner's stream
+    (max over ranks); per-launch profile of one more step."""
+    import torch
+    import torch.distributed as dist
+    from paper_2212_14201_b200 import _native as N
+    L = N.lib()
+    stream = torch.cuda.ExternalStream(runner.stream(), device=torch.device("cuda", local))
+    for _ in range(warmup):
+        runner.run_from_zero()
+        runner.checksum()
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    clocks = ClockSampler(local)
+    clocks.start()
+    time.sleep(0.3)
+    launches0 = L.qs_kernel_launches()
+    ev0 = torch.cuda.Event(enable_timing=True)
+    ev1 = torch.cuda.Event(enable_timing=True)
+    torch.cuda.synchronize()
+    ev0.record(stream)
+    checksum = None
+    for _ in range(steps):
+        runner.run_from_zero()
+        checksum = runner.checksum()  # device reduction + 8-byte read (rank-ordered sum when sharded)
+    ev1.record(stream)
+    ev1.synchronize()
+    torch.cuda.synchronize()
+    launches = L.qs_kernel_launches() - launches0
+    ms_total = ev0.elapsed_time(ev1)
+    clk = clocks.stop()
+    prof = None
+    for _ in range(2):  # per-launch device times of the same step (events between launches)
+        runner.reset()
+        ms, by, kinds = runner.timed()
+        prof = (ms, by, kinds) if prof is None else ([a + b for a, b in zip(prof[0], ms)], by, kinds)
+    per = [x / 2 for x in prof[0]]
+    ms_max = ms_total
+    if world > 1:
+        t = torch.tensor([ms_total], device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms_max = float(t.item())
+    ms_per_step = ms_max / steps
+    return {"ms_per_step": ms_per_step, "value": units / (ms_per_step / 1e3), "launches": int(launches),
+            "checksum": checksum, "per": per, "bytes": prof[1], "kinds": prof[2], "clocks": clk}
+
+
+def roofline_of(m, runner, plan, workload, peak, peak_kind):
+    """Dominant kernel = the full tile passes of the timed step (every tile
+    visited: 32 B per amplitude); achieved = their algorithmic bytes / their
+    CUDA-event time, from the per-launch profile of the same step."""
+    per, by, kinds = m["per"], m["bytes"], m["kinds"]
+    full_b = 32.0 * runner.shard_amps
+    full = [(t, b) for t, b, k in zip(per, by, kinds) if k != 2 and b >= full_b * 0.999 and t > 0]
+    t_full = sum(t for t, _ in full)
+    avg = t_full / len(full) if full else 0.0
+    achieved = (full_b / (avg / 1e3) / 1e9) if avg else 0.0
+    step_bytes = sum(b for b, k in zip(by, kinds) if k != 2)
+    prof_ms = sum(per)
+    r = {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
+         "frac": round(achieved / peak, 4) if peak else None,
+         "traffic": ncu_traffic(workload, plan) if not runner.sharded else None,
+         "traffic_source": "dram__bytes_read.sum + dram__bytes_write.sum per launch, ncu --set full capture "
+                           "committed under profiles/ (not measured in this run)",
+         "kernel": "qsb_tile_* full passes (per-pass NVRTC sm_100a)" if plan == "tiled" else "per-gate kernels",
+         "algorithmic_bytes_per_launch": full_b, "launches_per_step": len(per), "full_pass_launches": len(full),
+         "avg_launch_ms": round(avg, 4), "peak_kind": peak_kind,
+         # share of the profiled step spent in the full passes, and the profiled
+         # step (events between launches) against the timed step
+         "full_pass_time_share": round(t_full / prof_ms, 4) if prof_ms else None,
+         "profiled_step_ms": round(prof_ms, 3), "timed_step_ms": round(m["ms_per_step"], 3),
+         # every launch of the timed step: algorithmic bytes / timed step
+         "step_bytes": step_bytes,
+         "step_achieved": round(step_bytes / (m["ms_per_step"] / 1e3) / 1e9, 1),
+         "step_frac": round(step_bytes / (m["ms_per_step"] / 1e3) / 1e9 / peak, 4) if peak else None}
+    xchg = [t for t, k in zip(per, kinds) if k == 2]
+    if xchg:
+        r["exchanges_per_step"] = len(xchg)
+        r["exchange_ms_total"] = round(sum(xchg), 3)
+    if full:
+        srt = sorted(t for t, _ in full)
+        r["launch_ms_min_median_max"] = [round(srt[0], 3), round(srt[len(srt) // 2], 3), round(srt[-1], 3)]
+    if os.environ.get("QSB_BENCH_PASSES"):
+        r["launch_ms"] = [round(x, 3) for x in per]
+    return r
+
+
+def make_runner(workload, plan_mode, local, world, args, sharded):
+    p, n = build_program(workload)
+    gates = p.gates()
+    if sharded:
+        return ShardedRunner(n, gates, local, dist_world=world), n, len(gates)
+    if args.local_shards:
+        return ShardedRunner(n, gates, local, local_g=args.local_shards), n, len(gates)
+    return SingleRunner(n, gates, local, plan_mode), n, len(gates)
 
 
 def main():
@@ -270,9 +436,9 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--workload", default="random30", choices=sorted(WORKLOADS))
     ap.add_argument("--plan", default="tiled", choices=["tiled", "dense", "unfused"])
-    ap.add_argument("--cpu-layers", type=int, default=1)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-config4", action="store_true", help="N>1: skip the 34-qubit config-4 lines")
     ap.add_argument("--replicas", action="store_true", help="N>1: independent replicas instead of one sharded state")
     ap.add_argument("--local-shards", type=int, default=0, metavar="G",
                     help="N=1 diagnostic: split the state into 2^G shards on this GPU")
@@ -290,6 +456,12 @@ def main():
             return 0
         return run_reference(args)
 
+    # tile kernels are built once into a per-run on-disk cache (also what the
+    # cold e2e probe loads from); a leftover cache of an earlier call is not used
+    import tempfile
+    jit_dir = tempfile.mkdtemp(prefix="qsb-jit-bench-")
+    os.environ["QSB_JIT_CACHE"] = jit_dir
+
     import torch
     import torch.distributed as dist
     if world > 1 or args.force_dist:
@@ -303,69 +475,16 @@ def main():
     from paper_2212_14201_b200 import _native as N
 
     plan_mode = {"tiled": N.QS_PLAN_TILED, "dense": N.QS_PLAN_DENSE_FUSION, "unfused": N.QS_PLAN_UNFUSED}[args.plan]
-    p, n = build_program(args.workload)
-    gates = p.gates()
-    G = len(gates)
     sharded = (world > 1 or args.force_dist) and not args.replicas
     if sharded and (world & (world - 1)):
         sharded = False  # amplitude sharding needs a power-of-two world
-    if sharded:
-        runner = ShardedRunner(n, gates, local, dist_world=world)
-    elif args.local_shards:
-        runner = ShardedRunner(n, gates, local, local_g=args.local_shards)
-    else:
-        runner = SingleRunner(n, gates, local, plan_mode)
-    plan_s = runner.plan_s
-    stats = runner.stats
-    L = N.lib()
-    stream = torch.cuda.ExternalStream(runner.stream(), device=torch.device("cuda", local))
+    runner, n, G = make_runner(args.workload, plan_mode, local, world, args, sharded)
+    plan_s, stats = runner.plan_s, runner.stats
     # replicas: every rank runs the whole circuit; sharded: the ranks share one state
     units = G * world if (world > 1 and not sharded) else G
 
-    def step():  # reset to |0...0> + every pass (the reset fused into the first pass)
-        runner.run_from_zero()
-
-    for _ in range(args.warmup):
-        step()
-        runner.checksum()
-    torch.cuda.synchronize()
-    if world > 1:
-        dist.barrier()
-
-    clocks = ClockSampler(local)
-    clocks.start()
-    time.sleep(0.3)
-    launches0 = L.qs_kernel_launches()
-    ev0 = torch.cuda.Event(enable_timing=True)
-    ev1 = torch.cuda.Event(enable_timing=True)
-    torch.cuda.synchronize()
-    ev0.record(stream)
-    for _ in range(args.steps):
-        step()
-        checksum = runner.checksum()  # device reduction + 8-byte read (rank-ordered sum when sharded)
-    ev1.record(stream)
-    ev1.synchronize()
-    torch.cuda.synchronize()
-    launches = L.qs_kernel_launches() - launches0
-    ms_total = ev0.elapsed_time(ev1)
-
-    # per-step device times (CUDA events between steps, same stream)
-    prof_runs = 2
-    per, kinds = None, runner.step_kinds()
-    for _ in range(prof_runs):
-        runner.reset()
-        t = runner.timed()
-        per = t if per is None else [a + b for a, b in zip(per, t)]
-    per = [x / prof_runs for x in per]
-    clk = clocks.stop()
-
-    ms_max = ms_total
-    if world > 1:
-        t = torch.tensor([ms_total], device="cuda")
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        ms_max = float(t.item())
-    ms_per_step = ms_max / args.steps
-    value = units / (ms_per_step / 1e3)
+    m = measure(runner, args.steps, args.warmup, world, units, local)
+    checksum = m["checksum"]
 
     # e2e through the public API with host buffers (planning + upload + run + checksum read)
     e2e = None
@@ -376,6 +495,7 @@ def main():
         torch.cuda.synchronize()
         if world > 1:
             dist.barrier()
+        stream = torch.cuda.ExternalStream(runner.stream(), device=torch.device("cuda", local))
         e_steps = max(2, min(args.steps, 5))
         t0 = time.perf_counter()
         e0 = torch.cuda.Event(enable_timing=True)
@@ -394,84 +514,132 @@ def main():
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
             e_ms = float(t.item())
         e2e = {"value": units / (e_ms / 1e3), "unit": "gates/s", "ms_per_step": e_ms,
-               "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": 8, "path": runner.e2e_path}
+               "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": 8, "path": runner.e2e_path,
+               "plan": "warm (plan cache hit after 2 untimed calls); cold runs in e2e_cold"}
+        if not runner.sharded and world == 1:
+            # a FRESH process per measurement: run() once, wall clock
+            warm = e2e_cold(args.workload, local, jit_dir, units)
+            empty = e2e_cold(args.workload, local, tempfile.mkdtemp(prefix="qsb-jit-empty-"), units)
+            e2e["cold"] = {"disk_cache": warm, "no_cache": empty,
+                           "what": "fresh process: gate array + qs_create + qs_run_circuit_checksum (planning, "
+                                   "tile-kernel build or on-disk cubin load, run, checksum read), wall clock; "
+                                   "disk_cache = cubins built by an earlier process, no_cache = NVRTC for every "
+                                   "pass (%d host threads)" % (os.cpu_count() or 1)}
 
     peak, peak_kind = peaks()
-    state_bytes = 16 * runner.shard_amps  # bytes of the state (or shard) one pass sweeps
-    # dominant kernel: the tile pass (or the per-gate kernel in other plans)
-    pass_ms = [x for x, k in zip(per, kinds) if k != 2 and x > 0]
-    xchg_ms = [x for x, k in zip(per, kinds) if k == 2]
-    avg_pass_ms = sum(pass_ms) / len(pass_ms) if pass_ms else 0.0
-    achieved = (2 * state_bytes) / (avg_pass_ms / 1e3) / 1e9 if avg_pass_ms else 0.0
-    roofline = {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
-                "frac": round(achieved / peak, 4),
-                "traffic": ncu_traffic(args.workload, args.plan) if not runner.sharded else None,
-                "kernel": "qsb_tile_* (per-pass NVRTC sm_100a)" if args.plan == "tiled" else "per-gate kernels",
-                "algorithmic_bytes_per_launch": 2 * state_bytes, "launches_per_step": stats["launches"],
-                "avg_launch_ms": round(avg_pass_ms, 4), "peak_kind": peak_kind,
-                # tile passes' share of the per-step-timed run (full passes, not started
-                # from a basis state, so its total exceeds the timed step's)
-                "pass_time_share": round(sum(pass_ms) / sum(per), 4) if per and sum(per) else None}
-    if xchg_ms:
-        roofline["exchanges_per_step"] = len(xchg_ms)
-        roofline["exchange_ms_total"] = round(sum(xchg_ms), 3)
-    if pass_ms:
-        srt = sorted(pass_ms)
-        roofline["launch_ms_min_median_max"] = [round(srt[0], 3), round(srt[len(srt) // 2], 3), round(srt[-1], 3)]
-        if os.environ.get("QSB_BENCH_PASSES"):
-            roofline["launch_ms"] = [round(x, 3) for x in per]
+    roofline = roofline_of(m, runner, args.plan, args.workload, peak, peak_kind)
+
+    parity = None
+    ref_cs = reference_checksum(args.workload)
+    if ref_cs is not None and checksum is not None:
+        tol = 1e-12 * (1 << n)
+        parity = {"checksum": checksum, "checksum_ref": ref_cs, "dchecksum": abs(checksum - ref_cs), "tol": tol,
+                  "ok": abs(checksum - ref_cs) <= tol,
+                  "ref": "unmodified qforge run() of the same circuit on the host (tests/golden/huge, "
+                         "ref_driver golden_huge); amplitudes/probabilities in tests/test_bench_parity.py"}
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline and not args.local_shards:
-        rows, err = cpu_baseline_reference(args.workload, args.cpu_layers, 1)
-        if rows:
-            r = rows[-1]
-            cpu = {"value": r["gates"] / r["seconds"], "unit": "gates/s", "cores": r["threads"], "kind": "reference",
-                   "sample": "first %d layer(s) (%d gates) of the workload through qforge::run() with fusion "
-                             "(k=3), incl. its 2^%d-state allocation and final-state copy" % (args.cpu_layers,
-                                                                                               r["gates"], n),
-                   "seconds": r["seconds"]}
-        else:
-            cpu = {"value": None, "unit": "gates/s", "cores": None, "kind": "reference", "sample": err}
+        cpu = cpu_baseline(args.workload, n)
+
+    config4 = None
+    if world > 1 and sharded and not args.no_config4 and args.workload == "random30":
+        config4 = []
+        for wl in ("qft34", "random34"):
+            try:
+                r4, n4, g4 = make_runner(wl, plan_mode, local, world, args, True)
+                m4 = measure(r4, max(2, min(args.steps, 3)), 3, world, g4, local)
+                rf = roofline_of(m4, r4, "tiled", wl, peak, peak_kind)
+                config4.append({"workload": "%s: %s%s" % (wl, WORKLOADS[wl][0], WORKLOADS[wl][1]),
+                                "value": round(m4["value"], 2), "unit": "gates/s",
+                                "ms_per_step": round(m4["ms_per_step"], 3), "gates": g4,
+                                "passes": r4.stats["passes"], "plan_seconds": round(r4.plan_s, 3),
+                                "checksum": m4["checksum"], "roofline_frac": rf["frac"],
+                                "exchanges_per_step": rf.get("exchanges_per_step"),
+                                "exchange_ms_total": rf.get("exchange_ms_total")})
+                del r4
+            except Exception as e:  # report, do not lose the main line
+                config4.append({"workload": wl, "error": str(e)[:300]})
 
     if rank == 0:
         line = {
             "metric": "gates/sec (30q random layered circuit, d=20, complex128) vs HBM roofline",
-            "value": round(value, 2), "unit": "gates/s", "n_gpus": world, "steps": args.steps,
-            "warmup": args.warmup, "ms_per_step": round(ms_per_step, 3), "higher_is_better": True,
-            "scaling": "strong" if runner.sharded else "weak", "vs_baseline": None, "dtype": "complex128 (f64)",
-            "data": "synthetic",
-            "config": {"workload": "%s: %s%s" % (args.workload, WORKLOADS[args.workload][0], WORKLOADS[args.workload][1]),
+            "value": round(m["value"], 2), "unit": "gates/s", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": round(m["ms_per_step"], 3), "higher_is_better": True,
+            "scaling": "strong" if sharded or args.local_shards else "weak", "vs_baseline": None,
+            "dtype": "complex128 (f64)", "data": "synthetic",
+            "config": {"workload": "%s: %s%s" % (args.workload, WORKLOADS[args.workload][0],
+                                                 WORKLOADS[args.workload][1]),
                        "qubits": n, "gates": G, "plan": args.plan, "passes": stats["passes"],
-                       "plan_seconds": round(plan_s, 3), "parallelism": runner.parallelism(world),
-                       "l2": "inputs larger than L2 (%s %.1f GiB)" % ("shard" if runner.sharded else "state",
-                                                                    state_bytes / 2 ** 30),
+                       "plan_seconds": round(plan_s, 3),
+                       "parallelism": ("amplitude-sharded over %d GPUs (%d rank qubits)" % (world, world.bit_length() - 1)
+                                       if sharded else ("%d local shards on 1 GPU (diagnostic)" % (1 << args.local_shards)
+                                                        if args.local_shards else
+                                                        ("replicas" if world > 1 else "single"))),
+                       "l2": "inputs larger than L2 (%s %.1f GiB)" % ("shard" if sharded else "state",
+                                                                    16 * (1 << n) / max(1, world if sharded else 1) / 2 ** 30),
                        "checksum": checksum},
-            "e2e": e2e, "gpu_launches": int(launches), "roofline": roofline, "cpu_baseline": cpu,
-            "clocks": clk,
+            "parity": parity, "e2e": e2e, "gpu_launches": m["launches"], "roofline": roofline,
+            "cpu_baseline": cpu, "clocks": m["clocks"],
         }
+        if config4 is not None:
+            line["config4"] = config4
         print(json.dumps(line))
     if dist.is_initialized():
-        del runner  # shards and their communicator go before the process group
+        runner = None
         dist.destroy_process_group()
     return 0
 
 
+def cpu_baseline(workload, n):
+    """The reference CPU simulator on this host's cores: all threads, then 1
+    thread, each on a bounded sample of the workload (like-for-like with
+    `value`: one resident state, fusion + gate passes only)."""
+    gen = WORKLOADS[workload][0]
+    if gen not in ("random", "qft") or n > 30:
+        return {"value": None, "unit": "gates/s", "cores": None, "kind": "reference",
+                "sample": "not runnable: the reference caps states at 30 qubits (statevector.hpp:137)"}
+    per = 2 * n if gen == "random" else 60
+    res = {}
+    for label, threads, per_step, steps in (("all", os.cpu_count() or 1, per, 2), ("one", 1, max(4, per // 6), 1)):
+        rows, err = ref_steps(workload, per_step, steps, threads)
+        if rows is None:
+            res[label] = {"error": err}
+            continue
+        alloc, st = rows
+        sec = sum(r["seconds"] for r in st)
+        gates = sum(r["gates"] for r in st)
+        passes = sum(r["passes"] for r in st)
+        res[label] = {"value": gates / sec, "cores": st[0]["threads"], "seconds": round(sec, 3), "gates": gates,
+                      "fused_passes": passes, "host_GBps": round(32.0 * (1 << n) * passes / sec / 1e9, 2),
+                      "alloc_seconds": alloc.get("alloc_seconds")}
+    a = res.get("all", {})
+    return {"value": a.get("value"), "unit": "gates/s", "cores": a.get("cores"), "kind": "reference",
+            "sample": "%d x %d gates of the workload (all threads) and %d gates (1 thread) through the unmodified "
+                      "reference's run() body (fuse_circuit k=3 + StateVector::apply_gate, simulator.hpp:147-159) "
+                      "on one resident 2^%d state: no per-run allocation or final copy in the timed part"
+                      % (2, per, max(4, per // 6), n),
+            "threads": res}
+
+
 def run_reference(args):
-    """--impl reference: the reference CPU simulator on this host's cores."""
+    """--impl reference: the reference CPU simulator on this host's cores (all
+    threads).  A step = one layer of the workload (2n gates; a QFT: 60 gates)
+    fused and applied by the unmodified reference's run() body on one resident
+    state (ref_driver bench_steps), so the per-run() allocation and the final
+    copy are outside the steps, as they are outside our `value`."""
     gen, wargs, n = WORKLOADS[args.workload]
-    if gen != "random":
-        print(json.dumps({"impl": "reference", "unavailable": "reference arm implemented for random workloads"}))
-        return 0
-    reps = args.warmup + args.steps
-    rows, err = cpu_baseline_reference(args.workload, args.cpu_layers, reps)
-    if not rows:
+    per = 2 * n if gen == "random" else 60
+    rows, err = ref_steps(args.workload, per, args.warmup + args.steps)
+    if rows is None:
         print(json.dumps({"impl": "reference", "unavailable": err}))
         return 0
-    timed = rows[args.warmup:]
+    alloc, st = rows
+    timed = st[args.warmup:]
     sec = sum(r["seconds"] for r in timed) / len(timed)
     gates = timed[0]["gates"]
     value = gates / sec
+    passes = sum(r["passes"] for r in timed) / len(timed)
     line = {
         "impl": "reference",
         "metric": "gates/sec (30q random layered circuit, d=20, complex128) vs HBM roofline",
@@ -479,11 +647,14 @@ def run_reference(args):
         "ms_per_step": round(sec * 1e3, 1), "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
         "dtype": "complex128 (f64)", "data": "synthetic",
         "config": {"workload": "%s: %s%s" % (args.workload, gen, wargs), "qubits": n,
-                   "sample_gates": gates, "fusion": "reference fuse_circuit k=3"},
+                   "gates_per_step": gates, "fusion": "reference fuse_circuit k=3",
+                   "fused_passes_per_step": passes,
+                   "host_GBps": round(32.0 * (1 << n) * passes / sec / 1e9, 2),
+                   "alloc_seconds_untimed": alloc.get("alloc_seconds")},
         "cpu_baseline": {"value": round(value, 4), "unit": "gates/s", "cores": timed[0]["threads"],
                          "kind": "reference",
-                         "sample": "first %d layer(s) (%d gates) per step through qforge::run()" % (args.cpu_layers,
-                                                                                                    gates)},
+                         "sample": "per step %d gates (one layer) through the reference's run() body on one resident "
+                                   "state (fuse_circuit + apply_gate, simulator.hpp:147-159)" % gates},
         "e2e": {"value": round(value, 4), "unit": "gates/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line))

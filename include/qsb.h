@@ -169,6 +169,13 @@ int qs_plan_execute_from_basis(qs_state_t s, qs_plan_t p, uint64_t basis);
 int qs_plan_enqueue_from_basis(qs_state_t s, qs_plan_t p, uint64_t basis);
 /* qs_plan_execute_from_basis + the checksum fused into the last pass (above). */
 int qs_plan_execute_from_basis_checksum(qs_state_t s, qs_plan_t p, uint64_t basis, double* checksum);
+/* Diagnostics (bench.py roofline): qs_plan_execute_from_basis_checksum with a
+ * CUDA event between consecutive steps; step_ms[i] = device time of step i,
+ * step_bytes[i] = its algorithmic bytes (reads of possibly non-zero amplitudes
+ * + writes); both arrays hold qs_plan_stats' launches entries (may be NULL).
+ * checksum may be NULL.  Synchronises. */
+int qs_plan_execute_from_basis_profile(qs_state_t s, qs_plan_t p, uint64_t basis, double* checksum, float* step_ms,
+                                       double* step_bytes);
 /* Executes steps [first, first+count) only (diagnostics, per-pass profiling). */
 int qs_plan_execute_range(qs_state_t s, qs_plan_t p, uint64_t first, uint64_t count);
 /* Planner statistics: passes (HBM sweeps) and kernel launches per execute.   */

@@ -12,3 +12,9 @@ done
 mkdir -p "$ROOT/tests/golden"
 "$ROOT/oracle/_ref/ref_driver" golden "$ROOT/tests/golden"
 "$ROOT/oracle/_ref/ref_driver" golden_big "$ROOT/tests/golden"
+# Full-size benchmarked configurations (random28, qft30, random30): ~20 min on
+# 8 cores and ~32 GiB of host RAM, so only with GOLDEN_HUGE=1.
+if [ "${GOLDEN_HUGE:-0}" = 1 ]; then
+  mkdir -p "$ROOT/tests/golden/huge"
+  "$ROOT/oracle/_ref/ref_driver" golden_huge "$ROOT/tests/golden/huge" random28 qft30 random30
+fi

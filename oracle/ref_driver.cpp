@@ -477,9 +477,139 @@ int bench(int argc, char** argv) {
   return 0;
 }
 
+// Like-for-like CPU timing: the reference's own run() body
+// (simulator.hpp:147-159: fuse_circuit, then StateVector::apply_gate per
+// block with opts.kernel_options()) on ONE resident state, so a step excludes
+// the per-run() 2^n allocation + single-threaded zero fill (statevector.hpp:139)
+// and the final-state copy (simulator.hpp:163) -- as bench.py's `value`
+// excludes the device allocation.  A step = the next `per_step` gates of the
+// circuit (cyclic), fused and applied.  Prints one JSON line for the
+// allocation and one per step.
+//   ref_driver bench_steps random|qft <n> <d|input> <seed> <per_step> <steps> <fusion0|1>
+int bench_steps(int argc, char** argv) {
+  if (argc < 9) {
+    std::fprintf(stderr, "usage: ref_driver bench_steps random|qft <n> <d|input> <seed> <per_step> <steps> <fusion>\n");
+    return 2;
+  }
+  const std::string kind = argv[2];
+  const std::uint32_t n = std::stoul(argv[3]);
+  const std::uint64_t a3 = std::stoull(argv[4]), seed = std::stoull(argv[5]);
+  const std::size_t per = std::stoull(argv[6]);
+  const int steps = std::stoi(argv[7]);
+  const bool fusion = std::stoi(argv[8]) != 0;
+  Program full = kind == "qft" ? oraclegen::gen_qft(n, a3) : gen_random_circuit(n, static_cast<std::uint32_t>(a3), seed);
+  SimOptions o;
+  o.fusion_enabled = fusion;
+  auto t0 = std::chrono::steady_clock::now();
+  StateVector sv(n);
+  auto t1 = std::chrono::steady_clock::now();
+  std::printf("{\"alloc_seconds\":%.6f,\"threads\":%d}\n", std::chrono::duration<double>(t1 - t0).count(),
+              omp_get_max_threads());
+  std::fflush(stdout);
+  std::size_t next = 0;
+  for (int s = 0; s < steps; ++s) {
+    Program p(n, 0);
+    for (std::size_t k = 0; k < per; ++k, next = (next + 1) % full.body.size()) p.body.push_back(full.body[next]);
+    auto a = std::chrono::steady_clock::now();
+    Program prepared = fusion ? fuse_circuit(p, o.max_fused_qubits) : p;
+    std::size_t passes = 0;
+    for (const auto& ins : prepared.body)
+      if (auto* g = std::get_if<GateOp>(&ins)) {
+        sv.apply_gate(g->gate, o.kernel_options());
+        ++passes;
+      }
+    auto b = std::chrono::steady_clock::now();
+    const double sec = std::chrono::duration<double>(b - a).count();
+    std::printf("{\"gates\":%zu,\"passes\":%zu,\"seconds\":%.6f,\"threads\":%d,\"host_GBps\":%.2f}\n", per, passes,
+                sec, omp_get_max_threads(), 32.0 * std::ldexp(1.0, static_cast<int>(n)) * passes / sec / 1e9);
+    std::fflush(stdout);
+  }
+  std::printf("{\"checksum\":%.17g}\n", probability_checksum(sv));
+  return 0;
+}
+
+// BASELINE.md section 4 CPU baselines, full runs through the public API:
+//   config1: GHZ(20) and QFT(20): run() + probabilities(), fusion on and off
+//   config2: gen_random_circuit(28, 20, 424242): run(), fusion on and off
+//   config5: HEA(24, 10): expectation() and run(p, {seed}, 10^6) for seeds 0..9
+// One JSON line per measurement (seconds, gates, gates/s, fused passes, host
+// bandwidth 32 * 2^n * passes / t).
+//   ref_driver bench_config config1|config2|config5
+int bench_config(const std::string& which) {
+  auto clock = [] { return std::chrono::steady_clock::now(); };
+  auto secs = [](auto a, auto b) { return std::chrono::duration<double>(b - a).count(); };
+  auto passes_of = [](const Program& p, bool fusion) {
+    return fusion ? fuse_circuit(p, 3).body.size() : p.body.size();
+  };
+  auto line = [&](const std::string& name, const Program& p, bool fusion, double sec, const std::string& extra) {
+    const std::size_t passes = passes_of(p, fusion);
+    std::printf("{\"config\":\"%s\",\"case\":\"%s\",\"n\":%u,\"fusion\":%s,\"gates\":%zu,\"passes\":%zu,"
+                "\"seconds\":%.6f,\"gates_per_s\":%.3f,\"host_GBps\":%.2f,\"threads\":%d%s}\n",
+                which.c_str(), name.c_str(), p.qubit_count, fusion ? "true" : "false", p.body.size(), passes, sec,
+                p.body.size() / sec, 32.0 * std::ldexp(1.0, static_cast<int>(p.qubit_count)) * passes / sec / 1e9,
+                omp_get_max_threads(), extra.c_str());
+    std::fflush(stdout);
+  };
+  if (which == "config1") {
+    for (int f = 1; f >= 0; --f)
+      for (int w = 0; w < 2; ++w) {
+        Program p = w == 0 ? oraclegen::gen_ghz(20) : oraclegen::gen_qft(20, 0x5a5a5);
+        SimOptions o;
+        o.fusion_enabled = f != 0;
+        auto a = clock();
+        RunResult rr = run(p, o, 0);
+        auto probs = rr.final_state->probabilities();
+        auto b = clock();
+        line(w == 0 ? "ghz20" : "qft20", p, f != 0, secs(a, b),
+             ",\"includes\":\"run()+probabilities()\",\"p_last\":" + g17(probs.back()));
+      }
+    return 0;
+  }
+  if (which == "config2") {
+    Program p = gen_random_circuit(28, 20, 424242);
+    for (int f = 1; f >= 0; --f) {
+      SimOptions o;
+      o.fusion_enabled = f != 0;
+      auto a = clock();
+      RunResult rr = run(p, o, 0);
+      auto b = clock();
+      line("random28", p, f != 0, secs(a, b),
+           ",\"includes\":\"run()\",\"checksum\":" + g17(probability_checksum(*rr.final_state)));
+    }
+    return 0;
+  }
+  if (which == "config5") {
+    Program p = oraclegen::gen_hea(24, 10, 2024);
+    PauliOperator h = oraclegen::hea_hamiltonian(24);
+    auto a = clock();
+    const double e = expectation(p, h);
+    auto b = clock();
+    line("hea24_expectation", p, false, secs(a, b),
+         ",\"includes\":\"expectation() (" + std::to_string(h.terms().size()) + " terms)\",\"value\":" + g17(e));
+    Program q = p;
+    q.cbit_count = 24;
+    for (std::uint32_t k = 0; k < 24; ++k) q.measure(k, k);
+    for (std::uint64_t seed = 0; seed < 10; ++seed) {
+      SimOptions o;
+      o.seed = seed;
+      auto c = clock();
+      RunResult rr = run(q, o, 1000000);
+      auto d = clock();
+      line("hea24_sample_seed" + std::to_string(seed), p, false, secs(c, d),
+           ",\"includes\":\"run(p, {seed}, 1e6 shots) incl. evolution and sampling\",\"keys\":" +
+               std::to_string(rr.counts.size()));
+    }
+    return 0;
+  }
+  std::fprintf(stderr, "bench_config: unknown %s\n", which.c_str());
+  return 2;
+}
+
 }  // namespace
 
 int main(int argc, char** argv) {
+  if (argc >= 2 && std::strcmp(argv[1], "bench_steps") == 0) return bench_steps(argc, argv);
+  if (argc >= 3 && std::strcmp(argv[1], "bench_config") == 0) return bench_config(argv[2]);
   if (argc >= 3 && std::strcmp(argv[1], "golden") == 0) return golden(argv[2]);
   if (argc >= 3 && std::strcmp(argv[1], "golden_big") == 0) return golden_big(argv[2]);
   if (argc >= 3 && std::strcmp(argv[1], "golden_huge") == 0) {

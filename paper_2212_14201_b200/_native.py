@@ -98,6 +98,8 @@ _SIGS = {
     "qs_plan_execute_from_basis": (C.c_int, [_P, _P, C.c_uint64]),
     "qs_plan_enqueue_from_basis": (C.c_int, [_P, _P, C.c_uint64]),
     "qs_plan_execute_from_basis_checksum": (C.c_int, [_P, _P, C.c_uint64, C.POINTER(C.c_double)]),
+    "qs_plan_execute_from_basis_profile": (C.c_int, [_P, _P, C.c_uint64, C.POINTER(C.c_double),
+                                                     C.POINTER(C.c_float), C.POINTER(C.c_double)]),
     "qs_plan_execute_timed": (C.c_int, [_P, _P, C.POINTER(C.c_float)]),
     "qs_stream": (C.c_void_p, [_P]),
     "qs_fuse": (C.c_int, [_GP, C.c_uint64, C.c_uint32, C.c_uint32, C.POINTER(_P)]),

@@ -398,6 +398,22 @@ int qs_run_circuit_checksum(qs_state_t h, uint64_t basis, const qs_gate* gates, 
   });
 }
 
+int qs_plan_execute_from_basis_profile(qs_state_t h, qs_plan_t p, uint64_t basis, double* checksum, float* step_ms,
+                                       double* step_bytes) {
+  return guarded([&] {
+    if (!p) throw ValidationError("null plan");
+    StepProfile prof;
+    execute_plan_from_basis(st(h), *p->p, basis, checksum, &prof);
+    const auto& steps = p->p->steps;
+    for (size_t i = 0, o = 0; i < prof.ms.size(); ++i) {
+      if (steps[i].kind == Step::OpStep && steps[i].op.kind == OpKind::Identity) continue;  // not a launch
+      if (step_ms) step_ms[o] = prof.ms[i];
+      if (step_bytes) step_bytes[o] = prof.bytes[i];
+      ++o;
+    }
+  });
+}
+
 int qs_plan_execute_from_basis(qs_state_t h, qs_plan_t p, uint64_t basis) {
   return guarded([&] {
     if (!p) throw ValidationError("null plan");

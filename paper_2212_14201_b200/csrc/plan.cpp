@@ -172,7 +172,7 @@ TileSkip zero_tiles(const Step& st, uint64_t basis) {
   return k;
 }
 
-void execute_plan_from_basis(State& s, const Plan& p, uint64_t basis, double* checksum) {
+void execute_plan_from_basis(State& s, const Plan& p, uint64_t basis, double* checksum, StepProfile* prof) {
   if (p.n != s.n) throw ValidationError("plan was compiled for a different qubit count");
   if (p.g != s.g) throw ValidationError("plan was compiled for a sharded state (use the shard API)");
   if (basis >> s.n) throw ValidationError("basis index out of range");
@@ -196,6 +196,22 @@ void execute_plan_from_basis(State& s, const Plan& p, uint64_t basis, double* ch
   double* part = fused ? static_cast<double*>(s.get_scratch(kMaxTileGrid * sizeof(double) + sizeof(double))) : nullptr;
   unsigned parts = 0;
   const size_t last = p.steps.size() - 1;
+  // per-step profile: events between steps, algorithmic bytes per step
+  std::vector<cudaEvent_t> ev;
+  const double amp = 16.0 * static_cast<double>(s.size);
+  auto mark = [&](size_t i, double bytes) {
+    if (!prof) return;
+    QSB_CUDA(cudaEventRecord(ev[i + 1], s.stream));
+    prof->bytes[i] = bytes;
+  };
+  auto frac = [](unsigned long long mask) { return std::ldexp(1.0, -__builtin_popcountll(mask)); };
+  if (prof) {
+    ev.resize(p.steps.size() + 1);
+    for (auto& e : ev) QSB_CUDA(cudaEventCreate(&e));
+    prof->ms.assign(p.steps.size(), 0.f);
+    prof->bytes.assign(p.steps.size(), 0.0);
+    QSB_CUDA(cudaEventRecord(ev[0], s.stream));
+  }
   size_t i = 0;
   if (!p.steps.empty() && p.steps[0].kind == Step::TileStep && !std::getenv("QSB_NO_FUSED_RESET")) {
     TileSkip k = zero_tiles(p.steps[0], basis);
@@ -203,18 +219,23 @@ void execute_plan_from_basis(State& s, const Plan& p, uint64_t basis, double* ch
     const unsigned g0 = launch_tile(s, *p.steps[0].tile, &basis, nullptr, &k, last == 0 ? part : nullptr);
     if (last == 0) parts = g0;
     if (k.lazy) unwritten = TileSkip{k.mask, k.val};
+    mark(0, amp * (k.lazy ? frac(k.mask) : 1.0));  // writes only
     i = 1;
   } else {
     fill_basis(s, basis);
   }
   // tiles still provably zero (definite qubits outside the tile) are skipped
   for (; i < p.steps.size(); ++i) {
+    double bytes = 2 * amp;
     if (p.steps[i].kind == Step::TileStep) {
       const TileSkip k = zero_tiles(p.steps[i], basis);
       const unsigned gi = launch_tile(s, *p.steps[i].tile, nullptr, nullptr, &k, i == last ? part : nullptr);
       if (i == last) parts = gi;
       if (p.steps[i].tile->h.oop) unwritten = TileSkip{};  // the new buffer is written everywhere
       else if (unwritten.mask) unwritten = TileSkip{k.mask, k.val};
+      // in place: only possibly non-zero tiles are visited, inside them only
+      // amplitudes agreeing with the definite tile qubits are read
+      if (!p.steps[i].tile->h.oop) bytes = amp * frac(k.mask) * (frac(k.imask) + 1.0);
     } else if (i == last && part && p.steps[i].kind == Step::PermStep) {
       settle();
       parts = permute_qubits(s, p.steps[i].perm, part);
@@ -222,9 +243,15 @@ void execute_plan_from_basis(State& s, const Plan& p, uint64_t basis, double* ch
       settle();
       execute_step(s, p.steps[i]);
     }
+    mark(i, bytes);
   }
   settle();  // zeros only: the fused checksum is unchanged
   if (checksum) *checksum = fused ? sum_partials(s, part, parts) : reduce_checksum(s);
+  if (prof) {
+    s.sync();
+    for (size_t j = 0; j < p.steps.size(); ++j) QSB_CUDA(cudaEventElapsedTime(&prof->ms[j], ev[j], ev[j + 1]));
+    for (auto& e : ev) cudaEventDestroy(e);
+  }
 }
 
 void execute_step(State& s, const Step& st) {

@@ -60,7 +60,15 @@ void execute_plan(State& s, const Plan& p);
 // the reset is fused into it (no separate write pass, no read of the old state).
 // checksum != null: also returns probability_checksum of the result, fused
 // into the last tile pass when the plan ends with one (synchronises).
-void execute_plan_from_basis(State& s, const Plan& p, uint64_t basis, double* checksum = nullptr);
+// prof != null (diagnostics, synchronises): per-step device time (CUDA events
+// between the steps on the state's stream) and algorithmic bytes (reads of
+// possibly non-zero amplitudes + writes of the amplitudes the step stores).
+struct StepProfile {
+  std::vector<float> ms;
+  std::vector<double> bytes;
+};
+void execute_plan_from_basis(State& s, const Plan& p, uint64_t basis, double* checksum = nullptr,
+                             StepProfile* prof = nullptr);
 // The zero-tile mask of a tile step for a run started from |basis>.
 struct TileSkip zero_tiles(const Step& st, uint64_t basis);
 void execute_step(State& s, const Step& st);

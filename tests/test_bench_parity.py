@@ -1,0 +1,120 @@
+"""Parity of the BENCHMARKED configurations at their real size against the
+reference itself (VERDICT r1 "What's weak" 1 / "Next round" 1).
+
+`tests/golden/huge/manifest_huge.json` holds the unmodified reference's
+results (oracle/_ref/ref_driver golden_huge: qforge::run() with its default
+k=3 fusion, simulator.hpp:142-194) for
+  random28 = gen_random_circuit(28, 20, 424242)   (BASELINE config 2)
+  random30 = gen_random_circuit(30, 20, 424242)   (bench.py default workload)
+  qft30    = QFT(30) of |0x2AAAAAAA>              (bench.py --workload qft30)
+: probability_checksum (bench.hpp:141-148), norm_squared, 8 windows of 4096
+amplitudes, the first 256 probabilities and a 6-qubit marginal.
+
+Each test runs EXACTLY the path bench.py times -- the default plan
+(13-qubit tile passes at >= 26 qubits), reset to |0...0> fused into the first
+pass, zero-tile skipping / sparse reads / lazy zeros, checksum fused into the
+last pass (qs_plan_execute_from_basis_checksum) -- and the e2e path
+(qs_run_circuit_checksum with the host gate array), unsharded; plus the P=8
+sharded plan on one GPU for random30 (the config-4 data path).
+
+Tolerances (BASELINE.json north_star): |d amplitude| <= 1e-10,
+|d prob| <= 1e-12, checksum sum_i p_i (i+1) within 1e-12 * 2^n.
+"""
+import json
+import os
+
+import numpy as np
+import pytest
+
+from paper_2212_14201_b200 import _native as N
+from paper_2212_14201_b200 import qforge as Q
+
+pytestmark = pytest.mark.gpu
+
+HERE = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden", "huge")
+AMP_TOL, PROB_TOL = 1e-10, 1e-12
+
+
+def manifest():
+    with open(os.path.join(HERE, "manifest_huge.json")) as f:
+        return {c["name"]: c for c in json.load(f)}
+
+
+CASES = manifest()
+
+
+def program(c):
+    if c["gen"] == "random":
+        return Q.gen_random_circuit(*c["args"])
+    return Q.gen_qft(*c["args"])
+
+
+def windows(c):
+    a = np.fromfile(os.path.join(HERE, c["amps"]), dtype=np.complex128)
+    return a.reshape(len(c["starts"]), c["window"])
+
+
+def check_state(c, read, checksum, norm2, marginal):
+    n = c["n"]
+    assert abs(checksum - c["checksum"]) <= PROB_TOL * (1 << n), (checksum, c["checksum"])
+    assert abs(norm2 - c["norm2"]) <= PROB_TOL
+    want = windows(c)
+    for s, w in zip(c["starts"], want):
+        got = read(s, c["window"])
+        assert np.max(np.abs(got - w)) <= AMP_TOL, s
+    head = np.abs(read(0, 256)) ** 2
+    assert np.max(np.abs(head - np.array(c["probs_head"]))) <= PROB_TOL
+    assert np.max(np.abs(np.asarray(marginal) - np.array(c["marginal"]))) <= PROB_TOL
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _gpu_present():
+    import torch
+    assert torch.cuda.is_available(), "the -m gpu suite needs a CUDA device"
+    N.lib()
+
+
+@pytest.mark.parametrize("name", sorted(CASES))
+def test_bench_path_matches_reference(name):
+    """bench.py's timed step: CompiledCircuit (default plan) +
+    qs_plan_execute_from_basis_checksum(|0...0>), checksum fused into the last pass."""
+    c = CASES[name]
+    n = c["n"]
+    gates = program(c).gates()
+    assert len(gates) == c["gates"]
+    cc = Q.CompiledCircuit(n, gates)
+    if n >= 26:
+        assert cc.stats()["passes"] < len(gates) // 10  # the tile-pass plan, not per-gate kernels
+    sv = Q.StateVector(n)
+    cs = cc.execute_checksum(sv, 0)
+    check_state(c, lambda o, k: sv.amplitudes(o, k), cs, sv.norm_squared(),
+                sv.probabilities(c["marginal_qubits"]))
+    # the same state again through the public e2e call bench.py times
+    # (qs_run_circuit_checksum: validation, cached plan, upload, run, checksum)
+    arr, keep = N.gate_array(gates)
+    cs2 = N.C.c_double()
+    sv.set_amplitudes(np.full(4096, np.nan + 0j), 0)  # stale data must not leak into the result
+    N.check(N.lib().qs_run_circuit_checksum(sv.handle(), 0, arr, len(gates), N.QS_PLAN_TILED, 3,
+                                            N.C.byref(cs2)))
+    assert abs(cs2.value - c["checksum"]) <= PROB_TOL * (1 << n)
+    assert np.max(np.abs(sv.amplitudes(0, 4096) - windows(c)[0])) <= AMP_TOL
+    del sv
+
+
+def test_random30_sharded_p8_matches_reference():
+    """The P = 8 sharded plan (rank bits = top 3 qubits, batched all-to-all
+    exchanges, peer transport) executed as 8 shards on one GPU reproduces the
+    reference's random30 results: the config-4 data path against the reference."""
+    from paper_2212_14201_b200.sharded import ShardedState
+    c = CASES["random30"]
+    n = c["n"]
+    gates = program(c).gates()
+    os.environ["QSB_SHARD_EXCHANGE"] = "peer"
+    try:
+        st = ShardedState.local(n, 3)
+    finally:
+        del os.environ["QSB_SHARD_EXCHANGE"]
+    st.run_circuit(gates)
+    check_state(c, lambda o, k: st.amplitudes(o, k), st.checksum(), st.norm_squared(),
+                st.probabilities(c["marginal_qubits"]))
+    st.close()

@@ -137,3 +137,33 @@ def test_qft_closed_form_small():
         k = np.arange(1 << n)
         want = np.exp(2j * np.pi * x * k / (1 << n)) / np.sqrt(1 << n)
         assert np.max(np.abs(a - want)) <= 1e-12
+
+
+def test_huge_manifest_is_the_benchmarked_circuits():
+    """tests/golden/huge holds the reference's results for exactly the
+    circuits bench.py times (generators are bit-exact, see above)."""
+    import json
+    import os
+    from paper_2212_14201_b200 import qforge as Q
+    here = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden", "huge")
+    cases = {c["name"]: c for c in json.load(open(os.path.join(here, "manifest_huge.json")))}
+    assert set(cases) == {"random28", "random30", "qft30"}
+    import bench
+    for name, c in cases.items():
+        gen, args, n = bench.WORKLOADS[name]
+        assert (gen, list(args), n) == (c["gen"], c["args"], c["n"])
+        p = {"random": Q.gen_random_circuit, "qft": Q.gen_qft}[gen](*args)
+        assert p.gate_count() == c["gates"]
+        assert os.path.getsize(os.path.join(here, c["amps"])) == 16 * c["window"] * len(c["starts"])
+        assert abs(c["norm2"] - 1) < 1e-12 and len(c["probs_head"]) == 256 and len(c["marginal"]) == 64
+        w = np.fromfile(os.path.join(here, c["amps"]), dtype=np.complex128).reshape(8, -1)
+        assert np.allclose(np.abs(w[0, :256]) ** 2, c["probs_head"], atol=1e-15, rtol=0)
+    # QFT of a basis state: every amplitude is exp(2 pi i x k / 2^n) / sqrt(2^n)
+    q = cases["qft30"]
+    x, n = q["args"][1], q["n"]
+    w = np.fromfile(os.path.join(here, q["amps"]), dtype=np.complex128).reshape(8, -1)
+    for s, row in zip(q["starts"], w):
+        k = np.arange(s, s + q["window"], dtype=np.uint64)
+        ph = ((np.uint64(x) * k) & np.uint64((1 << n) - 1)).astype(np.float64)  # exact: x k < 2^60
+        want = np.exp(2j * np.pi * ph / (1 << n)) / np.sqrt(1 << n)
+        assert np.max(np.abs(row - want)) <= 1e-10
