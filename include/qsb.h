@@ -201,6 +201,12 @@ int qs_probs(qs_state_t s, const uint32_t* qubits, uint32_t m, double* out);
 int qs_probs_full(qs_state_t s, double* out, uint64_t offset, uint64_t count);
 /* sum_i |a_i|^2 (i+1), the bench digest                                  [bench.hpp:141-148] */
 int qs_checksum(qs_state_t s, double* out);
+/* The same digest rounded exactly as the reference's serial loop (t_i =
+ * fl(|a_i|^2 (i+1)), sum += t_i in index order): bit-identical to it on the
+ * same amplitudes (serial-equivalent scan, DESIGN 3.4).  qs_checksum's tree
+ * sum is the more accurate value; this one is for parity with the reference's
+ * own rounding error (2^n serial adds).                       [bench.hpp:141-148] */
+int qs_checksum_serial(qs_state_t s, double* out);
 
 /* --- measurement ------------------------------------------------------------ */
 /* collapse onto outcome with known probability                 [statevector.hpp:228-247] */

@@ -111,6 +111,7 @@ _SIGS = {
     "qs_probs": (C.c_int, [_P, _UP, C.c_uint32, _DP]),
     "qs_probs_full": (C.c_int, [_P, _DP, C.c_uint64, C.c_uint64]),
     "qs_checksum": (C.c_int, [_P, _DP]),
+    "qs_checksum_serial": (C.c_int, [_P, _DP]),
     "qs_collapse": (C.c_int, [_P, C.c_uint32, C.c_int, C.c_double]),
     "qs_measure_collapse": (C.c_int, [_P, C.c_uint32, C.c_double, C.POINTER(C.c_int)]),
     "qs_scale": (C.c_int, [_P, C.c_double, C.c_double]),

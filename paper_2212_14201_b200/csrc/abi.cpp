@@ -537,6 +537,10 @@ int qs_checksum(qs_state_t h, double* out) {
   return guarded([&] { *out = reduce_checksum(st(h)); });
 }
 
+int qs_checksum_serial(qs_state_t h, double* out) {
+  return guarded([&] { *out = serial_checksum(st(h)); });
+}
+
 int qs_collapse(qs_state_t h, uint32_t q, int outcome, double prob) {
   return guarded([&] {
     State& s = st(h);

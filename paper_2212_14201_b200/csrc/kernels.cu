@@ -1451,6 +1451,36 @@ void pauli_cross(State& s, const double2* a, const double2* partner, uint64_t si
   out2[1] = h.y;
 }
 
+// probability_checksum rounded exactly as the reference's serial loop rounds
+// it (bench.hpp:141-148, as g++ -O3 compiles it: t_i = fl(fl(|a_i|^2) * (i+1)),
+// then sum += t_i in index order): the serial-equivalent scan of the t_i.
+__global__ void __launch_bounds__(kThreads) k_checksum_terms(const double2* __restrict__ a, uint64_t count,
+                                                             uint64_t base, double* __restrict__ t) {
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < count; i += (uint64_t)gridDim.x * blockDim.x)
+    t[i] = __dmul_rn(norm_ref(a[i]), (double)(base + i + 1));
+}
+
+double serial_checksum(State& s) {
+  DeviceGuard dg(s.device);
+  char* extra;
+  SamplerBuffers b = sampler_buffers(s, 0, &extra);
+  const uint64_t N = s.size;
+  k_checksum_terms<<<grid_for(N, s.device), kThreads, 0, s.stream>>>(s.amps, N, s.rank_base, b.p);
+  QSB_LAUNCHED();
+  k_chunk_sum<<<b.nc, kThreads, 0, s.stream>>>(b.p, N, b.C, b.S);
+  QSB_LAUNCHED();
+  k_scan_estimate<<<1, 32, 0, s.stream>>>(b.S, b.nc, b.E, nullptr);
+  QSB_LAUNCHED();
+  k_chunk_ints<<<b.nc, kThreads, 0, s.stream>>>(b.p, N, b.C, b.E, b.info);
+  QSB_LAUNCHED();
+  k_sequential<<<1, 32, 0, s.stream>>>(b.p, N, b.C, b.nc, b.info, b.start, b.fast, b.cum, b.total, nullptr);
+  QSB_LAUNCHED();
+  double* h = static_cast<double*>(s.get_pinned(8));
+  QSB_CUDA(cudaMemcpyAsync(h, b.total, 8, cudaMemcpyDeviceToHost, s.stream));
+  QSB_CUDA(cudaStreamSynchronize(s.stream));
+  return *h;
+}
+
 double exact_cumulative(State& s, double* d_probs, double* d_cum) {
   DeviceGuard dg(s.device);
   char* extra;

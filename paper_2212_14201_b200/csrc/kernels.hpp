@@ -89,5 +89,8 @@ void pauli_axpy(State& s, double2* dst, const double2* src, uint64_t xmask, uint
 
 // Exposed for tests of the exact scan (cum must hold s.size doubles on device).
 double exact_cumulative(State& s, double* d_probs, double* d_cum);
+// probability_checksum with the reference's serial rounding (bench.hpp:141-148):
+// bitwise equal to the serial loop on the same amplitudes.
+double serial_checksum(State& s);
 
 }  // namespace qsb

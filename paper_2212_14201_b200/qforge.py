@@ -283,6 +283,12 @@ class StateVector:
         N.check(N.lib().qs_checksum(self._h, N.C.byref(out)))
         return out.value
 
+    def checksum_serial(self):
+        """probability_checksum with the reference's serial rounding (bench.hpp:141-148)."""
+        out = N.C.c_double()
+        N.check(N.lib().qs_checksum_serial(self._h, N.C.byref(out)))
+        return out.value
+
     def expect_pauli(self, words):
         """words: list of per-qubit letter strings of length n -> complex array."""
         letters = "".join(words).encode()

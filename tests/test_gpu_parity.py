@@ -525,3 +525,23 @@ def test_tile_knobs_keep_parity(monkeypatch, knobs):
         cc.execute(sv2)  # in place from an arbitrary state
         ref2 = ol.run_gates(n, gates, state=ref)
         assert np.max(np.abs(sv2.amplitudes() - ref2)) <= 1e-10
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("which,n", [("random", 16), ("qft", 18), ("random", 22), ("ghz", 20), ("qft", 22)])
+def test_serial_checksum_is_bitwise_the_reference_loop(which, n):
+    """qs_checksum_serial rounds probability_checksum exactly as the
+    reference's serial loop (bench.hpp:141-148): bit-identical to the C
+    oracle's loop (itself bitwise the reference's, tests/test_oracle.py) on
+    the same amplitudes -- including QFT states whose terms tie at every
+    32nd index (the scan's replay path)."""
+    gates = {"random": lambda: Q.gen_random_circuit(n, 5, 424242).gates(),
+             "qft": lambda: Q.gen_qft(n, 0x2AAAA).gates(),
+             "ghz": lambda: Q.gen_ghz(n).gates()}[which]()
+    sv = Q.StateVector(n)
+    sv.apply_circuit(gates)
+    a = sv.amplitudes()
+    want = ol.checksum(a, n)
+    got = sv.checksum_serial()
+    assert got == want, (got, want, got - want)
+    assert abs(sv.checksum() - want) <= 1e-9 * want
