@@ -321,12 +321,14 @@ def e2e_cold(workload, device, jit_dir, units):
     planning, tile-kernel build (on-disk cubin cache `jit_dir`), execution and
     the checksum read-back, wall clock (the CUDA context is created before)."""
     env = dict(os.environ, QSB_JIT_CACHE=jit_dir)
+    files = len([f for f in os.listdir(jit_dir) if f.endswith(".qsbcubin")]) if os.path.isdir(jit_dir) else 0
     r = subprocess.run([sys.executable, "-c", COLD_PROBE % {"root": ROOT, "workload": workload, "device": device}],
                        capture_output=True, text=True, env=env, timeout=1800)
     if r.returncode != 0:
         return {"error": r.stderr.strip()[-300:]}
     d = json.loads(r.stdout.strip().splitlines()[-1])
     d["value"] = units / (d["ms"] / 1e3)
+    d["cache_files_before"] = files
     return d
 
 
@@ -517,9 +519,13 @@ def main():
                "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": 8, "path": runner.e2e_path,
                "plan": "warm (plan cache hit after 2 untimed calls); cold runs in e2e_cold"}
         if not runner.sharded and world == 1:
-            # a FRESH process per measurement: run() once, wall clock
-            warm = e2e_cold(args.workload, local, jit_dir, units)
-            empty = e2e_cold(args.workload, local, tempfile.mkdtemp(prefix="qsb-jit-empty-"), units)
+            # a FRESH process per measurement: run() once, wall clock.  The first
+            # starts from an empty kernel cache (NVRTC for every pass) and fills it,
+            # the second finds the cubins on disk.  (This process's own builds are
+            # not reused: torch loads its own NVRTC, a different cache key.)
+            cold_dir = tempfile.mkdtemp(prefix="qsb-jit-cold-")
+            empty = e2e_cold(args.workload, local, cold_dir, units)
+            warm = e2e_cold(args.workload, local, cold_dir, units)
             e2e["cold"] = {"disk_cache": warm, "no_cache": empty,
                            "what": "fresh process: gate array + qs_create + qs_run_circuit_checksum (planning, "
                                    "tile-kernel build or on-disk cubin load, run, checksum read), wall clock; "
