@@ -117,6 +117,9 @@ constexpr uint32_t kParamLimitBytes = 32 * 1024 - 256;
 struct TileOptions {
   uint32_t m = 12;  // tile qubits
   uint32_t r = 4;   // register qubits per thread
+  // 13-qubit passes: compile every pass with 4 and 5 register bits and keep
+  // the cheaper by pass_cost (QSB_TILE_R fixes r instead)
+  bool choose_r = true;
   uint32_t low = 4; // qubits 0..low-1 always in the tile: 256 B contiguous runs
                     // (measured: 128 B runs 70% of HBM per pass, 256 B 80%)
   bool remap = true;  // plan-level qubit relabelling (low slots hold the qubits needed next)
@@ -140,6 +143,8 @@ void plan_tiles(uint32_t n, std::vector<Op>& ops, std::vector<Step>& steps, cons
 // qubits, profiles/r1/random30_per_pass.txt: 12- and 13-qubit passes with <= 2
 // shared-memory exchanges 5.8 ms, each further exchange +17%).
 double plan_cost(const std::vector<Step>& steps);
+// Estimated time of one tile pass in the same units (see plan_cost).
+double pass_cost(const TileProgram& tp);
 // Plans with and without qubit relabelling (unless fixed by QSB_TILE_REMAP),
 // with 12- and, for large unsharded states, 13-qubit tiles (unless fixed by
 // QSB_TILE_M), and keeps the cheapest plan.

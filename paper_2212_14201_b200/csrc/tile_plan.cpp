@@ -666,7 +666,10 @@ std::vector<uint32_t> C_S_debug(uint64_t S, uint32_t n) {
 TileOptions tile_options_from_env() {
   TileOptions o;
   if (const char* e = std::getenv("QSB_TILE_M")) o.m = static_cast<uint32_t>(std::atoi(e));
-  if (const char* e = std::getenv("QSB_TILE_R")) o.r = static_cast<uint32_t>(std::atoi(e));
+  if (const char* e = std::getenv("QSB_TILE_R")) {
+    o.r = static_cast<uint32_t>(std::atoi(e));
+    o.choose_r = false;
+  }
   if (const char* e = std::getenv("QSB_TILE_LOW")) o.low = static_cast<uint32_t>(std::atoi(e));
   if (const char* e = std::getenv("QSB_TILE_REMAP")) o.remap = std::atoi(e) != 0;
   if (const char* e = std::getenv("QSB_PERM_STEP")) o.perm_step = std::atoi(e) != 0;
@@ -1026,14 +1029,14 @@ void plan_tiles(uint32_t n, std::vector<Op>& ops, std::vector<Step>& steps, cons
     emit_swaps(pairs);
   };
 
-  auto compile_pass = [&](uint64_t S, const std::vector<const POp*>& list, const std::vector<uint64_t>& srcs,
-                          const std::vector<uint32_t>* sigma = nullptr) {
+  auto compile_pass_r = [&](uint64_t S, const std::vector<const POp*>& list, const std::vector<uint64_t>& srcs,
+                            const std::vector<uint32_t>* sigma, uint32_t Rp) {
     Compiler C;
     C.n = n;
     C.m = m;
-    C.R = static_cast<int>(R);
-    C.t = m - R;
-    C.L = L;
+    C.R = static_cast<int>(Rp);
+    C.t = m - Rp;
+    C.L = std::min<uint32_t>(opt.low, m - Rp);
     C.free_load = opt.free_load;
     for (int q = 0; q < 64; ++q) C.tb[q] = -1;
     for (uint32_t q = 0; q < n; ++q)
@@ -1047,6 +1050,17 @@ void plan_tiles(uint32_t n, std::vector<Op>& ops, std::vector<Step>& steps, cons
           if ((*sigma)[q] == k) C.lane[k] = C.tb[q];
     C.compile(list);
     return finalize(C, list.size(), srcs, sigma);
+  };
+  // 13-qubit tiles: 4 register bits (512 threads) or 5 (256 threads x 32
+  // amplitudes: fewer shared-memory exchanges, fewer resident warps) -- per
+  // pass, whichever pass_cost (measured on B200) says is faster.
+  const bool try_r5 = opt.choose_r && m >= 13 && R == 4 && m >= 5 + 4;
+  auto compile_pass = [&](uint64_t S, const std::vector<const POp*>& list, const std::vector<uint64_t>& srcs,
+                          const std::vector<uint32_t>* sigma = nullptr) {
+    auto a = compile_pass_r(S, list, srcs, sigma, R);
+    if (!try_r5) return a;
+    auto b = compile_pass_r(S, list, srcs, sigma, 5);
+    return pass_cost(*b) < pass_cost(*a) - 1e-9 && b->h.bytes <= kTileBlobBytes ? b : a;
   };
   // inputs of the most recent tile pass (to recompile it storing out of place)
   uint64_t last_S = 0;
@@ -1300,20 +1314,28 @@ void plan_tiles(uint32_t n, std::vector<Op>& ops, std::vector<Step>& steps, cons
   }
 }
 
+// Per-pass times measured on B200 (30 qubits, random30 plan, both register
+// widths on the same passes; profiles/r2/random30_r4_vs_r5.txt), in units of
+// a light 13-qubit pass (5.65 ms): with 4 register bits <= 2 buffered
+// exchanges 1.0, 3: 1.28, 4: 1.5; with 5 register bits <= 1: 1.05, 2: 1.13,
+// 3: 1.26, 4: 1.37.  12-qubit passes (two CTAs per SM): 1.0 up to two
+// exchanges, +17% per further one.
+double pass_cost(const TileProgram& tp) {
+  const uint32_t tr = buffered_transposes(tp, true);
+  if (tp.h.m >= 13) {
+    if (tp.h.r >= 5) {
+      static const double c5[] = {1.05, 1.05, 1.13, 1.26};
+      return tr < 4 ? c5[tr] : 1.26 + 0.11 * (tr - 3);
+    }
+    static const double c4[] = {1.0, 1.0, 1.0, 1.28};
+    return tr < 4 ? c4[tr] : 1.28 + 0.22 * (tr - 3);
+  }
+  return 1.0 + 0.17 * (tr > 2 ? tr - 2 : 0);
+}
+
 double plan_cost(const std::vector<Step>& steps) {
   double c = 0;
-  for (const Step& st : steps) {
-    if (st.kind != Step::TileStep) {
-      c += 1.0;
-      continue;
-    }
-    // measured on B200 (30 qubits): a pass with <= 2 shared-memory exchanges
-    // costs one HBM sweep (12- and 13-qubit tiles alike: 5.8 ms), each further
-    // exchange +17% (3: 6.8 ms, 4: 7.75 ms)
-    const TileProgram& tp = *st.tile;
-    const uint32_t tr = buffered_transposes(tp, true);
-    c += 1.0 + 0.17 * (tr > 2 ? tr - 2 : 0);
-  }
+  for (const Step& st : steps) c += st.kind == Step::TileStep ? pass_cost(*st.tile) : 1.0;
   return c;
 }
 

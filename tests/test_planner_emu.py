@@ -92,3 +92,18 @@ def test_emulated_sharded_plans(which, g):
     for remap in (0, 1):
         got, steps = emu_lib.run(n, gates, N.QS_PLAN_TILED, tile_m=9, low=3, global_qubits=g, remap=remap)
         assert np.max(np.abs(got - want)) <= 1e-10, (remap, steps)
+
+
+@pytest.mark.parametrize("which", ["random", "qft", "mixed", "hea"])
+@pytest.mark.parametrize("n", [16, 18])
+def test_emulated_13_qubit_plans_with_register_width_choice(which, n):
+    """13-qubit tiles: every pass is compiled with 4 and with 5 register bits
+    and the cheaper kept (pass_cost); plans mixing both widths replay to the
+    oracle's state."""
+    gates = {"random": lambda: Q.gen_random_circuit(n, 8, 424242).gates(),
+             "qft": lambda: Q.gen_qft(n, 0x2345).gates(),
+             "mixed": lambda: mixed_gates(n, 300, 99 + n),
+             "hea": lambda: Q.gen_hea(n, 6, 9).gates()}[which]()
+    want = ol.run_gates(n, gates)
+    got, passes = emu_lib.run(n, gates, N.QS_PLAN_TILED, tile_m=13, low=4)
+    assert np.max(np.abs(got - want)) <= 1e-10
