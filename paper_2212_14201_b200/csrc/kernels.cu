@@ -137,16 +137,74 @@ struct TargetMasks {
   unsigned long long m[QS_MAX_TARGETS];  // m[b] = 1 << targets[K-1-b]
 };
 
+// The block's matrix travels as a __grid_constant__ kernel parameter
+// (constant bank: uniform operands of the FMAs; no upload, no host sync).
+template <int K>
+struct DenseM {
+  double2 m[1 << (2 * K)];
+};
+
+// Dense 2^K x 2^K block, K <= 4: one thread per amplitude group.  Consecutive
+// lanes take consecutive groups, so every load / store instruction of a warp
+// covers contiguous runs (2^lowest-target amplitudes); the 2^K inputs stay in
+// registers and each output row is an FMA chain with constant-bank
+// coefficients (same summation order as the reference's row dot product,
+// statevector.hpp:69-106).
+template <int K>
+__global__ void __launch_bounds__(kThreads) k_dense_g(double2* __restrict__ a, uint64_t groups, Slots sl,
+                                                      TargetMasks tm, const __grid_constant__ DenseM<K> M) {
+  constexpr int G = 1 << K;
+  for (uint64_t g = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; g < groups;
+       g += (uint64_t)gridDim.x * blockDim.x) {
+    const uint64_t base = deposit(g, sl);
+    double2 x[G];
+#pragma unroll
+    for (int c = 0; c < G; ++c) {
+      uint64_t off = 0;
+#pragma unroll
+      for (int b = 0; b < K; ++b)
+        if ((c >> b) & 1) off |= tm.m[b];
+      x[c] = __ldcs(a + (base | off));
+    }
+#pragma unroll
+    for (int r = 0; r < G; ++r) {
+      double re = 0, im = 0;
+#pragma unroll
+      for (int c = 0; c < G; ++c) {
+        const double2 m = M.m[r * G + c];
+        re = fma(m.x, x[c].x, re);
+        re = fma(-m.y, x[c].y, re);
+        im = fma(m.x, x[c].y, im);
+        im = fma(m.y, x[c].x, im);
+      }
+      uint64_t off = 0;
+#pragma unroll
+      for (int b = 0; b < K; ++b)
+        if ((r >> b) & 1) off |= tm.m[b];
+      __stcs(a + (base | off), make_double2(re, im));
+    }
+  }
+}
+
+// Lane-cooperative form (K = 5, which is FP64-bound at 8 * 32 flop per
+// amplitude, and blocks on the lowest qubits, whose 2^K amplitudes are
+// contiguous): a group of 2^K consecutive lanes handles one amplitude group;
+// lane r owns output row r; inputs are exchanged through shared memory
+// (broadcast reads).  The matrix is staged transposed in shared memory first
+// (a per-lane row read straight from the parameter bank would serialise).
 template <int K>
 __global__ void __launch_bounds__(kThreads) k_dense(double2* __restrict__ a, uint64_t groups, Slots sl,
-                                                    TargetMasks tm, const double2* __restrict__ M) {
+                                                    TargetMasks tm, const __grid_constant__ DenseM<K> M) {
   constexpr int G = 1 << K;
   constexpr int GPB = kThreads / G;  // groups per block iteration
   __shared__ double2 v[kThreads];
+  __shared__ double2 mt[G * G];  // mt[c * G + r] = M[r][c]
+  for (int i = threadIdx.x; i < G * G; i += blockDim.x) mt[(i % G) * G + i / G] = M.m[i];
+  __syncthreads();
   const int tid = threadIdx.x, r = tid & (G - 1), gl = tid >> K;
   double2 row[G];
 #pragma unroll
-  for (int c = 0; c < G; ++c) row[c] = M[r * G + c];
+  for (int c = 0; c < G; ++c) row[c] = mt[c * G + r];
   uint64_t offr = 0;
 #pragma unroll
   for (int b = 0; b < K; ++b)
@@ -155,7 +213,7 @@ __global__ void __launch_bounds__(kThreads) k_dense(double2* __restrict__ a, uin
     const uint64_t g = gb + gl;
     const bool valid = g < groups;
     const uint64_t idx = valid ? (deposit(g, sl) | offr) : 0;
-    v[tid] = valid ? a[idx] : make_double2(0, 0);
+    v[tid] = valid ? __ldcs(a + idx) : make_double2(0, 0);
     __syncwarp();
     double re = 0, im = 0;
 #pragma unroll
@@ -167,7 +225,7 @@ __global__ void __launch_bounds__(kThreads) k_dense(double2* __restrict__ a, uin
       im = fma(row[c].y, x.x, im);
     }
     __syncwarp();
-    if (valid) a[idx] = make_double2(re, im);
+    if (valid) __stcs(a + idx, make_double2(re, im));
   }
 }
 
@@ -267,6 +325,50 @@ __global__ void __launch_bounds__(kThreads) k_marginal(const double2* __restrict
   for (uint64_t g = lo + threadIdx.x; g < hi; g += blockDim.x) s += norm_ref(a[deposit(g, sl) | fixed]);
   const double t = block_sum(s, sh);
   if (threadIdx.x == 0) partial[(uint64_t)bin * gridDim.x + blockIdx.x] = t;
+}
+
+// Marginal with coalesced reads (m <= 12, >= 5 local qubits): lane l of every
+// warp reads amplitude (.. | l) of a 32-amplitude aligned run, so the marginal
+// qubits below 5 are lane bits (each lane's bin part is fixed) and those
+// above are fixed per block (blockIdx.y enumerates them).  A lane sums its
+// amplitudes; lanes that differ only in non-marginal bits are combined by a
+// fixed xor butterfly, warps in index order: deterministic, no atomics, and
+// every byte of the state is read once (the strided per-bin form re-read the
+// 32 B sectors of bins that fix low qubits).
+struct MarginalMap {
+  uint32_t kh;            // marginal qubits >= 5
+  uint32_t qh[12];        // ... ascending
+  uint32_t rh[12];        // their result bits
+  int rl[5];              // result bit of lane bit b, -1 if b is not a marginal qubit
+  uint32_t lane_free;     // lane bits that are not marginal qubits
+};
+
+__global__ void __launch_bounds__(kThreads) k_marginal_lanes(const double2* __restrict__ a, uint64_t per_hi, Slots slh,
+                                                             MarginalMap mm, double* __restrict__ partial) {
+  __shared__ double sh[kThreads / 32][32];
+  const uint32_t bh = blockIdx.y, lane = threadIdx.x & 31u, w = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  uint64_t fixed = 0;
+  uint32_t bin = 0;
+  for (uint32_t j = 0; j < mm.kh; ++j)
+    if ((bh >> j) & 1u) {
+      fixed |= 1ull << mm.qh[j];
+      bin |= 1u << mm.rh[j];
+    }
+  for (int b = 0; b < 5; ++b)
+    if (mm.rl[b] >= 0 && ((lane >> b) & 1u)) bin |= 1u << mm.rl[b];
+  const uint64_t chunk = (per_hi + gridDim.x - 1) / gridDim.x;
+  const uint64_t lo = blockIdx.x * chunk, hi = min(per_hi, lo + chunk);
+  double s = 0;
+  for (uint64_t g = lo + w; g < hi; g += nw) s += norm_ref(__ldcs(a + ((deposit(g, slh) << 5) | fixed | lane)));
+  for (int b = 0; b < 5; ++b)
+    if ((mm.lane_free >> b) & 1u) s += __shfl_xor_sync(0xffffffffu, s, 1 << b);
+  sh[w][lane] = s;
+  __syncthreads();
+  if (w == 0 && (lane & mm.lane_free) == 0) {
+    double t = 0;
+    for (uint32_t i = 0; i < nw; ++i) t += sh[i][lane];
+    partial[(uint64_t)bin * gridDim.x + blockIdx.x] = t;
+  }
 }
 
 __global__ void k_marginal_finalize(const double* __restrict__ partial, uint32_t per, uint32_t bins,
@@ -475,15 +577,21 @@ __global__ void __launch_bounds__(kThreads) k_chunk_sum(const double* __restrict
   if (threadIdx.x == 0) S[blockIdx.x] = t;
 }
 
-// exclusive scan of chunk sums (estimates only), single block
+// exclusive scan of chunk sums (estimates only: they pick each chunk's binade
+// guess, any summation order will do), one warp
 __global__ void k_scan_estimate(const double* __restrict__ S, uint32_t nc, double* __restrict__ E,
                                 const double* __restrict__ carry) {
-  if (threadIdx.x == 0) {
-    double acc = carry ? *carry : 0.0;
-    for (uint32_t c = 0; c < nc; ++c) {
-      E[c] = acc;
-      acc += S[c];
+  const int lane = threadIdx.x & 31;
+  double acc = carry ? *carry : 0.0;
+  for (uint32_t c0 = 0; c0 < nc; c0 += 32) {
+    const double x = c0 + lane < nc ? S[c0 + lane] : 0.0;
+    double v = x;
+    for (int o = 1; o < 32; o <<= 1) {
+      const double t = __shfl_up_sync(0xffffffffu, v, o);
+      if (lane >= o) v += t;
     }
+    if (c0 + lane < nc) E[c0 + lane] = acc + (v - x);
+    acc += __shfl_sync(0xffffffffu, v, 31);
   }
 }
 
@@ -551,7 +659,9 @@ __device__ __forceinline__ long long warp_incl_scan_ll(long long v) {
   return v;
 }
 
-// Phase C: one warp walks the chunks in order.
+// Phase C: one warp walks the chunks in order.  Chunk records are fetched 32
+// at a time (lane j loads chunk c0 + j, then they are broadcast in order), so
+// the walk over clean chunks is not one dependent memory round trip per chunk.
 __global__ void k_sequential(const double* __restrict__ p, uint64_t n, uint64_t C, uint32_t nc,
                              const ChunkInfo* __restrict__ info, double* __restrict__ start,
                              unsigned char* __restrict__ fast, double* __restrict__ cum, double* __restrict__ total,
@@ -559,52 +669,65 @@ __global__ void k_sequential(const double* __restrict__ p, uint64_t n, uint64_t 
   const int lane = threadIdx.x & 31;
   double A = carry ? *carry : 0.0;  // sharded states: the previous shard's final running sum
   const double kMinNormalScaled = 2.2250738585072014e-308 * 4503599627370496.0;
-  for (uint32_t c = 0; c < nc; ++c) {
-    const ChunkInfo ci = info[c];
-    const uint64_t lo = (uint64_t)c * C, hi = min(n, lo + C);
-    if (ci.clean && A >= kMinNormalScaled && ilogb(A) == ci.e) {
-      const double u = ldexp(1.0, ci.e - 52);
-      const long long a = (long long)(A / u);
-      if (a + ci.K < 9007199254740991LL) {  // stays below 2^53: no binade exit
-        if (lane == 0) {
-          start[c] = A;
-          fast[c] = 1;
+  for (uint32_t c0 = 0; c0 < nc; c0 += 32) {
+    ChunkInfo mine{0, 0, 0};
+    if (c0 + lane < nc) mine = info[c0 + lane];
+    double my_start = 0.0;
+    unsigned char my_fast = 0;
+    const uint32_t cn = min(32u, nc - c0);
+    for (uint32_t t = 0; t < cn; ++t) {
+      const uint32_t c = c0 + t;
+      const long long ciK = __shfl_sync(0xffffffffu, mine.K, t);
+      const int cie = __shfl_sync(0xffffffffu, mine.e, t);
+      const int ciclean = __shfl_sync(0xffffffffu, mine.clean, t);
+      const uint64_t lo = (uint64_t)c * C, hi = min(n, lo + C);
+      if (ciclean && A >= kMinNormalScaled && ilogb(A) == cie) {
+        const double u = ldexp(1.0, cie - 52);
+        const long long a = (long long)(A / u);
+        if (a + ciK < 9007199254740991LL) {  // stays below 2^53: no binade exit
+          if (lane == (int)t) {
+            my_start = A;
+            my_fast = 1;
+          }
+          A = (double)(a + ciK) * u;
+          continue;
         }
-        A = (double)(a + ci.K) * u;
-        continue;
+      }
+      for (uint64_t j0 = lo; j0 < hi; j0 += 32) {
+        const uint64_t j = j0 + lane;
+        const double pj = j < hi ? p[j] : 0.0;
+        bool done = false;
+        if (A >= kMinNormalScaled) {
+          const double u = ldexp(1.0, ilogb(A) - 52);
+          long long k = 0;
+          const bool ok = int_step(pj, u, k);
+          if (__all_sync(0xffffffffu, ok)) {
+            const long long incl = warp_incl_scan_ll(k);
+            const long long Ksum = __shfl_sync(0xffffffffu, incl, 31);
+            const long long a = (long long)(A / u);
+            if (a + Ksum < 9007199254740991LL) {
+              if (j < hi) cum[j] = (double)(a + incl) * u;
+              A = (double)(a + Ksum) * u;
+              done = true;
+            }
+          }
+        }
+        if (!done) {
+          double acc = A;
+          for (int t2 = 0; t2 < 32; ++t2) {
+            const double pt = __shfl_sync(0xffffffffu, pj, t2);
+            if (j0 + t2 < hi) {
+              acc = __dadd_rn(acc, pt);
+              if (lane == t2) cum[j] = acc;
+            }
+          }
+          A = acc;
+        }
       }
     }
-    if (lane == 0) fast[c] = 0;
-    for (uint64_t j0 = lo; j0 < hi; j0 += 32) {
-      const uint64_t j = j0 + lane;
-      const double pj = j < hi ? p[j] : 0.0;
-      bool done = false;
-      if (A >= kMinNormalScaled) {
-        const double u = ldexp(1.0, ilogb(A) - 52);
-        long long k = 0;
-        const bool ok = int_step(pj, u, k);
-        if (__all_sync(0xffffffffu, ok)) {
-          const long long incl = warp_incl_scan_ll(k);
-          const long long Ksum = __shfl_sync(0xffffffffu, incl, 31);
-          const long long a = (long long)(A / u);
-          if (a + Ksum < 9007199254740991LL) {
-            if (j < hi) cum[j] = (double)(a + incl) * u;
-            A = (double)(a + Ksum) * u;
-            done = true;
-          }
-        }
-      }
-      if (!done) {
-        double acc = A;
-        for (int t = 0; t < 32; ++t) {
-          const double pt = __shfl_sync(0xffffffffu, pj, t);
-          if (j0 + t < hi) {
-            acc = __dadd_rn(acc, pt);
-            if (lane == t) cum[j] = acc;
-          }
-        }
-        A = acc;
-      }
+    if (c0 + lane < nc) {
+      start[c0 + lane] = my_start;
+      fast[c0 + lane] = my_fast;
     }
   }
   if (lane == 0) *total = A;
@@ -1121,24 +1244,44 @@ void launch_op(State& s, const Op& op_in) {
       TargetMasks tm{};
       for (int b = 0; b < K; ++b) tm.m[b] = 1ull << op.targets[K - 1 - b];
       const size_t dim = size_t(1) << K;
-      double2* dM = static_cast<double2*>(s.get_scratch(dim * dim * sizeof(double2)));
-      std::vector<double2> hm(dim * dim);
-      for (size_t i = 0; i < dim * dim; ++i) hm[i] = d2(op.m[i]);
-      QSB_CUDA(cudaMemcpyAsync(dM, hm.data(), dim * dim * sizeof(double2), cudaMemcpyHostToDevice, s.stream));
-      const uint64_t work = groups << K;
+      auto fill = [&](auto& M) {
+        for (size_t i = 0; i < dim * dim; ++i) M.m[i] = d2(op.m[i]);
+      };
+      // thread per group when the lowest target leaves >= 8-amplitude runs
+      // for consecutive lanes; lane-cooperative otherwise (and for K = 5)
+      const bool per_group = *std::min_element(op.targets.begin(), op.targets.end()) >= 3;
       switch (K) {
-        case 2: k_dense<2><<<grid_for(work, s.device), kThreads, 0, s.stream>>>(s.amps, groups, sl, tm, dM); break;
-        case 3: k_dense<3><<<grid_for(work, s.device), kThreads, 0, s.stream>>>(s.amps, groups, sl, tm, dM); break;
-        case 4: k_dense<4><<<grid_for(work, s.device), kThreads, 0, s.stream>>>(s.amps, groups, sl, tm, dM); break;
-        case 5: k_dense<5><<<grid_for(work, s.device, 4), kThreads, 0, s.stream>>>(s.amps, groups, sl, tm, dM); break;
+        case 2: { DenseM<2> M; fill(M);
+          if (per_group) k_dense_g<2><<<grid_for(groups, s.device), kThreads, 0, s.stream>>>(s.amps, groups, sl, tm, M);
+          else k_dense<2><<<grid_for(groups << K, s.device), kThreads, 0, s.stream>>>(s.amps, groups, sl, tm, M);
+          break; }
+        case 3: { DenseM<3> M; fill(M);
+          if (per_group) k_dense_g<3><<<grid_for(groups, s.device), kThreads, 0, s.stream>>>(s.amps, groups, sl, tm, M);
+          else k_dense<3><<<grid_for(groups << K, s.device), kThreads, 0, s.stream>>>(s.amps, groups, sl, tm, M);
+          break; }
+        case 4: { static thread_local DenseM<4> M; fill(M);
+          if (per_group) k_dense_g<4><<<grid_for(groups, s.device), kThreads, 0, s.stream>>>(s.amps, groups, sl, tm, M);
+          else k_dense<4><<<grid_for(groups << K, s.device), kThreads, 0, s.stream>>>(s.amps, groups, sl, tm, M);
+          break; }
+        case 5: {
+          static thread_local DenseM<5> M;  // 16 KiB: off the stack; the launch copies it
+          fill(M);
+          k_dense<5><<<grid_for(groups << K, s.device, 4), kThreads, 0, s.stream>>>(s.amps, groups, sl, tm, M);
+          break;
+        }
         default: {
+          double2* dM = static_cast<double2*>(s.get_scratch(dim * dim * sizeof(double2)));
+          std::vector<double2> hm(dim * dim);
+          for (size_t i = 0; i < dim * dim; ++i) hm[i] = d2(op.m[i]);
+          QSB_CUDA(cudaMemcpyAsync(dM, hm.data(), dim * dim * sizeof(double2), cudaMemcpyHostToDevice, s.stream));
           const uint32_t blocks = static_cast<uint32_t>(std::min<uint64_t>(groups, num_sms(s.device) * 8ull));
           k_dense_wide<<<blocks, kThreads, dim * sizeof(double2), s.stream>>>(s.amps, groups, sl, tm, K, dM);
+          QSB_LAUNCHED();
+          QSB_CUDA(cudaStreamSynchronize(s.stream));  // the host staging vector must outlive the copy
+          return;
         }
       }
       QSB_LAUNCHED();
-      // the host staging vector must outlive the async copy
-      QSB_CUDA(cudaStreamSynchronize(s.stream));
       return;
     }
   }
@@ -1303,7 +1446,40 @@ void marginal_probs(State& s, const uint32_t* qubits, uint32_t m, double* host_o
   const uint64_t per_bin = 1ull << (s.local_qubits() - m);
   const uint64_t bins = 1ull << m;
   const size_t out_bytes = bins * sizeof(double);
-  if (m <= 12) {
+  uint32_t kh = 0;
+  for (uint32_t b = 0; b < m; ++b) kh += qubits[b] >= 5;
+  if (m <= 12 && s.local_qubits() >= 5 + kh) {
+    MarginalMap mm{};
+    std::vector<std::pair<uint32_t, uint32_t>> hq;  // (qubit, result bit)
+    for (int b = 0; b < 5; ++b) mm.rl[b] = -1;
+    for (uint32_t b = 0; b < m; ++b) {
+      if (qubits[b] >= 5) hq.push_back({qubits[b], b});
+      else mm.rl[qubits[b]] = static_cast<int>(b);
+    }
+    std::sort(hq.begin(), hq.end());
+    mm.kh = kh;
+    std::vector<uint32_t> rel;
+    for (uint32_t j = 0; j < kh; ++j) {
+      mm.qh[j] = hq[j].first;
+      mm.rh[j] = hq[j].second;
+      rel.push_back(hq[j].first - 5);
+    }
+    for (int b = 0; b < 5; ++b)
+      if (mm.rl[b] < 0) mm.lane_free |= 1u << b;
+    const Slots slh = make_slots(rel, {});
+    const uint64_t per_hi = 1ull << (s.local_qubits() - 5 - kh);
+    const uint64_t ybins = 1ull << kh;
+    const uint32_t per = static_cast<uint32_t>(std::max<uint64_t>(1, std::min<uint64_t>(kRedBlocks / ybins + 1, per_hi)));
+    char* scr = static_cast<char*>(s.get_scratch(bins * per * sizeof(double) + out_bytes));
+    double* part = reinterpret_cast<double*>(scr);
+    double* dout = part + bins * per;
+    k_marginal_lanes<<<dim3(per, static_cast<uint32_t>(ybins)), kThreads, 0, s.stream>>>(s.amps, per_hi, slh, mm, part);
+    QSB_LAUNCHED();
+    k_marginal_finalize<<<static_cast<uint32_t>((bins + 255) / 256), 256, 0, s.stream>>>(part, per,
+                                                                                         static_cast<uint32_t>(bins), dout);
+    QSB_LAUNCHED();
+    QSB_CUDA(cudaMemcpyAsync(host_out, dout, out_bytes, cudaMemcpyDeviceToHost, s.stream));
+  } else if (m <= 12) {
     const uint32_t per = static_cast<uint32_t>(std::max<uint64_t>(1, std::min<uint64_t>(kRedBlocks / bins + 1, per_bin)));
     char* scr = static_cast<char*>(s.get_scratch(256 + m * 4 + bins * per * sizeof(double) + out_bytes));
     uint32_t* dq = reinterpret_cast<uint32_t*>(scr);

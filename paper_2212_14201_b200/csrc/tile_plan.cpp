@@ -666,7 +666,7 @@ std::vector<uint32_t> C_S_debug(uint64_t S, uint32_t n) {
 TileOptions tile_options_from_env() {
   TileOptions o;
   if (const char* e = std::getenv("QSB_TILE_M")) o.m = static_cast<uint32_t>(std::atoi(e));
-  if (const char* e = std::getenv("QSB_TILE_R")) {
+  if (const char* e = std::getenv("QSB_TILE_R"); e && std::atoi(e) > 0) {
     o.r = static_cast<uint32_t>(std::atoi(e));
     o.choose_r = false;
   }
