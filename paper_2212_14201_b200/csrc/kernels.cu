@@ -113,9 +113,9 @@ __global__ void __launch_bounds__(kThreads) k_flip(double2* __restrict__ a, uint
   for (uint64_t g = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; g < groups;
        g += (uint64_t)gridDim.x * blockDim.x) {
     const uint64_t i0 = deposit(g, sl);
-    const double2 x = a[i0], y = a[i0 | bit];
-    a[i0] = y;
-    a[i0 | bit] = x;
+    const double2 x = __ldcs(a + i0), y = __ldcs(a + (i0 | bit));
+    __stcs(a + i0, y);
+    __stcs(a + (i0 | bit), x);
   }
 }
 
@@ -124,9 +124,9 @@ __global__ void __launch_bounds__(kThreads) k_swap(double2* __restrict__ a, uint
   for (uint64_t g = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; g < groups;
        g += (uint64_t)gridDim.x * blockDim.x) {
     const uint64_t base = deposit(g, sl);
-    const double2 x = a[base | ba], y = a[base | bb];
-    a[base | ba] = y;
-    a[base | bb] = x;
+    const double2 x = __ldcs(a + (base | ba)), y = __ldcs(a + (base | bb));
+    __stcs(a + (base | ba), y);
+    __stcs(a + (base | bb), x);
   }
 }
 
@@ -359,7 +359,18 @@ __global__ void __launch_bounds__(kThreads) k_marginal_lanes(const double2* __re
   const uint64_t chunk = (per_hi + gridDim.x - 1) / gridDim.x;
   const uint64_t lo = blockIdx.x * chunk, hi = min(per_hi, lo + chunk);
   double s = 0;
-  for (uint64_t g = lo + w; g < hi; g += nw) s += norm_ref(__ldcs(a + ((deposit(g, slh) << 5) | fixed | lane)));
+  uint64_t g = lo + w;
+  for (; g + 3 * nw < hi; g += 4 * nw) {  // four runs in flight per lane, summed in order
+    const double2 v0 = __ldcs(a + ((deposit(g, slh) << 5) | fixed | lane));
+    const double2 v1 = __ldcs(a + ((deposit(g + nw, slh) << 5) | fixed | lane));
+    const double2 v2 = __ldcs(a + ((deposit(g + 2 * nw, slh) << 5) | fixed | lane));
+    const double2 v3 = __ldcs(a + ((deposit(g + 3 * nw, slh) << 5) | fixed | lane));
+    s += norm_ref(v0);
+    s += norm_ref(v1);
+    s += norm_ref(v2);
+    s += norm_ref(v3);
+  }
+  for (; g < hi; g += nw) s += norm_ref(__ldcs(a + ((deposit(g, slh) << 5) | fixed | lane)));
   for (int b = 0; b < 5; ++b)
     if ((mm.lane_free >> b) & 1u) s += __shfl_xor_sync(0xffffffffu, s, 1 << b);
   sh[w][lane] = s;
@@ -1247,9 +1258,10 @@ void launch_op(State& s, const Op& op_in) {
       auto fill = [&](auto& M) {
         for (size_t i = 0; i < dim * dim; ++i) M.m[i] = d2(op.m[i]);
       };
-      // thread per group when the lowest target leaves >= 8-amplitude runs
-      // for consecutive lanes; lane-cooperative otherwise (and for K = 5)
-      const bool per_group = *std::min_element(op.targets.begin(), op.targets.end()) >= 3;
+      // thread per group (measured on B200, 28 qubits: 0.88-0.93 of HBM for
+      // targets >= 3, 0.6-0.71 on the lowest qubits, where the lane-cooperative
+      // form was slower still); QSB_DENSE_LANES=1 forces the lane-cooperative form
+      const bool per_group = !std::getenv("QSB_DENSE_LANES");
       switch (K) {
         case 2: { DenseM<2> M; fill(M);
           if (per_group) k_dense_g<2><<<grid_for(groups, s.device), kThreads, 0, s.stream>>>(s.amps, groups, sl, tm, M);
@@ -1266,7 +1278,8 @@ void launch_op(State& s, const Op& op_in) {
         case 5: {
           static thread_local DenseM<5> M;  // 16 KiB: off the stack; the launch copies it
           fill(M);
-          k_dense<5><<<grid_for(groups << K, s.device, 4), kThreads, 0, s.stream>>>(s.amps, groups, sl, tm, M);
+          if (per_group) k_dense_g<5><<<grid_for(groups, s.device), kThreads, 0, s.stream>>>(s.amps, groups, sl, tm, M);
+          else k_dense<5><<<grid_for(groups << K, s.device, 4), kThreads, 0, s.stream>>>(s.amps, groups, sl, tm, M);
           break;
         }
         default: {
