@@ -306,6 +306,19 @@ typedef struct qs_dist* qs_dist_t;
 typedef struct qs_shards* qs_shards_t;
 int qs_dist_unique_id(unsigned char out[128]);
 int qs_dist_create(const unsigned char id[128], int world, int rank, int device, qs_dist_t* out);
+/* A communicator whose collectives are the caller's (no NCCL): allgather
+ * gathers `bytes` from every rank into recv in rank order, barrier blocks
+ * until every rank arrived; both return 0 on success.  The state's exchanges
+ * then run only over CUDA-IPC peer memory (one kernel storing into the other
+ * ranks' buffers, the stream drained, then the host barrier).  Used to run
+ * the multi-process data path with torch.distributed over gloo -- e.g. ranks
+ * as processes sharing one GPU, which NCCL refuses.                          */
+typedef struct {
+  void* ctx;
+  int (*allgather)(void* ctx, const void* send, void* recv, uint64_t bytes);
+  int (*barrier)(void* ctx);
+} qs_host_collectives;
+int qs_dist_create_host(const qs_host_collectives* c, int world, int rank, int device, qs_dist_t* out);
 int qs_dist_destroy(qs_dist_t d);
 int qs_shards_create_local(uint32_t num_qubits, uint32_t global_qubits, int device, qs_shards_t* out);
 int qs_shards_create_dist(uint32_t num_qubits, qs_dist_t d, qs_shards_t* out);

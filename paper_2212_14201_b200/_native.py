@@ -63,6 +63,15 @@ _DP = C.POINTER(C.c_double)
 _UP = C.POINTER(C.c_uint32)
 _U64P = C.POINTER(C.c_uint64)
 _GP = C.POINTER(QsGate)
+HostAllgather = C.CFUNCTYPE(C.c_int, C.c_void_p, C.c_void_p, C.c_void_p, C.c_uint64)
+HostBarrier = C.CFUNCTYPE(C.c_int, C.c_void_p)
+
+
+class HostCollectives(C.Structure):
+    """qs_host_collectives (include/qsb.h)."""
+    _fields_ = [("ctx", C.c_void_p), ("allgather", HostAllgather), ("barrier", HostBarrier)]
+
+
 _SIGS = {
     "qs_last_error": (C.c_char_p, []),
     "qs_abi_version": (C.c_int, []),
@@ -129,6 +138,7 @@ _SIGS = {
     # sharded state vectors
     "qs_dist_unique_id": (C.c_int, [C.c_char_p]),
     "qs_dist_create": (C.c_int, [C.c_char_p, C.c_int, C.c_int, C.c_int, C.POINTER(_P)]),
+    "qs_dist_create_host": (C.c_int, [C.POINTER(HostCollectives), C.c_int, C.c_int, C.c_int, C.POINTER(_P)]),
     "qs_dist_destroy": (C.c_int, [_P]),
     "qs_shards_create_local": (C.c_int, [C.c_uint32, C.c_uint32, C.c_int, C.POINTER(_P)]),
     "qs_shards_create_dist": (C.c_int, [C.c_uint32, _P, C.POINTER(_P)]),

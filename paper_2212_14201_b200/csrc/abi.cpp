@@ -726,6 +726,24 @@ int qs_dist_create(const unsigned char id[128], int world, int rank, int device,
   });
 }
 
+int qs_dist_create_host(const qs_host_collectives* c, int world, int rank, int device, qs_dist_t* out) {
+  return guarded([&] {
+    if (!c || !out) throw ValidationError("null collectives or output handle");
+    *out = nullptr;
+    int ndev = 0;
+    QSB_CUDA(cudaGetDeviceCount(&ndev));
+    if (device < 0 || device >= ndev) throw ValidationError("CUDA device " + std::to_string(device) + " not present");
+    auto* h = new qs_dist();
+    try {
+      h->d = dist_create_host(*c, world, rank, device);
+    } catch (...) {
+      delete h;
+      throw;
+    }
+    *out = h;
+  });
+}
+
 int qs_dist_destroy(qs_dist_t d) {
   return guarded([&] {
     if (!d) return;

@@ -249,7 +249,50 @@ void nccl_check(int r, const char* what) {
 struct Dist {
   ncclComm_t comm = nullptr;
   int world = 1, rank = 0, device = 0;
+  // Host collectives (qs_dist_create_host): the caller's all-gather and barrier
+  // (e.g. torch.distributed over gloo) stand in for NCCL.  Needs peer memory:
+  // every data movement between ranks goes through the CUDA-IPC mappings.
+  qs_host_collectives host{};
+  bool hosted() const { return host.allgather != nullptr; }
 };
+
+namespace {
+void host_check(int rc, const char* what) {
+  if (rc != 0) throw RuntimeError(std::string("host collective failed: ") + what);
+}
+// all-gather of `bytes` per rank (rank order) between device buffers, ordered on `st`
+void coll_allgather(Dist* d, const void* dsend, void* drecv, size_t bytes, cudaStream_t st) {
+  if (!d->hosted()) {
+    nccl_check(nccl().allGather(dsend, drecv, bytes, kNcclUint8, d->comm, st), "ncclAllGather");
+    return;
+  }
+  std::vector<unsigned char> hs(bytes), hr(bytes * d->world);
+  QSB_CUDA(cudaMemcpyAsync(hs.data(), dsend, bytes, cudaMemcpyDeviceToHost, st));
+  QSB_CUDA(cudaStreamSynchronize(st));
+  host_check(d->host.allgather(d->host.ctx, hs.data(), hr.data(), bytes), "allgather");
+  QSB_CUDA(cudaMemcpyAsync(drecv, hr.data(), hr.size(), cudaMemcpyHostToDevice, st));
+  QSB_CUDA(cudaStreamSynchronize(st));
+}
+// element-wise all-reduce of `count` doubles / uint64 in place (device buffer)
+template <class T, class F>
+void coll_allreduce(Dist* d, T* dbuf, size_t count, int nccl_type, int nccl_op, F op, cudaStream_t st) {
+  if (!d->hosted()) {
+    nccl_check(nccl().allReduce(dbuf, dbuf, count, nccl_type, nccl_op, d->comm, st), "ncclAllReduce");
+    return;
+  }
+  std::vector<T> mine(count), all(count * d->world);
+  QSB_CUDA(cudaMemcpyAsync(mine.data(), dbuf, count * sizeof(T), cudaMemcpyDeviceToHost, st));
+  QSB_CUDA(cudaStreamSynchronize(st));
+  host_check(d->host.allgather(d->host.ctx, mine.data(), all.data(), count * sizeof(T)), "allgather");
+  for (size_t i = 0; i < count; ++i) {
+    T acc = all[i];
+    for (int r = 1; r < d->world; ++r) acc = op(acc, all[static_cast<size_t>(r) * count + i]);  // rank order
+    mine[i] = acc;
+  }
+  QSB_CUDA(cudaMemcpyAsync(dbuf, mine.data(), count * sizeof(T), cudaMemcpyHostToDevice, st));
+  QSB_CUDA(cudaStreamSynchronize(st));
+}
+}  // namespace
 
 namespace {
 
@@ -274,7 +317,15 @@ struct NcclTransport : Transport {
   }
   // Stream-ordered barrier: completes on every rank only after every rank's
   // prior work on its stream (incl. remote stores) has finished.
+  // Host collectives: the stream is drained first, so every store of this
+  // rank (incl. remote ones over the IPC mappings) is complete before the
+  // host barrier releases the other ranks.
   void stream_barrier(cudaStream_t st) {
+    if (d_->hosted()) {
+      QSB_CUDA(st ? cudaStreamSynchronize(st) : cudaDeviceSynchronize());
+      host_check(d_->host.barrier(d_->host.ctx), "barrier");
+      return;
+    }
     double* r = scratch();
     nccl_check(nccl().allReduce(r, r, 1, kNcclDouble, kNcclSum, d_->comm, st), "ncclAllReduce");
   }
@@ -299,7 +350,7 @@ struct NcclTransport : Transport {
     const size_t hb = sizeof(h);
     QSB_CUDA(cudaMalloc(&dev, hb * (W + 1)));
     QSB_CUDA(cudaMemcpy(dev + hb * W, h, hb, cudaMemcpyHostToDevice));
-    nccl_check(nccl().allGather(dev + hb * W, dev, hb, kNcclUint8, d_->comm, nullptr), "ncclAllGather");
+    coll_allgather(d_, dev + hb * W, dev, hb, nullptr);
     std::vector<cudaIpcMemHandle_t> all(2 * W);
     QSB_CUDA(cudaMemcpy(all.data(), dev, hb * W, cudaMemcpyDeviceToHost));
     cudaFree(dev);
@@ -333,11 +384,12 @@ struct NcclTransport : Transport {
     double* r = scratch();
     double mine = ok;
     QSB_CUDA(cudaMemcpy(r, &mine, sizeof(double), cudaMemcpyHostToDevice));
-    nccl_check(nccl().allReduce(r, r, 1, kNcclDouble, kNcclMin, d_->comm, nullptr), "ncclAllReduce");
+    coll_allreduce(d_, r, 1, kNcclDouble, kNcclMin, [](double a, double b) { return std::min(a, b); }, nullptr);
     double all_ok = 0;
     QSB_CUDA(cudaMemcpy(&all_ok, r, sizeof(double), cudaMemcpyDeviceToHost));
     peer = all_ok > 0.5;
     if (!peer) close_peers(s);
+    if (!peer && d_->hosted()) throw RuntimeError("host-collective communicator: CUDA IPC peer mapping failed");
   }
   void close_peers(State& s) {
     DeviceGuard dg(d_->device);
@@ -403,7 +455,6 @@ struct NcclTransport : Transport {
   void exchange(std::vector<State*>& shards, const std::vector<uint32_t>& gpos,
                 const std::vector<uint32_t>& lpos) override {
     State& s = *shards.at(0);
-    const Nccl& N = nccl();
     DeviceGuard dg(s.device);
     const uint32_t k = static_cast<uint32_t>(gpos.size()), K = 1u << k;
     const uint32_t a = rank_bits(s.rank, gpos);
@@ -418,6 +469,8 @@ struct NcclTransport : Transport {
       s.alt = bufs[cur ^ 1][s.rank];
       return;
     }
+    if (d_->hosted()) throw RuntimeError("host-collective communicators exchange over peer memory only");
+    const Nccl& N = nccl();
     // All-to-all among the 2^k ranks that differ in the exchanged rank bits:
     // block d (local bits lpos = d) goes to the peer whose rank bits are d, and
     // that peer's block a (a = our rank bits) lands in our block d.
@@ -442,13 +495,12 @@ struct NcclTransport : Transport {
     }
   }
   double sum(const std::vector<double>& v) override {
-    const Nccl& N = nccl();
     DeviceGuard dg(d_->device);
     double* r = scratch();
     double mine = 0;
     for (double x : v) mine += x;
     QSB_CUDA(cudaMemcpy(r + d_->world, &mine, sizeof(double), cudaMemcpyHostToDevice));
-    nccl_check(N.allGather(r + d_->world, r, 1, kNcclDouble, d_->comm, nullptr), "ncclAllGather");
+    coll_allgather(d_, r + d_->world, r, sizeof(double), nullptr);
     std::vector<double> all(d_->world);
     QSB_CUDA(cudaMemcpy(all.data(), r, d_->world * sizeof(double), cudaMemcpyDeviceToHost));
     double t = 0;
@@ -521,6 +573,18 @@ Dist* dist_create(const unsigned char id[128], int world, int rank, int device) 
   return d.release();
 }
 
+Dist* dist_create_host(const qs_host_collectives& c, int world, int rank, int device) {
+  if (world < 1 || (world & (world - 1))) throw ValidationError("world size must be a power of two");
+  if (rank < 0 || rank >= world) throw ValidationError("rank out of range");
+  if (!c.allgather || !c.barrier) throw ValidationError("host collectives need allgather and barrier callbacks");
+  auto d = std::make_unique<Dist>();
+  d->world = world;
+  d->rank = rank;
+  d->device = device;
+  d->host = c;
+  return d.release();
+}
+
 void dist_destroy(Dist* d) {
   if (!d) return;
   if (d->comm && nccl().commDestroy) nccl().commDestroy(d->comm);
@@ -545,7 +609,7 @@ std::unique_ptr<ShardSet> make_dist_shard(uint32_t n, Dist* d) {
   auto tr = std::make_unique<NcclTransport>(d);
   tr->owner = ss->shards[0].get();
   // peer memory (CUDA IPC over NVLink) unless disabled; collective on all ranks
-  if (d->world > 1 && exchange_mode() != "nccl") tr->setup_peer(*ss->shards[0]);
+  if (d->world > 1 && (exchange_mode() != "nccl" || d->hosted())) tr->setup_peer(*ss->shards[0]);
   ss->tr = std::move(tr);
   shard_fill_basis(*ss, 0);
   return ss;
@@ -767,7 +831,7 @@ void shard_probs(ShardSet& ss, const uint32_t* qubits, uint32_t m, double* out) 
     DevBuf buf(R * 8 * (W + 1), ss.device);
     double* d = buf.as<double>();
     QSB_CUDA(cudaMemcpy(d + R * W, mine.data(), R * 8, cudaMemcpyHostToDevice));
-    nccl_check(nccl().allGather(d + R * W, d, R, kNcclDouble, nt->d_->comm, nullptr), "ncclAllGather");
+    coll_allgather(nt->d_, d + R * W, d, R * 8, nullptr);
     all.resize(R * W);
     QSB_CUDA(cudaMemcpy(all.data(), d, R * W * 8, cudaMemcpyDeviceToHost));
   } else {
@@ -790,6 +854,36 @@ void shard_sample(ShardSet& ss, const double* u_host, uint64_t shots, bool exact
     DevBuf small(32, ss.device);
     double* carry = small.as<double>();
     double* total = carry + 1;
+    if (nt->d_->hosted()) {
+      // the serial chain, one all-gather per rank: rank k scans its shard
+      // continuing from rank k-1's final running sum, then publishes its own
+      double* u = nullptr;
+      unsigned long long* out = nullptr;
+      ShardCum c{};
+      double prev = 0.0, fin = 0.0;
+      for (int k = 0; k < W; ++k) {
+        double mine = 0.0;
+        if (k == r) {
+          if (r > 0) QSB_CUDA(cudaMemcpyAsync(carry, &prev, 8, cudaMemcpyHostToDevice, s.stream));
+          c = shard_cumulative(s, exact, r > 0 ? carry : nullptr, shots, &u, &out);
+          QSB_CUDA(cudaMemcpyAsync(&mine, c.total, 8, cudaMemcpyDeviceToHost, s.stream));
+          QSB_CUDA(cudaStreamSynchronize(s.stream));
+        }
+        std::vector<double> all(W);
+        host_check(nt->d_->host.allgather(nt->d_->host.ctx, &mine, all.data(), 8), "allgather");
+        if (k + 1 == r) prev = all[k];
+        if (k + 1 == W) fin = all[k];
+      }
+      QSB_CUDA(cudaMemcpyAsync(total, &fin, 8, cudaMemcpyHostToDevice, s.stream));
+      QSB_CUDA(cudaMemcpyAsync(u, u_host, shots * 8, cudaMemcpyHostToDevice, s.stream));
+      QSB_CUDA(cudaMemsetAsync(out, 0, shots * 8, s.stream));
+      search_range(s, c, total, r > 0 ? carry : nullptr, r + 1 == W, u, shots, out);
+      coll_allreduce(nt->d_, out, shots, kNcclUint64, kNcclMax,
+                     [](unsigned long long a, unsigned long long b) { return std::max(a, b); }, s.stream);
+      QSB_CUDA(cudaMemcpyAsync(out_host, out, shots * 8, cudaMemcpyDeviceToHost, s.stream));
+      QSB_CUDA(cudaStreamSynchronize(s.stream));
+      return;
+    }
     // serial chain: rank r continues the running sum of ranks < r (bit-exact serial order)
     if (r > 0) nccl_check(nccl().recv(carry, 1, kNcclDouble, r - 1, nt->d_->comm, s.stream), "ncclRecv");
     double* u = nullptr;
@@ -844,6 +938,7 @@ void shard_expect_pauli(ShardSet& ss, const std::vector<uint64_t>& xm, const std
         const uint32_t pr = s.rank ^ static_cast<uint32_t>(xr);
         pauli_cross(s, s.amps, nt->bufs[nt->cur][pr], s.size, xl, zl, v);
       } else {  // stream the partner's shard in aligned chunks (X maps each chunk onto itself)
+        if (nt->d_->hosted()) throw RuntimeError("host-collective communicators need peer memory");
         const uint32_t pr = s.rank ^ static_cast<uint32_t>(xr);
         uint64_t C = exchange_chunk(s.size, 1);
         const uint64_t need = xl ? (1ull << (64 - __builtin_clzll(xl))) : 1;

@@ -75,6 +75,8 @@ std::unique_ptr<ShardSet> make_local_shards(uint32_t n, uint32_t g, int device);
 struct Dist;
 void dist_unique_id(unsigned char out[128]);
 Dist* dist_create(const unsigned char id[128], int world, int rank, int device);
+// Communicator over the caller's host collectives (no NCCL; peer memory only).
+Dist* dist_create_host(const qs_host_collectives& c, int world, int rank, int device);
 void dist_destroy(Dist* d);
 int dist_rank(const Dist* d);
 int dist_world(const Dist* d);

@@ -51,6 +51,46 @@ class DistComm:
         dist.broadcast_object_list(obj, src=0)
         return cls(obj[0], world, rank, device)
 
+    @classmethod
+    def host_from_torch(cls, device=None, group=None):
+        """Communicator whose collectives run through torch.distributed on the
+        host (any backend, e.g. gloo) instead of NCCL: qs_dist_create_host.
+        Rank-to-rank data then moves only over CUDA-IPC peer memory.  This is
+        what lets two processes share one GPU (NCCL refuses duplicate devices),
+        so the multi-process IPC data path can be tested on one B200."""
+        import torch
+        import torch.distributed as dist
+
+        rank, world = dist.get_rank(group), dist.get_world_size(group)
+        if device is None:
+            device = torch.cuda.current_device()
+        self = cls.__new__(cls)
+
+        def allgather(ctx, send, recv, nbytes):
+            try:
+                mine = torch.frombuffer(bytearray(C.string_at(send, nbytes)), dtype=torch.uint8)
+                outs = [torch.empty(nbytes, dtype=torch.uint8) for _ in range(world)]
+                dist.all_gather(outs, mine, group=group)
+                C.memmove(recv, b"".join(o.numpy().tobytes() for o in outs), nbytes * world)
+                return 0
+            except Exception:  # reported to the library as a failed collective
+                return 1
+
+        def barrier(ctx):
+            try:
+                dist.barrier(group=group)
+                return 0
+            except Exception:
+                return 1
+
+        self._cbs = (N.HostAllgather(allgather), N.HostBarrier(barrier))
+        coll = N.HostCollectives(None, self._cbs[0], self._cbs[1])
+        h = C.c_void_p()
+        N.check(N.lib().qs_dist_create_host(C.byref(coll), world, rank, device, C.byref(h)))
+        self._h = h
+        self.world, self.rank, self.device = world, rank, device
+        return self
+
     def close(self):
         h = getattr(self, "_h", None)
         if h is not None and N._lib is not None:

@@ -1,0 +1,66 @@
+"""BASELINE.json configs 1, 2 and 5 through the public Python API on cuda:0,
+wall clock (the same measurements `oracle/_ref/ref_driver bench_config
+config1|config2|config5` makes for the reference on the host, BASELINE.md
+section 4).  One JSON line per measurement; each is run once untimed first
+(planning, tile-kernel build) and then timed.
+
+    python tools/config_sweep.py [config1 config2 config5]
+"""
+import json
+import os
+import sys
+import time
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+from paper_2212_14201_b200 import qforge as Q  # noqa: E402
+
+
+def line(config, case, p, sec, **kw):
+    d = {"config": config, "case": case, "n": p.qubit_count, "gates": p.gate_count(), "seconds": round(sec, 6),
+         "gates_per_s": round(p.gate_count() / sec, 1), "device": "B200 (cuda:0)"}
+    d.update(kw)
+    print(json.dumps(d), flush=True)
+
+
+def timed(fn, reps=3):
+    fn()
+    best = None
+    for _ in range(reps):
+        t0 = time.perf_counter()
+        out = fn()
+        dt = time.perf_counter() - t0
+        best = dt if best is None else min(best, dt)
+    return best, out
+
+
+which = sys.argv[1:] or ["config1", "config2", "config5"]
+if "config1" in which:
+    for name, p in (("ghz20", Q.gen_ghz(20)), ("qft20", Q.gen_qft(20, 0x5A5A5))):
+        def job(p=p):
+            r = Q.run(p)
+            return r.final_state.probabilities()
+        sec, probs = timed(job)
+        line("config1", name, p, sec, includes="run() + probabilities() (2^20 doubles to the host)",
+             p_last=float(probs[-1]))
+if "config2" in which:
+    p = Q.gen_random_circuit(28, 20, 424242)
+    sec, r = timed(lambda: Q.run(p))
+    line("config2", "random28", p, sec, includes="run(): state allocation, plan (cached after the first call), "
+                                                 "execution; final state resident on the GPU",
+         checksum=r.final_state.checksum())
+if "config5" in which:
+    p = Q.gen_hea(24, 10, 2024)
+    terms = {"Z%d Z%d" % (i, i + 1): 1.0 for i in range(23)}
+    terms.update({"X%d" % i: 0.5 for i in range(24)})
+    H = Q.PauliOperator(terms)
+    sec, e = timed(lambda: Q.expectation(p, H))
+    line("config5", "hea24_expectation", p, sec, includes="expectation() (%d terms)" % len(terms), value=e)
+    q = Q.gen_hea(24, 10, 2024)
+    q.cbit_count = 24
+    for k in range(24):
+        q.measure(k, k)
+    for seed in range(10):
+        o = Q.SimOptions(seed=seed)
+        sec, r = timed(lambda o=o: Q.run(q, o, 1000000), reps=1)
+        line("config5", "hea24_sample_seed%d" % seed, q, sec,
+             includes="run(p, {seed}, 1e6 shots): evolution + exact sampling + counts", keys=len(r.counts))
