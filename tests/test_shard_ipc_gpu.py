@@ -65,7 +65,7 @@ def test_ipc_exchanges_across_processes_match_oracle(tmp_path, world, fuse):
             assert np.array_equal(r[name + "_samples"], ol.sample_seeded(want, n, 7, 4000))
         ex = np.array([complex(*ol.expectation(want, n, [(w, 1.0)])) for w in words])
         for r in res:
-            assert np.max(np.abs(r[name + "_pauli"] - ex)) <= 1e-12, name
+            assert np.max(np.abs(r[name + "_pauli"] - ex)) <= 1e-11, name  # sums of 2^n terms
         for r in res[1:]:
             assert np.array_equal(r[name + "_cs"], res[0][name + "_cs"])
 
