@@ -282,6 +282,20 @@ int qs_gradient(qs_state_t s, const qs_gate* gates, uint64_t count, const uint64
  * double accumulation                                  [statevector.hpp:544-552] */
 int qs_cumulative(qs_state_t s, double* cum_out, double* total_out);
 
+/* --- partial amplitudes (cut method) ------------------------------------------
+ * partial_amplitude [pathsum.hpp:317-459]: the qubits split into block A
+ * (block_a[0..na), ascending or not) and block B (the rest); every CZ / CNOT
+ * across the cut is a branch variable.  Returns out[2t], out[2t+1] = the
+ * amplitude <targets[t]|U|0...0> (targets as basis indices, qubit q = bit q),
+ * summed over all 2^k branches.  The branches are batched as extra qubits of
+ * two half-size states (2^batch_qubits amplitudes per block state at most;
+ * 0 = 2^26), each block circuit runs as tile passes on `device`.  Gates: no
+ * extra controls, 1 target or CNOT/CZ (QS_ERR_UNSUPPORTED otherwise, as the
+ * reference's check_cuttable_gate).  The facade (qforge/pathsum.hpp,
+ * qforge.plan_cut) chooses the cut and checks the CutPlan.                   */
+int qs_partial_amplitude(uint32_t num_qubits, const qs_gate* gates, uint64_t n, const uint32_t* block_a, uint32_t na,
+                         const uint64_t* targets, uint64_t ntargets, int device, uint32_t batch_qubits, double* out);
+
 /* --- sharded state vectors (multi-GPU) -----------------------------------------
  * The reference keeps one 2^n vector in host memory [statevector.hpp:111-118]
  * and has no distributed mode; these entry points are the B200 extension the

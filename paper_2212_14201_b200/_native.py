@@ -41,6 +41,10 @@ class CudaError(QforgeError):
     pass
 
 
+class UnsupportedError(QforgeError):
+    """qforge::UnsupportedError (error.hpp:30-33)."""
+
+
 class QsGate(C.Structure):
     """struct qs_gate (include/qsb.h)."""
     _fields_ = [
@@ -138,6 +142,8 @@ _SIGS = {
     # sharded state vectors
     "qs_dist_unique_id": (C.c_int, [C.c_char_p]),
     "qs_dist_create": (C.c_int, [C.c_char_p, C.c_int, C.c_int, C.c_int, C.POINTER(_P)]),
+    "qs_partial_amplitude": (C.c_int, [C.c_uint32, C.POINTER(QsGate), C.c_uint64, C.POINTER(C.c_uint32), C.c_uint32,
+                                       C.POINTER(C.c_uint64), C.c_uint64, C.c_int, C.c_uint32, C.POINTER(C.c_double)]),
     "qs_dist_create_host": (C.c_int, [C.POINTER(HostCollectives), C.c_int, C.c_int, C.c_int, C.POINTER(_P)]),
     "qs_dist_destroy": (C.c_int, [_P]),
     "qs_shards_create_local": (C.c_int, [C.c_uint32, C.c_uint32, C.c_int, C.POINTER(_P)]),
@@ -195,6 +201,8 @@ def check(rc):
         raise CudaError(msg)
     if rc == QS_ERR_MEMORY:
         raise MemoryError(msg)
+    if rc == QS_ERR_UNSUPPORTED:
+        raise UnsupportedError(msg)
     raise QforgeError(msg)
 
 

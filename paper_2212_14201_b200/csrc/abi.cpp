@@ -18,6 +18,9 @@
 #include "shard.hpp"
 
 namespace qsb {
+void partial_amplitude(uint32_t n, const qs_gate* gates, uint64_t count, const uint32_t* block_a, uint32_t na,
+                       const uint64_t* targets, uint64_t ntargets, int device, uint32_t batch_qubits,
+                       double* out);  // pathsum.cpp
 void gradient_adjoint(State& s, const qs_gate* gates, uint64_t count, const uint64_t* slots, uint64_t nslots,
                       const std::vector<uint64_t>& xm, const std::vector<uint64_t>& zm, const std::vector<int>& ny,
                       const double* coeffs, double* out);  // gradient.cpp
@@ -60,6 +63,9 @@ int guarded(F&& f) {
   } catch (const MemoryError& e) {
     g_last_error = e.what();
     return QS_ERR_MEMORY;
+  } catch (const UnsupportedError& e) {
+    g_last_error = e.what();
+    return QS_ERR_UNSUPPORTED;
   } catch (const CudaError& e) {
     g_last_error = e.what();
     return QS_ERR_CUDA;
@@ -723,6 +729,18 @@ int qs_dist_create(const unsigned char id[128], int world, int rank, int device,
       throw;
     }
     *out = h;
+  });
+}
+
+int qs_partial_amplitude(uint32_t num_qubits, const qs_gate* gates, uint64_t n, const uint32_t* block_a, uint32_t na,
+                         const uint64_t* targets, uint64_t ntargets, int device, uint32_t batch_qubits, double* out) {
+  return guarded([&] {
+    if ((n && !gates) || (na && !block_a) || (ntargets && (!targets || !out))) throw ValidationError("null argument");
+    if (num_qubits > 60) throw ValidationError("partial amplitude: at most 60 qubits");
+    int ndev = 0;
+    QSB_CUDA(cudaGetDeviceCount(&ndev));
+    if (device < 0 || device >= ndev) throw ValidationError("CUDA device " + std::to_string(device) + " not present");
+    partial_amplitude(num_qubits, gates, n, block_a, na, targets, ntargets, device, batch_qubits, out);
   });
 }
 

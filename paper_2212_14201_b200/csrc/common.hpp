@@ -29,6 +29,10 @@ struct CudaError : std::runtime_error {
 struct MemoryError : std::runtime_error {
   using std::runtime_error::runtime_error;
 };
+// Mirrors qforge::UnsupportedError (error.hpp): valid input the operation does not handle.
+struct UnsupportedError : std::runtime_error {
+  using std::runtime_error::runtime_error;
+};
 
 #define QSB_CUDA(expr)                                                                     \
   do {                                                                                     \

@@ -1670,6 +1670,51 @@ double serial_checksum(State& s) {
   return *h;
 }
 
+// partial_amplitude's branch sum (pathsum.hpp:453-456), one block per target:
+// sum over b < 2^c of A[b 2^na + ta] * B[b 2^nb + tb] -- fixed per-thread
+// ranges + fixed-order block tree (deterministic).
+__global__ void __launch_bounds__(kThreads) k_branch_dot(const double2* __restrict__ A, const double2* __restrict__ B,
+                                                         uint32_t na, uint32_t nb, uint64_t branches,
+                                                         const unsigned long long* __restrict__ ta,
+                                                         const unsigned long long* __restrict__ tb,
+                                                         double2* __restrict__ out) {
+  __shared__ double sh[kThreads / 32];
+  const unsigned long long a0 = ta[blockIdx.x], b0 = tb[blockIdx.x];
+  double re = 0, im = 0;
+  for (uint64_t b = threadIdx.x; b < branches; b += blockDim.x) {
+    const double2 x = A[(b << na) | a0], y = B[(b << nb) | b0];
+    re += x.x * y.x - x.y * y.y;
+    im += x.x * y.y + x.y * y.x;
+  }
+  const double tr = block_sum(re, sh);
+  const double ti = block_sum(im, sh);
+  if (threadIdx.x == 0) out[blockIdx.x] = make_double2(tr, ti);
+}
+
+void branch_dot(State& a, State& b, uint32_t na, uint32_t nb, uint32_t c, const std::vector<uint64_t>& ta,
+                const std::vector<uint64_t>& tb, std::vector<cd>& out) {
+  DeviceGuard dg(a.device);
+  const size_t T = ta.size();
+  out.assign(T, cd(0));
+  if (!T) return;
+  QSB_CUDA(cudaStreamSynchronize(b.stream));
+  char* scr = static_cast<char*>(a.get_scratch(T * (16 + 16)));
+  unsigned long long* dta = reinterpret_cast<unsigned long long*>(scr);
+  unsigned long long* dtb = dta + T;
+  double2* dout = reinterpret_cast<double2*>(dtb + T);
+  QSB_CUDA(cudaMemcpyAsync(dta, ta.data(), T * 8, cudaMemcpyHostToDevice, a.stream));
+  QSB_CUDA(cudaMemcpyAsync(dtb, tb.data(), T * 8, cudaMemcpyHostToDevice, a.stream));
+  for (size_t t0 = 0; t0 < T; t0 += 65535) {
+    const unsigned blocks = static_cast<unsigned>(std::min<size_t>(65535, T - t0));
+    k_branch_dot<<<blocks, kThreads, 0, a.stream>>>(a.amps, b.amps, na, nb, 1ull << c, dta + t0, dtb + t0, dout + t0);
+    QSB_LAUNCHED();
+  }
+  std::vector<double2> h(T);
+  QSB_CUDA(cudaMemcpyAsync(h.data(), dout, T * 16, cudaMemcpyDeviceToHost, a.stream));
+  QSB_CUDA(cudaStreamSynchronize(a.stream));
+  for (size_t t = 0; t < T; ++t) out[t] = cd(h[t].x, h[t].y);
+}
+
 double exact_cumulative(State& s, double* d_probs, double* d_cum) {
   DeviceGuard dg(s.device);
   char* extra;

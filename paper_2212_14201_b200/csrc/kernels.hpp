@@ -92,5 +92,8 @@ double exact_cumulative(State& s, double* d_probs, double* d_cum);
 // probability_checksum with the reference's serial rounding (bench.hpp:141-148):
 // bitwise equal to the serial loop on the same amplitudes.
 double serial_checksum(State& s);
+// sum_b a[b 2^na + ta[t]] * b[b 2^nb + tb[t]] over b < 2^c, per target t (partial_amplitude).
+void branch_dot(State& a, State& b, uint32_t na, uint32_t nb, uint32_t c, const std::vector<uint64_t>& ta,
+                const std::vector<uint64_t>& tb, std::vector<cd>& out);
 
 }  // namespace qsb

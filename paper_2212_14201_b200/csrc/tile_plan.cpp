@@ -363,9 +363,13 @@ struct Compiler {
             order.insert(order.end(), p.op.controls.begin(), p.op.controls.end());
             for (uint32_t q : order) {
               const bool one = (vals >> q) & 1;
+              if (!one && d == cd(0)) continue;  // 1/d: a projector (partial_amplitude) has no weight form here
               reps.push_back({lits & ~bit(q), vals & ~bit(q), one ? cd(1.0) : d, q, one ? d : 1.0 / d});
             }
+            // always valid: d under the full conjunction, no weight (1^b)
+            if (reps.empty()) reps.push_back({lits, vals, d, tq, cd(1.0)});
           } else {
+            if (d0 == cd(0)) throw RuntimeError("tile planner: diagonal (0, d) without a unit entry");
             reps.push_back({ctrl, cval, d0, tq, d1 / d0});
           }
           bool merged = false;

@@ -11,6 +11,7 @@
 #include "qforge/gates.hpp"
 #include "qforge/linalg.hpp"
 #include "qforge/noise.hpp"
+#include "qforge/pathsum.hpp"
 #include "qforge/pauli.hpp"
 #include "qforge/rng.hpp"
 #include "qforge/simulator.hpp"

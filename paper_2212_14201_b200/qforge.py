@@ -13,7 +13,7 @@ from dataclasses import dataclass, field
 import numpy as np
 
 from . import _native as N
-from ._native import QforgeError, ValidationError  # noqa: F401  (re-exported)
+from ._native import QforgeError, UnsupportedError, ValidationError  # noqa: F401  (re-exported)
 
 
 class GateKind(enum.IntEnum):
@@ -723,3 +723,199 @@ def gradient(pc, H, at, opts=None):
     N.check(N.lib().qs_gradient(work.handle(), arr, len(p.body), slots.ctypes.data_as(N._U64P), len(slots),
                                 "".join(words).encode(), N.dptr(coeffs), len(terms), N.dptr(per)))
     return [float(sum(per[i] for i, (_, nm) in enumerate(pc.slots) if nm == name)) for name in pc.names]
+
+
+# ------------------------------------------------------------------ pathsum.hpp
+
+class FlatCircuitRequired(QforgeError):
+    """qforge::FlatCircuitRequired (error.hpp:23-26)."""
+
+
+class BudgetExceeded(QforgeError):
+    """qforge::BudgetExceeded (error.hpp:43-48): carries the path / branch estimate."""
+
+    def __init__(self, msg, estimated_paths):
+        super().__init__(msg)
+        self.estimated_paths = estimated_paths
+
+
+DEFAULT_PATH_BUDGET = 1 << 22  # pathsum.hpp:183
+
+
+def _gates_only(p, what):
+    for ins in p.body:
+        if isinstance(ins, Measure):
+            raise UnsupportedError("%s is defined for measurement-free programs" % what)
+        if not isinstance(ins, Gate):
+            raise FlatCircuitRequired("%s requires a flat program" % what)
+
+
+def path_count_estimate(p):
+    """2^(control count after rewriting each gate as controlled one-target
+    operators), as the reference's path evaluator branches (pathsum.hpp:30-101):
+    CNOT / CZ one control, TOFFOLI two, SWAP three CNOTs, plus extra controls."""
+    bits = 0
+    for g in p.body:
+        if g.kind == GateKind.I:
+            continue
+        extra = len(g.controls)
+        if g.kind in (GateKind.CNOT, GateKind.CZ):
+            bits += extra + 1
+        elif g.kind == GateKind.TOFFOLI:
+            bits += extra + 2
+        elif g.kind == GateKind.SWAP:
+            bits += 3 * (extra + 1)
+        elif g.kind == GateKind.Custom and len(g.targets) != 1:
+            raise UnsupportedError("path-sum evaluation supports custom gates on one target only")
+        else:
+            bits += extra
+    return (1 << bits) if bits <= 62 else (1 << 64) - 1
+
+
+def _parse_bitstring(bits, n):
+    """pathsum.hpp:165-178: rightmost character is qubit 0 -> basis index."""
+    if len(bits) != n:
+        raise ValidationError("target bitstring length %d does not match %d qubits" % (len(bits), n))
+    if any(c not in "01" for c in bits):
+        raise ValidationError("target bitstring must contain only 0/1")
+    return int(bits, 2) if n else 0
+
+
+def single_amplitude(p, target, path_budget=DEFAULT_PATH_BUDGET, device=0):
+    """<target|U|0...0> (pathsum.hpp:188-202).  Same validation, errors and
+    budget as the reference's path evaluator; the value comes from the GPU
+    state vector (one tile-pass run, one amplitude read), which the budget does
+    not limit -- it is kept only so callers see the reference's behaviour."""
+    validate_or_throw(p)
+    _gates_only(p, "path-sum evaluation")
+    est = path_count_estimate(p)
+    idx = _parse_bitstring(target, p.qubit_count)
+    if est > path_budget:
+        raise BudgetExceeded("path count %s exceeds budget %d" % ("overflows" if est >= (1 << 64) - 1 else est,
+                                                                  path_budget), est)
+    sv = StateVector(p.qubit_count, device)
+    if p.body:
+        sv.apply_circuit(p.body)
+    return complex(sv.amplitude(idx))
+
+
+@dataclass
+class CutPlan:
+    """pathsum.hpp:208-213."""
+    block_a: list = field(default_factory=list)
+    block_b: list = field(default_factory=list)
+    crossing_gates: list = field(default_factory=list)
+    branch_count: int = 1
+
+
+def _check_cuttable(g):
+    if g.controls:
+        raise UnsupportedError("cut planning expects gates without extra controls")
+    if len(g.targets) == 1 or g.kind in (GateKind.CNOT, GateKind.CZ):
+        return
+    raise UnsupportedError("cut planning cannot handle %s" % g.kind.name)
+
+
+def plan_cut(p):
+    """Balanced bipartition with few crossing 2-qubit gates (pathsum.hpp:232-310):
+    exhaustive over the ceil(n/2)-subsets for n <= 12, otherwise first-improving
+    pair swaps from the low half.  Host-side combinatorics."""
+    validate_or_throw(p)
+    _gates_only(p, "cut planning")
+    n = p.qubit_count
+    if n < 2:
+        raise ValidationError("cut planning needs at least 2 qubits")
+    pairs = []
+    for g in p.body:
+        _check_cuttable(g)
+        if len(g.targets) == 2:
+            pairs.append((g.targets[0], g.targets[1]))
+    size_a = (n + 1) // 2
+
+    def cross(mask):
+        return sum(((mask >> a) ^ (mask >> b)) & 1 for a, b in pairs)
+
+    if n <= 12:
+        best, best_c = 0, None
+        for mask in range(1 << n):
+            if bin(mask).count("1") != size_a:
+                continue
+            c = cross(mask)
+            if best_c is None or c < best_c:
+                best, best_c = mask, c
+    else:
+        mask = (1 << size_a) - 1
+        cur = cross(mask)
+        improved = True
+        while improved:
+            improved = False
+            for a in range(n):
+                if not (mask >> a) & 1:
+                    continue
+                for b in range(n):
+                    if (mask >> b) & 1:
+                        continue
+                    m2 = (mask & ~(1 << a)) | (1 << b)
+                    c = cross(m2)
+                    if c < cur:
+                        mask, cur, improved = m2, c, True
+                        break
+                if improved:
+                    break
+        best = mask
+    plan = CutPlan([q for q in range(n) if (best >> q) & 1], [q for q in range(n) if not (best >> q) & 1])
+    for i, g in enumerate(p.body):
+        if len(g.targets) == 2 and ((best >> g.targets[0]) & 1) != ((best >> g.targets[1]) & 1):
+            plan.crossing_gates.append(i)
+    k = len(plan.crossing_gates)
+    plan.branch_count = (1 << 64) - 1 if k >= 63 else 1 << k
+    return plan
+
+
+def partial_amplitude(p, plan, targets, branch_budget=DEFAULT_PATH_BUDGET, device=0, batch_qubits=0):
+    """pathsum.hpp:317-459: amplitudes of `targets` (bitstrings, qubit 0
+    rightmost) summed over the 2^k branches of the cut -- all branches batched
+    as extra qubits of two half-size GPU states (qs_partial_amplitude)."""
+    validate_or_throw(p)
+    n = p.qubit_count
+    side = [-1] * n
+    for q in plan.block_a:
+        if q >= n:
+            raise ValidationError("cut plan qubit out of range")
+        side[q] = 0
+    for q in plan.block_b:
+        if q >= n or side[q] != -1:
+            raise ValidationError("cut plan blocks must partition the qubits")
+        side[q] = 1
+    if any(s == -1 for s in side):
+        raise ValidationError("cut plan blocks must partition the qubits")
+    if plan.branch_count > branch_budget:
+        raise BudgetExceeded("branch count %d exceeds budget %d" % (plan.branch_count, branch_budget),
+                             plan.branch_count)
+    crossing = []
+    for i, ins in enumerate(p.body):
+        if not isinstance(ins, Gate):
+            raise UnsupportedError("partial amplitude expects a gates-only program")
+        _check_cuttable(ins)
+        if len(ins.targets) == 2 and side[ins.targets[0]] != side[ins.targets[1]]:
+            crossing.append(i)
+    if crossing != list(plan.crossing_gates):
+        raise ValidationError("cut plan does not match the program's gates")
+    keys, idx = [], []
+    for t in targets:
+        b = _parse_bitstring(t, n)
+        if t not in keys:
+            keys.append(t)
+            idx.append(b)
+    out = {t: 0j for t in targets}
+    if not keys:
+        return out
+    arr, keep = N.gate_array(p.body)
+    ba = np.array(plan.block_a, dtype=np.uint32)
+    ti = np.array(idx, dtype=np.uint64)
+    res = np.zeros(2 * len(keys), dtype=np.float64)
+    N.check(N.lib().qs_partial_amplitude(n, arr, len(p.body), ba.ctypes.data_as(N.C.POINTER(N.C.c_uint32)), len(ba),
+                                         ti.ctypes.data_as(N._U64P), len(keys), device, batch_qubits, N.dptr(res)))
+    for j, t in enumerate(keys):
+        out[t] = complex(res[2 * j], res[2 * j + 1])
+    return out

@@ -1,4 +1,4 @@
-"""The reference's own GoogleTest sources (statevector, simulator, bench, noise,
+"""The reference's own GoogleTest sources (statevector, simulator, bench, noise, pathsum,
 variational), compiled UNMODIFIED against the drop-in qforge facade
 (paper_2212_14201_b200/include/qforge) and libqsb.so, run on the GPU.
 
@@ -22,7 +22,8 @@ pytestmark = pytest.mark.gpu
 INTERNALS = "-GroupIndexer.*:Kernels.ChunkedSumMatchesSerialBitwise"
 
 
-@pytest.mark.parametrize("suite", ["statevector_test", "simulator_test", "bench_test", "variational_test", "noise_test"])
+@pytest.mark.parametrize("suite", ["statevector_test", "simulator_test", "bench_test", "variational_test", "noise_test",
+                                   "pathsum_test"])
 def test_reference_suite_passes_against_dropin(suite):
     exe = os.path.join(DROP, suite)
     assert os.path.exists(exe), "drop-in test binaries not built (run __graft_entry__.build() with /root/reference)"
