@@ -133,9 +133,12 @@ def ncu_traffic(workload, plan):
         return None
 
 
-def build_program(workload):
+def build_program(workload, qubits=None):
     from paper_2212_14201_b200 import qforge as Q
     gen, args, n = WORKLOADS[workload]
+    if qubits is not None and qubits != n:  # diagnostics: the same generator at another size
+        args = (qubits,) + tuple(args[1:])
+        n = qubits
     p = {"random": Q.gen_random_circuit, "qft": Q.gen_qft, "hea": Q.gen_hea, "ghz": Q.gen_ghz}[gen](*args)
     return p, n
 
@@ -423,8 +426,8 @@ def roofline_of(m, runner, plan, workload, peak, peak_kind):
     return r
 
 
-def make_runner(workload, plan_mode, local, world, args, sharded):
-    p, n = build_program(workload)
+def make_runner(workload, plan_mode, local, world, args, sharded, qubits=None):
+    p, n = build_program(workload, qubits)
     gates = p.gates()
     if sharded:
         return ShardedRunner(n, gates, local, dist_world=world), n, len(gates)
@@ -444,6 +447,8 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-config4", action="store_true", help="N>1: skip the 34-qubit config-4 lines")
+    ap.add_argument("--config4-qubits", type=int, default=34,
+                    help="size of the config-4 lines (34; smaller only to exercise the path on fewer GPUs)")
     ap.add_argument("--replicas", action="store_true", help="N>1: independent replicas instead of one sharded state")
     ap.add_argument("--local-shards", type=int, default=0, metavar="G",
                     help="N=1 diagnostic: split the state into 2^G shards on this GPU")
@@ -563,14 +568,17 @@ def main():
         cpu = cpu_baseline(args.workload, n)
 
     config4 = None
-    if world > 1 and sharded and not args.no_config4 and args.workload == "random30":
+    if sharded and (world > 1 or args.config4_qubits < 34) and not args.no_config4 and args.workload == "random30":
         config4 = []
+        runner = None  # the 30-qubit shards go before the 34-qubit ones are allocated
+        torch.cuda.empty_cache()
         for wl in ("qft34", "random34"):
             try:
-                r4, n4, g4 = make_runner(wl, plan_mode, local, world, args, True)
+                r4, n4, g4 = make_runner(wl, plan_mode, local, world, args, True, args.config4_qubits)
                 m4 = measure(r4, max(2, min(args.steps, 3)), 3, world, g4, local)
                 rf = roofline_of(m4, r4, "tiled", wl, peak, peak_kind)
                 config4.append({"workload": "%s: %s%s" % (wl, WORKLOADS[wl][0], WORKLOADS[wl][1]),
+                                "qubits": n4,
                                 "value": round(m4["value"], 2), "unit": "gates/s",
                                 "ms_per_step": round(m4["ms_per_step"], 3), "gates": g4,
                                 "passes": r4.stats["passes"], "plan_seconds": round(r4.plan_s, 3),

@@ -612,9 +612,15 @@ struct ChunkInfo {
   int clean;    // no ties, no oversize addend, normal range
 };
 
-__device__ __forceinline__ bool int_step(double p, double u, long long& k) {
-  // returns false for a tie or an addend too large for the one-binade model
-  const double x = p / u;  // exact: u is a power of two
+// Exponent / power-of-two helpers by bit manipulation (exact; normal,
+// positive arguments): no DDIV, no libm ilogb / ldexp in the scan loops.
+__device__ __forceinline__ int exp_of(double x) { return (int)((__double_as_longlong(x) >> 52) & 0x7ff) - 1023; }
+__device__ __forceinline__ double pow2(int k) { return __longlong_as_double((long long)(k + 1023) << 52); }
+
+// returns false for a tie or an addend too large for the one-binade model;
+// inv_u = 1/u = 2^(52-e), so p * inv_u is p/u exactly
+__device__ __forceinline__ bool int_step(double p, double inv_u, long long& k) {
+  const double x = p * inv_u;
   if (!(x < 4503599627370496.0)) return false;  // 2^52
   const double f = floor(x);
   const double frac = x - f;
@@ -630,14 +636,14 @@ __global__ void __launch_bounds__(kThreads) k_chunk_ints(const double* __restric
   const uint64_t lo = blockIdx.x * C, hi = min(n, lo + C);
   const double est = E[blockIdx.x];
   const bool usable = est >= 2.2250738585072014e-308 * 4503599627370496.0;  // u stays normal
-  const int e = usable ? ilogb(est) : 0;
-  const double u = usable ? ldexp(1.0, e - 52) : 1.0;
+  const int e = usable ? exp_of(est) : 0;
+  const double inv_u = usable ? pow2(52 - e) : 1.0;
   long long K = 0;
   int bad = usable ? 0 : 1;
   if (usable)
     for (uint64_t j = lo + threadIdx.x; j < hi; j += blockDim.x) {
       long long k;
-      if (int_step(p[j], u, k)) K += k;
+      if (int_step(p[j], inv_u, k)) K += k;
       else bad = 1;
     }
   for (int o = 16; o > 0; o >>= 1) {
@@ -692,9 +698,9 @@ __global__ void k_sequential(const double* __restrict__ p, uint64_t n, uint64_t 
       const int cie = __shfl_sync(0xffffffffu, mine.e, t);
       const int ciclean = __shfl_sync(0xffffffffu, mine.clean, t);
       const uint64_t lo = (uint64_t)c * C, hi = min(n, lo + C);
-      if (ciclean && A >= kMinNormalScaled && ilogb(A) == cie) {
-        const double u = ldexp(1.0, cie - 52);
-        const long long a = (long long)(A / u);
+      if (ciclean && A >= kMinNormalScaled && exp_of(A) == cie) {
+        const double u = pow2(cie - 52);
+        const long long a = (long long)(A * pow2(52 - cie));
         if (a + ciK < 9007199254740991LL) {  // stays below 2^53: no binade exit
           if (lane == (int)t) {
             my_start = A;
@@ -709,13 +715,14 @@ __global__ void k_sequential(const double* __restrict__ p, uint64_t n, uint64_t 
         const double pj = j < hi ? p[j] : 0.0;
         bool done = false;
         if (A >= kMinNormalScaled) {
-          const double u = ldexp(1.0, ilogb(A) - 52);
+          const int eA = exp_of(A);
+          const double u = pow2(eA - 52), inv_u = pow2(52 - eA);
           long long k = 0;
-          const bool ok = int_step(pj, u, k);
+          const bool ok = int_step(pj, inv_u, k);
           if (__all_sync(0xffffffffu, ok)) {
             const long long incl = warp_incl_scan_ll(k);
             const long long Ksum = __shfl_sync(0xffffffffu, incl, 31);
-            const long long a = (long long)(A / u);
+            const long long a = (long long)(A * inv_u);
             if (a + Ksum < 9007199254740991LL) {
               if (j < hi) cum[j] = (double)(a + incl) * u;
               A = (double)(a + Ksum) * u;
@@ -752,14 +759,14 @@ __global__ void __launch_bounds__(kThreads) k_expand(const double* __restrict__ 
   if (!fast[blockIdx.x]) return;
   __shared__ long long warp_tot[kThreads / 32];
   const ChunkInfo ci = info[blockIdx.x];
-  const double u = ldexp(1.0, ci.e - 52);
-  long long carry = (long long)(start[blockIdx.x] / u);
+  const double u = pow2(ci.e - 52), inv_u = pow2(52 - ci.e);
+  long long carry = (long long)(start[blockIdx.x] * inv_u);
   const uint64_t lo = blockIdx.x * C, hi = min(n, lo + C);
   const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
   for (uint64_t base = lo; base < hi; base += blockDim.x) {
     const uint64_t j = base + threadIdx.x;
     long long k = 0;
-    if (j < hi) int_step(p[j], u, k);
+    if (j < hi) int_step(p[j], inv_u, k);
     const long long incl = warp_incl_scan_ll(k);
     if (l == 31) warp_tot[w] = incl;
     __syncthreads();
@@ -1139,9 +1146,7 @@ __global__ void __launch_bounds__(kThreads) k_pauli_group(const double2* __restr
   double re[kPauliGroup], im[kPauliGroup];
 #pragma unroll
   for (int t = 0; t < kPauliGroup; ++t) re[t] = im[t] = 0;
-  for (uint64_t j = lo + threadIdx.x; j < hi; j += blockDim.x) {
-    const double2 x = a[j];
-    const double2 y = xmask ? a[j ^ xmask] : x;
+  auto add = [&](uint64_t j, double2 x, double2 y) {
     const double pr = fma(y.x, x.x, y.y * x.y);
     const double pi = fma(y.x, x.y, -y.y * x.x);
 #pragma unroll
@@ -1151,6 +1156,23 @@ __global__ void __launch_bounds__(kThreads) k_pauli_group(const double2* __restr
       re[t] += neg ? -pr : pr;
       im[t] += neg ? -pi : pi;
     }
+  };
+  // four elements in flight per thread (memory-level parallelism), summed in
+  // the same per-thread order as one at a time
+  const uint64_t bd = blockDim.x;
+  uint64_t j = lo + threadIdx.x;
+  for (; j + 3 * bd < hi; j += 4 * bd) {
+    double2 x[4], y[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) x[u] = a[j + u * bd];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) y[u] = xmask ? a[(j + u * bd) ^ xmask] : x[u];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) add(j + u * bd, x[u], y[u]);
+  }
+  for (; j < hi; j += bd) {
+    const double2 x = a[j];
+    add(j, x, xmask ? a[j ^ xmask] : x);
   }
   for (int t = 0; t < T; ++t) {
     const double tr = block_sum(re[t], sh);
