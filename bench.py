@@ -119,13 +119,15 @@ class ClockSampler:
 
 def ncu_traffic(workload, plan):
     """dram__bytes_read.sum + dram__bytes_write.sum of one tile pass from the
-    committed ncu --set full capture (profiles/), per launch; None if absent."""
+    committed ncu --set full capture (profiles/r2: passes 0-5 of the current
+    random30 plan, 13-qubit tiles, 4 and 5 register bits), average per launch;
+    None if absent or another workload."""
     if workload != "random30" or plan != "tiled":
         return None
-    try:  # passes 0-3 of the current (13-qubit tile) plan, one `ncu --set full` capture; average per launch
-        with open(os.path.join(ROOT, "profiles", "r1", "ncu_full_random30_m13_passes0-3.json")) as f:
+    try:
+        with open(os.path.join(ROOT, "profiles", "r2", "ncu_full_random30_passes0-5.json")) as f:
             rows = json.load(f)
-        scale = {"Gbyte": 1e9, "Mbyte": 1e6}
+        scale = {"Gbyte": 1e9, "Mbyte": 1e6, "byte": 1.0}
         tot = [float(d["dram__bytes_read.sum"][0]) * scale[d["dram__bytes_read.sum"][1]] +
                float(d["dram__bytes_write.sum"][0]) * scale[d["dram__bytes_write.sum"][1]] for d in rows]
         return sum(tot) / len(tot)

@@ -46,7 +46,11 @@ Slots make_slots(const std::vector<uint32_t>& targets, const std::vector<uint32_
 }
 
 __device__ __forceinline__ uint64_t deposit(uint64_t g, const Slots& s) {
-  for (uint32_t k = 0; k < s.count; ++k) {
+  // static indices (unrolled to kMaxSlots, early exit): the slot positions are
+  // read from the parameter bank, no local-memory copy of the struct
+#pragma unroll
+  for (uint32_t k = 0; k < kMaxSlots; ++k) {
+    if (k >= s.count) break;
     const uint32_t p = s.pos[k];
     const uint64_t low = g & ((1ull << p) - 1);
     g = ((g >> p) << (p + 1)) | low;
@@ -349,8 +353,9 @@ __global__ void __launch_bounds__(kThreads) k_marginal_lanes(const double2* __re
   const uint32_t bh = blockIdx.y, lane = threadIdx.x & 31u, w = threadIdx.x >> 5, nw = blockDim.x >> 5;
   uint64_t fixed = 0;
   uint32_t bin = 0;
-  for (uint32_t j = 0; j < mm.kh; ++j)
-    if ((bh >> j) & 1u) {
+#pragma unroll
+  for (uint32_t j = 0; j < 12; ++j)  // static indices: no local copy of the map
+    if (j < mm.kh && ((bh >> j) & 1u)) {
       fixed |= 1ull << mm.qh[j];
       bin |= 1u << mm.rh[j];
     }
@@ -1174,7 +1179,9 @@ __global__ void __launch_bounds__(kThreads) k_pauli_group(const double2* __restr
     const double2 x = a[j];
     add(j, x, xmask ? a[j ^ xmask] : x);
   }
-  for (int t = 0; t < T; ++t) {
+#pragma unroll
+  for (int t = 0; t < kPauliGroup; ++t) {  // static indices: re/im stay in registers
+    if (t >= T) break;
     const double tr = block_sum(re[t], sh);
     const double ti = block_sum(im[t], sh);
     if (threadIdx.x == 0) partial[(uint64_t)blockIdx.x * kPauliGroup + t] = make_double2(tr, ti);

@@ -138,8 +138,13 @@ os.environ["QSB_SHARD_EXCHANGE"] = "peer"
 st = ShardedState.local(n, 3)
 os.environ.pop("QSB_SHARD_EXCHANGE")
 st.apply_circuit(Q.gen_random_circuit(n, 1, 9).gates())
-for g in (1, 2, 3):
-    gl = [gate(G.H, [n - 1 - i]) for i in range(g)]
-    timeit("k_scatter_exchange %d rank bit(s) (+ tile pass)" % g, lambda gl=gl: st.apply_circuit(gl), 32 * A,
-           h=st.handle(), sharded=True, note="exchange + the H tile pass + restore exchange (see launch list)")
+for fuse in ("1", "0"):
+    os.environ["QSB_FUSE_EXCHANGE"] = fuse
+    for g in (1, 2, 3):
+        gl = [gate(G.H, [n - 1 - i]) for i in range(g)]
+        timeit("%s %d rank bit(s)" % ("exchange-fused tile pass" if fuse == "1" else "k_scatter_exchange", g),
+               lambda gl=gl: st.apply_circuit(gl), 32 * A * (2 if fuse == "1" else 3), h=st.handle(), sharded=True,
+               note="one step = exchange + H pass + restore exchange; bytes = its HBM sweeps "
+                    "(fused: 2, separate: 3; see the launch list per kernel)")
+os.environ.pop("QSB_FUSE_EXCHANGE")
 st.close()
