@@ -46,11 +46,7 @@ Slots make_slots(const std::vector<uint32_t>& targets, const std::vector<uint32_
 }
 
 __device__ __forceinline__ uint64_t deposit(uint64_t g, const Slots& s) {
-  // static indices (unrolled to kMaxSlots, early exit): the slot positions are
-  // read from the parameter bank, no local-memory copy of the struct
-#pragma unroll
-  for (uint32_t k = 0; k < kMaxSlots; ++k) {
-    if (k >= s.count) break;
+  for (uint32_t k = 0; k < s.count; ++k) {
     const uint32_t p = s.pos[k];
     const uint64_t low = g & ((1ull << p) - 1);
     g = ((g >> p) << (p + 1)) | low;
@@ -1162,20 +1158,7 @@ __global__ void __launch_bounds__(kThreads) k_pauli_group(const double2* __restr
       im[t] += neg ? -pi : pi;
     }
   };
-  // four elements in flight per thread (memory-level parallelism), summed in
-  // the same per-thread order as one at a time
-  const uint64_t bd = blockDim.x;
-  uint64_t j = lo + threadIdx.x;
-  for (; j + 3 * bd < hi; j += 4 * bd) {
-    double2 x[4], y[4];
-#pragma unroll
-    for (int u = 0; u < 4; ++u) x[u] = a[j + u * bd];
-#pragma unroll
-    for (int u = 0; u < 4; ++u) y[u] = xmask ? a[(j + u * bd) ^ xmask] : x[u];
-#pragma unroll
-    for (int u = 0; u < 4; ++u) add(j + u * bd, x[u], y[u]);
-  }
-  for (; j < hi; j += bd) {
+  for (uint64_t j = lo + threadIdx.x; j < hi; j += blockDim.x) {
     const double2 x = a[j];
     add(j, x, xmask ? a[j ^ xmask] : x);
   }

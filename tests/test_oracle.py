@@ -167,3 +167,28 @@ def test_huge_manifest_is_the_benchmarked_circuits():
         ph = ((np.uint64(x) * k) & np.uint64((1 << n) - 1)).astype(np.float64)  # exact: x k < 2^60
         want = np.exp(2j * np.pi * ph / (1 << n)) / np.sqrt(1 << n)
         assert np.max(np.abs(row - want)) <= 1e-10
+
+
+def test_reference_cpu_arm_steps_and_configs():
+    """bench.py's CPU arm: ref_driver bench_steps runs the reference's run()
+    body (fuse_circuit + apply_gate) on one resident state, one JSON line per
+    step, and its final digest equals the reference's full run() of the same
+    gates (a small circuit; the bench uses the 30-qubit workload)."""
+    import json
+    import os
+    import subprocess
+    exe = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "oracle", "_ref", "ref_driver")
+    if not os.path.exists(exe):
+        pytest.skip("oracle/_ref/ref_driver not built (needs /root/reference at build time)")
+    env = dict(os.environ, OMP_NUM_THREADS="2")
+    n, d = 10, 3
+    out = subprocess.run([exe, "bench_steps", "random", str(n), str(d), "424242", str(2 * n), str(d), "1"],
+                         capture_output=True, text=True, env=env, timeout=300)
+    assert out.returncode == 0, out.stderr
+    rows = [json.loads(l) for l in out.stdout.splitlines() if l.startswith("{")]
+    steps = [r for r in rows if "seconds" in r]
+    assert len(steps) == d and all(r["gates"] == 2 * n and r["passes"] >= 1 for r in steps)
+    assert rows[0]["threads"] == 2 and "alloc_seconds" in rows[0]
+    from paper_2212_14201_b200 import qforge as Q
+    want = ol.checksum(ol.run_gates(n, Q.gen_random_circuit(n, d, 424242).gates()), n)
+    assert abs(rows[-1]["checksum"] - want) <= 1e-9 * want
