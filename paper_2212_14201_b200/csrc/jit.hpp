@@ -38,6 +38,7 @@ struct JitModule {
   void* mod[64] = {};   // CUmodule per device
   void* fn[64] = {};    // CUfunction per device
   int per_sm[64] = {};  // occupancy cache (for the smem size it was queried with)
+  int tma = -1;         // the kernel stages tiles with a TMA tensor copy (-1: not checked yet)
 };
 
 // CUDA source of one tile pass (kernel name `name`).

@@ -71,6 +71,13 @@ struct Gen {
   // bench checksum, bench.hpp:141-148) -- one partial per CTA into red[]
   bool reduce = false;
   int transposes_total = 0;
+  // tma: the next tile is staged by bulk copies (cp.async.bulk, one per run of
+  // the always-resident low qubits, issued by warp 0 and completing on one
+  // mbarrier) into a run-major buffer, instead of 16 per-thread LDGSTS; the
+  // first register layout is the coalesced load layout (no fused transpose)
+  bool tma = false;
+  bool use_tma = false;
+  uint32_t trank = 0, ta[5] = {}, tl[5] = {};  // tensor-map segments (tma_segments)
   // Warp-local transposes: when the qubits on thread bits >= 5 stay put, every
   // warp exchanges only its own amplitudes (under one exchange's swizzle each
   // has its own smem slot), so the barrier between the writes and the reads
@@ -101,6 +108,25 @@ struct Gen {
   }
 
   std::string fresh(const char* pfx = "v") { return pfx + std::to_string(counter++); }
+  // tile-local bit (position in S) of global qubit q
+  uint32_t tile_bit(uint32_t q) const {
+    for (uint32_t b = 0; b < tp.h.m; ++b)
+      if (tp.h.S[b] == q) return b;
+    throw RuntimeError("jit: qubit outside the tile");
+  }
+  // tile-local index offset of register slot p in the load layout
+  uint32_t tile_off(int p) const {
+    uint32_t o = 0;
+    for (int k = 0; k < R; ++k)
+      if ((p >> k) & 1) o |= 1u << tile_bit(static_cast<uint32_t>(__builtin_ctzll(tp.h.load.rs[k])));
+    return o;
+  }
+  // leading tile bits that are the global qubits 0, 1, ...: one contiguous run
+  uint32_t run_bits() const {
+    uint32_t b = 0;
+    while (b < tp.h.m && tp.h.S[b] == b) ++b;
+    return b;
+  }
   std::string coef(uint32_t i) { return "P.c[" + std::to_string(i) + "]"; }
   cd coefv(uint32_t i) const { return cd(tp.coef[i].x, tp.coef[i].y); }
   // compile-time constants, one coefficient slot per distinct value (equal
@@ -502,6 +528,9 @@ struct Gen {
     // parameters; dmask = 0 otherwise) is zero before and after the pass.  In
     // place it is skipped outright; a pass that writes elsewhere (the reset
     // fused into the first pass, an out-of-place pass) writes its zeros.
+    use_tma = tma && prefetch && !lead && early == 0 && !sparse && !from_basis && tma_segments(h, ta, tl) > 0;
+    trank = use_tma ? tma_segments(h, ta, tl) : 0;
+    if (use_tma) s << "    mbar_wait(&QMB, QPH); QPH ^= 1u;  // this tile's bulk copies (or the zero-tile arrive)\n";
     if (!xk) {
       s << "    if ((base & dmask) != dval) {\n";
       if (from_basis || h.oop) {
@@ -548,6 +577,14 @@ struct Gen {
         s << "    const double2 " << name[p] << " = make_double2(((G | " << hexll(off[p])
           << ") == basis) ? 1.0 : 0.0, 0.0);\n";
       }
+    } else if (use_tma) {
+      // run-major buffer: amplitude (thread t, slot p) of the load layout sits
+      // at its tile-local index; lanes 0-2 hold tile bits 0-2 (conflict-free)
+      for (int p = 0; p < NS; ++p) {
+        name[p] = fresh();
+        s << "    const double2 " << name[p] << " = PB[TQ + " << tile_off(p) << "u];\n";
+      }
+      if (!single_buf || transposes_total == 0) s << "    __syncthreads();\n" << kIssueNext;
     } else if (prefetch) {
       s << "    cp_async_wait_all();\n";
       if (lead) {
@@ -654,6 +691,7 @@ struct Gen {
     std::ostringstream k;
     k << "struct __align__(16) QsbCoef { double2 c[" << std::max<size_t>(1, tp.coef.size() + extra.size()) << "]; };\n";
     k << "struct QsbPeers { double2* p[16]; };\n";
+    k << "struct __align__(64) QsbTmap { unsigned long long v[16]; };\n";
     k << "extern \"C\" __global__ void __launch_bounds__(" << threads << ", " << minb << ") " << kname
       << "(double2* __restrict__ amps, double2* __restrict__ out, const unsigned long long rank_base,\n"
       << "    const unsigned long long lmask,\n"
@@ -661,8 +699,8 @@ struct Gen {
     << "    const unsigned long long xaval, const unsigned long long dmask, const unsigned long long dval,\n"
     << "    const unsigned long long imask, const unsigned long long ival,\n"
     << "    const unsigned long long tmask, const unsigned long long tval, double* __restrict__ red,\n"
-    << "    const __grid_constant__ QsbCoef P) {\n";
-    k << "  extern __shared__ double2 sm[];\n";
+    << "    const __grid_constant__ QsbCoef P, const __grid_constant__ QsbTmap TMAP) {\n";
+    k << "  extern __shared__ __align__(1024) double2 sm[];\n";
     if (reduce) k << "  double ACC = 0.0;\n";
     k << "  const unsigned tid = threadIdx.x;\n";
     k << "  const unsigned long long TL = 0ull";
@@ -725,7 +763,37 @@ struct Gen {
       }
       k << "  __syncthreads();\n";
     }
-    if (prefetch) {
+    if (use_tma) {
+      // one tensor copy per tile: dimension i of the map (built per launch by
+      // launch_tile from the same segments) spans positions [a_i, a_(i+1));
+      // the coordinates are the tile index bits between the runs
+      k << "  double2* const PB = sm + " << (tbuf && !single_buf ? (1u << h.m) : 0u) << ";\n";
+      k << "  __shared__ unsigned long long QMB;\n  unsigned QPH = 0;\n";
+      k << "  if (tid == 0) { mbar_init(&QMB, 1u); fence_mbar_init(); }\n  __syncthreads();\n";
+      k << "  const unsigned TQ = 0u";
+      for (uint32_t b = 0; b < h.t; ++b) k << " | (((tid >> " << b << ") & 1u) << " << tile_bit(h.load.tq[b]) << ")";
+      k << ";\n";
+      k << "  auto prefetch = [&](unsigned long long t) {\n"
+           "    if (tid != 0u) return;\n"
+           "    const unsigned long long tb = base_of(t) | rank_base;\n"
+           "    if ((tb & dmask) != dval) { mbar_arrive(&QMB); return; }  // zero tile: nothing to read\n"
+           "    const unsigned long long lb = tb & lmask;\n"
+           "    fence_proxy_async();  // the buffer's previous reads (ordered by the barrier) before these writes\n"
+           "    mbar_expect_tx(&QMB, " << ((1u << h.m) * 16u) << "u);\n";
+      for (uint32_t i = 0; i < trank; ++i) {
+        const uint32_t hi = i + 1 < trank ? ta[i + 1] : 64u;
+        const uint32_t span = hi - ta[i];
+        const std::string mask = span >= 32 ? "0xffffffffull" : hexll((1ull << span) - 1);
+        k << "    const int c" << i << " = (int)(((lb >> " << ta[i] << ") & " << mask << ")" << (i == 0 ? " << 1" : "")
+          << ");\n";
+      }
+      k << "    tma_load_" << trank << "d(PB, &TMAP, &QMB";
+      for (uint32_t i = 0; i < trank; ++i) k << ", c" << i;
+      k << ");\n  };\n";
+      k << "  unsigned long long kk = blockIdx.x;\n";
+      k << "  if (kk < ntiles) prefetch(expand(kk));\n";
+      k << "  for (; kk < ntiles; kk += gridDim.x) {\n";
+    } else if (prefetch) {
       // Each thread stages its own 16 amplitudes of the next tile in its own
       // shared-memory slots (slot p*T + tid: conflict-free) with cp.async, so
       // HBM reads of tile i+1 overlap the arithmetic of tile i.

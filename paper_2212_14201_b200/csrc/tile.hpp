@@ -114,6 +114,42 @@ constexpr uint32_t kTileBlobBytes = 24 * 1024;
 // Hard limit of the __grid_constant__ parameter (CUDA 12.1+: 32764 bytes).
 constexpr uint32_t kParamLimitBytes = 32 * 1024 - 256;
 
+// Bulk-copy (TMA) staging of the next tile instead of per-thread cp.async
+// (jit_gen.hpp `tma`); QSB_TMA=1/0.
+inline bool tma_enabled() {
+  const char* e = std::getenv("QSB_TMA");
+  return e && std::atoi(e) != 0;
+}
+
+// TMA tensor view of a tile: the tile qubits S split into <= 5 runs of
+// consecutive positions (a[i], l[i]) -- a tensor map whose dimension i covers
+// positions [a[i], a[i+1]) with a box of 2^l[i] (the tile's run) addresses one
+// tile per coordinate set.  Boxes are at most 256 elements per dimension (8-B
+// elements: the innermost run holds <= 128 amplitudes, the others <= 256), so
+// long runs are split.  Returns the rank, or 0 when the tile needs more than 5
+// dimensions or does not start with a 16-amplitude run.
+inline uint32_t tma_segments(const TileHeader& h, uint32_t a[5], uint32_t l[5]) {
+  uint32_t k = 0, b = 0;
+  while (b < h.m) {
+    uint32_t e = b + 1;
+    while (e < h.m && h.S[e] == h.S[e - 1] + 1) ++e;
+    uint32_t pos = h.S[b], len = e - b;
+    while (len) {
+      const uint32_t cap = k == 0 ? 7u : 8u;
+      const uint32_t take = len < cap ? len : cap;
+      if (k == 5) return 0;
+      a[k] = pos;
+      l[k] = take;
+      ++k;
+      pos += take;
+      len -= take;
+    }
+    b = e;
+  }
+  if (a[0] != 0 || l[0] < 4) return 0;
+  return k;
+}
+
 struct TileOptions {
   uint32_t m = 12;  // tile qubits
   uint32_t r = 4;   // register qubits per thread

@@ -679,6 +679,7 @@ TileOptions tile_options_from_env() {
   if (const char* e = std::getenv("QSB_PERM_STEP")) o.perm_step = std::atoi(e) != 0;
   if (const char* e = std::getenv("QSB_ABSORB_X")) o.absorb_x = std::atoi(e) != 0;
   if (const char* e = std::getenv("QSB_FOLD_PERM")) o.fold_perm = std::atoi(e) != 0;
+  o.free_load = !tma_enabled();  // a bulk-copied tile starts in the load layout
   if (const char* e = std::getenv("QSB_FREE_LOAD")) o.free_load = std::atoi(e) != 0;
   o.m = std::max<uint32_t>(8, std::min<uint32_t>(kTileMaxM, o.m));
   o.r = std::max<uint32_t>(kTileMinR, std::min<uint32_t>(kTileMaxR, o.r));
