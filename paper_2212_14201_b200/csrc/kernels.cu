@@ -630,37 +630,48 @@ __device__ __forceinline__ bool int_step(double p, double inv_u, long long& k) {
   return true;
 }
 
+// Each chunk is also split into kSub sub-chunks with their own records: a
+// chunk that cannot advance in one step (a tie, a binade exit) is walked
+// sub-chunk by sub-chunk, and only the sub-chunks that fail are replayed
+// element by element.
+constexpr int kSub = 16;
+
 __global__ void __launch_bounds__(kThreads) k_chunk_ints(const double* __restrict__ p, uint64_t n, uint64_t C,
-                                                         const double* __restrict__ E, ChunkInfo* __restrict__ info) {
-  __shared__ long long shk[kThreads / 32];
-  __shared__ int shb[kThreads / 32];
-  const uint64_t lo = blockIdx.x * C, hi = min(n, lo + C);
+                                                         const double* __restrict__ E, ChunkInfo* __restrict__ info,
+                                                         ChunkInfo* __restrict__ sub) {
+  __shared__ long long shk[kSub];
+  __shared__ int shb[kSub];
+  const uint64_t lo = blockIdx.x * C, hi = min(n, lo + C), Cs = C / kSub;
   const double est = E[blockIdx.x];
   const bool usable = est >= 2.2250738585072014e-308 * 4503599627370496.0;  // u stays normal
   const int e = usable ? exp_of(est) : 0;
   const double inv_u = usable ? pow2(52 - e) : 1.0;
-  long long K = 0;
-  int bad = usable ? 0 : 1;
-  if (usable)
-    for (uint64_t j = lo + threadIdx.x; j < hi; j += blockDim.x) {
-      long long k;
-      if (int_step(p[j], inv_u, k)) K += k;
-      else bad = 1;
-    }
-  for (int o = 16; o > 0; o >>= 1) {
-    K += __shfl_down_sync(0xffffffffu, K, o);
-    bad |= __shfl_down_sync(0xffffffffu, bad, o);
-  }
   const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
-  if (l == 0) {
-    shk[w] = K;
-    shb[w] = bad;
+  for (int sc = w; sc < kSub; sc += (int)(blockDim.x >> 5)) {  // one warp per sub-chunk
+    const uint64_t slo = min(hi, lo + sc * Cs), shi = min(hi, slo + Cs);
+    long long K = 0;
+    int bad = usable ? 0 : 1;
+    if (usable)
+      for (uint64_t jj = slo + l; jj < shi; jj += 32) {
+        long long k;
+        if (int_step(p[jj], inv_u, k)) K += k;
+        else bad = 1;
+      }
+    for (int o = 16; o > 0; o >>= 1) {
+      K += __shfl_down_sync(0xffffffffu, K, o);
+      bad |= __shfl_down_sync(0xffffffffu, bad, o);
+    }
+    if (l == 0) {
+      shk[sc] = K;
+      shb[sc] = bad;
+      sub[(uint64_t)blockIdx.x * kSub + sc] = ChunkInfo{K, e, !bad};
+    }
   }
   __syncthreads();
   if (threadIdx.x == 0) {
     long long t = 0;
     int b = 0;
-    for (int i = 0; i < (int)(blockDim.x >> 5); ++i) {
+    for (int i = 0; i < kSub; ++i) {
       t += shk[i];
       b |= shb[i];
     }
@@ -678,15 +689,66 @@ __device__ __forceinline__ long long warp_incl_scan_ll(long long v) {
 }
 
 // Phase C: one warp walks the chunks in order.  Chunk records are fetched 32
-// at a time (lane j loads chunk c0 + j, then they are broadcast in order), so
-// the walk over clean chunks is not one dependent memory round trip per chunk.
-__global__ void k_sequential(const double* __restrict__ p, uint64_t n, uint64_t C, uint32_t nc,
-                             const ChunkInfo* __restrict__ info, double* __restrict__ start,
-                             unsigned char* __restrict__ fast, double* __restrict__ cum, double* __restrict__ total,
-                             const double* __restrict__ carry) {
-  const int lane = threadIdx.x & 31;
-  double A = carry ? *carry : 0.0;  // sharded states: the previous shard's final running sum
+// at a time (lane j loads chunk c0 + j, then they are broadcast in order).  A
+// chunk that cannot advance in one exact integer step is walked through its
+// kSub sub-chunk records the same way; only a failing sub-chunk is replayed 32
+// elements at a time (integer trick per 32, true serial adds when that fails).
+// cum == nullptr: only the final sum is wanted (nothing is written per element).
+__device__ __forceinline__ bool int_advance(double& A, long long K, int e, bool clean) {
   const double kMinNormalScaled = 2.2250738585072014e-308 * 4503599627370496.0;
+  if (!clean || !(A >= kMinNormalScaled) || exp_of(A) != e) return false;
+  const long long a = (long long)(A * pow2(52 - e));
+  if (a + K >= 9007199254740991LL) return false;  // would leave the binade
+  A = (double)(a + K) * pow2(e - 52);
+  return true;
+}
+
+__device__ void replay_range(const double* __restrict__ p, uint64_t lo, uint64_t hi, double& A,
+                             double* __restrict__ cum) {
+  const int lane = threadIdx.x & 31;
+  const double kMinNormalScaled = 2.2250738585072014e-308 * 4503599627370496.0;
+  for (uint64_t j0 = lo; j0 < hi; j0 += 32) {
+    const uint64_t j = j0 + lane;
+    const double pj = j < hi ? p[j] : 0.0;
+    bool done = false;
+    if (A >= kMinNormalScaled) {
+      const int eA = exp_of(A);
+      const double u = pow2(eA - 52), inv_u = pow2(52 - eA);
+      long long k = 0;
+      const bool ok = int_step(pj, inv_u, k);
+      if (__all_sync(0xffffffffu, ok)) {
+        const long long incl = warp_incl_scan_ll(k);
+        const long long Ksum = __shfl_sync(0xffffffffu, incl, 31);
+        const long long a = (long long)(A * inv_u);
+        if (a + Ksum < 9007199254740991LL) {
+          if (cum && j < hi) cum[j] = (double)(a + incl) * u;
+          A = (double)(a + Ksum) * u;
+          done = true;
+        }
+      }
+    }
+    if (!done) {
+      double acc = A;
+      for (int t2 = 0; t2 < 32; ++t2) {
+        const double pt = __shfl_sync(0xffffffffu, pj, t2);
+        if (j0 + t2 < hi) {
+          acc = __dadd_rn(acc, pt);
+          if (cum && lane == t2) cum[j] = acc;
+        }
+      }
+      A = acc;
+    }
+  }
+}
+
+__global__ void k_sequential(const double* __restrict__ p, uint64_t n, uint64_t C, uint32_t nc,
+                             const ChunkInfo* __restrict__ info, const ChunkInfo* __restrict__ sub,
+                             double* __restrict__ start, unsigned char* __restrict__ fast,
+                             double* __restrict__ sub_start, unsigned char* __restrict__ sub_fast,
+                             double* __restrict__ cum, double* __restrict__ total, const double* __restrict__ carry) {
+  const int lane = threadIdx.x & 31;
+  const uint64_t Cs = C / kSub;
+  double A = carry ? *carry : 0.0;  // sharded states: the previous shard's final running sum
   for (uint32_t c0 = 0; c0 < nc; c0 += 32) {
     ChunkInfo mine{0, 0, 0};
     if (c0 + lane < nc) mine = info[c0 + lane];
@@ -698,50 +760,38 @@ __global__ void k_sequential(const double* __restrict__ p, uint64_t n, uint64_t 
       const long long ciK = __shfl_sync(0xffffffffu, mine.K, t);
       const int cie = __shfl_sync(0xffffffffu, mine.e, t);
       const int ciclean = __shfl_sync(0xffffffffu, mine.clean, t);
+      const double A0 = A;
+      if (int_advance(A, ciK, cie, ciclean)) {
+        if (lane == (int)t) {
+          my_start = A0;
+          my_fast = 1;
+        }
+        continue;
+      }
+      // sub-chunk walk (records of this chunk: lanes 0..kSub-1)
+      ChunkInfo sm{0, 0, 0};
+      if (lane < kSub) sm = sub[(uint64_t)c * kSub + lane];
+      double s_start = 0.0;
+      unsigned char s_fast = 0;
       const uint64_t lo = (uint64_t)c * C, hi = min(n, lo + C);
-      if (ciclean && A >= kMinNormalScaled && exp_of(A) == cie) {
-        const double u = pow2(cie - 52);
-        const long long a = (long long)(A * pow2(52 - cie));
-        if (a + ciK < 9007199254740991LL) {  // stays below 2^53: no binade exit
-          if (lane == (int)t) {
-            my_start = A;
-            my_fast = 1;
+      for (int sc = 0; sc < kSub; ++sc) {
+        const long long sK = __shfl_sync(0xffffffffu, sm.K, sc);
+        const int se = __shfl_sync(0xffffffffu, sm.e, sc);
+        const int sclean = __shfl_sync(0xffffffffu, sm.clean, sc);
+        const uint64_t slo = min(hi, lo + sc * Cs), shi = min(hi, slo + Cs);
+        const double As = A;
+        if (slo < shi && int_advance(A, sK, se, sclean)) {
+          if (lane == sc) {
+            s_start = As;
+            s_fast = 1;
           }
-          A = (double)(a + ciK) * u;
           continue;
         }
+        replay_range(p, slo, shi, A, cum);
       }
-      for (uint64_t j0 = lo; j0 < hi; j0 += 32) {
-        const uint64_t j = j0 + lane;
-        const double pj = j < hi ? p[j] : 0.0;
-        bool done = false;
-        if (A >= kMinNormalScaled) {
-          const int eA = exp_of(A);
-          const double u = pow2(eA - 52), inv_u = pow2(52 - eA);
-          long long k = 0;
-          const bool ok = int_step(pj, inv_u, k);
-          if (__all_sync(0xffffffffu, ok)) {
-            const long long incl = warp_incl_scan_ll(k);
-            const long long Ksum = __shfl_sync(0xffffffffu, incl, 31);
-            const long long a = (long long)(A * inv_u);
-            if (a + Ksum < 9007199254740991LL) {
-              if (j < hi) cum[j] = (double)(a + incl) * u;
-              A = (double)(a + Ksum) * u;
-              done = true;
-            }
-          }
-        }
-        if (!done) {
-          double acc = A;
-          for (int t2 = 0; t2 < 32; ++t2) {
-            const double pt = __shfl_sync(0xffffffffu, pj, t2);
-            if (j0 + t2 < hi) {
-              acc = __dadd_rn(acc, pt);
-              if (lane == t2) cum[j] = acc;
-            }
-          }
-          A = acc;
-        }
+      if (cum && lane < kSub) {
+        sub_start[(uint64_t)c * kSub + lane] = s_start;
+        sub_fast[(uint64_t)c * kSub + lane] = s_fast;
       }
     }
     if (c0 + lane < nc) {
@@ -752,17 +802,12 @@ __global__ void k_sequential(const double* __restrict__ p, uint64_t n, uint64_t 
   if (lane == 0) *total = A;
 }
 
-// Phase D: expand clean chunks in parallel (block per chunk).
-__global__ void __launch_bounds__(kThreads) k_expand(const double* __restrict__ p, uint64_t n, uint64_t C,
-                                                     const ChunkInfo* __restrict__ info,
-                                                     const double* __restrict__ start,
-                                                     const unsigned char* __restrict__ fast, double* __restrict__ cum) {
-  if (!fast[blockIdx.x]) return;
-  __shared__ long long warp_tot[kThreads / 32];
-  const ChunkInfo ci = info[blockIdx.x];
-  const double u = pow2(ci.e - 52), inv_u = pow2(52 - ci.e);
-  long long carry = (long long)(start[blockIdx.x] * inv_u);
-  const uint64_t lo = blockIdx.x * C, hi = min(n, lo + C);
+// Phase D: expand the chunks (or the sub-chunks) the walk advanced in one
+// integer step, in parallel (block per chunk): cum_j = (a + prefix_j) * u.
+__device__ void expand_range(const double* __restrict__ p, uint64_t lo, uint64_t hi, int e, double start,
+                             double* __restrict__ cum, long long* warp_tot) {
+  const double u = pow2(e - 52), inv_u = pow2(52 - e);
+  long long carry = (long long)(start * inv_u);
   const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
   for (uint64_t base = lo; base < hi; base += blockDim.x) {
     const uint64_t j = base + threadIdx.x;
@@ -779,6 +824,29 @@ __global__ void __launch_bounds__(kThreads) k_expand(const double* __restrict__ 
     if (j < hi) cum[j] = (double)(carry + before + incl) * u;
     carry += all;
     __syncthreads();
+  }
+}
+
+__global__ void __launch_bounds__(kThreads) k_expand(const double* __restrict__ p, uint64_t n, uint64_t C,
+                                                     const ChunkInfo* __restrict__ info,
+                                                     const ChunkInfo* __restrict__ sub,
+                                                     const double* __restrict__ start,
+                                                     const unsigned char* __restrict__ fast,
+                                                     const double* __restrict__ sub_start,
+                                                     const unsigned char* __restrict__ sub_fast,
+                                                     double* __restrict__ cum) {
+  __shared__ long long warp_tot[kThreads / 32];
+  const uint64_t lo = blockIdx.x * C, hi = min(n, lo + C);
+  if (fast[blockIdx.x]) {
+    expand_range(p, lo, hi, info[blockIdx.x].e, start[blockIdx.x], cum, warp_tot);
+    return;
+  }
+  const uint64_t Cs = C / kSub;
+  for (int sc = 0; sc < kSub; ++sc) {
+    const uint64_t k = (uint64_t)blockIdx.x * kSub + sc;
+    if (!sub_fast[k]) continue;  // replayed by the walk (cum already written)
+    const uint64_t slo = min(hi, lo + sc * Cs), shi = min(hi, slo + Cs);
+    expand_range(p, slo, shi, sub[k].e, sub_start[k], cum, warp_tot);
   }
 }
 
@@ -1561,8 +1629,11 @@ struct SamplerBuffers {
   double* S;
   double* E;
   ChunkInfo* info;
+  ChunkInfo* sub;          // kSub records per chunk
   double* start;
   unsigned char* fast;
+  double* sub_start;
+  unsigned char* sub_fast;
   double* total;
   uint64_t C;
   uint32_t nc;
@@ -1574,7 +1645,8 @@ SamplerBuffers sampler_buffers(State& s, uint64_t extra_bytes, char** extra) {
   b.C = std::max<uint64_t>(1024, N / 16384);
   b.nc = static_cast<uint32_t>((N + b.C - 1) / b.C);
   auto al = [](uint64_t x) { return (x + 255) & ~uint64_t(255); };
-  const uint64_t bytes = al(N * 8) * 2 + al(b.nc * 8) * 3 + al(b.nc * sizeof(ChunkInfo)) + al(b.nc) + 256 + al(extra_bytes);
+  const uint64_t bytes = al(N * 8) * 2 + al(b.nc * 8) * 3 + al(b.nc * sizeof(ChunkInfo)) + al(b.nc) + 256 +
+                         al(b.nc * kSub * sizeof(ChunkInfo)) + al(b.nc * kSub * 8) + al(b.nc * kSub) + al(extra_bytes);
   char* base = static_cast<char*>(s.get_scratch(bytes));
   char* q = base;
   auto take = [&](uint64_t sz) {
@@ -1589,6 +1661,9 @@ SamplerBuffers sampler_buffers(State& s, uint64_t extra_bytes, char** extra) {
   b.start = reinterpret_cast<double*>(take(b.nc * 8));
   b.info = reinterpret_cast<ChunkInfo*>(take(b.nc * sizeof(ChunkInfo)));
   b.fast = reinterpret_cast<unsigned char*>(take(b.nc));
+  b.sub = reinterpret_cast<ChunkInfo*>(take(b.nc * kSub * sizeof(ChunkInfo)));
+  b.sub_start = reinterpret_cast<double*>(take(b.nc * kSub * 8));
+  b.sub_fast = reinterpret_cast<unsigned char*>(take(b.nc * kSub));
   b.total = reinterpret_cast<double*>(take(256));
   *extra = take(extra_bytes);
   return b;
@@ -1603,11 +1678,13 @@ void build_cumulative(State& s, SamplerBuffers& b, bool exact, const double* car
   k_scan_estimate<<<1, 32, 0, s.stream>>>(b.S, b.nc, b.E, carry);
   QSB_LAUNCHED();
   if (exact) {
-    k_chunk_ints<<<b.nc, kThreads, 0, s.stream>>>(b.p, N, b.C, b.E, b.info);
+    k_chunk_ints<<<b.nc, kThreads, 0, s.stream>>>(b.p, N, b.C, b.E, b.info, b.sub);
     QSB_LAUNCHED();
-    k_sequential<<<1, 32, 0, s.stream>>>(b.p, N, b.C, b.nc, b.info, b.start, b.fast, b.cum, b.total, carry);
+    k_sequential<<<1, 32, 0, s.stream>>>(b.p, N, b.C, b.nc, b.info, b.sub, b.start, b.fast, b.sub_start, b.sub_fast,
+                                         b.cum, b.total, carry);
     QSB_LAUNCHED();
-    k_expand<<<b.nc, kThreads, 0, s.stream>>>(b.p, N, b.C, b.info, b.start, b.fast, b.cum);
+    k_expand<<<b.nc, kThreads, 0, s.stream>>>(b.p, N, b.C, b.info, b.sub, b.start, b.fast, b.sub_start, b.sub_fast,
+                                              b.cum);
     QSB_LAUNCHED();
   } else {
     k_expand_approx<<<b.nc, kThreads, 0, s.stream>>>(b.p, N, b.C, b.E, b.cum);
@@ -1672,9 +1749,10 @@ double serial_checksum(State& s) {
   QSB_LAUNCHED();
   k_scan_estimate<<<1, 32, 0, s.stream>>>(b.S, b.nc, b.E, nullptr);
   QSB_LAUNCHED();
-  k_chunk_ints<<<b.nc, kThreads, 0, s.stream>>>(b.p, N, b.C, b.E, b.info);
+  k_chunk_ints<<<b.nc, kThreads, 0, s.stream>>>(b.p, N, b.C, b.E, b.info, b.sub);
   QSB_LAUNCHED();
-  k_sequential<<<1, 32, 0, s.stream>>>(b.p, N, b.C, b.nc, b.info, b.start, b.fast, b.cum, b.total, nullptr);
+  k_sequential<<<1, 32, 0, s.stream>>>(b.p, N, b.C, b.nc, b.info, b.sub, b.start, b.fast, b.sub_start, b.sub_fast,
+                                       nullptr, b.total, nullptr);
   QSB_LAUNCHED();
   double* h = static_cast<double*>(s.get_pinned(8));
   QSB_CUDA(cudaMemcpyAsync(h, b.total, 8, cudaMemcpyDeviceToHost, s.stream));
