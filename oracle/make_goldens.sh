@@ -18,3 +18,4 @@ if [ "${GOLDEN_HUGE:-0}" = 1 ]; then
   mkdir -p "$ROOT/tests/golden/huge"
   "$ROOT/oracle/_ref/ref_driver" golden_huge "$ROOT/tests/golden/huge" random28 qft30 random30
 fi
+"$ROOT/oracle/_ref/ref_driver" golden_cut "$ROOT/tests/golden"

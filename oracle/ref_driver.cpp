@@ -20,6 +20,7 @@
 #include "circuits.hpp"
 #include "qforge/bench.hpp"
 #include "qforge/fusion.hpp"
+#include "qforge/pathsum.hpp"
 #include "qforge/simulator.hpp"
 #include "qforge/variational.hpp"
 #include "test_util.hpp"  // oracle::random_circuit (reference tests)
@@ -477,6 +478,45 @@ int bench(int argc, char** argv) {
   return 0;
 }
 
+// Cut planning and partial amplitudes (pathsum.hpp:232-459) of layered random
+// circuits: the reference's CutPlan and its partial_amplitude values for a few
+// targets, for tests/test_pathsum_gpu.py.  ref_driver golden_cut <dir>
+int golden_cut(const std::string& dir) {
+  Manifest man;
+  const std::uint32_t ns[] = {6, 9, 12, 14, 16, 20};
+  for (std::uint32_t n : ns) {
+    Program p = gen_random_circuit(n, 2, 7 + n);
+    const std::string name = "cut_random_" + std::to_string(n);
+    write_program(dir + "/" + name + ".circ", p);
+    CutPlan plan = plan_cut(p);
+    std::vector<std::string> targets;
+    Rng r(n);
+    std::vector<std::uint64_t> idx = {0, (std::uint64_t{1} << n) - 1};
+    for (int t = 0; t < 4; ++t) idx.push_back(r.below(std::uint64_t{1} << n));
+    for (auto i : idx) {
+      std::string b(n, '0');
+      for (std::uint32_t q = 0; q < n; ++q)
+        if ((i >> q) & 1) b[n - 1 - q] = '1';
+      targets.push_back(b);
+    }
+    auto amps = partial_amplitude(p, plan, targets);
+    std::vector<std::uint32_t> ca(plan.crossing_gates.begin(), plan.crossing_gates.end());
+    std::vector<double> re, im;
+    std::string ts = "[";
+    for (std::size_t t = 0; t < targets.size(); ++t) {
+      ts += std::string(t ? "," : "") + "\"" + targets[t] + "\"";
+      re.push_back(amps[targets[t]].real());
+      im.push_back(amps[targets[t]].imag());
+    }
+    man.add("{\"name\":\"" + name + "\",\"type\":\"cut\",\"n\":" + std::to_string(n) + ",\"block_a\":" +
+            qlist(plan.block_a) + ",\"block_b\":" + qlist(plan.block_b) + ",\"crossing_gates\":" + qlist(ca) +
+            ",\"branch_count\":" + std::to_string(plan.branch_count) + ",\"targets\":" + ts + "],\"re\":" +
+            dlist(re) + ",\"im\":" + dlist(im) + "}");
+  }
+  man.write(dir + "/manifest_cut.json");
+  return 0;
+}
+
 // Like-for-like CPU timing: the reference's own run() body
 // (simulator.hpp:147-159: fuse_circuit, then StateVector::apply_gate per
 // block with opts.kernel_options()) on ONE resident state, so a step excludes
@@ -609,6 +649,7 @@ int bench_config(const std::string& which) {
 
 int main(int argc, char** argv) {
   if (argc >= 2 && std::strcmp(argv[1], "bench_steps") == 0) return bench_steps(argc, argv);
+  if (argc >= 3 && std::strcmp(argv[1], "golden_cut") == 0) return golden_cut(argv[2]);
   if (argc >= 3 && std::strcmp(argv[1], "bench_config") == 0) return bench_config(argv[2]);
   if (argc >= 3 && std::strcmp(argv[1], "golden") == 0) return golden(argv[2]);
   if (argc >= 3 && std::strcmp(argv[1], "golden_big") == 0) return golden_big(argv[2]);

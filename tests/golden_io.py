@@ -83,7 +83,9 @@ def read_amps(path):
 
 
 def manifest(big=False):
-    with open(os.path.join(GOLDEN, "manifest_big.json" if big else "manifest.json")) as f:
+    """manifest.json; big=True: manifest_big.json; a string: that file."""
+    name = big if isinstance(big, str) else ("manifest_big.json" if big else "manifest.json")
+    with open(os.path.join(GOLDEN, name)) as f:
         return json.load(f)
 
 

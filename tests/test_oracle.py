@@ -192,3 +192,25 @@ def test_reference_cpu_arm_steps_and_configs():
     from paper_2212_14201_b200 import qforge as Q
     want = ol.checksum(ol.run_gates(n, Q.gen_random_circuit(n, d, 424242).gates()), n)
     assert abs(rows[-1]["checksum"] - want) <= 1e-9 * want
+
+
+def _qprogram(circ):
+    from paper_2212_14201_b200 import qforge as Q
+    p = Q.Program(circ.qubits, 0)
+    for g in circ.gates:
+        q = Q.make_gate(Q.GateKind(g.kind), g.targets, g.params)
+        q.controls = list(g.controls)
+        q.dagger = g.dagger
+        p.add(q)
+    return p
+
+
+@pytest.mark.parametrize("c", gio.cases("cut", "manifest_cut.json"), ids=lambda c: c["name"])
+def test_plan_cut_matches_reference(c):
+    """qforge.plan_cut (host combinatorics of the facade) chooses the same cut
+    as the reference's plan_cut (pathsum.hpp:232-310), exhaustive and greedy."""
+    from paper_2212_14201_b200 import qforge as Q
+    p = _qprogram(gio.read_circuit(c["name"] + ".circ"))
+    plan = Q.plan_cut(p)
+    assert plan.block_a == c["block_a"] and plan.block_b == c["block_b"]
+    assert plan.crossing_gates == c["crossing_gates"] and plan.branch_count == c["branch_count"]

@@ -101,3 +101,22 @@ def test_cut_planning_and_errors():
         assert abs(Q.single_amplitude(q, bits(i, 3)) - want[i]) <= 1e-12
     with pytest.raises(Q.ValidationError):
         Q.single_amplitude(q, "00")
+
+
+@pytest.mark.parametrize("c", __import__("golden_io").cases("cut", "manifest_cut.json"), ids=lambda c: c["name"])
+def test_partial_amplitude_matches_reference_values(c):
+    """The reference's own partial_amplitude values (ref_driver golden_cut: its
+    plan_cut + branch loop over StateVector runs) for layered random circuits,
+    6-20 qubits, against the batched GPU form with the same cut."""
+    import golden_io as gio
+    circ = gio.read_circuit(c["name"] + ".circ")
+    p = Q.Program(circ.qubits, 0)
+    for g in circ.gates:
+        q = Q.make_gate(Q.GateKind(g.kind), g.targets, g.params)
+        q.controls = list(g.controls)
+        q.dagger = g.dagger
+        p.add(q)
+    plan = Q.CutPlan(c["block_a"], c["block_b"], c["crossing_gates"], c["branch_count"])
+    got = Q.partial_amplitude(p, plan, c["targets"])
+    for t, re, im in zip(c["targets"], c["re"], c["im"]):
+        assert abs(got[t] - complex(re, im)) <= 1e-10, t
