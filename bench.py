@@ -500,6 +500,7 @@ def main():
 
     # e2e through the public API with host buffers (planning + upload + run + checksum read)
     e2e = None
+    cold_dir = None
     if not args.no_e2e:
         h2d = N.C.sizeof(N.QsGate) * G
         for _ in range(2):
@@ -618,6 +619,9 @@ def main():
     if dist.is_initialized():
         runner = None
         dist.destroy_process_group()
+    import shutil
+    for d in [jit_dir] + ([cold_dir] if cold_dir else []):
+        shutil.rmtree(d, ignore_errors=True)
     return 0
 
 

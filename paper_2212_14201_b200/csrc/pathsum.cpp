@@ -173,6 +173,9 @@ void partial_amplitude(uint32_t n, const qs_gate* gates, uint64_t count, const u
   const uint32_t big = std::max(nx[0], nx[1]);
   const uint32_t c = static_cast<uint32_t>(std::min<int64_t>(k, std::max<int64_t>(0, int64_t(cap) - big)));
   if (big > 30) throw ValidationError("each block is limited to 30 qubits");
+  if (k - static_cast<int>(c) > 40)
+    throw ValidationError("partial amplitude: " + std::to_string(k) + " crossing gates need 2^" +
+                          std::to_string(k - static_cast<int>(c)) + " sequential branch batches");
   std::unique_ptr<OwnedState> st[2] = {std::make_unique<OwnedState>(nx[0] + c, device),
                                        std::make_unique<OwnedState>(nx[1] + c, device)};
   std::vector<cd> acc(ntargets, cd(0)), part;
