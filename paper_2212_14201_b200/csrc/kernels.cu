@@ -54,6 +54,25 @@ __device__ __forceinline__ uint64_t deposit(uint64_t g, const Slots& s) {
   return g | s.force;
 }
 
+// deposit specialised for at most MS slots (fully unrolled, early exit); MS =
+// 0 is the general loop.  Per-gate kernels with <= 3 slots (1 target + 2
+// controls) use MS = 3: no loop control per amplitude group.
+template <int MS>
+__device__ __forceinline__ uint64_t deposit_n(uint64_t g, const Slots& s) {
+  if constexpr (MS == 0) {
+    return deposit(g, s);
+  } else {
+#pragma unroll
+    for (int k = 0; k < MS; ++k) {
+      if (k >= static_cast<int>(s.count)) break;
+      const uint32_t p = s.pos[k];
+      const uint64_t low = g & ((1ull << p) - 1);
+      g = ((g >> p) << (p + 1)) | low;
+    }
+    return g | s.force;
+  }
+}
+
 __device__ __forceinline__ double2 cmul(double2 a, double2 b) {
   return make_double2(fma(a.x, b.x, -a.y * b.y), fma(a.x, b.y, a.y * b.x));
 }
@@ -80,12 +99,13 @@ uint32_t grid_for(uint64_t work, int device, int per_sm = 8) {
 
 // ------------------------------------------------------------------ gates
 
+template <int MS>
 __global__ void __launch_bounds__(kThreads) k_mat1(double2* __restrict__ a, uint64_t groups, Slots sl,
                                                    uint64_t bit, double2 m0, double2 m1, double2 m2,
                                                    double2 m3) {
   for (uint64_t g = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; g < groups;
        g += (uint64_t)gridDim.x * blockDim.x) {
-    const uint64_t i0 = deposit(g, sl), i1 = i0 | bit;
+    const uint64_t i0 = deposit_n<MS>(g, sl), i1 = i0 | bit;
     const double2 x = a[i0], y = a[i1];
     a[i0] = cmv2(m0, x, m1, y);
     a[i1] = cmv2(m2, x, m3, y);
@@ -94,11 +114,12 @@ __global__ void __launch_bounds__(kThreads) k_mat1(double2* __restrict__ a, uint
 
 // skip_zero: only the bit-set half is multiplied by d1 (the target is then a
 // forced-one slot); otherwise pairs get (d0, d1).
+template <int MS>
 __global__ void __launch_bounds__(kThreads) k_diag(double2* __restrict__ a, uint64_t groups, Slots sl,
                                                    uint64_t bit, double2 d0, double2 d1, int skip_zero) {
   for (uint64_t g = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; g < groups;
        g += (uint64_t)gridDim.x * blockDim.x) {
-    const uint64_t i0 = deposit(g, sl);
+    const uint64_t i0 = deposit_n<MS>(g, sl);
     if (skip_zero) {
       a[i0] = cmul(a[i0], d1);
     } else {
@@ -108,22 +129,24 @@ __global__ void __launch_bounds__(kThreads) k_diag(double2* __restrict__ a, uint
   }
 }
 
+template <int MS>
 __global__ void __launch_bounds__(kThreads) k_flip(double2* __restrict__ a, uint64_t groups, Slots sl,
                                                    uint64_t bit) {
   for (uint64_t g = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; g < groups;
        g += (uint64_t)gridDim.x * blockDim.x) {
-    const uint64_t i0 = deposit(g, sl);
+    const uint64_t i0 = deposit_n<MS>(g, sl);
     const double2 x = __ldcs(a + i0), y = __ldcs(a + (i0 | bit));
     __stcs(a + i0, y);
     __stcs(a + (i0 | bit), x);
   }
 }
 
+template <int MS>
 __global__ void __launch_bounds__(kThreads) k_swap(double2* __restrict__ a, uint64_t groups, Slots sl,
                                                    uint64_t ba, uint64_t bb) {
   for (uint64_t g = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; g < groups;
        g += (uint64_t)gridDim.x * blockDim.x) {
-    const uint64_t base = deposit(g, sl);
+    const uint64_t base = deposit_n<MS>(g, sl);
     const double2 x = __ldcs(a + (base | ba)), y = __ldcs(a + (base | bb));
     __stcs(a + (base | ba), y);
     __stcs(a + (base | bb), x);
@@ -1226,9 +1249,32 @@ __global__ void __launch_bounds__(kThreads) k_pauli_group(const double2* __restr
       im[t] += neg ? -pi : pi;
     }
   };
-  for (uint64_t j = lo + threadIdx.x; j < hi; j += blockDim.x) {
-    const double2 x = a[j];
-    add(j, x, xmask ? a[j ^ xmask] : x);
+  if (!xmask) {
+    for (uint64_t j = lo + threadIdx.x; j < hi; j += blockDim.x) {
+      const double2 x = __ldcs(a + j);
+      add(j, x, x);
+    }
+  } else {
+    // each pair (j, j ^ x) once, from the member whose top bit of x is clear:
+    // c = conj(a[j ^ x]) a[j] contributes s_t(j) c + s_t(j ^ x) conj(c) --
+    // every amplitude is read once
+    const int hb = 63 - __clzll(xmask);
+    const uint64_t half = size >> 1;
+    const uint64_t pchunk = (half + gridDim.x - 1) / gridDim.x;
+    const uint64_t plo = blockIdx.x * pchunk, phi = min(half, plo + pchunk);
+    for (uint64_t k = plo + threadIdx.x; k < phi; k += blockDim.x) {
+      const uint64_t j = ((k >> hb) << (hb + 1)) | (k & ((1ull << hb) - 1));
+      const double2 x = __ldcs(a + j), y = __ldcs(a + (j ^ xmask));
+      const double pr = fma(y.x, x.x, y.y * x.y);
+      const double pi = fma(y.x, x.y, -y.y * x.x);
+#pragma unroll
+      for (int t = 0; t < kPauliGroup; ++t) {
+        if (t >= T) break;
+        const bool n1 = __popcll(j & zm.z[t]) & 1, n2 = __popcll((j ^ xmask) & zm.z[t]) & 1;
+        re[t] += (n1 ? -pr : pr) + (n2 ? -pr : pr);
+        im[t] += (n1 ? -pi : pi) - (n2 ? -pi : pi);
+      }
+    }
   }
 #pragma unroll
   for (int t = 0; t < kPauliGroup; ++t) {  // static indices: re/im stay in registers
@@ -1295,7 +1341,7 @@ void launch_op(State& s, const Op& op_in) {
     case OpKind::Mat1: {
       const Slots sl = make_slots(op.targets, op.controls);
       const uint64_t groups = 1ull << (n - sl.count);
-      k_mat1<<<grid_for(groups, s.device), kThreads, 0, s.stream>>>(
+      (sl.count <= 3 ? k_mat1<3> : k_mat1<0>)<<<grid_for(groups, s.device), kThreads, 0, s.stream>>>(
           s.amps, groups, sl, 1ull << op.targets[0], d2(op.m[0]), d2(op.m[1]), d2(op.m[2]), d2(op.m[3]));
       QSB_LAUNCHED();
       return;
@@ -1308,23 +1354,24 @@ void launch_op(State& s, const Op& op_in) {
       else targs.push_back(op.targets[0]);
       const Slots sl = make_slots(targs, ctrls);
       const uint64_t groups = 1ull << (n - sl.count);
-      k_diag<<<grid_for(groups, s.device), kThreads, 0, s.stream>>>(s.amps, groups, sl, 1ull << op.targets[0],
-                                                                      d2(op.m[0]), d2(op.m[1]), skip_zero ? 1 : 0);
+      (sl.count <= 3 ? k_diag<3> : k_diag<0>)<<<grid_for(groups, s.device), kThreads, 0, s.stream>>>(
+          s.amps, groups, sl, 1ull << op.targets[0], d2(op.m[0]), d2(op.m[1]), skip_zero ? 1 : 0);
       QSB_LAUNCHED();
       return;
     }
     case OpKind::Flip: {
       const Slots sl = make_slots(op.targets, op.controls);
       const uint64_t groups = 1ull << (n - sl.count);
-      k_flip<<<grid_for(groups, s.device), kThreads, 0, s.stream>>>(s.amps, groups, sl, 1ull << op.targets[0]);
+      (sl.count <= 3 ? k_flip<3> : k_flip<0>)<<<grid_for(groups, s.device), kThreads, 0, s.stream>>>(
+          s.amps, groups, sl, 1ull << op.targets[0]);
       QSB_LAUNCHED();
       return;
     }
     case OpKind::Swap: {
       const Slots sl = make_slots(op.targets, op.controls);
       const uint64_t groups = 1ull << (n - sl.count);
-      k_swap<<<grid_for(groups, s.device), kThreads, 0, s.stream>>>(s.amps, groups, sl, 1ull << op.targets[0],
-                                                                      1ull << op.targets[1]);
+      (sl.count <= 3 ? k_swap<3> : k_swap<0>)<<<grid_for(groups, s.device), kThreads, 0, s.stream>>>(
+          s.amps, groups, sl, 1ull << op.targets[0], 1ull << op.targets[1]);
       QSB_LAUNCHED();
       return;
     }
