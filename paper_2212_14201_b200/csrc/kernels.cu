@@ -209,6 +209,57 @@ __global__ void __launch_bounds__(kThreads) k_dense_g(double2* __restrict__ a, u
   }
 }
 
+// Dense block on the low qubits (every target < 12, no controls): a block
+// owns a contiguous 4096-amplitude chunk -- read and written back with
+// coalesced 512 B warp accesses through shared memory (XOR-swizzled 16 B
+// slots: conflict-free for the strided per-group reads of targets {0..K-1})
+// -- and each thread applies the block to the complete groups it is given.
+constexpr int kStageLog = 12;
+__device__ __forceinline__ uint32_t stage_slot(uint32_t i) { return i ^ ((i >> 3) & 7u); }
+
+template <int K>
+__global__ void __launch_bounds__(kThreads) k_dense_s(double2* __restrict__ a, uint64_t chunks, Slots sl,
+                                                      TargetMasks tm, const __grid_constant__ DenseM<K> M) {
+  constexpr int G = 1 << K;
+  constexpr uint32_t C = 1u << kStageLog, NG = C >> K;
+  extern __shared__ double2 st[];
+  for (uint64_t ch = blockIdx.x; ch < chunks; ch += gridDim.x) {
+    double2* base = a + (ch << kStageLog);
+    for (uint32_t i = threadIdx.x; i < C; i += blockDim.x) st[stage_slot(i)] = __ldcs(base + i);
+    __syncthreads();
+    for (uint32_t g = threadIdx.x; g < NG; g += blockDim.x) {
+      const uint32_t b0 = static_cast<uint32_t>(deposit(g, sl));
+      double2 x[G];
+      uint32_t off[G];
+#pragma unroll
+      for (int c = 0; c < G; ++c) {
+        uint32_t o = 0;
+#pragma unroll
+        for (int b = 0; b < K; ++b)
+          if ((c >> b) & 1) o |= static_cast<uint32_t>(tm.m[b]);
+        off[c] = b0 | o;
+        x[c] = st[stage_slot(off[c])];
+      }
+#pragma unroll
+      for (int r = 0; r < G; ++r) {
+        double re = 0, im = 0;
+#pragma unroll
+        for (int c = 0; c < G; ++c) {
+          const double2 m = M.m[r * G + c];
+          re = fma(m.x, x[c].x, re);
+          re = fma(-m.y, x[c].y, re);
+          im = fma(m.x, x[c].y, im);
+          im = fma(m.y, x[c].x, im);
+        }
+        st[stage_slot(off[r])] = make_double2(re, im);  // this thread's own group: no other reader
+      }
+    }
+    __syncthreads();
+    for (uint32_t i = threadIdx.x; i < C; i += blockDim.x) __stcs(base + i, st[stage_slot(i)]);
+    __syncthreads();
+  }
+}
+
 // Lane-cooperative form (K = 5, which is FP64-bound at 8 * 32 flop per
 // amplitude, and blocks on the lowest qubits, whose 2^K amplitudes are
 // contiguous): a group of 2^K consecutive lanes handles one amplitude group;
@@ -283,6 +334,48 @@ __global__ void __launch_bounds__(kThreads) k_dense_wide(double2* __restrict__ a
       a[base | off] = make_double2(re, im);
     }
     __syncthreads();
+  }
+}
+
+// Dense 64 x 64 block (K = 6, wider than the fusion cap): one warp per
+// amplitude group, the matrix transposed in shared memory (lane r reads row r
+// of column c: consecutive 16 B, conflict-free), the group's 64 inputs in a
+// per-warp slice (broadcast reads); lane l owns rows l and l + 32.
+__global__ void __launch_bounds__(kThreads) k_dense6(double2* __restrict__ a, uint64_t groups, Slots sl, TargetMasks tm,
+                                                     const double2* __restrict__ Mg) {
+  extern __shared__ double2 s6[];
+  double2* Mt = s6;                 // Mt[c * 64 + r] = M[r][c]
+  double2* xin = s6 + 64 * 64;      // 64 inputs per warp
+  for (int i = threadIdx.x; i < 64 * 64; i += blockDim.x) Mt[(i & 63) * 64 + (i >> 6)] = Mg[i];
+  __syncthreads();
+  const int w = threadIdx.x >> 5, l = threadIdx.x & 31, nw = blockDim.x >> 5;
+  double2* xw = xin + w * 64;
+  uint64_t off0 = 0, off1 = 0;
+#pragma unroll
+  for (int b = 0; b < 6; ++b) {
+    if ((l >> b) & 1) off0 |= tm.m[b];
+    if (((l + 32) >> b) & 1) off1 |= tm.m[b];
+  }
+  for (uint64_t g = (uint64_t)blockIdx.x * nw + w; g < groups; g += (uint64_t)gridDim.x * nw) {
+    const uint64_t base = deposit(g, sl);
+    xw[l] = a[base | off0];
+    xw[l + 32] = a[base | off1];
+    __syncwarp();
+    double r0 = 0, i0 = 0, r1 = 0, i1 = 0;
+    for (int c = 0; c < 64; ++c) {
+      const double2 x = xw[c], m0 = Mt[c * 64 + l], m1 = Mt[c * 64 + l + 32];
+      r0 = fma(m0.x, x.x, r0);
+      r0 = fma(-m0.y, x.y, r0);
+      i0 = fma(m0.x, x.y, i0);
+      i0 = fma(m0.y, x.x, i0);
+      r1 = fma(m1.x, x.x, r1);
+      r1 = fma(-m1.y, x.y, r1);
+      i1 = fma(m1.x, x.y, i1);
+      i1 = fma(m1.y, x.x, i1);
+    }
+    __syncwarp();
+    a[base | off0] = make_double2(r0, i0);
+    a[base | off1] = make_double2(r1, i1);
   }
 }
 
@@ -1389,6 +1482,27 @@ void launch_op(State& s, const Op& op_in) {
       // targets >= 3, 0.6-0.71 on the lowest qubits, where the lane-cooperative
       // form was slower still); QSB_DENSE_LANES=1 forces the lane-cooperative form
       const bool per_group = !std::getenv("QSB_DENSE_LANES");
+      // blocks wholly inside the low 12 qubits, without controls: staged chunks
+      // (measured at 28 qubits: K = 3 on qubits 2,1,0: 0.85 of HBM staged vs 0.60
+      // per group; K = 2 and 4 stay per group, 0.83 / 0.60 vs 0.78 / 0.51 staged)
+      const bool staged = op.controls.empty() && n >= kStageLog && K == 3 &&
+                          *std::max_element(op.targets.begin(), op.targets.end()) < static_cast<uint32_t>(kStageLog) &&
+                          *std::min_element(op.targets.begin(), op.targets.end()) < 3 && !std::getenv("QSB_NO_DENSE_STAGE");
+      if (staged) {
+        const uint64_t chunks = s.size >> kStageLog;
+        const Slots sls = make_slots(op.targets, {});
+        const uint32_t blocks = static_cast<uint32_t>(std::min<uint64_t>(chunks, num_sms(s.device) * 3ull));
+        const size_t smem = (size_t(1) << kStageLog) * sizeof(double2);
+        auto launch = [&](auto kern, auto& M) {  // 64 KiB of dynamic smem needs the opt-in
+          QSB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
+          kern<<<blocks, kThreads, smem, s.stream>>>(s.amps, chunks, sls, tm, M);
+        };
+        DenseM<3> M;
+        fill(M);
+        launch(k_dense_s<3>, M);
+        QSB_LAUNCHED();
+        return;
+      }
       switch (K) {
         case 2: { DenseM<2> M; fill(M);
           if (per_group) k_dense_g<2><<<grid_for(groups, s.device), kThreads, 0, s.stream>>>(s.amps, groups, sl, tm, M);
@@ -1414,8 +1528,17 @@ void launch_op(State& s, const Op& op_in) {
           std::vector<double2> hm(dim * dim);
           for (size_t i = 0; i < dim * dim; ++i) hm[i] = d2(op.m[i]);
           QSB_CUDA(cudaMemcpyAsync(dM, hm.data(), dim * dim * sizeof(double2), cudaMemcpyHostToDevice, s.stream));
-          const uint32_t blocks = static_cast<uint32_t>(std::min<uint64_t>(groups, num_sms(s.device) * 8ull));
-          k_dense_wide<<<blocks, kThreads, dim * sizeof(double2), s.stream>>>(s.amps, groups, sl, tm, K, dM);
+          if (K == 6) {
+            const size_t smem6 = (64 * 64 + 64 * (kThreads / 32)) * sizeof(double2);
+            QSB_CUDA(cudaFuncSetAttribute(k_dense6, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                          static_cast<int>(smem6)));
+            const uint32_t b6 = static_cast<uint32_t>(
+                std::min<uint64_t>((groups + kThreads / 32 - 1) / (kThreads / 32), num_sms(s.device) * 3ull));
+            k_dense6<<<b6, kThreads, smem6, s.stream>>>(s.amps, groups, sl, tm, dM);
+          } else {
+            const uint32_t blocks = static_cast<uint32_t>(std::min<uint64_t>(groups, num_sms(s.device) * 8ull));
+            k_dense_wide<<<blocks, kThreads, dim * sizeof(double2), s.stream>>>(s.amps, groups, sl, tm, K, dM);
+          }
           QSB_LAUNCHED();
           QSB_CUDA(cudaStreamSynchronize(s.stream));  // the host staging vector must outlive the copy
           return;
