@@ -53,6 +53,8 @@ WORKLOADS = {
 # reference results of the unmodified qforge run() for these workloads
 # (oracle/_ref/ref_driver golden_huge; tests/test_bench_parity.py)
 HUGE = os.path.join(ROOT, "tests", "golden", "huge", "manifest_huge.json")
+# in-place stream over a 64 MiB (L2-resident) buffer on this pool's B200s, GB/s
+L2_STREAM_GBS = 9353.3
 
 
 def peaks():
@@ -394,13 +396,16 @@ def roofline_of(m, runner, plan, workload, peak, peak_kind):
     CUDA-event time, from the per-launch profile of the same step."""
     per, by, kinds = m["per"], m["bytes"], m["kinds"]
     full_b = 32.0 * runner.shard_amps
+    l2_resident = 16.0 * runner.shard_amps <= 64 * 2 ** 20  # SURVEY 8(d): 20q (16 MiB) sits in the 126 MB L2
+    if l2_resident:  # in-place read-modify-write stream over a 64 MiB L2-resident buffer (tools/l2_probe.cu)
+        peak, peak_kind = L2_STREAM_GBS, "measured L2-resident stream (profiles/r2/l2_probe.jsonl)"
     full = [(t, b) for t, b, k in zip(per, by, kinds) if k != 2 and b >= full_b * 0.999 and t > 0]
     t_full = sum(t for t, _ in full)
     avg = t_full / len(full) if full else 0.0
     achieved = (full_b / (avg / 1e3) / 1e9) if avg else 0.0
     step_bytes = sum(b for b, k in zip(by, kinds) if k != 2)
     prof_ms = sum(per)
-    r = {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
+    r = {"bound": "l2" if l2_resident else "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
          "frac": round(achieved / peak, 4) if peak else None,
          "traffic": ncu_traffic(workload, plan) if not runner.sharded else None,
          "traffic_source": "dram__bytes_read.sum + dram__bytes_write.sum per launch, ncu --set full capture "
