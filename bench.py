@@ -620,7 +620,7 @@ def main():
         }
         if config4 is not None:
             line["config4"] = config4
-        print(json.dumps(line))
+        emit(line)
     if dist.is_initialized():
         runner = None
         dist.destroy_process_group()
@@ -671,7 +671,7 @@ def run_reference(args):
     per = 2 * n if gen == "random" else 60
     rows, err = ref_steps(args.workload, per, args.warmup + args.steps)
     if rows is None:
-        print(json.dumps({"impl": "reference", "unavailable": err}))
+        emit({"impl": "reference", "unavailable": err})
         return 0
     alloc, st = rows
     timed = st[args.warmup:]
@@ -696,9 +696,20 @@ def run_reference(args):
                                    "state (fuse_circuit + apply_gate, simulator.hpp:147-159)" % gates},
         "e2e": {"value": round(value, 4), "unit": "gates/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
-    print(json.dumps(line))
+    emit(line)
     return 0
 
 
+def emit(line):
+    """The one JSON line of the bench contract, on the process's real stdout
+    (library / NCCL banners printed during the run go to stderr, see below)."""
+    os.write(_REAL_STDOUT, (json.dumps(line) + "\n").encode())
+
+
 if __name__ == "__main__":
+    # stdout carries exactly one line: everything else written to fd 1 during
+    # the run (NCCL's version banner, library diagnostics) is sent to stderr
+    sys.stdout.flush()
+    _REAL_STDOUT = os.dup(1)
+    os.dup2(2, 1)
     sys.exit(main())
