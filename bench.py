@@ -405,12 +405,18 @@ def roofline_of(m, runner, plan, workload, peak, peak_kind):
     achieved = (full_b / (avg / 1e3) / 1e9) if avg else 0.0
     step_bytes = sum(b for b, k in zip(by, kinds) if k != 2)
     prof_ms = sum(per)
+    no_full = not full  # e.g. GHZ from |0...0>: every pass visits only the non-zero tiles
+    if no_full and prof_ms:
+        achieved = step_bytes / (m["ms_per_step"] / 1e3) / 1e9
     r = {"bound": "l2" if l2_resident else "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
          "frac": round(achieved / peak, 4) if peak else None,
          "traffic": ncu_traffic(workload, plan) if not runner.sharded else None,
          "traffic_source": "dram__bytes_read.sum + dram__bytes_write.sum per launch, ncu --set full capture "
                            "committed under profiles/ (not measured in this run)",
-         "kernel": "qsb_tile_* full passes (per-pass NVRTC sm_100a)" if plan == "tiled" else "per-gate kernels",
+         "kernel": ("qsb_tile_* " + ("launches of the step (no pass visits every tile: runs from a basis state "
+                                     "skip zero tiles); achieved = their algorithmic bytes / the step" if no_full
+                                     else "full passes") + " (per-pass NVRTC sm_100a)") if plan == "tiled"
+                   else "per-gate kernels",
          "algorithmic_bytes_per_launch": full_b, "launches_per_step": len(per), "full_pass_launches": len(full),
          "avg_launch_ms": round(avg, 4), "peak_kind": peak_kind,
          # share of the profiled step spent in the full passes, and the profiled
