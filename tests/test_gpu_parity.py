@@ -568,3 +568,17 @@ def test_per_gate_dense_kernels_match_oracle(targets):
     sv.apply_gate(g)
     want = ol.run_gates(n, [g], state=a0.copy())
     assert np.max(np.abs(sv.amplitudes() - want)) <= 1e-10
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("n", [1, 2, 5, 9, 13])
+def test_serial_checksum_and_sampler_small_states(n):
+    """States smaller than one scan chunk (1024 amplitudes) and than one
+    sub-chunk: the serial digest and the exact sampler still match the
+    reference loops bitwise."""
+    gates = Q.gen_random_circuit(n, 3, 5).gates() if n > 1 else [Q.make_gate(Q.GateKind.RY, [0], [0.7])]
+    sv = Q.StateVector(n)
+    sv.apply_circuit(gates)
+    a = sv.amplitudes()
+    assert sv.checksum_serial() == ol.checksum(a, n)
+    assert np.array_equal(sv.sample_seeded(3, 2000, exact=True), ol.sample_seeded(a, n, 3, 2000))

@@ -49,22 +49,23 @@ def test_partial_amplitude_matches_full_state(n, gates, two, seed):
 def test_partial_amplitude_branch_chunks():
     """More branch variables than fit the batch: the remaining ones are fixed
     per chunk (batch_qubits small) -- same amplitudes.  A fixed cut (qubits
-    0-7 | 8-15) with 6 crossing CZ/CNOTs."""
+    0-7 | 8-15) with 4 crossing CZ/CNOTs (each chunk of fixed variables is its
+    own plan, so the test keeps the chunk count small)."""
     n = 16
     p = random_cut_circuit(n, 100, 9, 0)
     rng = np.random.default_rng(21)
     body = list(p.body)
-    for j in range(6):
+    for j in range(4):
         a, b = int(rng.integers(8)), 8 + int(rng.integers(8))
         g = Q.make_gate(Q.GateKind.CZ if j % 2 else Q.GateKind.CNOT, [a, b] if j % 3 else [b, a])
         body.insert(15 * (j + 1), g)
     p.body = body
     cross = [i for i, g in enumerate(p.body) if len(g.targets) == 2 and (g.targets[0] < 8) != (g.targets[1] < 8)]
     plan = Q.CutPlan(list(range(8)), list(range(8, 16)), cross, 1 << len(cross))
-    assert len(cross) == 6
+    assert len(cross) == 4
     want = ol.run_gates(n, p.gates())
     targets = [bits(i, n) for i in (0, 5, 777, (1 << n) - 3)]
-    for bq in (0, 8 + 1, 8 + 2):  # blocks of 8: all 6, 1 or 2 branch qubits batched, the rest chunked
+    for bq in (0, 8 + 1, 8 + 2):  # blocks of 8: all 4, 1 or 2 branch qubits batched, the rest chunked
         got = Q.partial_amplitude(p, plan, targets, batch_qubits=bq)
         for t in targets:
             assert abs(got[t] - want[int(t, 2)]) <= 1e-10, (bq, t)
@@ -120,3 +121,30 @@ def test_partial_amplitude_matches_reference_values(c):
     got = Q.partial_amplitude(p, plan, c["targets"])
     for t, re, im in zip(c["targets"], c["re"], c["im"]):
         assert abs(got[t] - complex(re, im)) <= 1e-10, t
+
+
+def test_partial_amplitude_edge_cases():
+    """No crossing gates (one branch), empty target list, duplicate targets,
+    one-qubit blocks, an empty program."""
+    p = Q.Program(2, 0)
+    p.add(Q.make_gate(Q.GateKind.H, [0]))
+    p.add(Q.make_gate(Q.GateKind.RY, [1], [0.3]))
+    plan = Q.plan_cut(p)
+    assert plan.crossing_gates == [] and plan.branch_count == 1
+    want = ol.run_gates(2, p.gates())
+    got = Q.partial_amplitude(p, plan, ["00", "01", "10", "11", "01"])
+    assert set(got) == {"00", "01", "10", "11"}
+    for t in got:
+        assert abs(got[t] - want[int(t, 2)]) <= 1e-12
+    assert Q.partial_amplitude(p, plan, []) == {}
+    e = Q.Program(3, 0)
+    pe = Q.plan_cut(e)
+    got = Q.partial_amplitude(e, pe, ["000", "101"])
+    assert abs(got["000"] - 1) <= 1e-15 and abs(got["101"]) <= 1e-15
+    c = Q.Program(2, 0)
+    c.add(Q.make_gate(Q.GateKind.H, [0]))
+    c.add(Q.make_gate(Q.GateKind.CNOT, [0, 1]))
+    pc = Q.plan_cut(c)
+    assert pc.branch_count == 2
+    got = Q.partial_amplitude(c, pc, ["00", "11", "01"])
+    assert abs(got["00"] - 2 ** -0.5) <= 1e-12 and abs(got["11"] - 2 ** -0.5) <= 1e-12 and abs(got["01"]) <= 1e-12
