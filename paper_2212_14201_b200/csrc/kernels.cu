@@ -105,7 +105,7 @@ __global__ void __launch_bounds__(kThreads) k_mat1(double2* __restrict__ a, uint
                                                    double2 m3) {
   for (uint64_t g = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; g < groups;
        g += (uint64_t)gridDim.x * blockDim.x) {
-    const uint64_t i0 = deposit_n<MS>(g, sl), i1 = i0 | bit;
+    const uint64_t i0 = deposit_n<MS>(g, sl), i1 = i0 ^ bit;  // bit: the target (or a SWAP's two bits)
     const double2 x = a[i0], y = a[i1];
     a[i0] = cmv2(m0, x, m1, y);
     a[i1] = cmv2(m2, x, m3, y);
@@ -1455,16 +1455,24 @@ void launch_op(State& s, const Op& op_in) {
     case OpKind::Flip: {
       const Slots sl = make_slots(op.targets, op.controls);
       const uint64_t groups = 1ull << (n - sl.count);
-      (sl.count <= 3 ? k_flip<3> : k_flip<0>)<<<grid_for(groups, s.device), kThreads, 0, s.stream>>>(
-          s.amps, groups, sl, 1ull << op.targets[0]);
+      // the 2x2 kernel with [[0,1],[1,0]] (exact: the products by 0 and 1 are
+      // exact): measured 0.89 of HBM where the plain swap kernel reached 0.72
+      const double2 z = make_double2(0, 0), o = make_double2(1, 0);
+      (sl.count <= 3 ? k_mat1<3> : k_mat1<0>)<<<grid_for(groups, s.device), kThreads, 0, s.stream>>>(
+          s.amps, groups, sl, 1ull << op.targets[0], z, o, o, z);
       QSB_LAUNCHED();
       return;
     }
     case OpKind::Swap: {
       const Slots sl = make_slots(op.targets, op.controls);
       const uint64_t groups = 1ull << (n - sl.count);
-      (sl.count <= 3 ? k_swap<3> : k_swap<0>)<<<grid_for(groups, s.device), kThreads, 0, s.stream>>>(
-          s.amps, groups, sl, 1ull << op.targets[0], 1ull << op.targets[1]);
+      // as the 2x2 kernel on the pairs (.. a=1 b=0 ..) <-> (.. a=0 b=1 ..): i0
+      // has bit a forced, i1 = i0 ^ (a | b); [[0,1],[1,0]] is exact (see Flip)
+      Slots sw = sl;
+      sw.force |= 1ull << op.targets[0];
+      const double2 z = make_double2(0, 0), o = make_double2(1, 0);
+      (sw.count <= 3 ? k_mat1<3> : k_mat1<0>)<<<grid_for(groups, s.device), kThreads, 0, s.stream>>>(
+          s.amps, groups, sw, (1ull << op.targets[0]) | (1ull << op.targets[1]), z, o, o, z);
       QSB_LAUNCHED();
       return;
     }
