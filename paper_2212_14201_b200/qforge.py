@@ -400,17 +400,35 @@ def _trailing_measure_form(p):
     return True
 
 
+_KEY_BITS = 12
+_KEY_TABLE = {}
+
+
+def _key_table(width):
+    t = _KEY_TABLE.get(width)
+    if t is None:
+        t = _KEY_TABLE[width] = [format(i, "0%db" % width) for i in range(1 << width)]
+    return t
+
+
 def counts_from_indices(indices, measures, cbits):
-    """Key construction of run() (simulator.hpp:170-177)."""
+    """Key construction of run() (simulator.hpp:170-177): c[0] rightmost.
+    Keys are assembled from 12-bit string tables (one lookup per 12 classical
+    bits) instead of one format() per distinct outcome."""
     idx = np.asarray(indices, dtype=np.uint64)
     keyint = np.zeros(idx.shape, dtype=np.uint64)
     for m in measures:
         keyint |= ((idx >> np.uint64(m.qubit)) & np.uint64(1)) << np.uint64(m.cbit)
     vals, cnt = np.unique(keyint, return_counts=True)
-    out = {}
-    for v, c in zip(vals.tolist(), cnt.tolist()):
-        out[format(v, "0%db" % cbits) if cbits else ""] = c
-    return out
+    if not cbits:
+        return {"": int(cnt.sum())} if len(vals) else {}
+    parts = []  # most significant chunk first
+    for lo in range(0, cbits, _KEY_BITS):
+        w = min(_KEY_BITS, cbits - lo)
+        tab = _key_table(w)
+        parts.insert(0, [tab[v] for v in ((vals >> np.uint64(lo)) & np.uint64((1 << w) - 1)).astype(np.int64).tolist()])
+    keys = parts[0] if len(parts) == 1 else ["".join(k) for k in zip(*parts)]
+    return dict(zip(keys, cnt.tolist()))
 
 
 def run_plan_mode(opts):
