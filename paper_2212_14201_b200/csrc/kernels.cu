@@ -91,6 +91,19 @@ __device__ __forceinline__ double2 cmv2(double2 m0, double2 a, double2 m1, doubl
 // |a|^2 exactly as g++ contracts std::norm: fma(re, re, im*im).
 __device__ __forceinline__ double norm_ref(double2 a) { return __fma_rn(a.x, a.x, __dmul_rn(a.y, a.y)); }
 
+// 32 B (two adjacent amplitudes) per instruction: sm_100's 256-bit global
+// accesses (SASS LDG.E.ENL2.256 / STG.E.ENL2.256).  Used where an amplitude
+// pair differs in qubit 0, so one thread's accesses fill whole sectors.
+__device__ __forceinline__ void ld_pair(const double2* p, double2& x, double2& y) {
+  asm volatile("ld.global.v4.f64 {%0, %1, %2, %3}, [%4];"
+               : "=d"(x.x), "=d"(x.y), "=d"(y.x), "=d"(y.y)
+               : "l"(p));
+}
+__device__ __forceinline__ void st_pair(double2* p, double2 x, double2 y) {
+  asm volatile("st.global.v4.f64 [%0], {%1, %2, %3, %4};" ::"l"(p), "d"(x.x), "d"(x.y), "d"(y.x), "d"(y.y)
+               : "memory");
+}
+
 uint32_t grid_for(uint64_t work, int device, int per_sm = 8) {
   const uint64_t blocks = (work + kThreads - 1) / kThreads;
   const uint64_t cap = static_cast<uint64_t>(num_sms(device)) * per_sm;
@@ -112,6 +125,19 @@ __global__ void __launch_bounds__(kThreads) k_mat1(double2* __restrict__ a, uint
   }
 }
 
+// Target qubit 0: each pair is 32 contiguous bytes, one 256-bit load / store.
+template <int MS>
+__global__ void __launch_bounds__(kThreads) k_mat1_q0(double2* __restrict__ a, uint64_t groups, Slots sl, double2 m0,
+                                                      double2 m1, double2 m2, double2 m3) {
+  for (uint64_t g = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; g < groups;
+       g += (uint64_t)gridDim.x * blockDim.x) {
+    const uint64_t i0 = deposit_n<MS>(g, sl);
+    double2 x, y;
+    ld_pair(a + i0, x, y);
+    st_pair(a + i0, cmv2(m0, x, m1, y), cmv2(m2, x, m3, y));
+  }
+}
+
 // skip_zero: only the bit-set half is multiplied by d1 (the target is then a
 // forced-one slot); otherwise pairs get (d0, d1).
 template <int MS>
@@ -126,6 +152,19 @@ __global__ void __launch_bounds__(kThreads) k_diag(double2* __restrict__ a, uint
       a[i0] = cmul(a[i0], d0);
       a[i0 | bit] = cmul(a[i0 | bit], d1);
     }
+  }
+}
+
+// Diagonal on qubit 0 (both entries applied): one 256-bit access per pair.
+template <int MS>
+__global__ void __launch_bounds__(kThreads) k_diag_q0(double2* __restrict__ a, uint64_t groups, Slots sl, double2 d0,
+                                                      double2 d1) {
+  for (uint64_t g = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; g < groups;
+       g += (uint64_t)gridDim.x * blockDim.x) {
+    const uint64_t i0 = deposit_n<MS>(g, sl);
+    double2 x, y;
+    ld_pair(a + i0, x, y);
+    st_pair(a + i0, cmul(x, d0), cmul(y, d1));
   }
 }
 
@@ -166,6 +205,8 @@ template <int K>
 struct DenseM {
   double2 m[1 << (2 * K)];
 };
+template <int K>
+constexpr int dense_k(const DenseM<K>*) { return K; }
 
 // Dense 2^K x 2^K block, K <= 4: one thread per amplitude group.  Consecutive
 // lanes take consecutive groups, so every load / store instruction of a warp
@@ -173,38 +214,50 @@ struct DenseM {
 // registers and each output row is an FMA chain with constant-bank
 // coefficients (same summation order as the reference's row dot product,
 // statevector.hpp:69-106).
-template <int K>
+// P >= 0: the block's bit P is qubit 0 (tm.m[P] == 1), so x[c] and
+// x[c | 1 << P] are adjacent and travel as one 256-bit access.
+template <int K, int P = -1>
 __global__ void __launch_bounds__(kThreads) k_dense_g(double2* __restrict__ a, uint64_t groups, Slots sl,
                                                       TargetMasks tm, const __grid_constant__ DenseM<K> M) {
   constexpr int G = 1 << K;
+  auto offset = [&](int c) {
+    uint64_t off = 0;
+#pragma unroll
+    for (int b = 0; b < K; ++b)
+      if ((c >> b) & 1) off |= tm.m[b];
+    return off;
+  };
+  auto row = [&](int r, const double2* x) {
+    double re = 0, im = 0;
+#pragma unroll
+    for (int c = 0; c < G; ++c) {
+      const double2 m = M.m[r * G + c];
+      re = fma(m.x, x[c].x, re);
+      re = fma(-m.y, x[c].y, re);
+      im = fma(m.x, x[c].y, im);
+      im = fma(m.y, x[c].x, im);
+    }
+    return make_double2(re, im);
+  };
   for (uint64_t g = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; g < groups;
        g += (uint64_t)gridDim.x * blockDim.x) {
     const uint64_t base = deposit(g, sl);
     double2 x[G];
 #pragma unroll
     for (int c = 0; c < G; ++c) {
-      uint64_t off = 0;
-#pragma unroll
-      for (int b = 0; b < K; ++b)
-        if ((c >> b) & 1) off |= tm.m[b];
-      x[c] = __ldcs(a + (base | off));
+      if constexpr (P < 0) {
+        x[c] = __ldcs(a + (base | offset(c)));
+      } else if (!((c >> P) & 1)) {
+        ld_pair(a + (base | offset(c)), x[c], x[c | (1 << P)]);
+      }
     }
 #pragma unroll
     for (int r = 0; r < G; ++r) {
-      double re = 0, im = 0;
-#pragma unroll
-      for (int c = 0; c < G; ++c) {
-        const double2 m = M.m[r * G + c];
-        re = fma(m.x, x[c].x, re);
-        re = fma(-m.y, x[c].y, re);
-        im = fma(m.x, x[c].y, im);
-        im = fma(m.y, x[c].x, im);
+      if constexpr (P < 0) {
+        __stcs(a + (base | offset(r)), row(r, x));
+      } else if (!((r >> P) & 1)) {
+        st_pair(a + (base | offset(r)), row(r, x), row(r | (1 << P), x));
       }
-      uint64_t off = 0;
-#pragma unroll
-      for (int b = 0; b < K; ++b)
-        if ((r >> b) & 1) off |= tm.m[b];
-      __stcs(a + (base | off), make_double2(re, im));
     }
   }
 }
@@ -301,6 +354,29 @@ __global__ void __launch_bounds__(kThreads) k_dense(double2* __restrict__ a, uin
     __syncwarp();
     if (valid) __stcs(a + idx, make_double2(re, im));
   }
+}
+
+bool pair256_enabled() { return !std::getenv("QSB_NO_PAIR256"); }
+
+// k_dense_g with the pair bit P = pbit (qubit 0 at block bit P), or unpaired.
+template <int K, int P>
+void launch_dense_g(const State& s, uint64_t groups, const Slots& sl, const TargetMasks& tm, const DenseM<K>& M,
+                    int pbit) {
+  if constexpr (P < 0) {
+    k_dense_g<K><<<grid_for(groups, s.device), kThreads, 0, s.stream>>>(s.amps, groups, sl, tm, M);
+  } else {
+    if (pbit == P) k_dense_g<K, P><<<grid_for(groups, s.device), kThreads, 0, s.stream>>>(s.amps, groups, sl, tm, M);
+    else launch_dense_g<K, P - 1>(s, groups, sl, tm, M, pbit);
+  }
+}
+
+void launch_mat1(const State& s, uint64_t groups, const Slots& sl, uint64_t bit, double2 m0, double2 m1, double2 m2,
+                 double2 m3) {
+  const uint32_t grid = grid_for(groups, s.device);
+  if (bit == 1 && pair256_enabled())
+    (sl.count <= 3 ? k_mat1_q0<3> : k_mat1_q0<0>)<<<grid, kThreads, 0, s.stream>>>(s.amps, groups, sl, m0, m1, m2, m3);
+  else
+    (sl.count <= 3 ? k_mat1<3> : k_mat1<0>)<<<grid, kThreads, 0, s.stream>>>(s.amps, groups, sl, bit, m0, m1, m2, m3);
 }
 
 // Dense block with K > 5: one group per 2^K threads spread over the block,
@@ -1434,8 +1510,7 @@ void launch_op(State& s, const Op& op_in) {
     case OpKind::Mat1: {
       const Slots sl = make_slots(op.targets, op.controls);
       const uint64_t groups = 1ull << (n - sl.count);
-      (sl.count <= 3 ? k_mat1<3> : k_mat1<0>)<<<grid_for(groups, s.device), kThreads, 0, s.stream>>>(
-          s.amps, groups, sl, 1ull << op.targets[0], d2(op.m[0]), d2(op.m[1]), d2(op.m[2]), d2(op.m[3]));
+      launch_mat1(s, groups, sl, 1ull << op.targets[0], d2(op.m[0]), d2(op.m[1]), d2(op.m[2]), d2(op.m[3]));
       QSB_LAUNCHED();
       return;
     }
@@ -1447,8 +1522,12 @@ void launch_op(State& s, const Op& op_in) {
       else targs.push_back(op.targets[0]);
       const Slots sl = make_slots(targs, ctrls);
       const uint64_t groups = 1ull << (n - sl.count);
-      (sl.count <= 3 ? k_diag<3> : k_diag<0>)<<<grid_for(groups, s.device), kThreads, 0, s.stream>>>(
-          s.amps, groups, sl, 1ull << op.targets[0], d2(op.m[0]), d2(op.m[1]), skip_zero ? 1 : 0);
+      if (!skip_zero && op.targets[0] == 0 && pair256_enabled())
+        (sl.count <= 3 ? k_diag_q0<3> : k_diag_q0<0>)<<<grid_for(groups, s.device), kThreads, 0, s.stream>>>(
+            s.amps, groups, sl, d2(op.m[0]), d2(op.m[1]));
+      else
+        (sl.count <= 3 ? k_diag<3> : k_diag<0>)<<<grid_for(groups, s.device), kThreads, 0, s.stream>>>(
+            s.amps, groups, sl, 1ull << op.targets[0], d2(op.m[0]), d2(op.m[1]), skip_zero ? 1 : 0);
       QSB_LAUNCHED();
       return;
     }
@@ -1458,8 +1537,7 @@ void launch_op(State& s, const Op& op_in) {
       // the 2x2 kernel with [[0,1],[1,0]] (exact: the products by 0 and 1 are
       // exact): measured 0.89 of HBM where the plain swap kernel reached 0.72
       const double2 z = make_double2(0, 0), o = make_double2(1, 0);
-      (sl.count <= 3 ? k_mat1<3> : k_mat1<0>)<<<grid_for(groups, s.device), kThreads, 0, s.stream>>>(
-          s.amps, groups, sl, 1ull << op.targets[0], z, o, o, z);
+      launch_mat1(s, groups, sl, 1ull << op.targets[0], z, o, o, z);
       QSB_LAUNCHED();
       return;
     }
@@ -1489,13 +1567,16 @@ void launch_op(State& s, const Op& op_in) {
       // thread per group (measured on B200, 28 qubits: 0.88-0.93 of HBM for
       // targets >= 3, 0.6-0.71 on the lowest qubits, where the lane-cooperative
       // form was slower still); QSB_DENSE_LANES=1 forces the lane-cooperative form
-      const bool per_group = !std::getenv("QSB_DENSE_LANES");
+      const char* form_env = std::getenv("QSB_DENSE_FORM");  // g | lanes | s: force one form
+      const std::string form = form_env ? form_env : "";
+      bool per_group = !std::getenv("QSB_DENSE_LANES");
       // blocks wholly inside the low 12 qubits, without controls: staged chunks
       // (measured at 28 qubits: K = 3 on qubits 2,1,0: 0.85 of HBM staged vs 0.60
       // per group; K = 2 and 4 stay per group, 0.83 / 0.60 vs 0.78 / 0.51 staged)
       const bool staged = op.controls.empty() && n >= kStageLog && K == 3 &&
                           *std::max_element(op.targets.begin(), op.targets.end()) < static_cast<uint32_t>(kStageLog) &&
-                          *std::min_element(op.targets.begin(), op.targets.end()) < 3 && !std::getenv("QSB_NO_DENSE_STAGE");
+                          *std::min_element(op.targets.begin(), op.targets.end()) < 3 && !std::getenv("QSB_NO_DENSE_STAGE") &&
+                          (form.empty() || form == "s");
       if (staged) {
         const uint64_t chunks = s.size >> kStageLog;
         const Slots sls = make_slots(op.targets, {});
@@ -1511,23 +1592,34 @@ void launch_op(State& s, const Op& op_in) {
         QSB_LAUNCHED();
         return;
       }
+      if (form == "g") per_group = true;
+      if (form == "lanes") per_group = false;
+      // qubit 0 among the targets: pairs as 256-bit accesses
+      int pbit = -1;
+      for (int b = 0; b < K; ++b)
+        if (tm.m[b] == 1) pbit = b;
+      if (!pair256_enabled()) pbit = -1;
+      auto launch_g = [&](auto& M) {
+        constexpr int KK = dense_k(static_cast<std::decay_t<decltype(M)>*>(nullptr));
+        launch_dense_g<KK, KK - 1>(s, groups, sl, tm, M, pbit);
+      };
       switch (K) {
         case 2: { DenseM<2> M; fill(M);
-          if (per_group) k_dense_g<2><<<grid_for(groups, s.device), kThreads, 0, s.stream>>>(s.amps, groups, sl, tm, M);
+          if (per_group) launch_g(M);
           else k_dense<2><<<grid_for(groups << K, s.device), kThreads, 0, s.stream>>>(s.amps, groups, sl, tm, M);
           break; }
         case 3: { DenseM<3> M; fill(M);
-          if (per_group) k_dense_g<3><<<grid_for(groups, s.device), kThreads, 0, s.stream>>>(s.amps, groups, sl, tm, M);
+          if (per_group) launch_g(M);
           else k_dense<3><<<grid_for(groups << K, s.device), kThreads, 0, s.stream>>>(s.amps, groups, sl, tm, M);
           break; }
         case 4: { static thread_local DenseM<4> M; fill(M);
-          if (per_group) k_dense_g<4><<<grid_for(groups, s.device), kThreads, 0, s.stream>>>(s.amps, groups, sl, tm, M);
+          if (per_group) launch_g(M);
           else k_dense<4><<<grid_for(groups << K, s.device), kThreads, 0, s.stream>>>(s.amps, groups, sl, tm, M);
           break; }
         case 5: {
           static thread_local DenseM<5> M;  // 16 KiB: off the stack; the launch copies it
           fill(M);
-          if (per_group) k_dense_g<5><<<grid_for(groups, s.device), kThreads, 0, s.stream>>>(s.amps, groups, sl, tm, M);
+          if (per_group) launch_g(M);
           else k_dense<5><<<grid_for(groups << K, s.device, 4), kThreads, 0, s.stream>>>(s.amps, groups, sl, tm, M);
           break;
         }

@@ -571,6 +571,67 @@ def test_per_gate_dense_kernels_match_oracle(targets):
 
 
 @pytest.mark.gpu
+@pytest.mark.parametrize("n,targets,controls", [(18, [1, 0], []), (18, [16, 9, 3], []), (18, [3, 2, 1, 0], []),
+                                                (18, [17, 11, 5, 0], [8]), (18, [4, 3, 2, 1, 0], []),
+                                                (18, [17, 14, 11, 8, 5], []), (18, [9, 2, 16, 0, 7], [12, 13]),
+                                                (5, [4, 3, 2, 1, 0], []), (6, [5, 0, 3, 2, 1], []), (3, [2, 0], [1]),
+                                                (7, [1, 0], [6, 5, 4, 3, 2])])
+def test_dense_kernel_forms_agree_bitwise(monkeypatch, n, targets, controls):
+    """Every per-gate dense kernel form (QSB_DENSE_FORM: thread per group
+    k_dense_g with and without 256-bit pair accesses on qubit 0, the lane
+    form k_dense) sums each output row in the same order: results are
+    bitwise identical across forms and match the oracle."""
+    rng = np.random.default_rng(n * 1000 + len(targets) * 10 + len(controls))
+    k = len(targets)
+    z = rng.normal(size=(1 << k, 1 << k)) + 1j * rng.normal(size=(1 << k, 1 << k))
+    u, r = np.linalg.qr(z)
+    u = u * (np.diag(r) / np.abs(np.diag(r)))
+    a0 = rng.normal(size=1 << n) + 1j * rng.normal(size=1 << n)
+    a0 /= np.linalg.norm(a0)
+    g = Q.make_custom_gate(targets, u)
+    g.controls = list(controls)
+    want = ol.run_gates(n, [g], state=a0.copy())
+    outs = {}
+    for form in ("g", "g-nopair", "lanes"):
+        monkeypatch.setenv("QSB_DENSE_FORM", form.split("-")[0])
+        if form.endswith("nopair"):
+            monkeypatch.setenv("QSB_NO_PAIR256", "1")
+        sv = Q.StateVector(n)
+        sv.set_amplitudes(a0)
+        sv.apply_gate(g)
+        monkeypatch.delenv("QSB_NO_PAIR256", raising=False)
+        outs[form] = sv.amplitudes()
+        assert np.max(np.abs(outs[form] - want)) <= 1e-10, form
+    assert np.array_equal(outs["g"], outs["g-nopair"]) and np.array_equal(outs["g"], outs["lanes"])
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("kind,controls", [("H", []), ("U3", []), ("X", []), ("RX", [3]), ("X", [5, 2]),
+                                           ("Y", [1]), ("RZ", []), ("RZ", [4]), ("Z", [])])
+def test_qubit0_pair_kernel_bitwise(monkeypatch, kind, controls):
+    """2x2 and diagonal gates on qubit 0 take the 256-bit pair kernels
+    (k_mat1_q0, k_diag_q0): bitwise equal to the general kernels, and the
+    oracle's state at 1e-10."""
+    n = 14
+    rng = np.random.default_rng(7)
+    a0 = rng.normal(size=1 << n) + 1j * rng.normal(size=1 << n)
+    a0 /= np.linalg.norm(a0)
+    params = {"U3": [0.3, -1.1, 0.4], "RX": [0.9], "RZ": [-0.45]}.get(kind, [])
+    g = Q.make_gate(getattr(Q.GateKind, kind), [0], params)
+    g.controls = list(controls)
+    outs = []
+    for nopair in (False, True):
+        if nopair:
+            monkeypatch.setenv("QSB_NO_PAIR256", "1")
+        sv = Q.StateVector(n)
+        sv.set_amplitudes(a0)
+        sv.apply_gate(g)
+        outs.append(sv.amplitudes())
+    assert np.array_equal(outs[0], outs[1])
+    assert np.max(np.abs(outs[0] - ol.run_gates(n, [g], state=a0.copy()))) <= 1e-10
+
+
+@pytest.mark.gpu
 @pytest.mark.parametrize("n", [1, 2, 5, 9, 13])
 def test_serial_checksum_and_sampler_small_states(n):
     """States smaller than one scan chunk (1024 amplitudes) and than one

@@ -80,10 +80,15 @@ def gate(kind, targets, params=(), controls=()):
 
 # --- per-gate kernels (statevector.hpp:268-361): 32 B per touched amplitude
 for q in (0, n // 2, n - 1):
-    timeit("k_mat1 H q%d" % q, lambda q=q: sv.apply_gate(gate(G.H, [q])), 32 * A)
+    timeit("k_mat1 H q%d" % q, lambda q=q: sv.apply_gate(gate(G.H, [q])), 32 * A,
+           note="256-bit pair kernel k_mat1_q0" if q == 0 else "")
+os.environ["QSB_NO_PAIR256"] = "1"
+timeit("k_mat1 H q0 (QSB_NO_PAIR256)", lambda: sv.apply_gate(gate(G.H, [0])), 32 * A)
+os.environ.pop("QSB_NO_PAIR256")
 timeit("k_mat1 U3 ctrl", lambda: sv.apply_gate(gate(G.U3, [5], (0.1, 0.2, 0.3), [n - 2])), 16 * A,
        note="one control: half the amplitudes")
 timeit("k_diag RZ", lambda: sv.apply_gate(gate(G.RZ, [n // 3], (0.7,))), 32 * A)
+timeit("k_diag RZ q0", lambda: sv.apply_gate(gate(G.RZ, [0], (0.7,))), 32 * A, note="256-bit pair kernel k_diag_q0")
 timeit("k_diag Z (skip_zero)", lambda: sv.apply_gate(gate(G.Z, [n // 3])), 16 * A, note="bit-set half only")
 timeit("k_flip X", lambda: sv.apply_gate(gate(G.X, [n - 3])), 32 * A)
 timeit("k_flip CNOT", lambda: sv.apply_gate(gate(G.CNOT, [2, n - 4])), 16 * A, note="control: half")
@@ -91,8 +96,16 @@ timeit("k_swap SWAP", lambda: sv.apply_gate(gate(G.SWAP, [1, n - 1])), 16 * A, n
 for k in (2, 3, 4, 5):
     m = unitary(k)
     for tg in ([n - 1 - 3 * i for i in range(k)], list(range(k - 1, -1, -1))):
-        timeit("k_dense%s K=%d t=%s" % ("_g" if k <= 4 else "", k, tg),
-               lambda tg=tg, m=m: sv.apply_matrix(tg, m), 32 * A)
+        # default selection, then each form forced (QSB_DENSE_FORM)
+        for form in ("", "g", "g-nopair", "lanes"):
+            if form:
+                os.environ["QSB_DENSE_FORM"] = form.split("-")[0]
+            if form.endswith("nopair"):
+                os.environ["QSB_NO_PAIR256"] = "1"
+            timeit("k_dense K=%d t=%s form=%s" % (k, tg, form or "default"),
+                   lambda tg=tg, m=m: sv.apply_matrix(tg, m), 32 * A)
+            os.environ.pop("QSB_DENSE_FORM", None)
+            os.environ.pop("QSB_NO_PAIR256", None)
 m6 = unitary(6)
 timeit("k_dense_wide K=6", lambda: sv.apply_matrix([n - 1, n - 3, 7, 5, 3, 1], m6), 32 * A,
        note="correctness path for blocks wider than the fusion cap")
