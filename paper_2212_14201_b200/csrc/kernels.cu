@@ -15,6 +15,7 @@
 #include <atomic>
 #include <cmath>
 #include <cstring>
+#include <functional>
 
 #include "kernels.hpp"
 
@@ -575,6 +576,72 @@ __global__ void __launch_bounds__(kThreads) k_marginal_lanes(const double2* __re
   }
 }
 
+// Marginal over states of >= 8 + kh qubits: a warp reads whole 256-amplitude
+// runs (qubits 0..7: lane = qubits 0..4, j = qubits 5..7; eight 512 B loads in
+// flight per warp), so every block streams contiguous 4 KiB pieces whatever
+// low marginal qubits there are; per-lane accumulators per j, combined per
+// result bin in fixed order (deterministic).  blockIdx.y = the marginal
+// qubits >= 8.
+struct MarginalRuns {
+  uint32_t kh;         // marginal qubits >= 8
+  uint32_t qh[12];     // ... ascending
+  uint32_t rh[12];     // their result bits
+  int rl[5];           // result bit of lane bit b (qubit b), -1 if not marginal
+  int rm[3];           // result bit of j bit b (qubit 5 + b), -1 if not marginal
+  uint32_t lane_free;  // lane bits that are not marginal qubits
+  uint32_t mid_free;   // j bits that are not marginal qubits
+};
+
+__global__ void __launch_bounds__(kThreads) k_marginal_runs(const double2* __restrict__ a, uint64_t per_hi, Slots slh,
+                                                            MarginalRuns mm, double* __restrict__ partial) {
+  __shared__ double sh[kThreads / 32][8][32];
+  const uint32_t bh = blockIdx.y, lane = threadIdx.x & 31u, w = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  uint64_t fixed = 0;
+  uint32_t bin_hi = 0;
+#pragma unroll
+  for (uint32_t j = 0; j < 12; ++j)
+    if (j < mm.kh && ((bh >> j) & 1u)) {
+      fixed |= 1ull << mm.qh[j];
+      bin_hi |= 1u << mm.rh[j];
+    }
+  const uint64_t chunk = (per_hi + gridDim.x - 1) / gridDim.x;
+  const uint64_t lo = blockIdx.x * chunk, hi = min(per_hi, lo + chunk);
+  double acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+  for (uint64_t g = lo + w; g < hi; g += nw) {
+    const double2* r = a + ((deposit(g, slh) << 8) | fixed | lane);
+    double2 v[8];
+#pragma unroll
+    for (int j = 0; j < 8; ++j) v[j] = __ldcs(r + 32 * j);
+#pragma unroll
+    for (int j = 0; j < 8; ++j) acc[j] += norm_ref(v[j]);
+  }
+  // j values that differ only in non-marginal bits share a bin: fold them
+  // into the representative (free bits zero), in ascending j
+#pragma unroll
+  for (int j = 0; j < 8; ++j) {
+    if (j & mm.mid_free) continue;
+    double t = 0;
+#pragma unroll
+    for (int j2 = 0; j2 < 8; ++j2)
+      if ((j2 & ~mm.mid_free) == static_cast<uint32_t>(j)) t += acc[j2];
+    for (int b = 0; b < 5; ++b)
+      if ((mm.lane_free >> b) & 1u) t += __shfl_xor_sync(0xffffffffu, t, 1 << b);
+    sh[w][j][lane] = t;
+  }
+  __syncthreads();
+  const uint32_t j = threadIdx.x >> 5, l = threadIdx.x & 31u;  // one (j, lane) entry per thread
+  if ((j & mm.mid_free) == 0 && (l & mm.lane_free) == 0) {
+    double t = 0;
+    for (uint32_t i = 0; i < nw; ++i) t += sh[i][j][l];
+    uint32_t bin = bin_hi;
+    for (int b = 0; b < 5; ++b)
+      if (mm.rl[b] >= 0 && ((l >> b) & 1u)) bin |= 1u << mm.rl[b];
+    for (int b = 0; b < 3; ++b)
+      if (mm.rm[b] >= 0 && ((j >> b) & 1u)) bin |= 1u << mm.rm[b];
+    partial[(uint64_t)bin * gridDim.x + blockIdx.x] = t;
+  }
+}
+
 __global__ void k_marginal_finalize(const double* __restrict__ partial, uint32_t per, uint32_t bins,
                                     double* __restrict__ out) {
   const uint32_t b = blockIdx.x * blockDim.x + threadIdx.x;
@@ -802,7 +869,8 @@ __global__ void k_scan_estimate(const double* __restrict__ S, uint32_t nc, doubl
 struct ChunkInfo {
   long long K;  // sum of rint(p/u) over the chunk
   int e;        // assumed binade exponent at chunk start
-  int clean;    // no ties, no oversize addend, normal range
+  int clean;    // 1: no ties, no oversize addend, normal range; 2: every addend is
+                //    exactly 0 (the chunk leaves any running sum unchanged)
 };
 
 // Exponent / power-of-two helpers by bit manipulation (exact; normal,
@@ -842,32 +910,36 @@ __global__ void __launch_bounds__(kThreads) k_chunk_ints(const double* __restric
   for (int sc = w; sc < kSub; sc += (int)(blockDim.x >> 5)) {  // one warp per sub-chunk
     const uint64_t slo = min(hi, lo + sc * Cs), shi = min(hi, slo + Cs);
     long long K = 0;
-    int bad = usable ? 0 : 1;
-    if (usable)
-      for (uint64_t jj = slo + l; jj < shi; jj += 32) {
-        long long k;
-        if (int_step(p[jj], inv_u, k)) K += k;
-        else bad = 1;
-      }
+    int bad = usable ? 0 : 1, nz = 0;
+    for (uint64_t jj = slo + l; jj < shi; jj += 32) {
+      const double pj = p[jj];
+      nz |= pj != 0.0;
+      long long k;
+      if (usable && int_step(pj, inv_u, k)) K += k;
+      else bad = 1;
+    }
     for (int o = 16; o > 0; o >>= 1) {
       K += __shfl_down_sync(0xffffffffu, K, o);
       bad |= __shfl_down_sync(0xffffffffu, bad, o);
+      nz |= __shfl_down_sync(0xffffffffu, nz, o);
     }
     if (l == 0) {
+      const int cl = nz ? !bad : 2;
       shk[sc] = K;
-      shb[sc] = bad;
-      sub[(uint64_t)blockIdx.x * kSub + sc] = ChunkInfo{K, e, !bad};
+      shb[sc] = cl;
+      sub[(uint64_t)blockIdx.x * kSub + sc] = ChunkInfo{nz ? K : 0, e, cl};
     }
   }
   __syncthreads();
   if (threadIdx.x == 0) {
     long long t = 0;
-    int b = 0;
+    int all_zero = 1, all_clean = 1;
     for (int i = 0; i < kSub; ++i) {
       t += shk[i];
-      b |= shb[i];
+      all_zero &= shb[i] == 2;
+      all_clean &= shb[i] != 0;
     }
-    info[blockIdx.x] = ChunkInfo{t, e, !b};
+    info[blockIdx.x] = ChunkInfo{all_zero ? 0 : t, e, all_zero ? 2 : all_clean};
   }
 }
 
@@ -886,8 +958,9 @@ __device__ __forceinline__ long long warp_incl_scan_ll(long long v) {
 // kSub sub-chunk records the same way; only a failing sub-chunk is replayed 32
 // elements at a time (integer trick per 32, true serial adds when that fails).
 // cum == nullptr: only the final sum is wanted (nothing is written per element).
-__device__ __forceinline__ bool int_advance(double& A, long long K, int e, bool clean) {
+__device__ __forceinline__ bool int_advance(double& A, long long K, int e, int clean) {
   const double kMinNormalScaled = 2.2250738585072014e-308 * 4503599627370496.0;
+  if (clean == 2) return true;  // all addends zero: fl(A + 0) == A
   if (!clean || !(A >= kMinNormalScaled) || exp_of(A) != e) return false;
   const long long a = (long long)(A * pow2(52 - e));
   if (a + K >= 9007199254740991LL) return false;  // would leave the binade
@@ -899,36 +972,48 @@ __device__ void replay_range(const double* __restrict__ p, uint64_t lo, uint64_t
                              double* __restrict__ cum) {
   const int lane = threadIdx.x & 31;
   const double kMinNormalScaled = 2.2250738585072014e-308 * 4503599627370496.0;
-  for (uint64_t j0 = lo; j0 < hi; j0 += 32) {
-    const uint64_t j = j0 + lane;
-    const double pj = j < hi ? p[j] : 0.0;
-    bool done = false;
-    if (A >= kMinNormalScaled) {
-      const int eA = exp_of(A);
-      const double u = pow2(eA - 52), inv_u = pow2(52 - eA);
-      long long k = 0;
-      const bool ok = int_step(pj, inv_u, k);
-      if (__all_sync(0xffffffffu, ok)) {
-        const long long incl = warp_incl_scan_ll(k);
-        const long long Ksum = __shfl_sync(0xffffffffu, incl, 31);
-        const long long a = (long long)(A * inv_u);
-        if (a + Ksum < 9007199254740991LL) {
-          if (cum && j < hi) cum[j] = (double)(a + incl) * u;
-          A = (double)(a + Ksum) * u;
-          done = true;
-        }
-      }
+  constexpr int kAhead = 8;  // 8 x 32 addends loaded per trip: one dependent load latency per 256
+  for (uint64_t jb = lo; jb < hi; jb += 32 * kAhead) {
+    double pv[kAhead];
+#pragma unroll
+    for (int q = 0; q < kAhead; ++q) {
+      const uint64_t j = jb + 32 * q + lane;
+      pv[q] = j < hi ? p[j] : 0.0;
     }
-    if (!done) {
-      double acc = A;
-      for (int t2 = 0; t2 < 32; ++t2) {
-        const double pt = __shfl_sync(0xffffffffu, pj, t2);
-        if (j0 + t2 < hi) {
-          acc = __dadd_rn(acc, pt);
-          if (cum && lane == t2) cum[j] = acc;
+#pragma unroll
+    for (int q = 0; q < kAhead; ++q) {
+      const uint64_t j0 = jb + 32 * q;
+      if (j0 >= hi) break;
+      const uint64_t j = j0 + lane;
+      const double pj = pv[q];
+      bool done = false;
+      if (A >= kMinNormalScaled) {
+        const int eA = exp_of(A);
+        const double u = pow2(eA - 52), inv_u = pow2(52 - eA);
+        long long k = 0;
+        const bool ok = int_step(pj, inv_u, k);
+        if (__all_sync(0xffffffffu, ok)) {
+          const long long incl = warp_incl_scan_ll(k);
+          const long long Ksum = __shfl_sync(0xffffffffu, incl, 31);
+          const long long a = (long long)(A * inv_u);
+          if (a + Ksum < 9007199254740991LL) {
+            if (cum && j < hi) cum[j] = (double)(a + incl) * u;
+            A = (double)(a + Ksum) * u;
+            done = true;
+          }
         }
       }
-      A = acc;
+      if (!done) {
+        double acc = A;
+        for (int t2 = 0; t2 < 32; ++t2) {
+          const double pt = __shfl_sync(0xffffffffu, pj, t2);
+          if (j0 + t2 < hi) {
+            acc = __dadd_rn(acc, pt);
+            if (cum && lane == t2) cum[j] = acc;
+          }
+        }
+        A = acc;
+      }
     }
   }
 }
@@ -947,6 +1032,38 @@ __global__ void k_sequential(const double* __restrict__ p, uint64_t n, uint64_t 
     double my_start = 0.0;
     unsigned char my_fast = 0;
     const uint32_t cn = min(32u, nc - c0);
+    // All 32 chunks clean and guessed in the running value's binade: the
+    // serial integer advances are one warp prefix sum (K >= 0, so the group
+    // stays in the binade iff its total does) -- the same starts, exactly.
+    // (All-zero chunks join any group: they leave the running value as is.)
+    {
+      const double kMinNormalScaled = 2.2250738585072014e-308 * 4503599627370496.0;
+      const bool an = A >= kMinNormalScaled;
+      const int eA = an ? exp_of(A) : 0;
+      const bool zero = mine.clean == 2;
+      const bool ok = (uint32_t)lane >= cn || zero || (mine.clean == 1 && an && mine.e == eA);
+      if (__all_sync(0xffffffffu, ok)) {
+        const long long k = ((uint32_t)lane < cn && !zero) ? mine.K : 0;
+        const long long incl = warp_incl_scan_ll(k);
+        const long long tot = __shfl_sync(0xffffffffu, incl, 31);
+        if (!an) {  // only all-zero chunks (a clean one needs a normal running value)
+          if (c0 + lane < nc) {
+            start[c0 + lane] = A;
+            fast[c0 + lane] = 1;
+          }
+          continue;
+        }
+        const long long a = (long long)(A * pow2(52 - eA));
+        if (a + tot < 9007199254740991LL) {
+          if (c0 + lane < nc) {
+            start[c0 + lane] = (double)(a + incl - k) * pow2(eA - 52);
+            fast[c0 + lane] = 1;
+          }
+          A = (double)(a + tot) * pow2(eA - 52);
+          continue;
+        }
+      }
+    }
     for (uint32_t t = 0; t < cn; ++t) {
       const uint32_t c = c0 + t;
       const long long ciK = __shfl_sync(0xffffffffu, mine.K, t);
@@ -996,8 +1113,12 @@ __global__ void k_sequential(const double* __restrict__ p, uint64_t n, uint64_t 
 
 // Phase D: expand the chunks (or the sub-chunks) the walk advanced in one
 // integer step, in parallel (block per chunk): cum_j = (a + prefix_j) * u.
-__device__ void expand_range(const double* __restrict__ p, uint64_t lo, uint64_t hi, int e, double start,
+__device__ void expand_range(const double* __restrict__ p, uint64_t lo, uint64_t hi, int e, int clean, double start,
                              double* __restrict__ cum, long long* warp_tot) {
+  if (clean == 2) {  // all addends zero: every partial sum is the start value
+    for (uint64_t j = lo + threadIdx.x; j < hi; j += blockDim.x) cum[j] = start;
+    return;
+  }
   const double u = pow2(e - 52), inv_u = pow2(52 - e);
   long long carry = (long long)(start * inv_u);
   const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
@@ -1030,7 +1151,7 @@ __global__ void __launch_bounds__(kThreads) k_expand(const double* __restrict__ 
   __shared__ long long warp_tot[kThreads / 32];
   const uint64_t lo = blockIdx.x * C, hi = min(n, lo + C);
   if (fast[blockIdx.x]) {
-    expand_range(p, lo, hi, info[blockIdx.x].e, start[blockIdx.x], cum, warp_tot);
+    expand_range(p, lo, hi, info[blockIdx.x].e, info[blockIdx.x].clean, start[blockIdx.x], cum, warp_tot);
     return;
   }
   const uint64_t Cs = C / kSub;
@@ -1038,7 +1159,7 @@ __global__ void __launch_bounds__(kThreads) k_expand(const double* __restrict__ 
     const uint64_t k = (uint64_t)blockIdx.x * kSub + sc;
     if (!sub_fast[k]) continue;  // replayed by the walk (cum already written)
     const uint64_t slo = min(hi, lo + sc * Cs), shi = min(hi, slo + Cs);
-    expand_range(p, slo, shi, sub[k].e, sub_start[k], cum, warp_tot);
+    expand_range(p, slo, shi, sub[k].e, sub[k].clean, sub_start[k], cum, warp_tot);
   }
 }
 
@@ -1809,9 +1930,48 @@ void marginal_probs(State& s, const uint32_t* qubits, uint32_t m, double* host_o
   const uint64_t per_bin = 1ull << (s.local_qubits() - m);
   const uint64_t bins = 1ull << m;
   const size_t out_bytes = bins * sizeof(double);
-  uint32_t kh = 0;
-  for (uint32_t b = 0; b < m; ++b) kh += qubits[b] >= 5;
-  if (m <= 12 && s.local_qubits() >= 5 + kh) {
+  uint32_t kh = 0, k8 = 0;
+  for (uint32_t b = 0; b < m; ++b) {
+    kh += qubits[b] >= 5;
+    k8 += qubits[b] >= 8;
+  }
+  static_assert(kThreads == 8 * 32, "k_marginal_runs maps one (j, lane) entry per thread");
+  if (m <= 12 && s.local_qubits() >= 8 + k8 && !std::getenv("QSB_MARGINAL_LANES")) {
+    MarginalRuns mm{};
+    std::vector<std::pair<uint32_t, uint32_t>> hq;  // (qubit, result bit)
+    for (int b = 0; b < 5; ++b) mm.rl[b] = -1;
+    for (int b = 0; b < 3; ++b) mm.rm[b] = -1;
+    for (uint32_t b = 0; b < m; ++b) {
+      if (qubits[b] >= 8) hq.push_back({qubits[b], b});
+      else if (qubits[b] >= 5) mm.rm[qubits[b] - 5] = static_cast<int>(b);
+      else mm.rl[qubits[b]] = static_cast<int>(b);
+    }
+    std::sort(hq.begin(), hq.end());
+    mm.kh = k8;
+    std::vector<uint32_t> rel;
+    for (uint32_t j = 0; j < k8; ++j) {
+      mm.qh[j] = hq[j].first;
+      mm.rh[j] = hq[j].second;
+      rel.push_back(hq[j].first - 8);
+    }
+    for (int b = 0; b < 5; ++b)
+      if (mm.rl[b] < 0) mm.lane_free |= 1u << b;
+    for (int b = 0; b < 3; ++b)
+      if (mm.rm[b] < 0) mm.mid_free |= 1u << b;
+    const Slots slh = make_slots(rel, {});
+    const uint64_t per_hi = 1ull << (s.local_qubits() - 8 - k8);
+    const uint64_t ybins = 1ull << k8;
+    const uint32_t per = static_cast<uint32_t>(std::max<uint64_t>(1, std::min<uint64_t>(kRedBlocks / ybins + 1, per_hi)));
+    char* scr = static_cast<char*>(s.get_scratch(bins * per * sizeof(double) + out_bytes));
+    double* part = reinterpret_cast<double*>(scr);
+    double* dout = part + bins * per;
+    k_marginal_runs<<<dim3(per, static_cast<uint32_t>(ybins)), kThreads, 0, s.stream>>>(s.amps, per_hi, slh, mm, part);
+    QSB_LAUNCHED();
+    k_marginal_finalize<<<static_cast<uint32_t>((bins + 255) / 256), 256, 0, s.stream>>>(part, per,
+                                                                                         static_cast<uint32_t>(bins), dout);
+    QSB_LAUNCHED();
+    QSB_CUDA(cudaMemcpyAsync(host_out, dout, out_bytes, cudaMemcpyDeviceToHost, s.stream));
+  } else if (m <= 12 && s.local_qubits() >= 5 + kh) {
     MarginalMap mm{};
     std::vector<std::pair<uint32_t, uint32_t>> hq;  // (qubit, result bit)
     for (int b = 0; b < 5; ++b) mm.rl[b] = -1;
@@ -2088,19 +2248,30 @@ double exact_cumulative(State& s, double* d_probs, double* d_cum) {
   return *h;
 }
 
-void sample(State& s, const double* uniforms_host, uint64_t shots, bool exact, uint64_t* out_host) {
+// The cumulative array is built asynchronously while the host fills the
+// uniforms (gen: the Rng stream, or a copy of caller-supplied draws) into
+// pinned staging; then one H2D copy, the search, one D2H copy.
+void sample_gen(State& s, uint64_t shots, bool exact, uint64_t* out_host, const std::function<void(double*)>& gen) {
   DeviceGuard dg(s.device);
   if (shots == 0) return;
+  double* hu = static_cast<double*>(s.get_pinned(shots * 16));  // before any async work (may reallocate)
+  uint64_t* hout = reinterpret_cast<uint64_t*>(hu + shots);
   char* extra;
   SamplerBuffers b = sampler_buffers(s, shots * 16, &extra);
   double* du = reinterpret_cast<double*>(extra);
   unsigned long long* dout = reinterpret_cast<unsigned long long*>(extra + shots * 8);
   build_cumulative(s, b, exact);
-  QSB_CUDA(cudaMemcpyAsync(du, uniforms_host, shots * 8, cudaMemcpyHostToDevice, s.stream));
+  gen(hu);  // overlaps the cumulative build on the GPU
+  QSB_CUDA(cudaMemcpyAsync(du, hu, shots * 8, cudaMemcpyHostToDevice, s.stream));
   k_search<<<grid_for(shots, s.device), kThreads, 0, s.stream>>>(b.cum, s.size, b.total, du, shots, dout);
   QSB_LAUNCHED();
-  QSB_CUDA(cudaMemcpyAsync(out_host, dout, shots * 8, cudaMemcpyDeviceToHost, s.stream));
+  QSB_CUDA(cudaMemcpyAsync(hout, dout, shots * 8, cudaMemcpyDeviceToHost, s.stream));
   QSB_CUDA(cudaStreamSynchronize(s.stream));
+  std::memcpy(out_host, hout, shots * 8);
+}
+
+void sample(State& s, const double* uniforms_host, uint64_t shots, bool exact, uint64_t* out_host) {
+  sample_gen(s, shots, exact, out_host, [&](double* hu) { std::memcpy(hu, uniforms_host, shots * 8); });
 }
 
 void reduced_density(State& s, const uint32_t* targets, uint32_t k, double* out) {

@@ -4,6 +4,7 @@
 #pragma once
 
 #include <cstdint>
+#include <functional>
 #include <vector>
 
 #include "common.hpp"
@@ -49,6 +50,7 @@ void scale(State& s, double re, double im);                                     
 // BasisSampler (statevector.hpp:542-570) + draws.  exact: reproduce the serial
 // cumulative sum bit for bit (see kernels.cu, "serial-equivalent scan").
 void sample(State& s, const double* uniforms_host, uint64_t shots, bool exact, uint64_t* out_host);
+void sample_gen(State& s, uint64_t shots, bool exact, uint64_t* out_host, const std::function<void(double*)>& gen);
 
 // <psi|P|psi> for Pauli strings given as (xmask, zmask, #Y) per term.
 void expect_pauli(State& s, const std::vector<uint64_t>& xmask, const std::vector<uint64_t>& zmask,

@@ -125,6 +125,52 @@ def test_exact_cumulative_is_bitwise_serial(n, seed):
     assert np.array_equal(cum.view(np.uint64), want.view(np.uint64))
 
 
+@pytest.mark.parametrize("n,layout", [(20, "zero_runs"), (18, "zero_head"), (21, "sparse_tail"), (16, "all_but_one")])
+def test_exact_scan_zero_chunks_bitwise(n, layout):
+    """Runs of exactly-zero probabilities (a 1-layer random circuit zeroes the
+    last quarter of the index space; basis-like states): whole chunks of
+    zeros advance the serial-equivalent scan unchanged whatever binade the
+    parallel estimate guessed -- cumulative array, total, serial digest and
+    samples stay bitwise the reference's serial loops."""
+    rng = np.random.default_rng(n)
+    size = 1 << n
+    a = rng.normal(size=size) + 1j * rng.normal(size=size)
+    if layout == "zero_runs":
+        a[: size // 8] = 0
+        a[size // 2: size // 2 + size // 8] = 0
+        a[-size // 4:] = 0
+    elif layout == "zero_head":
+        a[: size - 5000] = 0
+    elif layout == "sparse_tail":
+        a[size // 3:] = 0
+        a[size // 3 + 7::4099] = 1e-3
+    else:
+        a[:] = 0
+        a[size // 2 + 3] = 1
+    a /= np.linalg.norm(a)
+    sv = Q.StateVector.from_amplitudes(n, a)
+    cum = np.empty(size)
+    tot = N.C.c_double()
+    N.check(N.lib().qs_cumulative(sv.handle(), N.dptr(cum), N.C.byref(tot)))
+    want, wtot = _oracle_serial_cum(a)
+    assert tot.value == wtot
+    assert np.array_equal(cum.view(np.uint64), want.view(np.uint64))
+    b = sv.amplitudes()
+    assert sv.checksum_serial() == ol.checksum(b, n)
+    assert np.array_equal(sv.sample_seeded(11, 5000, exact=True), ol.sample_seeded(b, n, 11, 5000))
+
+
+def test_random_one_layer_scan_bitwise():
+    """The state that exposed the zero-tail case: gen_random_circuit(n, 1, 7)
+    (a quarter of the probabilities exactly zero at the end)."""
+    n = 22
+    sv = Q.StateVector(n)
+    sv.apply_circuit(Q.gen_random_circuit(n, 1, 7).gates())
+    b = sv.amplitudes()
+    assert sv.checksum_serial() == ol.checksum(b, n)
+    assert np.array_equal(sv.sample_seeded(5, 20000, exact=True), ol.sample_seeded(b, n, 5, 20000))
+
+
 def test_collapse_sequence():
     c = gio.case("collapse")
     circ = gio.read_circuit(c["circuit"])
@@ -643,3 +689,29 @@ def test_serial_checksum_and_sampler_small_states(n):
     a = sv.amplitudes()
     assert sv.checksum_serial() == ol.checksum(a, n)
     assert np.array_equal(sv.sample_seeded(3, 2000, exact=True), ol.sample_seeded(a, n, 3, 2000))
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("n,qubits", [(8, [7, 5, 0]), (8, [6]), (9, [8, 2]), (12, [11, 7, 6, 5, 4, 0]),
+                                      (14, [13, 12, 9, 8, 7, 3, 2, 1, 0, 5, 6, 10]), (16, [5]), (16, [15, 14]),
+                                      (16, [0, 1, 2, 3, 4]), (20, [19, 17, 13, 5, 1, 0]), (10, [2, 9, 5, 8])])
+def test_marginal_run_kernel(monkeypatch, n, qubits):
+    """Marginals (StateVector::probabilities, statevector.hpp:190-215) through
+    the 256-amplitude run kernel and the 32-lane kernel (QSB_MARGINAL_LANES):
+    both match the sums over the amplitudes at 1e-13."""
+    rng = np.random.default_rng(n + len(qubits))
+    a0 = rng.normal(size=1 << n) + 1j * rng.normal(size=1 << n)
+    a0 /= np.linalg.norm(a0)
+    p = np.abs(a0) ** 2
+    idx = np.arange(1 << n)
+    key = np.zeros(1 << n, dtype=np.int64)
+    for b, q in enumerate(qubits):
+        key |= ((idx >> q) & 1) << b
+    want = np.bincount(key, weights=p, minlength=1 << len(qubits))
+    sv = Q.StateVector(n)
+    sv.set_amplitudes(a0)
+    got = sv.probabilities(qubits)
+    monkeypatch.setenv("QSB_MARGINAL_LANES", "1")
+    got_lanes = sv.probabilities(qubits)
+    assert np.max(np.abs(got - want)) <= 1e-13
+    assert np.max(np.abs(got_lanes - want)) <= 1e-13

@@ -114,7 +114,10 @@ timeit("k_dense_wide K=6", lambda: sv.apply_matrix([n - 1, n - 3, 7, 5, 3, 1], m
 timeit("k_reduce norm2", lambda: sv.norm_squared(), 16 * A)
 timeit("k_reduce checksum", lambda: sv.checksum(), 16 * A)
 timeit("k_reduce prob_one", lambda: sv.probability_of_one(n - 1), 8 * A, note="reads the bit-set half")
-timeit("k_marginal 6 qubits", lambda: sv.probabilities([n - 1, 17, 13, 5, 1, 0]), 16 * A)
+timeit("k_marginal_runs 6 qubits", lambda: sv.probabilities([n - 1, 17, 13, 5, 1, 0]), 16 * A)
+os.environ["QSB_MARGINAL_LANES"] = "1"
+timeit("k_marginal_lanes 6 qubits (QSB_MARGINAL_LANES)", lambda: sv.probabilities([n - 1, 17, 13, 5, 1, 0]), 16 * A)
+os.environ.pop("QSB_MARGINAL_LANES")
 cnt = 1 << 24
 buf = np.empty(cnt, dtype=np.float64)
 timeit("k_probs (2^24 window)", lambda: N.check(L.qs_probs_full(sv.handle(), N.dptr(buf), 0, cnt)), 24 * cnt,
