@@ -356,6 +356,12 @@ int qs_plan_exchanges(qs_plan_t p, uint64_t* exchanges);
  * lpos[b], b < *nbits (arrays of QS_MAX_EXCHANGE_BITS; nbits = 0 otherwise). */
 #define QS_MAX_EXCHANGE_BITS 16
 int qs_plan_step_info(qs_plan_t p, uint64_t i, int* kind, uint32_t* nbits, uint32_t* gpos, uint32_t* lpos);
+/* Tile pass i (diagnostics): tile qubits (*m of them, ascending, into
+ * qubits[16]), register bits *r (2^r amplitudes per thread), shared-memory
+ * exchanges *transposes, micro-ops *nops, source gates covered *gates.  *m = 0
+ * when step i is not a tile pass. */
+int qs_plan_tile_info(qs_plan_t p, uint64_t i, uint32_t* m, uint32_t* qubits, uint32_t* r, uint32_t* transposes,
+                      uint32_t* nops, uint64_t* gates);
 int qs_shards_plan_enqueue(qs_shards_t s, qs_plan_t p);
 /* Reset to |basis> (global index) fused into the plan's first tile pass; no wait. */
 int qs_shards_plan_enqueue_from_basis(qs_shards_t s, qs_plan_t p, uint64_t basis);

@@ -157,6 +157,7 @@ _SIGS = {
     "qs_shards_get_amplitudes": (C.c_int, [_P, _DP, C.c_uint64, C.c_uint64]),
     "qs_plan_create_sharded": (C.c_int, [C.c_uint32, C.c_uint32, _GP, C.c_uint64, C.POINTER(_P)]),
     "qs_plan_exchanges": (C.c_int, [_P, _U64P]),
+    "qs_plan_tile_info": (C.c_int, [_P, C.c_uint64, _UP, _UP, _UP, _UP, _UP, C.POINTER(C.c_uint64)]),
     "qs_plan_step_info": (C.c_int, [_P, C.c_uint64, C.POINTER(C.c_int), _UP, _UP, _UP]),
     "qs_shards_plan_enqueue": (C.c_int, [_P, _P]),
     "qs_shards_plan_enqueue_from_basis": (C.c_int, [_P, _P, C.c_uint64]),

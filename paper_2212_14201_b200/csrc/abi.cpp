@@ -864,6 +864,22 @@ int qs_plan_exchanges(qs_plan_t p, uint64_t* exchanges) {
   });
 }
 
+int qs_plan_tile_info(qs_plan_t p, uint64_t i, uint32_t* m, uint32_t* qubits, uint32_t* r, uint32_t* transposes,
+                      uint32_t* nops, uint64_t* gates) {
+  return guarded([&] {
+    if (!p || i >= p->p->steps.size()) throw ValidationError("bad plan step index");
+    const Step& st = p->p->steps[i];
+    const TileProgram* tp = st.kind == Step::TileStep ? st.tile.get() : nullptr;
+    if (m) *m = tp ? tp->h.m : 0;
+    if (!tp) return;
+    for (uint32_t b = 0; b < tp->h.m && qubits; ++b) qubits[b] = tp->h.S[b];
+    if (r) *r = tp->h.r;
+    if (transposes) *transposes = tp->transposes;
+    if (nops) *nops = static_cast<uint32_t>(tp->ops.size());
+    if (gates) *gates = tp->gates;
+  });
+}
+
 int qs_plan_step_info(qs_plan_t p, uint64_t i, int* kind, uint32_t* nbits, uint32_t* gpos, uint32_t* lpos) {
   return guarded([&] {
     if (!p || i >= p->p->steps.size()) throw ValidationError("bad plan step index");
