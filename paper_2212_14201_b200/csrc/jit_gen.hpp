@@ -85,6 +85,56 @@ struct Gen {
   bool tile_barrier_done = false;
   bool warp_local_ok = true;
 
+  // Per-thread flip frame: a CNOT whose control is a thread bit and whose
+  // target is register bit k is not applied with selects; it is recorded as
+  // "register slot p holds logical slot p ^ (t ? 2^k : 0)" (t: the thread's
+  // predicate).  Ops that commute with it (gates on other register bits,
+  // frame-invariant phases) run unchanged; the next exchange or the store
+  // absorbs it into its addresses (the smem swizzle and the register strides
+  // are XOR-linear in the slot index), and anything else materialises the
+  // selects first.  QSB_NO_FLIP_FRAME=1 applies every such flip at once.
+  bool flip_frame = true;
+  std::vector<std::pair<int, std::string>> frame;  // (register bit, predicate)
+  // applies the pending flips on the register bits in `bits` (selects)
+  const char* mat_reason = "";
+  void materialize(uint32_t bits) {
+    for (size_t i = 0; i < frame.size();) {
+      const int Kb = frame[i].first;
+      if (!((bits >> Kb) & 1u)) {
+        ++i;
+        continue;
+      }
+      const std::string t = frame[i].second;
+      if (std::getenv("QSB_FRAME_DEBUG")) s << "    // materialize: " << mat_reason << "\n";
+      frame.erase(frame.begin() + static_cast<long>(i));
+      for (int p = 0; p < NS; ++p) {
+        if ((p >> Kb) & 1) continue;
+        const int p1 = p | (1 << Kb);
+        flush_pair(p, p1);
+        const std::string a = name[p], b = name[p1];
+        const std::string na = fresh(), nb = fresh();
+        s << "    const double2 " << na << " = " << t << " ? " << b << " : " << a << ";\n";
+        s << "    const double2 " << nb << " = " << t << " ? " << a << " : " << b << ";\n";
+        name[p] = na;
+        name[p1] = nb;
+      }
+    }
+  }
+  // per-thread XOR of the frame's slot offsets (cols[k]: register bit k's
+  // smem swizzle column or HBM stride)
+  std::string frame_xor(const uint32_t* cols) const {
+    std::ostringstream e;
+    e << "0u";
+    for (auto& f : frame) e << " ^ (" << f.second << " ? " << cols[f.first] << "u : 0u)";
+    return e.str();
+  }
+  std::string frame_xor(const unsigned long long* cols) const {
+    std::ostringstream e;
+    e << "0ull";
+    for (auto& f : frame) e << " ^ (" << f.second << " ? " << hexll(cols[f.first]) << " : 0ull)";
+    return e.str();
+  }
+
   // Tile-wide phase factors from qubits outside the tile: a product over up
   // to n-m bits of the tile's global index.  Bits are grouped in chunks of 6
   // of the compact tile index tix (tile | rank_base >> m); a chunk holding >= 2
@@ -211,7 +261,10 @@ struct Gen {
   // rotations, H): M = f * N with one entry of each row of N exactly +-1, so
   // every output is a single fused multiply-add per real component; f joins
   // the tile-wide scalar Kg (commutes with every linear op, applied at store).
-  bool mat1_factored(const TOp& o) {
+  // tf: a pending frame flip on the target bit (predicate): threads with tf
+  // apply X M X instead -- accepted when it factors with the same pivots and
+  // signs, so only the per-thread x coefficients differ (one select per row).
+  bool mat1_factored(const TOp& o, const std::string& tf = "") {
     if (o.rmask != 0 || o.gmask != 0) return false;
     const cd m[4] = {coefv(o.coef), coefv(o.coef + 1), coefv(o.coef + 2), coefv(o.coef + 3)};
     // Pivot on the diagonal unless it is tiny: the generated code then does not
@@ -235,7 +288,23 @@ struct Gen {
     }
     const int Kb = o.k;
     std::string xc[2];
-    for (int r = 0; r < 2; ++r) xc[r] = kconst(rows[r].x);
+    if (!tf.empty()) {
+      const cd nx[4] = {n[3], n[2], n[1], n[0]};  // X M X / f
+      for (int r = 0; r < 2; ++r) {
+        const cd u = nx[2 * r], w = nx[2 * r + 1];
+        Row c;
+        if (unit(u)) c = {0, u.real(), w};
+        else if (unit(w)) c = {1, w.real(), u};
+        else return false;
+        const bool same_kind = (rows[r].x.imag() == 0.0) == (c.x.imag() == 0.0) &&
+                               (rows[r].x.real() == 0.0) == (c.x.real() == 0.0);
+        if (c.piv != rows[r].piv || c.sign != rows[r].sign || !same_kind) return false;
+        xc[r] = fresh("XS");
+        s << "    const double2 " << xc[r] << " = " << tf << " ? " << kconst(c.x) << " : " << kconst(rows[r].x) << ";\n";
+      }
+    } else {
+      for (int r = 0; r < 2; ++r) xc[r] = kconst(rows[r].x);
+    }
     for (int p = 0; p < NS; ++p) {
       if ((p >> Kb) & 1) continue;
       const int p1 = p | (1 << Kb);
@@ -266,10 +335,36 @@ struct Gen {
 
   // --- micro-ops ------------------------------------------------------------
   void mat1(const TOp& o) {
-    if (mat1_factored(o)) return;
+    mat_reason = o.rmask ? "mat1 rmask" : (o.type == TO_MAT1_RX ? "mat1 rx" : (o.type == TO_MAT1_REAL ? "mat1 real" : "mat1"));
+    // a pending frame flip on the target: M itself when X M X == M, else X M X
+    // through per-thread coefficients (factored rows, or the four entries)
+    std::string tf;
+    if (!o.rmask)
+      for (auto& f : frame)
+        if (f.first == static_cast<int>(o.k)) tf = f.second;
+    const bool symmetric = coefv(o.coef) == coefv(o.coef + 3) && coefv(o.coef + 1) == coefv(o.coef + 2);
+    std::string m0 = coef(o.coef), m1 = coef(o.coef + 1), m2 = coef(o.coef + 2), m3 = coef(o.coef + 3);
+    if (!tf.empty() && symmetric) {
+      materialize(static_cast<uint32_t>(o.rmask));
+      if (mat1_factored(o)) return;
+    } else if (!tf.empty()) {
+      materialize(static_cast<uint32_t>(o.rmask));
+      if (mat1_factored(o, tf)) return;
+      if (o.type == TO_MAT1_RX) {
+        materialize(1u << o.k);
+      } else {  // per-thread entries of X M X: (m3, m2; m1, m0)
+        const std::string e[4] = {fresh("ME"), fresh("ME"), fresh("ME"), fresh("ME")};
+        const std::string orig[4] = {m0, m1, m2, m3};
+        for (int i = 0; i < 4; ++i)
+          s << "    const double2 " << e[i] << " = " << tf << " ? " << orig[3 - i] << " : " << orig[i] << ";\n";
+        m0 = e[0], m1 = e[1], m2 = e[2], m3 = e[3];
+      }
+    } else {
+      materialize((1u << o.k) | static_cast<uint32_t>(o.rmask));
+      if (mat1_factored(o)) return;
+    }
     const std::string t = pred(o);
     const int Kb = o.k;
-    const std::string m0 = coef(o.coef), m1 = coef(o.coef + 1), m2 = coef(o.coef + 2), m3 = coef(o.coef + 3);
     for (int p = 0; p < NS; ++p) {
       if ((p >> Kb) & 1) continue;
       if ((p & o.rmask) != o.rval) continue;
@@ -294,6 +389,20 @@ struct Gen {
 
   void flip(const TOp& o) {
     const int Kb = o.k;
+    mat_reason = "flip rmask";
+    materialize(static_cast<uint32_t>(o.rmask));  // register controls select slots by logical bits
+    if (o.gmask && !o.rmask && flip_frame) {
+      const std::string t = pred(o);
+      for (auto& f : frame)
+        if (f.first == Kb) {  // two pending flips of one bit: XOR of the predicates
+          const std::string tc = fresh("t");
+          s << "    const bool " << tc << " = " << f.second << " != " << t << ";\n";
+          f.second = tc;
+          return;
+        }
+      frame.push_back({Kb, t});
+      return;
+    }
     const std::string t = o.gmask ? pred(o) : "";
     for (int p = 0; p < NS; ++p) {
       if ((p >> Kb) & 1) continue;
@@ -315,6 +424,14 @@ struct Gen {
   }
 
   void phase(const TOp& o) {
+    {  // register predicates and per-slot factors that differ across a pending flip
+      uint32_t dep = static_cast<uint32_t>(o.rmask);
+      for (auto& f : frame)
+        for (int p = 0; p < NS; ++p)
+          if (coefv(o.coef + p) != coefv(o.coef + (p ^ (1 << f.first)))) dep |= 1u << f.first;
+      mat_reason = o.rmask ? "phase rmask" : "phase factors";
+      materialize(dep);
+    }
     const std::string t = pred(o);
     // split the non-register factors into thread-bit and tile (outside) ones
     std::vector<std::pair<uint32_t, uint32_t>> thr;  // (tid bit, coef index)
@@ -425,6 +542,8 @@ struct Gen {
   }
 
   void dense(const TOp& o) {
+    mat_reason = "dense";
+    materialize(~0u);
     const std::string t = pred(o);
     const int KD = o.type == TO_DENSE2 ? 2 : 3, Gd = 1 << KD;
     for (int hi = 0; hi < (NS >> KD); ++hi) {
@@ -465,7 +584,10 @@ struct Gen {
     // reading from the previous one
     s << "    __syncthreads();\n";
     tile_barrier_done = true;
-    s << "    const unsigned " << Tw << " = " << xorexpr(mt) << ";\n";
+    s << "    const unsigned " << Tw << " = " << xorexpr(mt);
+    if (!frame.empty()) s << " ^ " << frame_xor(mt + TB);  // slot p holds logical p ^ f
+    s << ";\n";
+    frame.clear();
     for (int p = 0; p < NS; ++p) {
       uint32_t a = 0;
       for (int k = 0; k < R; ++k)
@@ -643,6 +765,8 @@ struct Gen {
       }
     }
     flush_all(true);
+    mat_reason = "store";
+    if (xk || h.oop) materialize(~0u);  // these stores compute each slot's index separately
     // Relabels (free SWAPs) make threads store where other threads loaded; with
     // no transpose barrier in the pass, every load must retire before any store.
     if (xk) {
@@ -676,15 +800,24 @@ struct Gen {
       // (G | off) & lmask == (G & lmask) + off: the register strides are local
       // bits that G does not have -- one base pointer, constant offsets
       s << "    double2* const SP = amps + (G & lmask);\n";
+      // pending flip frame: slot p goes to logical p ^ f, offset off(p) ^ off(f)
+      // (register strides are disjoint bits: still no carry into G)
+      std::string FO;
+      if (!frame.empty()) {
+        FO = fresh("FO");
+        s << "    const unsigned long long " << FO << " = " << frame_xor(h.store.rs) << ";\n";
+      }
       for (int p = 0; p < NS; ++p) {
         unsigned long long off = 0;
         for (int k = 0; k < R; ++k)
           if ((p >> k) & 1) off |= h.store.rs[k];
-        s << "    __stcs(SP + " << hexll(off) << ", " << name[p] << ");\n";
+        const std::string offs = FO.empty() ? hexll(off) : "(" + hexll(off) + " ^ " + FO + ")";
+        s << "    __stcs(SP + " << offs << ", " << name[p] << ");\n";
         if (reduce)
           s << "    ACC += __fma_rn(" << name[p] << ".x, " << name[p] << ".x, __dmul_rn(" << name[p] << ".y, " << name[p]
-            << ".y)) * (double)((G | " << hexll(off) << ") + 1ull);\n";
+            << ".y)) * (double)((G | " << offs << ") + 1ull);\n";
       }
+      frame.clear();
     }
 
     // ---- assemble
