@@ -99,6 +99,31 @@ def test_planner_runs_host_side_and_fuses_passes():
     assert dense["passes"] < 1120
 
 
+def test_plan_tile_info_describes_the_random30_passes():
+    # qs_plan_tile_info: every pass of the bench plan holds the 4 resident low
+    # qubits, 13 tile qubits, 4 or 5 register bits, <= 3 exchanges, and the
+    # passes together cover the layer's gates (3 passes per layer)
+    L = N.lib()
+    cc = Q.CompiledCircuit(30, Q.gen_random_circuit(30, 20, 424242).gates())
+    st = cc.stats()
+    covered = 0
+    for i in range(st["launches"]):
+        m, r, tr, nops = N.C.c_uint32(), N.C.c_uint32(), N.C.c_uint32(), N.C.c_uint32()
+        gates = N.C.c_uint64()
+        qs = (N.C.c_uint32 * 16)()
+        N.check(L.qs_plan_tile_info(cc._h, i, N.C.byref(m), qs, N.C.byref(r), N.C.byref(tr), N.C.byref(nops),
+                                    N.C.byref(gates)))
+        assert m.value == 13
+        q = list(qs)[:13]
+        assert q == sorted(q) and q[:4] == [0, 1, 2, 3]
+        assert r.value in (4, 5) and tr.value <= 3 and nops.value > 0
+        covered += gates.value
+    assert st["launches"] == 58
+    assert 1100 <= covered <= 1200
+    with pytest.raises(Q.ValidationError):
+        N.check(L.qs_plan_tile_info(cc._h, 10 ** 6, None, None, None, None, None, None))
+
+
 def test_validation_errors_without_gpu():
     bad = [Q.make_gate(Q.GateKind.H, [7])]
     with pytest.raises(Q.ValidationError):
