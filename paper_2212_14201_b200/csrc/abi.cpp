@@ -591,9 +591,9 @@ int qs_sample_seeded(qs_state_t h, uint64_t seed, uint64_t shots, int exact, uin
     if (shots && !out_index) throw ValidationError("null sample buffer");
     // Rng(seed).uniform() stream (rng.hpp:20-46): std::mt19937_64 raw draws
     // (generated while the GPU builds the cumulative array)
-    sample_gen(st(h), shots, exact != 0, out_index, [&](double* u) {
-      std::mt19937_64 eng(seed);
-      for (uint64_t i = 0; i < shots; ++i) u[i] = static_cast<double>(eng() >> 11) * 0x1.0p-53;
+    std::mt19937_64 eng(seed);
+    sample_gen(st(h), shots, exact != 0, out_index, [&](double* u, uint64_t cnt) {
+      for (uint64_t i = 0; i < cnt; ++i) u[i] = static_cast<double>(eng() >> 11) * 0x1.0p-53;
     });
   });
 }

@@ -2249,29 +2249,39 @@ double exact_cumulative(State& s, double* d_probs, double* d_cum) {
 }
 
 // The cumulative array is built asynchronously while the host fills the
-// uniforms (gen: the Rng stream, or a copy of caller-supplied draws) into
-// pinned staging; then one H2D copy, the search, one D2H copy.
-void sample_gen(State& s, uint64_t shots, bool exact, uint64_t* out_host, const std::function<void(double*)>& gen) {
+// uniforms (gen(dst, count): the next `count` draws of the Rng stream, or of
+// the caller's array) into pinned staging; then per batch of <= 2^24 shots one
+// H2D copy, the search and one D2H copy (bounded pinned / device staging).
+void sample_gen(State& s, uint64_t shots, bool exact, uint64_t* out_host,
+                const std::function<void(double*, uint64_t)>& gen) {
   DeviceGuard dg(s.device);
   if (shots == 0) return;
-  double* hu = static_cast<double*>(s.get_pinned(shots * 16));  // before any async work (may reallocate)
-  uint64_t* hout = reinterpret_cast<uint64_t*>(hu + shots);
+  const uint64_t B = std::min<uint64_t>(shots, 1ull << 24);
+  double* hu = static_cast<double*>(s.get_pinned(B * 16));  // before any async work (may reallocate)
+  uint64_t* hout = reinterpret_cast<uint64_t*>(hu + B);
   char* extra;
-  SamplerBuffers b = sampler_buffers(s, shots * 16, &extra);
+  SamplerBuffers b = sampler_buffers(s, B * 16, &extra);
   double* du = reinterpret_cast<double*>(extra);
-  unsigned long long* dout = reinterpret_cast<unsigned long long*>(extra + shots * 8);
+  unsigned long long* dout = reinterpret_cast<unsigned long long*>(extra + B * 8);
   build_cumulative(s, b, exact);
-  gen(hu);  // overlaps the cumulative build on the GPU
-  QSB_CUDA(cudaMemcpyAsync(du, hu, shots * 8, cudaMemcpyHostToDevice, s.stream));
-  k_search<<<grid_for(shots, s.device), kThreads, 0, s.stream>>>(b.cum, s.size, b.total, du, shots, dout);
-  QSB_LAUNCHED();
-  QSB_CUDA(cudaMemcpyAsync(hout, dout, shots * 8, cudaMemcpyDeviceToHost, s.stream));
-  QSB_CUDA(cudaStreamSynchronize(s.stream));
-  std::memcpy(out_host, hout, shots * 8);
+  for (uint64_t done = 0; done < shots; done += B) {
+    const uint64_t cnt = std::min(B, shots - done);
+    gen(hu, cnt);  // the first batch overlaps the cumulative build on the GPU
+    QSB_CUDA(cudaMemcpyAsync(du, hu, cnt * 8, cudaMemcpyHostToDevice, s.stream));
+    k_search<<<grid_for(cnt, s.device), kThreads, 0, s.stream>>>(b.cum, s.size, b.total, du, cnt, dout);
+    QSB_LAUNCHED();
+    QSB_CUDA(cudaMemcpyAsync(hout, dout, cnt * 8, cudaMemcpyDeviceToHost, s.stream));
+    QSB_CUDA(cudaStreamSynchronize(s.stream));
+    std::memcpy(out_host + done, hout, cnt * 8);
+  }
 }
 
 void sample(State& s, const double* uniforms_host, uint64_t shots, bool exact, uint64_t* out_host) {
-  sample_gen(s, shots, exact, out_host, [&](double* hu) { std::memcpy(hu, uniforms_host, shots * 8); });
+  uint64_t next = 0;
+  sample_gen(s, shots, exact, out_host, [&](double* hu, uint64_t cnt) {
+    std::memcpy(hu, uniforms_host + next, cnt * 8);
+    next += cnt;
+  });
 }
 
 void reduced_density(State& s, const uint32_t* targets, uint32_t k, double* out) {

@@ -50,7 +50,8 @@ void scale(State& s, double re, double im);                                     
 // BasisSampler (statevector.hpp:542-570) + draws.  exact: reproduce the serial
 // cumulative sum bit for bit (see kernels.cu, "serial-equivalent scan").
 void sample(State& s, const double* uniforms_host, uint64_t shots, bool exact, uint64_t* out_host);
-void sample_gen(State& s, uint64_t shots, bool exact, uint64_t* out_host, const std::function<void(double*)>& gen);
+void sample_gen(State& s, uint64_t shots, bool exact, uint64_t* out_host,
+                const std::function<void(double*, uint64_t)>& gen);
 
 // <psi|P|psi> for Pauli strings given as (xmask, zmask, #Y) per term.
 void expect_pauli(State& s, const std::vector<uint64_t>& xmask, const std::vector<uint64_t>& zmask,

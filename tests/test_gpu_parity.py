@@ -715,3 +715,21 @@ def test_marginal_run_kernel(monkeypatch, n, qubits):
     got_lanes = sv.probabilities(qubits)
     assert np.max(np.abs(got - want)) <= 1e-13
     assert np.max(np.abs(got_lanes - want)) <= 1e-13
+
+
+def test_sampler_batches_beyond_2_24_shots():
+    """More shots than one staging batch (2^24): the Rng stream continues
+    across batches -- identical to the reference's single loop; caller-given
+    uniforms are searched independently of the batch boundary."""
+    n, shots = 12, (1 << 24) + 777
+    sv = Q.StateVector(n)
+    sv.apply_circuit(Q.gen_random_circuit(n, 3, 11).gates())
+    a = sv.amplitudes()
+    got = sv.sample_seeded(9, shots, exact=True)
+    want = ol.sample_seeded(a, n, 9, shots)
+    assert got.shape == (shots,) and np.array_equal(got, want)
+    u = np.random.default_rng(3).random(shots)
+    full = sv.sample(u)
+    lo = (1 << 24) - 5
+    assert np.array_equal(full[lo:lo + 10], sv.sample(u[lo:lo + 10]))
+    assert np.array_equal(full[:1000], sv.sample(u[:1000]))
