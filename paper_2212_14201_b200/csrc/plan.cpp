@@ -1,5 +1,6 @@
 #include "plan.hpp"
 
+#include <cmath>
 #include <list>
 #include <mutex>
 #include <string>
@@ -172,6 +173,22 @@ TileSkip zero_tiles(const Step& st, uint64_t basis) {
   return k;
 }
 
+// Algorithmic bytes of one per-gate kernel (read + write of the amplitudes
+// it touches; `amp` = the state's bytes): controls halve the set per control,
+// a phase with d0 == 1 and a SWAP touch half of what remains.
+double op_bytes(const Op& op, double amp) {
+  double f = std::ldexp(1.0, -static_cast<int>(op.controls.size()));
+  switch (op.kind) {
+    case OpKind::Identity: return 0.0;
+    case OpKind::Diag:
+      if (op.m[0] == cd(1.0)) f *= 0.5;
+      break;
+    case OpKind::Swap: f *= 0.5; break;
+    default: break;
+  }
+  return 2.0 * amp * f;
+}
+
 void execute_plan_from_basis(State& s, const Plan& p, uint64_t basis, double* checksum, StepProfile* prof) {
   if (p.n != s.n) throw ValidationError("plan was compiled for a different qubit count");
   if (p.g != s.g) throw ValidationError("plan was compiled for a sharded state (use the shard API)");
@@ -242,6 +259,7 @@ void execute_plan_from_basis(State& s, const Plan& p, uint64_t basis, double* ch
     } else {
       settle();
       execute_step(s, p.steps[i]);
+      if (p.steps[i].kind == Step::OpStep) bytes = op_bytes(p.steps[i].op, amp);
     }
     mark(i, bytes);
   }
