@@ -1539,8 +1539,17 @@ __global__ void __launch_bounds__(kThreads) k_pauli_group(const double2* __restr
       im[t] += neg ? -pi : pi;
     }
   };
+  constexpr int U = 4;  // elements (pairs) in flight per thread
   if (!xmask) {
-    for (uint64_t j = lo + threadIdx.x; j < hi; j += blockDim.x) {
+    uint64_t j = lo + threadIdx.x;
+    for (; j + (U - 1) * blockDim.x < hi; j += U * blockDim.x) {
+      double2 x[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) x[u] = __ldcs(a + j + u * blockDim.x);
+#pragma unroll
+      for (int u = 0; u < U; ++u) add(j + u * blockDim.x, x[u], x[u]);
+    }
+    for (; j < hi; j += blockDim.x) {
       const double2 x = __ldcs(a + j);
       add(j, x, x);
     }
@@ -1552,9 +1561,7 @@ __global__ void __launch_bounds__(kThreads) k_pauli_group(const double2* __restr
     const uint64_t half = size >> 1;
     const uint64_t pchunk = (half + gridDim.x - 1) / gridDim.x;
     const uint64_t plo = blockIdx.x * pchunk, phi = min(half, plo + pchunk);
-    for (uint64_t k = plo + threadIdx.x; k < phi; k += blockDim.x) {
-      const uint64_t j = ((k >> hb) << (hb + 1)) | (k & ((1ull << hb) - 1));
-      const double2 x = __ldcs(a + j), y = __ldcs(a + (j ^ xmask));
+    auto pair = [&](uint64_t j, double2 x, double2 y) {
       const double pr = fma(y.x, x.x, y.y * x.y);
       const double pi = fma(y.x, x.y, -y.y * x.x);
 #pragma unroll
@@ -1564,6 +1571,23 @@ __global__ void __launch_bounds__(kThreads) k_pauli_group(const double2* __restr
         re[t] += (n1 ? -pr : pr) + (n2 ? -pr : pr);
         im[t] += (n1 ? -pi : pi) - (n2 ? -pi : pi);
       }
+    };
+    auto jof = [&](uint64_t k) { return ((k >> hb) << (hb + 1)) | (k & ((1ull << hb) - 1)); };
+    uint64_t k = plo + threadIdx.x;
+    for (; k + (U - 1) * blockDim.x < phi; k += U * blockDim.x) {
+      double2 x[U], y[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const uint64_t j = jof(k + u * blockDim.x);
+        x[u] = __ldcs(a + j);
+        y[u] = __ldcs(a + (j ^ xmask));
+      }
+#pragma unroll
+      for (int u = 0; u < U; ++u) pair(jof(k + u * blockDim.x), x[u], y[u]);
+    }
+    for (; k < phi; k += blockDim.x) {
+      const uint64_t j = jof(k);
+      pair(j, __ldcs(a + j), __ldcs(a + (j ^ xmask)));
     }
   }
 #pragma unroll
