@@ -733,3 +733,24 @@ def test_sampler_batches_beyond_2_24_shots():
     lo = (1 << 24) - 5
     assert np.array_equal(full[lo:lo + 10], sv.sample(u[lo:lo + 10]))
     assert np.array_equal(full[:1000], sv.sample(u[:1000]))
+
+
+@pytest.mark.parametrize("n", [1, 2, 3])
+def test_pair_kernels_on_tiny_states(n):
+    """256-bit pair kernels on states of 1-3 qubits (a single pair / group)."""
+    rng = np.random.default_rng(40 + n)
+    a0 = rng.normal(size=1 << n) + 1j * rng.normal(size=1 << n)
+    a0 /= np.linalg.norm(a0)
+    gates = [Q.make_gate(Q.GateKind.H, [0]), Q.make_gate(Q.GateKind.RZ, [0], [0.3]),
+             Q.make_gate(Q.GateKind.U3, [0], [0.2, 0.5, -0.7])]
+    if n > 1:
+        g = Q.make_gate(Q.GateKind.X, [0])
+        g.controls = [n - 1]
+        gates.append(g)
+        gates.append(Q.make_custom_gate([n - 1, 0], np.linalg.qr(rng.normal(size=(4, 4)) + 1j * rng.normal(size=(4, 4)))[0]))
+    sv = Q.StateVector(n)
+    sv.set_amplitudes(a0)
+    for g in gates:
+        sv.apply_gate(g)
+    want = ol.run_gates(n, gates, state=a0.copy())
+    assert np.max(np.abs(sv.amplitudes() - want)) <= 1e-12
