@@ -842,12 +842,12 @@ struct Gen {
     if (!h.oop) {
       k << "  const unsigned long long TLS = 0ull";
       for (uint32_t b = 0; b < h.t; ++b) k << " | ((unsigned long long)((tid >> " << b << ") & 1u) << " << h.store.tq[b] << ")";
-      k << ";\n";
+      k << ";\n  (void)TLS;\n";
     }
     if (h.oop) {
       k << "  const unsigned long long TLO = 0ull";
       for (uint32_t b = 0; b < h.t; ++b) k << " | ((unsigned long long)((tid >> " << b << ") & 1u) << " << h.store.tq[b] << ")";
-      k << ";\n";
+      k << ";\n  (void)TLO;\n";
     }
     // Runs from a basis state, in place: only the tiles that can be non-zero
     // are visited -- the compact counter kk is spread over the tile-index bits
@@ -977,8 +977,8 @@ struct Gen {
     }
     k << "    const unsigned long long tile = expand(kk);\n";
     k << "    const unsigned long long base = base_of(tile) | rank_base;\n";
-    k << "    const unsigned long long tix = tile | (rank_base >> " << h.m << ");\n";
-    k << "    unsigned long long G = base | TL;\n";
+    k << "    const unsigned long long tix = tile | (rank_base >> " << h.m << ");\n    (void)tix;\n";
+    k << "    unsigned long long G = base | TL;\n    (void)G;\n";
     k << s.str();
     k << "  }\n";
     // peer stores must be visible system-wide before the stream barrier that follows
