@@ -28,6 +28,20 @@ uint64_t Plan::launches() const {
   return l;
 }
 
+// An out-of-place permutation pass needs a second 2^n-amplitude buffer: plan
+// it only when two states fit in the current device's memory (a 33-qubit
+// state, 128 GiB, fits a B200 once, not twice).
+bool second_buffer_fits(uint32_t n) {
+  int dev = 0;
+  size_t free_b = 0, total_b = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess || cudaMemGetInfo(&free_b, &total_b) != cudaSuccess) {
+    cudaGetLastError();
+    return n <= 32;  // no device to ask (planning on a host without a GPU)
+  }
+  const double need = 2.0 * 16.0 * std::ldexp(1.0, static_cast<int>(n));
+  return need <= 0.9 * static_cast<double>(total_b);
+}
+
 std::unique_ptr<Plan> make_plan(uint32_t n, const qs_gate* gates, uint64_t count, uint32_t mode,
                                 uint32_t max_fused_qubits, uint32_t global_qubits, bool sharded) {
   auto plan = std::make_unique<Plan>();
@@ -60,7 +74,7 @@ std::unique_ptr<Plan> make_plan(uint32_t n, const qs_gate* gates, uint64_t count
     }
   }
   if (plan->mode == QS_PLAN_TILED) {
-    plan_tiles(n, ops, plan->steps, global_qubits, sharded);
+    plan_tiles(n, ops, plan->steps, global_qubits, sharded, !sharded && !second_buffer_fits(n));
     compile_tile_steps(plan->steps);
   } else {
     for (auto& op : ops) {

@@ -184,8 +184,10 @@ double pass_cost(const TileProgram& tp);
 // Plans with and without qubit relabelling (unless fixed by QSB_TILE_REMAP),
 // with 12- and, for large unsharded states, 13-qubit tiles (unless fixed by
 // QSB_TILE_M), and keeps the cheapest plan.
+// in_place_only: no out-of-place permutation pass (it needs a second state
+// buffer): the layout is restored by in-place relabel passes instead.
 void plan_tiles(uint32_t n, std::vector<Op>& ops, std::vector<Step>& steps, uint32_t global_qubits = 0,
-                bool sharded = false);
+                bool sharded = false, bool in_place_only = false);
 // basis != null: the pass starts from |*basis> (global index) instead of
 // reading the state -- a reset fused into the first pass.
 // Exchange fused into a pass (sharded plans, peer memory): after the pass,

@@ -1344,10 +1344,11 @@ double plan_cost(const std::vector<Step>& steps) {
   return c;
 }
 
-void plan_tiles(uint32_t n, std::vector<Op>& ops, std::vector<Step>& steps, uint32_t global_qubits, bool sharded) {
+void plan_tiles(uint32_t n, std::vector<Op>& ops, std::vector<Step>& steps, uint32_t global_qubits, bool sharded,
+                bool in_place_only) {
   TileOptions o = tile_options_from_env();
   o.global_qubits = global_qubits;
-  if (sharded) o.perm_step = false;  // shards restore their layout in place
+  if (sharded || in_place_only) o.perm_step = false;  // restore the layout in place
   std::vector<uint32_t> ms{o.m};
   // 13-qubit tiles when every shard has 2^13 tiles and more (enough CTAs)
   if (!std::getenv("QSB_TILE_M") && n - global_qubits >= 26) ms.push_back(13);

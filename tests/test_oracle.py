@@ -214,3 +214,13 @@ def test_plan_cut_matches_reference(c):
     plan = Q.plan_cut(p)
     assert plan.block_a == c["block_a"] and plan.block_b == c["block_b"]
     assert plan.crossing_gates == c["crossing_gates"] and plan.branch_count == c["branch_count"]
+
+
+def test_qft_closed_form_convention():
+    """QFT|b> = 2^(-n/2) sum_k exp(2 pi i b k / 2^n) |k> in the oracle (the
+    closed form the GPU tests use beyond 30 qubits)."""
+    from paper_2212_14201_b200 import qforge as Q
+    n, b = 8, 0xA5
+    a = ol.run_gates(n, Q.gen_qft(n, b).gates())
+    k = np.arange(1 << n)
+    assert np.max(np.abs(a - np.exp(2j * np.pi * b * k / 2 ** n) / 2 ** (n / 2))) <= 1e-12
