@@ -67,6 +67,7 @@ struct Gen {
   // parameters) disagree are zero -- they are set, not read (runs from a
   // basis state: the first passes touch only a sliver of each tile)
   bool sparse = false;
+  bool sparse_zero_store = false;  // QSB_SPARSE_ZERO_STORE=1: stage the zeros too (A/B)
   // reduce: the pass also sums |a_i|^2 (i + 1) over what it stores (the
   // bench checksum, bench.hpp:141-148) -- one partial per CTA into red[]
   bool reduce = false;
@@ -711,20 +712,35 @@ struct Gen {
       s << "    cp_async_wait_all();\n";
       if (lead) {
         s << "    __syncthreads();\n";
+        const bool zsel = sparse && !sparse_zero_store;  // zeros were not staged: select them here
+        if (zsel) emit_G(mt0 + 2 * TB + 2 * R, false);  // the global index of each slot after the transpose
         for (int p = 0; p < NS; ++p) {
           name[p] = fresh();
-          s << "    const double2 " << name[p] << " = PB[R0 ^ " << slot_xor(mt0 + 2 * TB + R, p) << "u];\n";
+          const std::string rd = "PB[R0 ^ " + std::to_string(slot_xor(mt0 + 2 * TB + R, p)) + "u]";
+          if (zsel) {
+            unsigned long long off = 0;  // register qubits of the first layout (transpose meta)
+            for (int k = 0; k < R; ++k)
+              if ((p >> k) & 1) off |= 1ull << mt0[3 * TB + 2 * R + k];
+            s << "    const double2 " << name[p] << " = (((G | " << hexll(off) << ") & imask) == ival) ? " << rd
+              << " : make_double2(0.0, 0.0);\n";
+          } else {
+            s << "    const double2 " << name[p] << " = " << rd << ";\n";
+          }
         }
-        emit_G(mt0 + 2 * TB + 2 * R, false);
+        if (!zsel) emit_G(mt0 + 2 * TB + 2 * R, false);
         ti = 1;
         if (!single_buf || transposes_total == 1) s << "    __syncthreads();\n" << kIssueNext;
       } else {
         for (int p = 0; p < NS; ++p) {
           name[p] = fresh();
-          if (static_cast<uint32_t>(p) < early)
-            s << "    const double2 " << name[p] << " = PE[" << p * T << " + tid];\n";
+          const std::string slot = static_cast<uint32_t>(p) < early
+                                       ? "PE[" + std::to_string(p * T) + " + tid]"
+                                       : "PB[" + std::to_string((p - static_cast<int>(early)) * T) + " + tid]";
+          if (sparse && !sparse_zero_store)  // slots of amplitudes that disagree with the definite qubits were not staged
+            s << "    const double2 " << name[p] << " = (((G | " << hexll(loff[p]) << ") & imask) == ival) ? " << slot
+              << " : make_double2(0.0, 0.0);\n";
           else
-            s << "    const double2 " << name[p] << " = PB[" << (p - static_cast<int>(early)) * T << " + tid];\n";
+            s << "    const double2 " << name[p] << " = " << slot << ";\n";
         }
         if (early) {  // own slots only: no barrier before re-filling them
           s << kIssueEarly;
@@ -947,8 +963,12 @@ struct Gen {
             if (lead) dst = "PB + (W0 ^ " + std::to_string(slot_xor(mt0 + TB, p)) + "u)";
             else if (static_cast<uint32_t>(p) < early) dst = "PE + " + std::to_string(p * T) + " + tid";
             else dst = "PB + " + std::to_string((p - static_cast<int>(early)) * T) + " + tid";
+            // the zero is selected where the slot is read (by the reading
+            // thread, from its own global index) instead of stored here
             k << "    { const unsigned long long a = g | " << hexll(loff[p]) << "; if ((a & imask) == ival) cp_async16("
-              << dst << ", amps + (a & lmask)); else *(" << dst << ") = make_double2(0.0, 0.0); }\n";
+              << dst << ", amps + (a & lmask));";
+            if (sparse_zero_store) k << " else *(" << dst << ") = make_double2(0.0, 0.0);";
+            k << " }\n";
             continue;
           }
           if (lead)
