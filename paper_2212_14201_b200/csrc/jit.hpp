@@ -44,7 +44,8 @@ struct JitModule {
 // CUDA source of one tile pass (kernel name `name`).
 std::string tile_source(const TileProgram& tp, const std::string& name, std::vector<double2>* params,
                         size_t* table_bytes = nullptr, int force_single = -1, bool from_basis = false,
-                        const struct TileXchg* xchg = nullptr, bool sparse = false, bool reduce = false);
+                        const struct TileXchg* xchg = nullptr, bool sparse = false, bool reduce = false,
+                        bool zskip = false);
 
 // Generates and compiles every tile step of a plan (parallel, cached by source).
 void compile_tile_steps(std::vector<Step>& steps);

@@ -68,6 +68,10 @@ struct Gen {
   // basis state: the first passes touch only a sliver of each tile)
   bool sparse = false;
   bool sparse_zero_store = false;  // QSB_SPARSE_ZERO_STORE=1: stage the zeros too (A/B)
+  // zskip: amplitudes whose qubits in omask disagree with oval (kernel
+  // parameters: qubits still definite when the pass ends) are zero after the
+  // pass and never read before they are written again -- not stored
+  bool zskip = false;
   // reduce: the pass also sums |a_i|^2 (i + 1) over what it stores (the
   // bench checksum, bench.hpp:141-148) -- one partial per CTA into red[]
   bool reduce = false;
@@ -828,7 +832,11 @@ struct Gen {
         for (int k = 0; k < R; ++k)
           if ((p >> k) & 1) off |= h.store.rs[k];
         const std::string offs = FO.empty() ? hexll(off) : "(" + hexll(off) + " ^ " + FO + ")";
-        s << "    __stcs(SP + " << offs << ", " << name[p] << ");\n";
+        if (zskip)  // known-zero amplitudes (omask / oval) stay unwritten
+          s << "    if (((G | " << offs << ") & omask) == oval) ";
+        else
+          s << "    ";
+        s << "__stcs(SP + " << offs << ", " << name[p] << ");\n";
         if (reduce)
           s << "    ACC += __fma_rn(" << name[p] << ".x, " << name[p] << ".x, __dmul_rn(" << name[p] << ".y, " << name[p]
             << ".y)) * (double)((G | " << offs << ") + 1ull);\n";
@@ -847,7 +855,8 @@ struct Gen {
       << "    const unsigned long long ntiles, const unsigned long long basis, const QsbPeers PEERS,\n"
     << "    const unsigned long long xaval, const unsigned long long dmask, const unsigned long long dval,\n"
     << "    const unsigned long long imask, const unsigned long long ival,\n"
-    << "    const unsigned long long tmask, const unsigned long long tval, double* __restrict__ red,\n"
+    << "    const unsigned long long tmask, const unsigned long long tval,\n"
+    << "    const unsigned long long omask, const unsigned long long oval, double* __restrict__ red,\n"
     << "    const __grid_constant__ QsbCoef P, const __grid_constant__ QsbTmap TMAP) {\n";
     k << "  extern __shared__ __align__(1024) double2 sm[];\n";
     if (reduce) k << "  double ACC = 0.0;\n";

@@ -243,14 +243,32 @@ void execute_plan_from_basis(State& s, const Plan& p, uint64_t basis, double* ch
     prof->bytes.assign(p.steps.size(), 0.0);
     QSB_CUDA(cudaEventRecord(ev[0], s.stream));
   }
+  // Known-zero stores skipped (kVarZeroSkip): an in-place pass that is not the
+  // last one does not store the amplitudes that disagree with the qubits still
+  // definite at the next step -- that step never reads them (zero tiles /
+  // sparse reads), and they join `unwritten`, zeroed by settle() only if a
+  // later step would read everything or at the end.
+  const bool zskip_on = !std::getenv("QSB_NO_ZERO_STORE_SKIP");
+  auto set_zskip = [&](size_t i, TileSkip& k) {
+    if (!zskip_on || i == last || p.steps[i].tile->h.oop) return false;
+    const TileSkip kn = zero_tiles(p.steps[i + 1], basis);
+    unsigned long long tb = 0;
+    for (uint32_t b = 0; b < p.steps[i].tile->h.m; ++b) tb |= 1ull << p.steps[i].tile->h.S[b];
+    k.omask = (kn.mask | kn.imask) & tb;
+    k.oval = (kn.val | kn.ival) & tb;
+    if (!k.omask) return false;
+    unwritten = TileSkip{kn.mask | kn.imask, kn.val | kn.ival};  // every amplitude disagreeing may be stale
+    return true;
+  };
   size_t i = 0;
   if (!p.steps.empty() && p.steps[0].kind == Step::TileStep && !std::getenv("QSB_NO_FUSED_RESET")) {
     TileSkip k = zero_tiles(p.steps[0], basis);
     k.lazy = lazy && !p.steps[0].tile->h.oop;
+    const bool zs = set_zskip(0, k);
     const unsigned g0 = launch_tile(s, *p.steps[0].tile, &basis, nullptr, &k, last == 0 ? part : nullptr);
     if (last == 0) parts = g0;
-    if (k.lazy) unwritten = TileSkip{k.mask, k.val};
-    mark(0, amp * (k.lazy ? frac(k.mask) : 1.0));  // writes only
+    if (k.lazy && !zs) unwritten = TileSkip{k.mask, k.val};
+    mark(0, amp * (k.lazy ? frac(k.mask) : 1.0) * (zs ? frac(k.omask) : 1.0));  // writes only
     i = 1;
   } else {
     fill_basis(s, basis);
@@ -259,14 +277,16 @@ void execute_plan_from_basis(State& s, const Plan& p, uint64_t basis, double* ch
   for (; i < p.steps.size(); ++i) {
     double bytes = 2 * amp;
     if (p.steps[i].kind == Step::TileStep) {
-      const TileSkip k = zero_tiles(p.steps[i], basis);
+      TileSkip k = zero_tiles(p.steps[i], basis);
+      const TileSkip before = unwritten;
+      const bool zs = set_zskip(i, k);
       const unsigned gi = launch_tile(s, *p.steps[i].tile, nullptr, nullptr, &k, i == last ? part : nullptr);
       if (i == last) parts = gi;
       if (p.steps[i].tile->h.oop) unwritten = TileSkip{};  // the new buffer is written everywhere
-      else if (unwritten.mask) unwritten = TileSkip{k.mask, k.val};
+      else if (!zs && before.mask) unwritten = TileSkip{k.mask, k.val};
       // in place: only possibly non-zero tiles are visited, inside them only
       // amplitudes agreeing with the definite tile qubits are read
-      if (!p.steps[i].tile->h.oop) bytes = amp * frac(k.mask) * (frac(k.imask) + 1.0);
+      if (!p.steps[i].tile->h.oop) bytes = amp * frac(k.mask) * (frac(k.imask) + (zs ? frac(k.omask) : 1.0));
     } else if (i == last && part && p.steps[i].kind == Step::PermStep) {
       settle();
       parts = permute_qubits(s, p.steps[i].perm, part);

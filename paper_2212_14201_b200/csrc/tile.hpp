@@ -205,6 +205,10 @@ constexpr unsigned kMaxTileGrid = 8192;  // CTAs of a reducing tile pass (partia
 struct TileSkip {
   unsigned long long mask = 0, val = 0;    // definite qubits outside the tile: zero tiles
   unsigned long long imask = 0, ival = 0;  // definite tile qubits: only matching amplitudes are read
+  // tile qubits still definite after the pass (the next step's definite qubits):
+  // amplitudes that disagree are zero and are not stored (the next step does
+  // not read them; in place, not the last step, only tile steps follow)
+  unsigned long long omask = 0, oval = 0;
   // first pass of a run from a basis state: write only the tiles that can be
   // non-zero (the rest is zeroed later, only if some step would read it)
   bool lazy = false;
