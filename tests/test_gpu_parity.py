@@ -777,3 +777,45 @@ def test_states_beyond_the_reference_cap(n):
             assert abs(sv.amplitude(k) - want) <= 1e-12, k
     finally:
         del sv
+
+
+def _partial_qft(n, lo, b):
+    """QFT on qubits lo..n-1 of |b> (qubits below lo stay definite to the end)."""
+    p = Q.gen_qft(n - lo, b >> lo)
+    gates = []
+    for g in p.gates():
+        g2 = Q.make_gate(Q.GateKind(g.kind), [t + lo for t in g.targets], list(g.params))
+        g2.controls = [c + lo for c in g.controls]
+        g2.dagger = g.dagger
+        gates.append(g2)
+    return gates
+
+
+@pytest.mark.parametrize("n,lo,tail", [(22, 4, "none"), (23, 6, "h_low"), (20, 2, "x_low"), (22, 5, "pergate")])
+def test_runs_from_basis_leave_no_stale_amplitudes(n, lo, tail):
+    """Runs from a basis state where low qubits stay definite through several
+    passes: the passes skip storing known-zero amplitudes, the lazily zeroed
+    set is settled before per-gate steps and at the end.  The state buffer is
+    filled with garbage first; every amplitude must match the oracle."""
+    b = 0x2AD5A5 & ((1 << n) - 1)
+    gates = _partial_qft(n, lo, b)
+    if tail == "h_low":
+        gates += [Q.make_gate(Q.GateKind.H, [1]), Q.make_gate(Q.GateKind.RY, [lo - 1], [0.4])]
+    elif tail == "x_low":
+        gates += [Q.make_gate(Q.GateKind.X, [0]), Q.make_gate(Q.GateKind.CNOT, [n - 1, 1])]
+    rng = np.random.default_rng(n + lo)
+    sv = Q.StateVector(n)
+    sv.set_amplitudes(rng.normal(size=1 << n) + 1j * rng.normal(size=1 << n))  # garbage everywhere
+    plan = N.QS_PLAN_UNFUSED if tail == "pergate" else N.QS_PLAN_TILED
+    if tail == "pergate":  # tile passes followed by per-gate kernels: settle() before them
+        cc = Q.CompiledCircuit(n, gates)
+        cc.execute(sv, from_basis=b)
+        extra = [Q.make_gate(Q.GateKind.H, [0]), Q.make_gate(Q.GateKind.Z, [2])]
+        sv.apply_circuit(extra, plan)
+        gates = gates + extra
+    else:
+        Q.CompiledCircuit(n, gates).execute(sv, from_basis=b)
+    a0 = np.zeros(1 << n, dtype=np.complex128)
+    a0[b] = 1
+    want = ol.run_gates(n, gates, state=a0)
+    assert np.max(np.abs(sv.amplitudes() - want)) <= 1e-10
