@@ -45,7 +45,7 @@ struct JitModule {
 std::string tile_source(const TileProgram& tp, const std::string& name, std::vector<double2>* params,
                         size_t* table_bytes = nullptr, int force_single = -1, bool from_basis = false,
                         const struct TileXchg* xchg = nullptr, bool sparse = false, bool reduce = false,
-                        bool zskip = false);
+                        bool zskip = false, unsigned long long zwarp = 0);
 
 // Generates and compiles every tile step of a plan (parallel, cached by source).
 void compile_tile_steps(std::vector<Step>& steps);

@@ -72,6 +72,15 @@ struct Gen {
   // parameters: qubits still definite when the pass ends) are zero after the
   // pass and never read before they are written again -- not stored
   bool zskip = false;
+  // zwarp_qubits (zskip passes): tile qubits definite from the start to the
+  // end of the pass.  If they sit on the same thread bits in every register
+  // layout of the pass (never gated, never exchanged), the thread index is
+  // permuted so that they land on the warp bits: a warp whose bits disagree
+  // with ival holds only zeros for the whole pass and just keeps the block
+  // barriers in step (no loads, arithmetic or stores).
+  unsigned long long zwarp_qubits = 0;
+  int zw_pos[kTileMaxT] = {};  // thread bit -> physical tid bit (identity unless zero warps apply)
+  std::string zw_cond;        // per-thread: this warp holds only zeros
   // reduce: the pass also sums |a_i|^2 (i + 1) over what it stores (the
   // bench checksum, bench.hpp:141-148) -- one partial per CTA into red[]
   bool reduce = false;
@@ -629,6 +638,42 @@ struct Gen {
     // cp.async destinations are its write slots) or, from a basis state, into
     // the register initialisation
     const bool lead = leading_transpose(tp) && (from_basis || (prefetch && early == 0));
+    // zero warps (see zwarp_qubits): every register layout must keep those
+    // qubits on the same thread bits; up to TB - 5 of them go to the warp bits
+    for (uint32_t b = 0; b < TB; ++b) zw_pos[b] = static_cast<int>(b);
+    zw_cond.clear();
+    if (zwarp_qubits && zskip && sparse && prefetch && early == 0 && !tma && !xk && !h.oop && !reduce && TB > 5) {
+      std::vector<const uint32_t*> layouts{h.load.tq, h.store.tq};
+      for (const TOp& o : tp.ops) {
+        if (o.type == TO_TRANSPOSE) layouts.push_back(tp.meta.data() + o.meta + 2 * TB + 2 * R);
+        if (o.type == TO_RELABEL) layouts.push_back(tp.meta.data() + o.meta);
+      }
+      std::vector<uint32_t> bits;  // thread bits holding zero-warp qubits, in every layout
+      for (uint32_t b = 0; b < TB; ++b) {
+        if (!((zwarp_qubits >> h.load.tq[b]) & 1)) continue;
+        bool same = true;
+        for (const uint32_t* tq : layouts) same = same && tq[b] == h.load.tq[b];
+        if (same) bits.push_back(b);
+      }
+      const uint32_t W = TB - 5;  // warp bits of the block
+      if (bits.size() > W) bits.resize(W);
+      if (!bits.empty()) {
+        std::vector<char> moved(TB, 0);
+        std::ostringstream c;
+        c << "(0u";
+        for (size_t i = 0; i < bits.size(); ++i) {  // zero-warp bits -> the top physical bits
+          zw_pos[bits[i]] = static_cast<int>(TB - 1 - i);
+          moved[bits[i]] = 1;
+          c << " | ((tid >> " << bits[i] << ") ^ (unsigned)(ival >> " << h.load.tq[bits[i]] << "))";
+        }
+        c << ") & 1u";
+        int next = 0;  // the other logical bits keep their order on the remaining physical bits
+        for (uint32_t b = 0; b < TB; ++b)
+          if (!moved[b]) zw_pos[b] = next++;
+        zw_cond = c.str();
+        warp_local_ok = false;  // logical lanes no longer form the physical warps
+      }
+    }
     const uint32_t* mt0 = lead ? tp.meta.data() + tp.ops[0].meta : nullptr;
     auto xorexpr = [&](const uint32_t* cols) {
       std::ostringstream e;
@@ -683,6 +728,7 @@ struct Gen {
       if (prefetch) s << "  " << kIssueNext;
       s << "      continue;\n    }\n";
     }
+    const size_t zw_at = s.str().size();  // the zero-warp path goes here (see below)
     int ti = 0;
     tile_barrier_done = lead && !from_basis;  // the fused leading exchange has its own block barrier
     if (from_basis) {
@@ -860,7 +906,14 @@ struct Gen {
     << "    const __grid_constant__ QsbCoef P, const __grid_constant__ QsbTmap TMAP) {\n";
     k << "  extern __shared__ __align__(1024) double2 sm[];\n";
     if (reduce) k << "  double ACC = 0.0;\n";
-    k << "  const unsigned tid = threadIdx.x;\n";
+    if (zw_cond.empty()) {
+      k << "  const unsigned tid = threadIdx.x;\n";
+    } else {  // logical thread bit b = physical bit zw_pos[b]
+      k << "  const unsigned tid = 0u";
+      for (uint32_t b = 0; b < h.t; ++b) k << " | (((threadIdx.x >> " << zw_pos[b] << ") & 1u) << " << b << ")";
+      k << ";\n";
+      k << "  const bool ZW = " << zw_cond << ";\n";
+    }
     k << "  const unsigned long long TL = 0ull";
     for (uint32_t b = 0; b < h.t; ++b) k << " | ((unsigned long long)((tid >> " << b << ") & 1u) << " << h.load.tq[b] << ")";
     k << ";\n";
@@ -1008,7 +1061,18 @@ struct Gen {
     k << "    const unsigned long long base = base_of(tile) | rank_base;\n";
     k << "    const unsigned long long tix = tile | (rank_base >> " << h.m << ");\n    (void)tix;\n";
     k << "    unsigned long long G = base | TL;\n    (void)G;\n";
-    k << s.str();
+    std::string body = s.str();
+    if (!zw_cond.empty()) {  // zero warps: only the block barriers of the pass, in the same order
+      const std::string tail = body.substr(zw_at);
+      size_t nb = 0;
+      for (size_t at = tail.find("__syncthreads();"); at != std::string::npos; at = tail.find("__syncthreads();", at + 1))
+        ++nb;
+      std::string zb = "    if (ZW) {\n      cp_async_wait_all();\n";
+      for (size_t i = 0; i < nb; ++i) zb += "      __syncthreads();\n";
+      zb += "      continue;\n    }\n";
+      body = body.substr(0, zw_at) + zb + tail;
+    }
+    k << body;
     k << "  }\n";
     // peer stores must be visible system-wide before the stream barrier that follows
     if (xk) k << "  __threadfence_system();\n";

@@ -139,7 +139,8 @@ std::shared_ptr<const Plan> cached_plan(uint32_t n, const qs_gate* gates, uint64
   for (const char* k : {"QSB_TILE_M", "QSB_TILE_R", "QSB_TILE_LOW", "QSB_TILE_REMAP", "QSB_PERM_STEP", "QSB_ABSORB_X",
                         "QSB_NO_ABSORB_X", "QSB_FOLD_PERM", "QSB_FREE_LOAD", "QSB_SHARD_BATCH", "QSB_TILE_PREFETCH",
                         "QSB_TILE_SINGLEBUF", "QSB_TILE_MINB", "QSB_BASIS_MINB", "QSB_TILE_EARLY",
-                        "QSB_NO_WARP_TRANSPOSE", "QSB_TILE_VARIANTS", "QSB_TMA", "QSB_NO_FLIP_FRAME", "QSB_SPARSE_ZERO_STORE"})
+                        "QSB_NO_WARP_TRANSPOSE", "QSB_TILE_VARIANTS", "QSB_TMA", "QSB_NO_FLIP_FRAME", "QSB_SPARSE_ZERO_STORE",
+                        "QSB_NO_ZERO_WARPS"})
     if (const char* v = std::getenv(k)) knobs += std::string(k) + "=" + v + ";";
   const std::string key =
       plan_key(n, gates, count, mode, max_fused_qubits, global_qubits) + (sharded ? "S" : "") + knobs;
