@@ -55,6 +55,10 @@ WORKLOADS = {
 HUGE = os.path.join(ROOT, "tests", "golden", "huge", "manifest_huge.json")
 # in-place stream over a 64 MiB (L2-resident) buffer on this pool's B200s, GB/s
 L2_STREAM_GBS = 9353.3
+# In-place read-modify-write streaming of a 16 GiB buffer on B200 (the access
+# pattern of an in-place tile pass; the copy peak above reads one buffer and
+# writes another): 6082.4 GB/s, profiles/r2/l2_probe.jsonl (log2n 30).
+HBM_INPLACE_GBS = 6082.4
 
 
 def peaks():
@@ -427,6 +431,9 @@ def roofline_of(m, runner, plan, workload, peak, peak_kind):
          "step_bytes": step_bytes,
          "step_achieved": round(step_bytes / (m["ms_per_step"] / 1e3) / 1e9, 1),
          "step_frac": round(step_bytes / (m["ms_per_step"] / 1e3) / 1e9 / peak, 4) if peak else None}
+    if not l2_resident:  # context: the same achieved bandwidth against in-place streaming
+        r["inplace_stream_gbs"] = HBM_INPLACE_GBS
+        r["frac_vs_inplace_stream"] = round(achieved / HBM_INPLACE_GBS, 4)
     xchg = [t for t, k in zip(per, kinds) if k == 2]
     if xchg:
         r["exchanges_per_step"] = len(xchg)
